@@ -1,0 +1,219 @@
+/*
+ * kareto.h -- C ABI of the B200-native Kareto configuration-evaluation hot path.
+ *
+ * Kareto (arXiv 2603.08739) searches tiered KV-cache storage configurations: a planner
+ * proposes configurations (DRAM capacity, disk TTL, disk medium; PAPER.md 4.1 line 506),
+ * a simulator replays "request arrival times, input/output token lengths, and
+ * token-level KV-block hashes" against each and a selector keeps the
+ * non-dominated ones (Alg. 1 line 22 "ParetoFilter(P)").  This library
+ * evaluates very many configurations against one trace on the GPU:
+ *
+ *   kareto_load_trace  -- ingest, chained 16-token block hashes ("salted hash
+ *                         blocks (16 tokens per block)"), previous access / reuse
+ *                         interval / prefix-subtree group of every block access
+ *                         (P:601), exact LRU stack depths.
+ *   kareto_eval_grid   -- per-configuration tier hit/miss/eviction counts and the
+ *                         objective vector of Eq. 1 with the cost of Eq. 2
+ *                         (P:227-231), for many configurations at once.
+ *   kareto_pareto      -- diminishing-return pruning (Alg. 1 expansion test,
+ *                         P:555-559) then non-dominance.
+ *
+ * Readings of the paper (R1..R35) and the exact semantics are in DESIGN.md.
+ *
+ * Conventions
+ *   - Every function returns a kareto_status; no exception crosses the ABI.  On failure a
+ *     message is available from kareto_last_error(ctx) until the next call on that ctx.
+ *   - Ownership: the caller owns every buffer it passes.  Trace inputs are copied at load;
+ *     handles (kareto_ctx, kareto_trace) are owned by the library and released with
+ *     kareto_destroy / kareto_trace_free.
+ *   - Synchronicity: every call returns after its work on the context stream is complete.
+ *   - Device pointers must be cudaMalloc'd (or cudaMallocAsync'd) memory of the context
+ *     device; host pointers are ordinary (pinned memory makes copies faster).
+ *   - Multi-GPU: with world > 1 every rank calls kareto_eval_grid collectively with the
+ *     FULL identical configuration list; each evaluates a deterministic shard and the
+ *     objective vectors and counts are all-gathered over NCCL (NVLink), so outputs are
+ *     complete and byte-identical on every rank.
+ */
+#ifndef KARETO_H
+#define KARETO_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  KARETO_OK = 0,
+  KARETO_E_INVALID = 1,     /* bad argument / configuration / model constant          */
+  KARETO_E_PARSE = 2,       /* malformed trace arrays (offsets decreasing, ...)       */
+  KARETO_E_CHAIN = 3,       /* block hashes are not chain-consistent (R7)   */
+  KARETO_E_OOM = 4,         /* device memory exhausted                                */
+  KARETO_E_CUDA = 5,        /* CUDA runtime error                                     */
+  KARETO_E_NCCL = 6,        /* NCCL error (world > 1)                                 */
+  KARETO_E_OVERFLOW = 7,    /* a 32/64-bit bound of the data layout is exceeded       */
+  KARETO_E_UNSUPPORTED = 8  /* valid request this build cannot evaluate               */
+} kareto_status;
+
+typedef struct kareto_ctx kareto_ctx;     /* device, borrowed stream, arena, NCCL comm */
+typedef struct kareto_trace kareto_trace; /* device-resident, immutable after load      */
+
+/* Create a context on CUDA `device`, enqueueing all work on `cuda_stream` (a cudaStream_t;
+ * NULL = legacy default stream; borrowed, not destroyed).  For world > 1 pass the 128-byte
+ * NCCL unique id produced on rank 0 by kareto_nccl_unique_id() and broadcast by the
+ * caller; for world == 1 pass NULL.  Errors: KARETO_E_INVALID (rank/world), _E_CUDA, _E_NCCL. */
+kareto_status kareto_create(int device, void *cuda_stream, const void *nccl_unique_id, int rank, int world,
+                            kareto_ctx **out);
+void kareto_destroy(kareto_ctx *ctx);
+/* Message of the last failed call on ctx (per-context buffer; valid until the next call). */
+const char *kareto_last_error(const kareto_ctx *ctx);
+/* Writes a 128-byte NCCL unique id to out (rank 0, world > 1). KARETO_E_NCCL if NCCL is absent. */
+kareto_status kareto_nccl_unique_id(void *out128);
+
+/* ---------------------------------------------------------------- trace ---- */
+typedef enum { KARETO_TOKENS = 0, KARETO_HASHES = 1 } kareto_input_mode;
+
+typedef struct {
+  int64_t n_requests;           /* R >= 1                                                     */
+  const int64_t *arrival_ms;    /* [R] arrival in ms, any order; stable-sorted by (arrival,
+                                   index) inside (R6)                               */
+  const int32_t *output_tokens; /* [R] >= 0 decode lengths                                    */
+  int32_t mode;                 /* kareto_input_mode                                          */
+  const int64_t *offsets;       /* [R+1] nondecreasing; TOKENS: token offsets into tokens;
+                                   HASHES: block offsets into block_hash                      */
+  const uint32_t *tokens;       /* TOKENS: [offsets[R]] input token ids; only full 16-token
+                                   blocks are hashed (R1, R3)                                 */
+  const uint64_t *block_hash;   /* HASHES: [offsets[R]] chained hashes, one per full block   */
+  const int64_t *input_tokens;  /* HASHES: [R] input lengths (>= 16*blocks) or NULL = 16*blocks */
+  uint64_t salt;                /* TOKENS: hash salt (R2)                                     */
+  int32_t top_k;                /* K >= 0 prefix-subtree groups (+1 residual, R23), K <= 1023  */
+  int32_t inputs_on_device;     /* 1: all pointers above are device pointers; 0: host         */
+} kareto_trace_desc;
+
+/* Load a trace: sort, hash (TOKENS), per-access previous position / reuse interval /
+ * group, LRU stack depth.  Validation errors: KARETO_E_INVALID
+ * (R < 1, K out of range, null pointers), _E_PARSE (offsets decreasing, output < 0,
+ * input_tokens < 16*blocks), _E_CHAIN (R7), _E_OVERFLOW (>= 2^32-1 block accesses or a
+ * reuse interval >= 2^32-1 ms), _E_OOM. */
+kareto_status kareto_load_trace(kareto_ctx *ctx, const kareto_trace_desc *desc, kareto_trace **out);
+void kareto_trace_free(kareto_trace *tr);
+
+typedef struct {
+  int64_t n_requests, n_accesses, n_unique, span_ms;
+  uint64_t input_tokens, output_tokens; /* Ltok = sum L_r, O = sum o_r               */
+  int32_t top_k;
+  int32_t max_blocks_per_request;
+} kareto_trace_info;
+/* Scalars, and per-group |B_g| (unique blocks) and N_g (reuse events) [K+1] (
+ * either array may be NULL).  Host pointers. */
+kareto_status kareto_trace_stats(const kareto_trace *tr, kareto_trace_info *info, int64_t *group_unique,
+                                 int64_t *group_reuse);
+
+typedef enum {
+  KARETO_X_HASH = 0,    /* uint64 [N] chained hash of each access, touch order         */
+  KARETO_X_PREV = 1,    /* uint32 [N] previous position of the same block, UINT32_MAX = none */
+  KARETO_X_DELTA = 2,   /* uint32 [N] reuse interval ms, UINT32_MAX = first access      */
+  KARETO_X_REQ = 3,     /* uint32 [N] request (sorted index) of each access             */
+  KARETO_X_DEPTH = 4,   /* uint32 [N] LRU depth d at request start, UINT32_MAX = first  */
+  KARETO_X_GROUP = 5,   /* uint16 [R] group of each request (sorted order)              */
+  KARETO_X_START = 6    /* uint32 [R+1] first touch position of each request            */
+} kareto_export;
+/* Copy one per-access array (touch order: request by request, blocks leaf -> root, R12)
+ * to host memory `out`.  Diagnostics / parity testing. */
+kareto_status kareto_trace_export(kareto_ctx *ctx, const kareto_trace *tr, int32_t which, void *out);
+
+/* ----------------------------------------------------------- evaluation ---- */
+enum { KARETO_LRU = 0, KARETO_FIFO = 1, KARETO_LFU = 2 };
+#define KARETO_INF UINT64_MAX   /* cap[2] == KARETO_INF => TTL (lease) mode (R19)           */
+#define KARETO_NA UINT64_MAX    /* counts: value not defined for this configuration        */
+#define KARETO_TTL_INF UINT32_MAX
+
+typedef struct {
+  uint64_t cap[3];   /* HBM, DRAM, disk capacities in 16-token blocks (R14); cap[2] == KARETO_INF
+                        selects TTL mode                                                  */
+  uint8_t policy;    /* KARETO_LRU / _FIFO / _LFU (R24)                                    */
+  uint8_t medium;    /* index into kareto_model.media                                      */
+  uint16_t tuner;    /* row of the per-group TTL table (ms) applied to the disk tier (R17) */
+  int32_t axis[3];   /* grid coordinates along HBM / DRAM / disk, used by pruning (R34)    */
+} kareto_config;     /* 40 bytes */
+
+typedef struct {
+  uint64_t hit[3];            /* prefix hits served by HBM, DRAM, disk                     */
+  uint64_t miss;              /* block accesses recomputed                                 */
+  uint64_t evict[3];          /* HBM->DRAM, out of DRAM, disk capacity drops (NA when a
+                                 finite TTL is in force in CAPACITY mode; 0 in TTL mode)   */
+  uint64_t disk_writes;       /* DRAM->disk demotions (CAPACITY, c3 > 0) / lease starts (TTL) */
+  uint64_t hit_pos_sum;       /* sum of chain positions k over hits                        */
+  uint64_t bytetime_block_ms; /* TTL mode: sum_g C_g(tau_g), block*ms              */
+  uint64_t resident_after_hole; /* diagnostic: resident blocks after the first miss        */
+} kareto_counts;              /* 88 bytes */
+
+typedef struct { double bw_base, bw_slope, bw_max, price; } kareto_medium;
+  /* bytes/s, bytes/s per provisioned GB, bytes/s cap, $ per GB-hour     */
+typedef struct { double breakpoint, rate, jump; } kareto_phi_segment;
+  /* phi_IOPS: usage >= breakpoint adds jump + rate*(min(usage, next) - breakpoint)
+     $/IOPS-month, right-continuous (R32)                                 */
+typedef struct {
+  int32_t instances, gpus_per_instance;   /* I, G                                      */
+  uint64_t alpha_ps, beta_ps, dec_ps;     /* prefill ps/token, ps/token/position, decode ps/token */
+  uint64_t block_bytes;                   /* Bb: KV bytes per 16-token block           */
+  double bw_dram;                         /* bytes/s                                   */
+  double c_hw, p_hbm, p_dram;             /* $/GPU-hour, $/GB-hour                     */
+  double iops_per_block;                  /* IOPS per block transfer                   */
+  double ttl_prov_gb;                     /* TTL mode: provisioned GB for the bandwidth curve */
+  int32_t n_media, n_phi;                 /* 1..8, 0..8                                */
+  kareto_medium media[8];
+  kareto_phi_segment phi[8];
+} kareto_model;
+
+/* Evaluate n_cfg configurations (host array) against a loaded trace.
+ *   ttl_ms    host [n_tuner][K+1] per-group disk TTLs in ms (KARETO_TTL_INF = infinity);
+ *             NULL with n_tuner == 0 means every tuner index reads an all-infinite row.
+ *   counts_out [n_cfg] or NULL; obj_out [n_cfg][3] = (mean TTFT ms, -tokens/s, cost $) or NULL;
+ *   outputs_on_device selects device (1) or host (0) output pointers.
+ * Errors: KARETO_E_INVALID (policy > 2, tuner >= n_tuner, medium >= n_media, TTL mode with
+ * an infinite TTL (R22), invalid model constants), _E_UNSUPPORTED (a configuration needs
+ * the per-configuration replay and this build has none for it), _E_OVERFLOW, _E_NCCL. */
+kareto_status kareto_eval_grid(kareto_ctx *ctx, const kareto_trace *tr, const kareto_config *cfg, int64_t n_cfg,
+                               const uint32_t *ttl_ms, int32_t n_tuner, const kareto_model *model,
+                               kareto_counts *counts_out, double *obj_out, int32_t outputs_on_device);
+
+typedef struct {
+  int32_t enabled; /* 0: no pruning                                                      */
+  double tau_e;    /* relative latency-gain threshold (default 0.05, R34)               */
+} kareto_prune;
+/* Select: status_out[i] = 2 pruned (R34), 1 frontier, 0 dominated (R35).  obj and
+ * status_out are device (on_device = 1) or host (0) pointers; cfg is a host array (its
+ * axis / policy / medium / tuner define the pruning lines; when pruning is enabled axis
+ * values must lie in [0, 65536) and tuner < 1024, else KARETO_E_INVALID).  n_frontier
+ * (host, may be NULL) receives the number of frontier configurations. */
+kareto_status kareto_pareto(kareto_ctx *ctx, const double *obj, const kareto_config *cfg, int64_t n,
+                            const kareto_prune *prune, uint8_t *status_out, int64_t *n_frontier,
+                            int32_t on_device);
+
+/* Host-only helper (no device work): the deterministic contiguous shard [*lo, *hi) of
+ * n configurations that `rank` of `world` evaluates inside kareto_eval_grid. */
+kareto_status kareto_shard_range(int64_t n, int32_t rank, int32_t world, int64_t *lo, int64_t *hi);
+
+/* ------------------------------------------------------------ profiling ---- */
+typedef struct {
+  char name[24];      /* kernel / pass name                                         */
+  double ms;          /* device time of the pass (CUDA events on the context stream),
+                         summed over its launches                                  */
+  int32_t launches;   /* number of timed launches of this pass                      */
+  int32_t own;        /* 1: a kernel of this library; 0: a CUB primitive           */
+} kareto_pass_time;
+/* Enable (1) / disable (0) per-pass CUDA-event timing of subsequent calls. */
+kareto_status kareto_set_profiling(kareto_ctx *ctx, int32_t on);
+/* Per-pass device times accumulated (while profiling is on) by all calls since context
+ * creation or the last reset; writes up to max entries and their number to *n; reset != 0
+ * clears the accumulators after reading.  *own_launches (kareto_launch_counter) counts
+ * launches of this library's own kernels (always on), reset the same way. */
+kareto_status kareto_get_pass_times(kareto_ctx *ctx, kareto_pass_time *out, int32_t max, int32_t *n,
+                                    int32_t reset);
+kareto_status kareto_launch_counter(kareto_ctx *ctx, int64_t *own_launches, int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KARETO_H */

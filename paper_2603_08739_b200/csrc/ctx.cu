@@ -1,0 +1,228 @@
+// ctx.cu -- context lifetime, device memory pool, NCCL bootstrap, pass timing, trace handles.
+#include <dlfcn.h>
+
+#include "internal.cuh"
+
+namespace kareto {
+
+// NCCL is dlopen'ed (libnccl.so.2, normally already loaded by torch.distributed), so the
+// library has no link-time NCCL dependency and world == 1 never touches it.
+
+static NcclApi *load_nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api.h ? &api : nullptr;
+  tried = true;
+  const char *names[] = {"libnccl.so.2", "libnccl.so"};
+  for (const char *n : names) {
+    api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+    if (api.h) break;
+  }
+  if (!api.h) return nullptr;
+  api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(api.h, "ncclGetUniqueId");
+  api.CommInitRank = (decltype(api.CommInitRank))dlsym(api.h, "ncclCommInitRank");
+  api.AllGather = (decltype(api.AllGather))dlsym(api.h, "ncclAllGather");
+  api.CommDestroy = (decltype(api.CommDestroy))dlsym(api.h, "ncclCommDestroy");
+  api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
+  if (!api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.CommDestroy) {
+    api.h = nullptr;
+    return nullptr;
+  }
+  return &api;
+}
+
+Pass::Pass(kareto_ctx *c, const char *name, int own, int launches) : ctx(c) {
+  if (own) ctx->own_launches += launches;
+  if (!ctx->profiling) return;
+  for (size_t i = 0; i < ctx->passes.size(); i++)
+    if (strncmp(ctx->passes[i].name, name, 23) == 0) { idx = (int)i; break; }
+  if (idx < 0 && (int)ctx->passes.size() < kMaxPasses) {
+    PassAcc p{};
+    strncpy(p.name, name, 23);
+    p.own = own;
+    ctx->passes.push_back(p);
+    idx = (int)ctx->passes.size() - 1;
+  }
+  if (idx < 0) return;
+  ctx->passes[idx].launches += launches;
+  auto take = [&]() {
+    cudaEvent_t e;
+    if (!ctx->event_pool.empty()) { e = ctx->event_pool.back(); ctx->event_pool.pop_back(); }
+    else cudaEventCreate(&e);
+    return e;
+  };
+  a = take();
+  b = take();
+  cudaEventRecord(a, ctx->stream);
+}
+
+Pass::~Pass() {
+  if (idx < 0 || !a) return;
+  cudaEventRecord(b, ctx->stream);
+  ctx->pending.push_back({idx, a, b});
+}
+
+void flush_pass_times(kareto_ctx *ctx) {
+  for (auto &p : ctx->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) ctx->passes[p.idx].ms += ms;
+    ctx->event_pool.push_back(p.a);
+    ctx->event_pool.push_back(p.b);
+  }
+  ctx->pending.clear();
+  (void)cudaGetLastError();
+}
+
+kareto_status sync(kareto_ctx *ctx, const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return fail(ctx, KARETO_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  flush_pass_times(ctx);
+  return KARETO_OK;
+}
+
+}  // namespace kareto
+
+using namespace kareto;
+
+extern "C" kareto_status kareto_nccl_unique_id(void *out128) {
+  if (!out128) return KARETO_E_INVALID;
+  NcclApi *api = load_nccl();
+  if (!api) return KARETO_E_NCCL;
+  ncclUniqueId id;
+  if (api->GetUniqueId(&id) != ncclSuccess) return KARETO_E_NCCL;
+  memcpy(out128, &id, sizeof(id) < 128 ? sizeof(id) : 128);
+  return KARETO_OK;
+}
+
+extern "C" kareto_status kareto_create(int device, void *cuda_stream, const void *nccl_unique_id, int rank, int world,
+                                       kareto_ctx **out) {
+  if (!out) return KARETO_E_INVALID;
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_unique_id)) return KARETO_E_INVALID;
+  kareto_ctx *ctx = new kareto_ctx();
+  ctx->device = device;
+  ctx->stream = (cudaStream_t)cuda_stream;
+  ctx->rank = rank;
+  ctx->world = world;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  int l2 = 0;
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
+  ctx->l2_bytes = (size_t)l2;
+  if (e == cudaSuccess) e = cudaDeviceGetDefaultMemPool(&ctx->pool, device);
+  if (e == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    e = cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    delete ctx;
+    return KARETO_E_CUDA;
+  }
+  if (world > 1) {
+    NcclApi *api = load_nccl();
+    if (!api) { delete ctx; return KARETO_E_NCCL; }
+    ncclUniqueId id;
+    memcpy(&id, nccl_unique_id, sizeof(id));
+    ncclComm_t comm;
+    if (api->CommInitRank(&comm, world, id, rank) != ncclSuccess) { delete ctx; return KARETO_E_NCCL; }
+    ctx->nccl = api;
+    ctx->nccl_comm = comm;
+  }
+  *out = ctx;
+  return KARETO_OK;
+}
+
+extern "C" void kareto_destroy(kareto_ctx *ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->stream);
+  flush_pass_times(ctx);
+  for (auto e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->nccl_comm && ctx->nccl) ctx->nccl->CommDestroy((ncclComm_t)ctx->nccl_comm);
+  delete ctx;
+}
+
+extern "C" const char *kareto_last_error(const kareto_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+extern "C" kareto_status kareto_set_profiling(kareto_ctx *ctx, int32_t on) {
+  if (!ctx) return KARETO_E_INVALID;
+  ctx->profiling = on != 0;
+  return KARETO_OK;
+}
+
+extern "C" kareto_status kareto_get_pass_times(kareto_ctx *ctx, kareto_pass_time *out, int32_t max, int32_t *n,
+                                               int32_t reset) {
+  if (!ctx || !n || (max > 0 && !out)) return KARETO_E_INVALID;
+  cudaStreamSynchronize(ctx->stream);
+  flush_pass_times(ctx);
+  int k = 0;
+  for (auto &p : ctx->passes) {
+    if (k >= max) break;
+    memset(&out[k], 0, sizeof(out[k]));
+    strncpy(out[k].name, p.name, 23);
+    out[k].ms = p.ms;
+    out[k].launches = p.launches;
+    out[k].own = p.own;
+    k++;
+  }
+  *n = k;
+  if (reset) ctx->passes.clear();
+  return KARETO_OK;
+}
+
+extern "C" kareto_status kareto_launch_counter(kareto_ctx *ctx, int64_t *own_launches, int32_t reset) {
+  if (!ctx) return KARETO_E_INVALID;
+  if (own_launches) *own_launches = ctx->own_launches;
+  if (reset) ctx->own_launches = 0;
+  return KARETO_OK;
+}
+
+extern "C" void kareto_trace_free(kareto_trace *tr) {
+  if (!tr) return;
+  kareto_ctx *ctx = tr->ctx;
+  void *ptrs[] = {tr->arr, tr->s, tr->grp, tr->hash, tr->req, tr->prev, tr->delta, tr->depth};
+  for (void *p : ptrs)
+    if (p) cudaFreeAsync(p, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  delete tr;
+}
+
+extern "C" kareto_status kareto_trace_stats(const kareto_trace *tr, kareto_trace_info *info, int64_t *group_unique,
+                                            int64_t *group_reuse) {
+  if (!tr) return KARETO_E_INVALID;
+  if (info) {
+    info->n_requests = tr->R;
+    info->n_accesses = tr->N;
+    info->n_unique = tr->U;
+    info->span_ms = tr->span_ms;
+    info->input_tokens = tr->Ltok;
+    info->output_tokens = tr->O;
+    info->top_k = tr->K;
+    info->max_blocks_per_request = tr->max_blocks;
+  }
+  for (int g = 0; g <= tr->K; g++) {
+    if (group_unique) group_unique[g] = tr->U_g[g];
+    if (group_reuse) group_reuse[g] = tr->reuse_g[g];
+  }
+  return KARETO_OK;
+}
+
+extern "C" kareto_status kareto_trace_export(kareto_ctx *ctx, const kareto_trace *tr, int32_t which, void *out) {
+  if (!ctx || !tr || !out) return KARETO_E_INVALID;
+  const void *src = nullptr;
+  size_t bytes = 0;
+  switch (which) {
+    case KARETO_X_HASH: src = tr->hash; bytes = 8 * (size_t)tr->N; break;
+    case KARETO_X_PREV: src = tr->prev; bytes = 4 * (size_t)tr->N; break;
+    case KARETO_X_DELTA: src = tr->delta; bytes = 4 * (size_t)tr->N; break;
+    case KARETO_X_REQ: src = tr->req; bytes = 4 * (size_t)tr->N; break;
+    case KARETO_X_DEPTH: src = tr->depth; bytes = 4 * (size_t)tr->N; break;
+    case KARETO_X_GROUP: src = tr->grp; bytes = 2 * (size_t)tr->R; break;
+    case KARETO_X_START: src = tr->s; bytes = 4 * (size_t)(tr->R + 1); break;
+    default: return fail(ctx, KARETO_E_INVALID, "unknown export %d", which);
+  }
+  if (bytes == 0) return KARETO_OK;
+  KCUDA(ctx, cudaMemcpyAsync(out, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return sync(ctx, "trace_export");
+}

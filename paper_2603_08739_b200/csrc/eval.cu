@@ -1,0 +1,521 @@
+// eval.cu -- kareto_eval_grid: rows a5 (K4 grid histograms), a6/a8 (K5+K7, objective.cu),
+// multi-GPU sharding + NCCL allgather (row e).
+//
+// Stack path: for LRU configurations in TTL mode,
+// or in CAPACITY mode with a uniform disk TTL, every count is a closed form of the
+// per-access quantities (d, D = d + n-1-k, delta, group, k):
+//   h1 = #{d <= c1}, h2 = #{c1 < d <= c12}, h3 = #{c12 < d <= C, delta <= tau}   (CAPACITY)
+//   h3 = sum_g #{d > c12, delta <= tau_g, g}                                   (TTL mode)
+//   e_t = #{D > b_t} - min(b_t, U);  writes / byte-time from the delta CDFs.
+// K4 builds, in ONE pass over the accesses, histograms of d (and delta) over the sorted set
+// of distinct boundaries used by the configurations of this rank's shard, privatised in
+// shared memory; inclusive scans turn them into cumulative tables; K5+K7 evaluates every
+// configuration from O(1) table lookups.
+#include <algorithm>
+#include <cub/cub.cuh>
+
+#include "eval.cuh"
+
+namespace kareto {
+
+constexpr int H_THREADS = 1024;
+constexpr int LUT_BITS = 12;                 // boundary lookup table: 4096 buckets
+constexpr int SMEM_BUDGET = 200 * 1024;
+
+// bucket LUT: lut[b] = first boundary index with Bd[i] >= (b << sh); lut[nbk] = nb
+__global__ void k_build_lut(const uint32_t *__restrict__ Bd, int nb, int sh, uint32_t *__restrict__ lut) {
+  int nbk = 1 << LUT_BITS;
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nbk; b += gridDim.x * blockDim.x) {
+    uint64_t v = (uint64_t)b << sh;
+    int lo = 0, hi = nb;
+    while (lo < hi) {
+      int m = (lo + hi) >> 1;
+      if ((uint64_t)Bd[m] >= v) hi = m; else lo = m + 1;
+    }
+    lut[b] = (uint32_t)lo;
+  }
+}
+
+// index of the first boundary >= v (nb if none)
+__device__ __forceinline__ int bin_of(uint32_t v, const uint32_t *__restrict__ Bd, int nb, const uint32_t *lut_s,
+                                      int sh) {
+  uint32_t b = v >> sh;
+  if (b >= (1u << LUT_BITS)) return nb;
+  int lo = lut_s[b], hi = lut_s[b + 1];
+  while (lo < hi) {
+    int m = (lo + hi) >> 1;
+    if (__ldg(&Bd[m]) >= v) hi = m; else lo = m + 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int tbin_of(uint32_t dl, const uint32_t *__restrict__ T, int nt) {
+  int lo = 0, hi = nt;
+  while (lo < hi) {
+    int m = (lo + hi) >> 1;
+    if (__ldg(&T[m]) >= dl) hi = m; else lo = m + 1;
+  }
+  return lo;
+}
+
+// K4a: histogram of (d-bin, tau-bin) with count and sum k, privatised in smem
+// (cells [tc][bd] restricted to the window [c_lo, c_hi)), flushed with atomics.
+__global__ void __launch_bounds__(H_THREADS) k_hist_d(uint64_t N, uint64_t per_cta, const uint32_t *__restrict__ depth,
+                                                      const uint32_t *__restrict__ req, const uint32_t *__restrict__ s,
+                                                      const uint32_t *__restrict__ delta,
+                                                      const uint32_t *__restrict__ Bd, int nb,
+                                                      const uint32_t *__restrict__ lut, int sh,
+                                                      const uint32_t *__restrict__ Tc, int ntc, int c_lo, int c_hi,
+                                                      unsigned long long *__restrict__ gcnt,
+                                                      unsigned long long *__restrict__ gsk) {
+  extern __shared__ uint32_t sm[];
+  uint32_t *lut_s = sm;                                  // (1<<LUT_BITS) + 1
+  uint32_t *cnt = lut_s + (1 << LUT_BITS) + 1;
+  const int W = c_hi - c_lo;
+  uint32_t *sk = cnt + W;
+  for (int i = threadIdx.x; i <= (1 << LUT_BITS); i += blockDim.x) lut_s[i] = lut[i];
+  for (int i = threadIdx.x; i < W; i += blockDim.x) { cnt[i] = 0; sk[i] = 0; }
+  __syncthreads();
+  uint64_t j0 = blockIdx.x * per_cta, j1 = j0 + per_cta < N ? j0 + per_cta : N;
+  for (uint64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+    uint32_t d = depth[j];
+    if (d == kNone) continue;
+    int bd = bin_of(d, Bd, nb, lut_s, sh);
+    if (bd >= nb) continue;
+    int tc = ntc > 0 ? tbin_of(delta[j], Tc, ntc) : 0;
+    int cell = tc * nb + bd - c_lo;
+    if (cell < 0 || cell >= W) continue;
+    uint32_t r = req[j];
+    uint32_t k = s[r + 1] - 1 - (uint32_t)j;
+    atomicAdd(&cnt[cell], 1u);
+    if (k) atomicAdd(&sk[cell], k);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < W; i += blockDim.x) {
+    if (cnt[i]) atomicAdd(&gcnt[c_lo + i], (unsigned long long)cnt[i]);
+    if (sk[i]) atomicAdd(&gsk[c_lo + i], (unsigned long long)sk[i]);
+  }
+}
+
+// K4b: histogram of D over the boundaries (count), window [b_lo, b_hi)
+__global__ void __launch_bounds__(H_THREADS) k_hist_D(uint64_t N, uint64_t per_cta, const uint32_t *__restrict__ depth,
+                                                      const uint32_t *__restrict__ req, const uint32_t *__restrict__ s,
+                                                      const uint32_t *__restrict__ Bd, int nb,
+                                                      const uint32_t *__restrict__ lut, int sh, int b_lo, int b_hi,
+                                                      unsigned long long *__restrict__ gD) {
+  extern __shared__ uint32_t sm[];
+  uint32_t *lut_s = sm;
+  uint32_t *cnt = lut_s + (1 << LUT_BITS) + 1;
+  const int W = b_hi - b_lo;
+  for (int i = threadIdx.x; i <= (1 << LUT_BITS); i += blockDim.x) lut_s[i] = lut[i];
+  for (int i = threadIdx.x; i < W; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  uint64_t j0 = blockIdx.x * per_cta, j1 = j0 + per_cta < N ? j0 + per_cta : N;
+  for (uint64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+    uint32_t d = depth[j];
+    if (d == kNone) continue;
+    uint32_t D = d + ((uint32_t)j - s[req[j]]);
+    int bd = bin_of(D, Bd, nb, lut_s, sh) - b_lo;
+    if (bd < 0 || bd >= W) continue;
+    atomicAdd(&cnt[bd], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < W; i += blockDim.x)
+    if (cnt[i]) atomicAdd(&gD[b_lo + i], (unsigned long long)cnt[i]);
+}
+
+// K4c (TTL mode): C2 histogram [(i12bin)*G + g][t] in global memory (count, sum k) and
+// per-group delta sums SDg[g][t] privatised in smem.
+__global__ void __launch_bounds__(256) k_hist_ttl(uint64_t N, const uint32_t *__restrict__ depth,
+                                                  const uint32_t *__restrict__ req, const uint32_t *__restrict__ s,
+                                                  const uint32_t *__restrict__ delta, const uint16_t *__restrict__ grp,
+                                                  const uint32_t *__restrict__ B12, int nb12,
+                                                  const uint32_t *__restrict__ Tt, int ntt, int G,
+                                                  unsigned long long *__restrict__ C2, unsigned long long *__restrict__ S2,
+                                                  unsigned long long *__restrict__ SDg) {
+  extern __shared__ unsigned long long sd[];  // G * (ntt+1)
+  const int nt1 = ntt + 1;
+  for (int i = threadIdx.x; i < G * nt1; i += blockDim.x) sd[i] = 0;
+  __syncthreads();
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t d = depth[j];
+    if (d == kNone) continue;
+    uint32_t r = req[j];
+    uint32_t k = s[r + 1] - 1 - (uint32_t)j;
+    int g = grp[r];
+    uint32_t dl = delta[j];
+    int t = tbin_of(dl, Tt, ntt);
+    int i = tbin_of(d, B12, nb12);  // first c12 boundary >= d (nb12: none)
+    size_t cell = ((size_t)i * G + g) * nt1 + t;
+    atomicAdd(&C2[cell], 1ull);
+    if (k) atomicAdd(&S2[cell], (unsigned long long)k);
+    atomicAdd(&sd[g * nt1 + t], (unsigned long long)dl);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * nt1; i += blockDim.x)
+    if (sd[i]) atomicAdd(&SDg[i], sd[i]);
+}
+
+// column-wise prefix helpers ---------------------------------------------------
+// C1: flat inclusive sums over [tc][bd] -> per-column prefix, then prefix over tc
+__global__ void k_col_fix(const unsigned long long *__restrict__ flat, int ncol, int nb,
+                          unsigned long long *__restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ncol * nb; i += gridDim.x * blockDim.x) {
+    int tc = i / nb;
+    unsigned long long base = tc > 0 ? flat[(size_t)tc * nb - 1] : 0ull;
+    out[i] = flat[i] - base;
+  }
+}
+__global__ void k_prefix_over_cols(unsigned long long *__restrict__ a, int ncol, int nb) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    unsigned long long acc = 0;
+    for (int tc = 0; tc < ncol; tc++) { acc += a[(size_t)tc * nb + b]; a[(size_t)tc * nb + b] = acc; }
+  }
+}
+// C2 [i][g][t]: prefix over i (per g,t), then over t (per i,g); SDg prefix over t
+__global__ void k_prefix_c2_i(unsigned long long *__restrict__ a, int ni, int G, int nt1) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < G * nt1; x += gridDim.x * blockDim.x) {
+    unsigned long long acc = 0;
+    for (int i = 0; i < ni; i++) { acc += a[(size_t)i * G * nt1 + x]; a[(size_t)i * G * nt1 + x] = acc; }
+  }
+}
+__global__ void k_prefix_t(unsigned long long *__restrict__ a, int rows, int nt1) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < rows; x += gridDim.x * blockDim.x) {
+    unsigned long long acc = 0;
+    for (int t = 0; t < nt1; t++) { acc += a[(size_t)x * nt1 + t]; a[(size_t)x * nt1 + t] = acc; }
+  }
+}
+
+template <typename F>
+static kareto_status cub_tmp(kareto_ctx *ctx, DBuf<uint8_t> &tmp, F &&f) {
+  size_t bytes = 0;
+  KCUDA(ctx, f((void *)nullptr, bytes));
+  if (bytes > tmp.n) KTRY(tmp.alloc(ctx, bytes));
+  size_t b2 = tmp.n;
+  KCUDA(ctx, f((void *)tmp.p, b2));
+  return KARETO_OK;
+}
+
+template <typename T>
+static kareto_status upload(kareto_ctx *ctx, DBuf<T> &b, const std::vector<T> &v) {
+  KTRY(b.alloc(ctx, v.size() ? v.size() : 1));
+  if (!v.empty()) KCUDA(ctx, cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  return KARETO_OK;
+}
+
+static bool model_valid(const kareto_model *m) {
+  if (m->instances < 1 || m->gpus_per_instance < 1 || m->block_bytes < 1 || !(m->bw_dram > 0)) return false;
+  if (m->n_media < 1 || m->n_media > 8 || m->n_phi < 0 || m->n_phi > 8) return false;
+  for (int i = 0; i < m->n_media; i++)
+    if (!(m->media[i].bw_max > 0) || m->media[i].bw_base < 0 || m->media[i].bw_slope < 0 || m->media[i].price < 0)
+      return false;
+  for (int i = 1; i < m->n_phi; i++)
+    if (!(m->phi[i].breakpoint > m->phi[i - 1].breakpoint)) return false;
+  if (m->n_phi > 0 && m->phi[0].breakpoint != 0.0) return false;
+  if (m->c_hw < 0 || m->p_hbm < 0 || m->p_dram < 0 || m->iops_per_block < 0 || m->ttl_prov_gb < 0) return false;
+  return true;
+}
+
+static inline uint64_t sat_add(uint64_t a, uint64_t b) { return a > UINT64_MAX - b ? UINT64_MAX : a + b; }
+
+// deterministic contiguous shard of [0, n) for `rank` of `world`
+static void shard_range(int64_t n, int rank, int world, int64_t &lo, int64_t &hi) {
+  lo = n * rank / world;
+  hi = n * (rank + 1) / world;
+}
+
+static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_config *cfg, int64_t n_cfg,
+                          const uint32_t *ttl_ms, int32_t n_tuner, const kareto_model *model,
+                          kareto_counts *counts_out, double *obj_out, int32_t on_dev) {
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+  if (n_cfg < 0 || (n_cfg > 0 && !cfg) || !model) return fail(ctx, KARETO_E_INVALID, "bad arguments");
+  if (!model_valid(model)) return fail(ctx, KARETO_E_INVALID, "invalid model constants");
+  if (n_tuner < 0 || (n_tuner > 0 && !ttl_ms)) return fail(ctx, KARETO_E_INVALID, "bad TTL table");
+  const int G = tr->K + 1;
+  const uint64_t N = (uint64_t)tr->N, U = (uint64_t)tr->U;
+  // rows (an all-infinite row when no table is given)
+  std::vector<uint32_t> rows;
+  int nrows = n_tuner;
+  if (n_tuner == 0) { rows.assign(G, KARETO_TTL_INF); nrows = 1; }
+  else rows.assign(ttl_ms, ttl_ms + (size_t)n_tuner * G);
+  // ---- validation + classification (every rank validates the full list identically)
+  for (int64_t i = 0; i < n_cfg; i++) {
+    const kareto_config &c = cfg[i];
+    if (c.policy > KARETO_LFU) return fail(ctx, KARETO_E_INVALID, "config %lld: policy %d", (long long)i, c.policy);
+    if (c.medium >= model->n_media) return fail(ctx, KARETO_E_INVALID, "config %lld: medium", (long long)i);
+    if (n_tuner > 0 && c.tuner >= n_tuner) return fail(ctx, KARETO_E_INVALID, "config %lld: tuner", (long long)i);
+    if (c.cap[0] == KARETO_INF || c.cap[1] == KARETO_INF)
+      return fail(ctx, KARETO_E_INVALID, "config %lld: infinite HBM/DRAM", (long long)i);
+    const uint32_t *row = rows.data() + (size_t)(n_tuner > 0 ? c.tuner : 0) * G;
+    bool ttl = c.cap[2] == KARETO_INF;
+    bool uniform = true, all_finite = true;
+    for (int g = 0; g < G; g++) {
+      if (row[g] != row[0]) uniform = false;
+      if (row[g] == KARETO_TTL_INF) all_finite = false;
+    }
+    if (ttl && !all_finite)
+      return fail(ctx, KARETO_E_INVALID, "config %lld: TTL mode needs finite TTLs (R22)", (long long)i);
+    bool stack = c.policy == KARETO_LRU && (ttl || uniform);
+    if (!stack)
+      return fail(ctx, KARETO_E_UNSUPPORTED, "config %lld needs the per-configuration replay (policy %d)", (long long)i,
+                  c.policy);
+    // overflow guards of the integer model terms
+    if (!ttl) {
+      unsigned __int128 cb = (unsigned __int128)sat_add(sat_add(c.cap[0], c.cap[1]), c.cap[2]) * model->block_bytes;
+      if (cb > (unsigned __int128)UINT64_MAX) return fail(ctx, KARETO_E_OVERFLOW, "config %lld: capacity x block bytes", (long long)i);
+    } else {
+      unsigned __int128 cb = (unsigned __int128)sat_add(c.cap[0], c.cap[1]) * model->block_bytes;
+      if (cb > (unsigned __int128)UINT64_MAX) return fail(ctx, KARETO_E_OVERFLOW, "config %lld: capacity x block bytes", (long long)i);
+    }
+  }
+  // trace x model integer constants
+  unsigned __int128 P0 = (unsigned __int128)model->alpha_ps * tr->SL + (unsigned __int128)model->beta_ps * tr->SQ;
+  if (P0 > (unsigned __int128)UINT64_MAX) return fail(ctx, KARETO_E_OVERFLOW, "no-cache prefill cost >= 2^64 ps");
+  if ((unsigned __int128)model->dec_ps * tr->O > (unsigned __int128)UINT64_MAX)
+    return fail(ctx, KARETO_E_OVERFLOW, "decode cost >= 2^64 ps");
+  if ((unsigned __int128)(2 * N + 2 * U) * model->block_bytes > (unsigned __int128)UINT64_MAX)
+    return fail(ctx, KARETO_E_OVERFLOW, "transfer bytes >= 2^64");
+  ModelConsts mc{(uint64_t)P0, (uint64_t)tr->R, N, U, tr->Ltok, tr->O, tr->span_ms};
+
+  // ---- shard
+  int64_t lo = 0, hi = n_cfg;
+  if (ctx->world > 1) shard_range(n_cfg, ctx->rank, ctx->world, lo, hi);
+  const int64_t ns = hi - lo;
+  const kareto_config *sc = cfg + lo;
+
+  // ---- boundary / TTL sets of the shard
+  std::vector<uint32_t> Bd, B12, Tc, Tt;
+  std::vector<char> row_used(nrows, 0);
+  auto clampU = [&](uint64_t v) -> uint32_t { return (uint32_t)(v < U ? v : U); };
+  for (int64_t i = 0; i < ns; i++) {
+    const kareto_config &c = sc[i];
+    uint64_t c12 = sat_add(c.cap[0], c.cap[1]);
+    Bd.push_back(clampU(c.cap[0]));
+    Bd.push_back(clampU(c12));
+    int ri = n_tuner > 0 ? c.tuner : 0;
+    if (c.cap[2] != KARETO_INF) {
+      Bd.push_back(clampU(sat_add(c12, c.cap[2])));
+      uint32_t tau = rows[(size_t)ri * G];
+      if (tau != KARETO_TTL_INF) Tc.push_back(tau);
+    } else {
+      B12.push_back(clampU(c12));
+      row_used[ri] = 1;
+    }
+  }
+  for (int r = 0; r < nrows; r++)
+    if (row_used[r])
+      for (int g = 0; g < G; g++) Tt.push_back(rows[(size_t)r * G + g]);
+  auto uniq = [](std::vector<uint32_t> &v) {
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+  };
+  uniq(Bd); uniq(B12); uniq(Tc); uniq(Tt);
+  const int nb = (int)Bd.size(), nb12 = (int)B12.size(), ntc = (int)Tc.size(), ntt = (int)Tt.size();
+  // per-config lookup indices
+  std::vector<CfgDev> cd(ns > 0 ? ns : 1);
+  auto idx = [](const std::vector<uint32_t> &v, uint32_t x) {
+    return (int32_t)(std::lower_bound(v.begin(), v.end(), x) - v.begin());
+  };
+  std::vector<uint32_t> tix((size_t)nrows * G, 0);
+  for (int r = 0; r < nrows; r++)
+    if (row_used[r])
+      for (int g = 0; g < G; g++) tix[(size_t)r * G + g] = (uint32_t)idx(Tt, rows[(size_t)r * G + g]);
+  for (int64_t i = 0; i < ns; i++) {
+    const kareto_config &c = sc[i];
+    uint64_t c12 = sat_add(c.cap[0], c.cap[1]);
+    int ri = n_tuner > 0 ? c.tuner : 0;
+    CfgDev x{};
+    x.i1 = idx(Bd, clampU(c.cap[0]));
+    x.i12 = idx(Bd, clampU(c12));
+    x.row = ri;
+    if (c.cap[2] != KARETO_INF) {
+      x.iC = idx(Bd, clampU(sat_add(c12, c.cap[2])));
+      uint32_t tau = rows[(size_t)ri * G];
+      x.tc = tau == KARETO_TTL_INF ? ntc : idx(Tc, tau);
+      x.i12t = 0;
+    } else {
+      x.iC = -1;
+      x.tc = ntc;
+      x.i12t = idx(B12, clampU(c12));
+    }
+    cd[i] = x;
+  }
+
+  // ---- K4: histograms over the accesses
+  DBuf<uint8_t> tmp;
+  DBuf<uint32_t> dBd, dB12, dTc, dTt, dlut, dtix, drows;
+  KTRY(upload(ctx, dBd, Bd)); KTRY(upload(ctx, dB12, B12)); KTRY(upload(ctx, dTc, Tc)); KTRY(upload(ctx, dTt, Tt));
+  KTRY(upload(ctx, dtix, tix)); KTRY(upload(ctx, drows, rows));
+  const int ncol = ntc + 1;
+  DBuf<unsigned long long> hC, hS, hD, C1, S1, CD;
+  size_t ncell = (size_t)ncol * (nb > 0 ? nb : 1);
+  KTRY(hC.alloc(ctx, ncell)); KTRY(hS.alloc(ctx, ncell)); KTRY(hD.alloc(ctx, nb > 0 ? nb : 1));
+  KTRY(hC.zero()); KTRY(hS.zero()); KTRY(hD.zero());
+  KTRY(C1.alloc(ctx, ncell)); KTRY(S1.alloc(ctx, ncell)); KTRY(CD.alloc(ctx, nb > 0 ? nb : 1));
+  KTRY(C1.zero()); KTRY(S1.zero()); KTRY(CD.zero());
+  int sh = 0;
+  while (((uint64_t)U >> sh) >= (1ull << LUT_BITS)) sh++;
+  KTRY(dlut.alloc(ctx, (1 << LUT_BITS) + 1));
+  const uint32_t *depth = tr->depth, *req = tr->req, *s = tr->s, *delta = tr->delta;
+  if (ns > 0 && N > 0 && nb > 0) {
+    k_build_lut<<<grid_for((1 << LUT_BITS) + 1, 256), 256, 0, st>>>(dBd.p, nb, sh, dlut.p);
+    ctx->own_launches++;
+    // CTA ranges bounded so that per-CTA u32 sums of k cannot overflow
+    uint64_t maxk = tr->max_blocks > 1 ? (uint64_t)tr->max_blocks - 1 : 1;
+    uint64_t cap_per = 0xFFFFFFFFull / maxk;
+    uint64_t per = (N + 2 * sms - 1) / (2 * sms);
+    if (per > cap_per) per = cap_per;
+    if (per < 1) per = 1;
+    unsigned g = (unsigned)((N + per - 1) / per);
+    const size_t lut_bytes = 4 * ((1 << LUT_BITS) + 1);
+    const int wcell = (int)((SMEM_BUDGET - lut_bytes) / 8);
+    const int wD = (int)((SMEM_BUDGET - lut_bytes) / 4);
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(k_hist_d, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BUDGET);
+      cudaFuncSetAttribute(k_hist_D, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BUDGET);
+      attr_set = true;
+    }
+    for (int c0 = 0; c0 < (int)ncell; c0 += wcell) {
+      int c1 = c0 + wcell < (int)ncell ? c0 + wcell : (int)ncell;
+      size_t smem = lut_bytes + 8 * (size_t)(c1 - c0);
+      Pass ps(ctx, "K4_hist_d", 1, 1);
+      k_hist_d<<<g, H_THREADS, smem, st>>>(N, per, depth, req, s, delta, dBd.p, nb, dlut.p, sh, dTc.p, ntc, c0, c1,
+                                           hC.p, hS.p);
+    }
+    for (int b0 = 0; b0 < nb; b0 += wD) {
+      int b1 = b0 + wD < nb ? b0 + wD : nb;
+      size_t smem = lut_bytes + 4 * (size_t)(b1 - b0);
+      Pass ps(ctx, "K4_hist_D", 1, 1);
+      k_hist_D<<<g, H_THREADS, smem, st>>>(N, per, depth, req, s, dBd.p, nb, dlut.p, sh, b0, b1, hD.p);
+    }
+    {
+      Pass ps(ctx, "K4_cumulate", 0, 3);
+      DBuf<unsigned long long> flat;
+      KTRY(flat.alloc(ctx, ncell));
+      KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+        return cub::DeviceScan::InclusiveSum(t, b, hC.p, flat.p, (int64_t)ncell, st);
+      }));
+      k_col_fix<<<grid_for(ncell, 256, 4 * sms), 256, 0, st>>>(flat.p, ncol, nb, C1.p);
+      KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+        return cub::DeviceScan::InclusiveSum(t, b, hS.p, flat.p, (int64_t)ncell, st);
+      }));
+      k_col_fix<<<grid_for(ncell, 256, 4 * sms), 256, 0, st>>>(flat.p, ncol, nb, S1.p);
+      k_prefix_over_cols<<<grid_for(nb, 256, 4 * sms), 256, 0, st>>>(C1.p, ncol, nb);
+      k_prefix_over_cols<<<grid_for(nb, 256, 4 * sms), 256, 0, st>>>(S1.p, ncol, nb);
+      KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+        return cub::DeviceScan::InclusiveSum(t, b, hD.p, CD.p, nb, st);
+      }));
+      ctx->own_launches += 4;
+    }
+  }
+  // TTL-mode tables
+  const int nt1 = ntt + 1;
+  DBuf<unsigned long long> C2, S2, SDg, dUg, dRg;
+  size_t n2 = (size_t)(nb12 + 1) * G * nt1;
+  KTRY(C2.alloc(ctx, n2)); KTRY(S2.alloc(ctx, n2)); KTRY(SDg.alloc(ctx, (size_t)G * nt1));
+  KTRY(C2.zero()); KTRY(S2.zero()); KTRY(SDg.zero());
+  std::vector<unsigned long long> hUg(G), hRg(G);
+  for (int g = 0; g < G; g++) { hUg[g] = (unsigned long long)tr->U_g[g]; hRg[g] = (unsigned long long)tr->reuse_g[g]; }
+  KTRY(upload(ctx, dUg, hUg)); KTRY(upload(ctx, dRg, hRg));
+  if (ns > 0 && N > 0 && nb12 > 0) {
+    size_t smem = 8 * (size_t)G * nt1;
+    if (smem > 200 * 1024) return fail(ctx, KARETO_E_UNSUPPORTED, "too many groups x TTL values (%d x %d)", G, nt1);
+    cudaFuncSetAttribute(k_hist_ttl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+      Pass ps(ctx, "K4_hist_ttl", 1, 1);
+      k_hist_ttl<<<grid_for(N, 256, 4 * sms), 256, smem, st>>>(N, depth, req, s, delta, tr->grp, dB12.p, nb12, dTt.p,
+                                                               ntt, G, C2.p, S2.p, SDg.p);
+    }
+    Pass ps(ctx, "K4_cumulate_ttl", 1, 5);
+    k_prefix_c2_i<<<grid_for(G * nt1, 256), 256, 0, st>>>(C2.p, nb12 + 1, G, nt1);
+    k_prefix_c2_i<<<grid_for(G * nt1, 256), 256, 0, st>>>(S2.p, nb12 + 1, G, nt1);
+    k_prefix_t<<<grid_for((nb12 + 1) * G, 256), 256, 0, st>>>(C2.p, (nb12 + 1) * G, nt1);
+    k_prefix_t<<<grid_for((nb12 + 1) * G, 256), 256, 0, st>>>(S2.p, (nb12 + 1) * G, nt1);
+    k_prefix_t<<<grid_for(G, 256), 256, 0, st>>>(SDg.p, G, nt1);
+  }
+
+  // ---- K5 + K7 on the shard
+  DBuf<kareto_config> dcfg;
+  DBuf<CfgDev> dcd;
+  DBuf<kareto_counts> dcounts;
+  DBuf<double> dobj;
+  int64_t nsa = ns > 0 ? ns : 1;
+  // gathered outputs are assembled in padded per-rank slots: slot = ceil(n / world)
+  const int64_t slot = ctx->world > 1 ? (n_cfg + ctx->world - 1) / ctx->world : nsa;
+  KTRY(dcfg.alloc(ctx, nsa)); KTRY(dcd.alloc(ctx, nsa));
+  KTRY(dcounts.alloc(ctx, slot > 0 ? slot : 1)); KTRY(dobj.alloc(ctx, 3 * (slot > 0 ? slot : 1)));
+  if (ns > 0) {
+    KCUDA(ctx, cudaMemcpyAsync(dcfg.p, sc, sizeof(kareto_config) * ns, cudaMemcpyHostToDevice, st));
+    KCUDA(ctx, cudaMemcpyAsync(dcd.p, cd.data(), sizeof(CfgDev) * ns, cudaMemcpyHostToDevice, st));
+  }
+  StackTables T{};
+  T.Bd = nullptr; T.nb = nb; T.Tc = dTc.p; T.ntc = ntc;
+  T.C1 = C1.p; T.S1 = S1.p; T.CD = CD.p;
+  T.B12 = nullptr; T.nb12 = nb12; T.Tt = dTt.p; T.ntt = ntt; T.G = G;
+  T.C2 = C2.p; T.S2 = S2.p; T.SDg = SDg.p; T.Ug = dUg.p; T.Rg = dRg.p;
+  launch_objective(ctx, T, dcfg.p, dcd.p, dtix.p, drows.p, ns, model, mc, dcounts.p, dobj.p);
+
+  // ---- gather (row e): one NCCL allgather of counts and objective vectors over NVLink
+  kareto_counts *all_counts = dcounts.p;
+  double *all_obj = dobj.p;
+  DBuf<kareto_counts> gcounts;
+  DBuf<double> gobj;
+  if (ctx->world > 1) {
+    const int W = ctx->world;
+    KTRY(gcounts.alloc(ctx, (size_t)slot * W)); KTRY(gobj.alloc(ctx, (size_t)3 * slot * W));
+    Pass ps(ctx, "K9_allgather", 0, 2);
+    ncclComm_t comm = (ncclComm_t)ctx->nccl_comm;
+    if (ctx->nccl->AllGather(dcounts.p, gcounts.p, sizeof(kareto_counts) * slot, ncclUint8, comm, st) != ncclSuccess ||
+        ctx->nccl->AllGather(dobj.p, gobj.p, (size_t)3 * slot, ncclFloat64, comm, st) != ncclSuccess)
+      return fail(ctx, KARETO_E_NCCL, "ncclAllGather failed");
+    // compact rank slots into [0, n): rank r's shard occupies [lo_r, hi_r)
+    DBuf<kareto_counts> ccounts;
+    DBuf<double> cobj;
+    KTRY(ccounts.alloc(ctx, n_cfg)); KTRY(cobj.alloc(ctx, 3 * n_cfg));
+    for (int r = 0; r < W; r++) {
+      int64_t l, h;
+      shard_range(n_cfg, r, W, l, h);
+      if (h > l) {
+        KCUDA(ctx, cudaMemcpyAsync(ccounts.p + l, gcounts.p + (size_t)r * slot, sizeof(kareto_counts) * (h - l),
+                                   cudaMemcpyDeviceToDevice, st));
+        KCUDA(ctx, cudaMemcpyAsync(cobj.p + 3 * l, gobj.p + (size_t)3 * r * slot, 24 * (h - l),
+                                   cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    gcounts = std::move(ccounts);
+    gobj = std::move(cobj);
+    all_counts = gcounts.p;
+    all_obj = gobj.p;
+  }
+  cudaMemcpyKind kind = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (n_cfg > 0) {
+    if (counts_out) KCUDA(ctx, cudaMemcpyAsync(counts_out, all_counts, sizeof(kareto_counts) * n_cfg, kind, st));
+    if (obj_out) KCUDA(ctx, cudaMemcpyAsync(obj_out, all_obj, 24 * n_cfg, kind, st));
+  }
+  return sync(ctx, "eval_grid");
+}
+
+}  // namespace kareto
+
+extern "C" kareto_status kareto_shard_range(int64_t n, int32_t rank, int32_t world, int64_t *lo, int64_t *hi) {
+  if (n < 0 || world < 1 || rank < 0 || rank >= world || !lo || !hi) return KARETO_E_INVALID;
+  kareto::shard_range(n, rank, world, *lo, *hi);
+  return KARETO_OK;
+}
+
+extern "C" kareto_status kareto_eval_grid(kareto_ctx *ctx, const kareto_trace *tr, const kareto_config *cfg,
+                                          int64_t n_cfg, const uint32_t *ttl_ms, int32_t n_tuner,
+                                          const kareto_model *model, kareto_counts *counts_out, double *obj_out,
+                                          int32_t outputs_on_device) {
+  if (!ctx || !tr) return KARETO_E_INVALID;
+  ctx->err.clear();
+  cudaSetDevice(ctx->device);
+  kareto_status s = kareto::eval(ctx, tr, cfg, n_cfg, ttl_ms, n_tuner, model, counts_out, obj_out, outputs_on_device);
+  if (s != KARETO_OK) {
+    cudaStreamSynchronize(ctx->stream);
+    (void)cudaGetLastError();
+  }
+  return s;
+}

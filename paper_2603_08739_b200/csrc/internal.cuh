@@ -1,0 +1,195 @@
+// internal.cuh -- shared internals of libkareto (context, device arena, errors, pass timing).
+// Not part of the ABI; see include/kareto.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kareto.h"
+
+namespace kareto {
+
+constexpr uint32_t kNone = 0xFFFFFFFFu;  // "no previous access" / "first access" / infinity
+constexpr int kMaxPasses = 64;
+
+struct PassAcc {
+  char name[24];
+  double ms;
+  int launches;
+  int own;
+};
+
+// dlopen'ed NCCL entry points (loaded by ctx.cu)
+struct NcclApi {
+  void *h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+}  // namespace kareto
+
+struct kareto_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int rank = 0, world = 1;
+  void *nccl_comm = nullptr;  // ncclComm_t
+  kareto::NcclApi *nccl = nullptr;
+  cudaMemPool_t pool = nullptr;
+  int num_sms = 148;
+  size_t l2_bytes = 0;
+  std::string err;
+  // profiling
+  bool profiling = false;
+  std::vector<kareto::PassAcc> passes;
+  struct Pending {
+    int idx;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+  int64_t own_launches = 0;
+};
+
+struct kareto_trace {
+  kareto_ctx *ctx = nullptr;
+  int64_t R = 0, N = 0, U = 0, span_ms = 1;
+  int32_t K = 0, max_blocks = 0;
+  uint64_t Ltok = 0, O = 0;
+  // sum_r L_r and sum_r L_r (L_r - 1) / 2 as exact 128-bit values (for P0 = alpha*SL + beta*SQ)
+  unsigned __int128 SL = 0, SQ = 0;
+  // per request (sorted order) [R] / [R+1]
+  int64_t *arr = nullptr;      // arrival ms
+  uint32_t *s = nullptr;       // first touch position [R+1]
+  uint16_t *grp = nullptr;     // group of request
+  // per access (touch order) [N]
+  uint64_t *hash = nullptr;
+  uint32_t *req = nullptr;
+  uint32_t *prev = nullptr;
+  uint32_t *delta = nullptr;
+  uint32_t *depth = nullptr;   // LRU depth d at request start (kNone: first access)
+  // group tables (host) [K+1]
+  std::vector<int64_t> U_g, reuse_g;
+};
+
+namespace kareto {
+
+// ----------------------------------------------------------------- errors ----
+inline kareto_status fail(kareto_ctx *ctx, kareto_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  return st;
+}
+
+#define KCUDA(ctx, call)                                                                              \
+  do {                                                                                                \
+    cudaError_t e_ = (call);                                                                          \
+    if (e_ != cudaSuccess) {                                                                          \
+      kareto_status st_ = (e_ == cudaErrorMemoryAllocation) ? KARETO_E_OOM : KARETO_E_CUDA;           \
+      (void)cudaGetLastError();                                                                       \
+      return ::kareto::fail(ctx, st_, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+    }                                                                                                 \
+  } while (0)
+
+#define KTRY(expr)                      \
+  do {                                  \
+    kareto_status st_ = (expr);         \
+    if (st_ != KARETO_OK) return st_;   \
+  } while (0)
+
+// ----------------------------------------------------- stream-ordered buffers ----
+// Device buffers come from the context's CUDA memory pool (cudaMallocAsync on the context
+// stream, release threshold = unlimited), so repeated loads/evals reuse HBM without
+// cudaMalloc/cudaFree synchronisation.
+template <typename T>
+struct DBuf {
+  kareto_ctx *ctx = nullptr;
+  T *p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf &) = delete;
+  DBuf &operator=(const DBuf &) = delete;
+  DBuf(DBuf &&o) noexcept : ctx(o.ctx), p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf &operator=(DBuf &&o) noexcept {
+    release();
+    ctx = o.ctx; p = o.p; n = o.n; o.p = nullptr; o.n = 0;
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, ctx->stream);
+    p = nullptr;
+    n = 0;
+  }
+  T *detach() { T *q = p; p = nullptr; n = 0; return q; }
+  kareto_status alloc(kareto_ctx *c, size_t count) {
+    release();
+    ctx = c;
+    n = count;
+    size_t bytes = (count ? count : 1) * sizeof(T);
+    cudaError_t e = cudaMallocAsync((void **)&p, bytes, c->stream);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      p = nullptr;
+      return fail(c, KARETO_E_OOM, "device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+    }
+    return KARETO_OK;
+  }
+  kareto_status zero() {
+    cudaError_t e = cudaMemsetAsync(p, 0, (n ? n : 1) * sizeof(T), ctx->stream);
+    if (e != cudaSuccess) return fail(ctx, KARETO_E_CUDA, "memset: %s", cudaGetErrorString(e));
+    return KARETO_OK;
+  }
+};
+
+// -------------------------------------------------------------- pass timing ----
+// Scope object bracketing one pass (one or more launches) with CUDA events on the
+// context stream when profiling is on.  Own-kernel launches are always counted.
+struct Pass {
+  kareto_ctx *ctx;
+  int idx = -1;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Pass(kareto_ctx *c, const char *name, int own, int launches);
+  ~Pass();
+};
+
+// Resolve pending pass events into the accumulators (after the call's final sync).
+void flush_pass_times(kareto_ctx *ctx);
+
+// final synchronisation of a call: stream sync + launch error check
+kareto_status sync(kareto_ctx *ctx, const char *what);
+
+inline unsigned grid_for(int64_t n, int threads, int64_t cap = 1 << 30) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+// ----------------------------------------------------------- device helpers ----
+// splitmix64 finaliser (R2); this library's own copy.
+__host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+constexpr uint64_t kChainR = 0x9E3779B97F4A7C15ULL;
+constexpr uint64_t kSaltC = 0x243F6A8885A308D3ULL;
+
+// trace-load building blocks (trace_load.cu / stack_depth.cu)
+kareto_status stack_depth(kareto_ctx *ctx, kareto_trace *tr);
+
+}  // namespace kareto

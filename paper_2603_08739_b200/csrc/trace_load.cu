@@ -1,0 +1,635 @@
+// trace_load.cu -- kareto_load_trace: rows a1 (ingest), a2 (K1 chained block hash) and
+// a3 (K2 previous access / reuse interval / chain check / prefix-subtree groups) of the
+// hot path; a4 (K3 LRU depth) lives in stack_depth.cu.
+//
+//   a1  requests stable-sorted by (arrival, file index) (R6); blocks are
+//       the full 16-token blocks of each input (R1, R3); touch order: request by
+//       request, blocks leaf -> root (R12), so request r owns positions [s_r, s_r + n_r)
+//       and block k sits at s_r + n_r - 1 - k.
+//   a2  K1 chain hash (R2): c_k = fmix64(NH(t[16k..16k+15])), P_k = R P_{k-1} + c_k,
+//       h_k = fmix64(P_k) -- an affine recurrence, computed as a segmented parallel
+//       scan instead of a serial per-request chain.
+//   a3  K2: radix sort (hash, position) [CUB], link equal neighbours -> prev, then one
+//       coalesced pass for delta (P:748-756 inter-arrival times), the chain check (R7),
+//       and per-request first/reuse counts; groups = top-K prefix subtrees by reuse
+//       (R23).
+#include <cub/cub.cuh>
+
+#include "internal.cuh"
+
+namespace kareto {
+
+enum : uint32_t { F_OFFSETS = 1, F_OUTPUT = 2, F_INPUT_LEN = 4, F_CHAIN = 8, F_DELTA = 16 };
+
+struct LoadStats {  // device-side accumulators, copied back once
+  unsigned long long sl_lo, sl_hi, sq_lo, sq_hi, O;
+  unsigned long long n_total;
+  unsigned int flags, max_blocks;
+  long long arr_first, arr_last;
+};
+
+template <typename F>
+static kareto_status cub_call(kareto_ctx *ctx, DBuf<uint8_t> &tmp, F &&f) {
+  size_t bytes = 0;
+  KCUDA(ctx, f((void *)nullptr, bytes));
+  if (bytes > tmp.n) KTRY(tmp.alloc(ctx, bytes));
+  size_t b2 = tmp.n;
+  KCUDA(ctx, f((void *)tmp.p, b2));
+  return KARETO_OK;
+}
+
+// ------------------------------------------------------------------ a1 ----
+__global__ void k_sort_keys(const int64_t *__restrict__ arrival, int64_t R, uint64_t *__restrict__ key,
+                            uint32_t *__restrict__ idx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R; i += (int64_t)gridDim.x * blockDim.x) {
+    key[i] = (uint64_t)arrival[i] ^ 0x8000000000000000ULL;  // order-preserving signed -> unsigned
+    idx[i] = (uint32_t)i;
+  }
+}
+
+__global__ void k_req_meta(int64_t R, int mode, const uint32_t *__restrict__ order, const int64_t *__restrict__ arrival,
+                           const int32_t *__restrict__ out_tok, const int64_t *__restrict__ offsets,
+                           const int64_t *__restrict__ input_tokens, int64_t *__restrict__ arr_sorted,
+                           int64_t *__restrict__ src_off, uint64_t *__restrict__ nblk, LoadStats *st) {
+  unsigned long long sl_lo = 0, sl_hi = 0, sq_lo = 0, sq_hi = 0, O = 0;
+  unsigned int flags = 0, maxb = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t f = order[r];
+    int64_t a = arrival[f];
+    arr_sorted[r] = a;
+    int64_t o0 = offsets[f], o1 = offsets[f + 1];
+    int64_t cnt = o1 - o0;
+    if (cnt < 0) { flags |= F_OFFSETS; cnt = 0; }
+    int32_t ot = out_tok[f];
+    if (ot < 0) { flags |= F_OUTPUT; ot = 0; }
+    O += (unsigned long long)ot;
+    uint64_t n, L;
+    if (mode == KARETO_TOKENS) {
+      L = (uint64_t)cnt;
+      n = L / 16;
+    } else {
+      n = (uint64_t)cnt;
+      int64_t li = input_tokens ? input_tokens[f] : (int64_t)(16 * n);
+      if (li < (int64_t)(16 * n)) { flags |= F_INPUT_LEN; li = (int64_t)(16 * n); }
+      L = (uint64_t)li;
+    }
+    src_off[r] = o0;
+    nblk[r] = n;
+    if (n > maxb) maxb = n > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)n;
+    // exact 128-bit sums split into 32-bit halves: SL = sum L, SQ = sum L(L-1)/2
+    unsigned __int128 q = L ? ((unsigned __int128)L * (unsigned __int128)(L - 1)) / 2 : 0;
+    sl_lo += L & 0xFFFFFFFFull;
+    sl_hi += L >> 32;
+    uint64_t q64 = (uint64_t)q;  // L < 2^32 in any sane trace; the high part is flagged below
+    if ((q >> 64) != 0) flags |= F_INPUT_LEN;
+    sq_lo += q64 & 0xFFFFFFFFull;
+    sq_hi += q64 >> 32;
+  }
+  atomicAdd(&st->sl_lo, sl_lo);
+  atomicAdd(&st->sl_hi, sl_hi);
+  atomicAdd(&st->sq_lo, sq_lo);
+  atomicAdd(&st->sq_hi, sq_hi);
+  atomicAdd(&st->O, O);
+  if (flags) atomicOr(&st->flags, flags);
+  atomicMax(&st->max_blocks, maxb);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->arr_first = arr_sorted[0];
+  }
+}
+
+__global__ void k_narrow_starts(int64_t R, const uint64_t *__restrict__ s64, uint32_t *__restrict__ s32,
+                                const int64_t *__restrict__ arr_sorted, LoadStats *st) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= R; r += (int64_t)gridDim.x * blockDim.x)
+    s32[r] = (uint32_t)s64[r];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->n_total = s64[R];
+    st->arr_first = arr_sorted[0];
+    st->arr_last = arr_sorted[R - 1];
+  }
+}
+
+// ------------------------------------------------------------------ a2: K1 ----
+// Segmented scan element: x -> a*x + b.  combine(earlier e, later l) = (l.a*e.a, l.a*e.b + l.b)
+struct Aff {
+  uint64_t a, b;
+};
+__device__ __forceinline__ Aff aff_compose(Aff e, Aff l) { return {l.a * e.a, l.a * e.b + l.b}; }
+
+__device__ __forceinline__ uint64_t nh_block(const uint32_t t[16], const uint32_t key[16]) {
+  uint64_t acc = 0;
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    uint32_t a = t[2 * j] + key[2 * j];
+    uint32_t b = t[2 * j + 1] + key[2 * j + 1];
+    acc += (uint64_t)a * (uint64_t)b;
+    acc += ((uint64_t)t[2 * j + 1] << 32) | (uint64_t)t[2 * j];
+  }
+  return fmix64(acc);
+}
+
+// Load the 16 tokens of a block starting at word pointer p (4-byte aligned).  Vector
+// loads of the covering 16-byte chunks + a two-level funnel select; a scalar fallback
+// near the end of the token buffer avoids reading past it.
+__device__ __forceinline__ void load_block_tokens(const uint32_t *p, const uint32_t *end, uint32_t t[16]) {
+  uintptr_t addr = (uintptr_t)p;
+  int mis = (int)((addr >> 2) & 3);
+  const uint4 *q = (const uint4 *)(addr & ~(uintptr_t)15);
+  if (mis != 0 && (const uint32_t *)(q + 5) > end) {
+#pragma unroll
+    for (int i = 0; i < 16; i++) t[i] = __ldg(p + i);
+    return;
+  }
+  uint32_t w[20];
+  uint4 c0 = __ldg(q), c1 = __ldg(q + 1), c2 = __ldg(q + 2), c3 = __ldg(q + 3);
+  uint4 c4 = mis ? __ldg(q + 4) : make_uint4(0, 0, 0, 0);
+  w[0] = c0.x; w[1] = c0.y; w[2] = c0.z; w[3] = c0.w;
+  w[4] = c1.x; w[5] = c1.y; w[6] = c1.z; w[7] = c1.w;
+  w[8] = c2.x; w[9] = c2.y; w[10] = c2.z; w[11] = c2.w;
+  w[12] = c3.x; w[13] = c3.y; w[14] = c3.z; w[15] = c3.w;
+  w[16] = c4.x; w[17] = c4.y; w[18] = c4.z; w[19] = c4.w;
+  uint32_t u[18];
+#pragma unroll
+  for (int i = 0; i < 18; i++) u[i] = (mis & 1) ? w[i + 1] : w[i];
+#pragma unroll
+  for (int i = 0; i < 16; i++) t[i] = (mis & 2) ? u[i + 2] : u[i];
+}
+
+constexpr int K1_THREADS = 256;
+
+// CTA c owns the sorted-block range [s[rb], s[re]) where rb, re are the first requests
+// starting at or after c*N/nCTA and (c+1)*N/nCTA: whole requests per CTA, so the scan
+// carry never crosses CTAs.  Rounds of 256 consecutive blocks; thread = block.
+__global__ void __launch_bounds__(K1_THREADS) k_chain_hash(const uint32_t *__restrict__ tokens, int64_t n_tokens,
+                                                            const int64_t *__restrict__ tok_off,
+                                                            const uint32_t *__restrict__ s, int64_t R, uint64_t N,
+                                                            uint64_t P_init, uint64_t *__restrict__ hash_out,
+                                                            uint32_t *__restrict__ req_out) {
+  __shared__ Aff warp_tot[K1_THREADS / 32];
+  __shared__ uint64_t carry_sh;
+  __shared__ uint32_t range_sh[2];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid < 2) {
+    uint64_t target = ((uint64_t)(blockIdx.x + tid) * N) / gridDim.x;
+    // first request r with s[r] >= target
+    int64_t lo = 0, hi = R;
+    while (lo < hi) {
+      int64_t m = (lo + hi) >> 1;
+      if ((uint64_t)s[m] >= target) hi = m; else lo = m + 1;
+    }
+    range_sh[tid] = (uint32_t)lo;
+  }
+  uint32_t key[16];
+#pragma unroll
+  for (int i = 0; i < 16; i++) key[i] = (uint32_t)fmix64((uint64_t)(i + 1));
+  if (tid == 0) carry_sh = 0;
+  __syncthreads();
+  const uint32_t rb = range_sh[0], re = range_sh[1];
+  const uint64_t B0 = s[rb], B1 = s[re];
+  const uint64_t RP = kChainR * P_init;
+  const uint32_t *tok_end = tokens + n_tokens;
+  uint32_t r = rb;  // per-thread request cursor (monotone across rounds)
+  for (uint64_t base = B0; base < B1; base += K1_THREADS) {
+    uint64_t b = base + tid;
+    bool valid = b < B1;
+    Aff e = {1, 0};
+    uint32_t k = 0, sr = 0, n = 0;
+    if (valid) {
+      while (r + 1 < re && (uint64_t)s[r + 1] <= b) r++;
+      sr = s[r];
+      n = s[r + 1] - sr;
+      k = (uint32_t)(b - sr);
+      uint32_t t[16];
+      load_block_tokens(tokens + tok_off[r] + 16 * (int64_t)k, tok_end, t);
+      uint64_t c = nh_block(t, key);
+      e = (k == 0) ? Aff{0, RP + c} : Aff{kChainR, c};
+    }
+    // warp inclusive scan
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      uint64_t ua = __shfl_up_sync(0xffffffffu, e.a, off);
+      uint64_t ub = __shfl_up_sync(0xffffffffu, e.b, off);
+      if (lane >= off) e = aff_compose(Aff{ua, ub}, e);
+    }
+    if (lane == 31) warp_tot[wid] = e;
+    __syncthreads();
+    if (wid == 0) {
+      Aff w = lane < K1_THREADS / 32 ? warp_tot[lane] : Aff{1, 0};
+#pragma unroll
+      for (int off = 1; off < K1_THREADS / 32; off <<= 1) {
+        uint64_t ua = __shfl_up_sync(0xffffffffu, w.a, off);
+        uint64_t ub = __shfl_up_sync(0xffffffffu, w.b, off);
+        if (lane >= off) w = aff_compose(Aff{ua, ub}, w);
+      }
+      if (lane < K1_THREADS / 32) warp_tot[lane] = w;  // inclusive prefix over warps
+    }
+    __syncthreads();
+    if (wid > 0) e = aff_compose(warp_tot[wid - 1], e);
+    uint64_t P = e.a * carry_sh + e.b;
+    __syncthreads();  // everyone has read carry_sh / warp_tot
+    if (valid) {
+      uint64_t j = (uint64_t)sr + n - 1 - k;
+      hash_out[j] = fmix64(P);
+      req_out[j] = r;
+    }
+    if (tid == K1_THREADS - 1) carry_sh = P;  // last block of the round (if beyond B1 its value is unused)
+    __syncthreads();
+  }
+}
+
+// HASHES mode: copy caller hashes into touch order (warp per request)
+__global__ void k_copy_hashes(const uint64_t *__restrict__ bh, const int64_t *__restrict__ src_off,
+                              const uint32_t *__restrict__ s, int64_t R, uint64_t *__restrict__ hash_out,
+                              uint32_t *__restrict__ req_out) {
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < R; r += nw) {
+    uint32_t sr = s[r], n = s[r + 1] - sr;
+    const uint64_t *src = bh + src_off[r];
+    for (uint32_t k = lane; k < n; k += 32) {
+      uint32_t j = sr + n - 1 - k;
+      hash_out[j] = src[k];
+      req_out[j] = (uint32_t)r;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ a3: K2 ----
+__global__ void k_iota(uint32_t *v, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    v[i] = (uint32_t)i;
+}
+
+__global__ void k_link_prev(const uint64_t *__restrict__ hs, const uint32_t *__restrict__ js, uint64_t N,
+                            uint32_t *__restrict__ prev) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t p = (i > 0 && hs[i] == hs[i - 1]) ? js[i - 1] : kNone;
+    prev[js[i]] = p;
+  }
+}
+
+__device__ __forceinline__ void warp_count_add(uint32_t *arr, uint32_t key, bool pred) {
+  unsigned active = __activemask();
+  unsigned pm = __ballot_sync(active, pred);
+  if (!pred) return;
+  unsigned same = __match_any_sync(pm, key);
+  if ((__ffs(same) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&arr[key], (uint32_t)__popc(same));
+}
+
+__global__ void k_access_info(uint64_t N, const uint32_t *__restrict__ prev, const uint32_t *__restrict__ req,
+                              const uint32_t *__restrict__ s, const int64_t *__restrict__ arr,
+                              const uint64_t *__restrict__ hash, uint32_t *__restrict__ delta,
+                              uint32_t *__restrict__ first_cnt, uint32_t *__restrict__ reuse_cnt, LoadStats *st) {
+  unsigned flags = 0;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t p = prev[j], r = req[j];
+    uint32_t dl = kNone;
+    if (p != kNone) {
+      uint32_t rp = req[p];
+      int64_t d = arr[r] - arr[rp];
+      if (d < 0 || d >= (int64_t)kNone) flags |= F_DELTA; else dl = (uint32_t)d;
+      uint32_t kj = s[r + 1] - 1 - (uint32_t)j;
+      uint32_t kp = s[rp + 1] - 1 - p;
+      if (kj != kp) flags |= F_CHAIN;
+      else if (kj > 0 && hash[j + 1] != hash[p + 1]) flags |= F_CHAIN;
+    }
+    delta[j] = dl;
+    warp_count_add(first_cnt, r, p == kNone);
+    warp_count_add(reuse_cnt, r, p != kNone);
+  }
+  if (flags) atomicOr(&st->flags, flags);
+}
+
+// groups: requests with at least one block, keyed by their root hash (block k = 0, the
+// last touch of the request)
+__global__ void k_root_keys(int64_t R, const uint32_t *__restrict__ s, const uint64_t *__restrict__ hash,
+                            uint64_t *__restrict__ key, uint32_t *__restrict__ val, uint8_t *__restrict__ flag) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
+    bool has = s[r + 1] > s[r];
+    flag[r] = has;
+    key[r] = has ? hash[s[r + 1] - 1] : 0;
+    val[r] = (uint32_t)r;
+  }
+}
+
+__global__ void k_run_heads(const uint64_t *__restrict__ key, const int *__restrict__ m_ptr, uint32_t *__restrict__ head) {
+  int m = *m_ptr;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    head[i] = (i == 0 || key[i] != key[i - 1]) ? 1u : 0u;
+}
+
+__global__ void k_run_reuse(const uint32_t *__restrict__ val, const uint32_t *__restrict__ run_incl,
+                            const int *__restrict__ m_ptr, const uint32_t *__restrict__ reuse_cnt,
+                            unsigned long long *__restrict__ run_reuse, uint32_t *__restrict__ n_runs) {
+  int m = *m_ptr;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    uint32_t rid = run_incl[i] - 1;
+    atomicAdd(&run_reuse[rid], (unsigned long long)reuse_cnt[val[i]]);
+    if (i == m - 1) *n_runs = run_incl[i];
+  }
+}
+
+__global__ void k_rank_keys(const unsigned long long *__restrict__ run_reuse, const uint32_t *__restrict__ n_runs,
+                            uint64_t *__restrict__ key, uint32_t *__restrict__ idx, uint32_t cap) {
+  uint32_t n = *n_runs;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
+    // runs are in ascending root-hash order; a stable sort by ~reuse gives (reuse desc, hash asc)
+    key[i] = i < n ? ~(uint64_t)run_reuse[i] : ~0ull;
+    idx[i] = i;
+  }
+}
+
+__global__ void k_rank_of_run(const uint32_t *__restrict__ ranked, const uint32_t *__restrict__ n_runs,
+                              uint32_t *__restrict__ rank) {
+  uint32_t n = *n_runs;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) rank[ranked[i]] = i;
+}
+
+__global__ void k_assign_groups(const uint32_t *__restrict__ val, const uint32_t *__restrict__ run_incl,
+                                const int *__restrict__ m_ptr, const uint32_t *__restrict__ rank, int K,
+                                uint16_t *__restrict__ grp) {
+  int m = *m_ptr;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    uint32_t rk = rank[run_incl[i] - 1];
+    grp[val[i]] = (uint16_t)(rk < (uint32_t)K ? rk : (uint32_t)K);
+  }
+}
+
+__global__ void k_fill_u16(uint16_t *p, int64_t n, uint16_t v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+__global__ void k_group_tables(int64_t R, const uint16_t *__restrict__ grp, const uint32_t *__restrict__ first_cnt,
+                               const uint32_t *__restrict__ reuse_cnt, unsigned long long *__restrict__ tab) {
+  // tab[2g] = U_g, tab[2g+1] = reuse_g
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
+    int g = grp[r];
+    if (first_cnt[r]) atomicAdd(&tab[2 * g], (unsigned long long)first_cnt[r]);
+    if (reuse_cnt[r]) atomicAdd(&tab[2 * g + 1], (unsigned long long)reuse_cnt[r]);
+  }
+}
+
+// ------------------------------------------------------------------ driver ----
+template <typename T>
+static kareto_status to_device(kareto_ctx *ctx, const T *src, size_t n, bool on_device, DBuf<T> &own,
+                               const T **out) {
+  if (on_device || n == 0) {
+    *out = src;
+    return KARETO_OK;
+  }
+  KTRY(own.alloc(ctx, n));
+  KCUDA(ctx, cudaMemcpyAsync(own.p, src, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  *out = own.p;
+  return KARETO_OK;
+}
+
+static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_trace **out) {
+  const int64_t R = d->n_requests;
+  if (R < 1) return fail(ctx, KARETO_E_INVALID, "n_requests must be >= 1");
+  if (R >= (int64_t)kNone) return fail(ctx, KARETO_E_OVERFLOW, "too many requests");
+  if (d->top_k < 0 || d->top_k > 1023) return fail(ctx, KARETO_E_INVALID, "top_k must be in [0, 1023]");
+  if (d->mode != KARETO_TOKENS && d->mode != KARETO_HASHES) return fail(ctx, KARETO_E_INVALID, "bad mode");
+  if (!d->arrival_ms || !d->output_tokens || !d->offsets) return fail(ctx, KARETO_E_INVALID, "null trace array");
+  const bool dev = d->inputs_on_device != 0;
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+
+  // total elements of the token / hash array (offsets[R])
+  int64_t total = 0;
+  if (dev) KCUDA(ctx, cudaMemcpyAsync(&total, d->offsets + R, 8, cudaMemcpyDeviceToHost, st));
+  else total = d->offsets[R];
+  KCUDA(ctx, cudaStreamSynchronize(st));
+  if (total < 0) return fail(ctx, KARETO_E_PARSE, "offsets[R] < 0");
+  if (d->mode == KARETO_TOKENS && total > 0 && !d->tokens) return fail(ctx, KARETO_E_INVALID, "tokens is null");
+  if (d->mode == KARETO_HASHES && total > 0 && !d->block_hash) return fail(ctx, KARETO_E_INVALID, "block_hash null");
+
+  DBuf<int64_t> h_arr, h_off, h_in;
+  DBuf<int32_t> h_out;
+  DBuf<uint32_t> h_tok;
+  DBuf<uint64_t> h_bh;
+  const int64_t *arrival, *offsets, *input_tokens = nullptr;
+  const int32_t *out_tok;
+  const uint32_t *tokens = nullptr;
+  const uint64_t *bhash = nullptr;
+  {
+    Pass ps(ctx, "h2d", 0, 0);
+    KTRY(to_device(ctx, d->arrival_ms, R, dev, h_arr, &arrival));
+    KTRY(to_device(ctx, d->output_tokens, R, dev, h_out, &out_tok));
+    KTRY(to_device(ctx, d->offsets, R + 1, dev, h_off, &offsets));
+    if (d->mode == KARETO_TOKENS) KTRY(to_device(ctx, d->tokens, (size_t)total, dev, h_tok, &tokens));
+    else {
+      KTRY(to_device(ctx, d->block_hash, (size_t)total, dev, h_bh, &bhash));
+      if (d->input_tokens) KTRY(to_device(ctx, d->input_tokens, R, dev, h_in, &input_tokens));
+    }
+  }
+
+  kareto_trace *tr = new kareto_trace();
+  tr->ctx = ctx;
+  tr->R = R;
+  tr->K = d->top_k;
+  struct Guard {
+    kareto_trace *&t;
+    bool keep = false;
+    ~Guard() { if (!keep) kareto_trace_free(t); }
+  } guard{tr};
+
+  DBuf<uint8_t> tmp;
+  DBuf<LoadStats> stats;
+  KTRY(stats.alloc(ctx, 1));
+  KTRY(stats.zero());
+
+  // ---- a1: sort requests, per-request metadata, block offsets
+  DBuf<uint64_t> skey, skey2, nblk, s64;
+  DBuf<uint32_t> sidx, order;
+  DBuf<int64_t> arr_sorted, src_off;
+  KTRY(skey.alloc(ctx, R)); KTRY(skey2.alloc(ctx, R)); KTRY(sidx.alloc(ctx, R)); KTRY(order.alloc(ctx, R));
+  KTRY(arr_sorted.alloc(ctx, R)); KTRY(src_off.alloc(ctx, R)); KTRY(nblk.alloc(ctx, R + 1)); KTRY(s64.alloc(ctx, R + 1));
+  {
+    Pass ps(ctx, "a1_sort_keys", 1, 1);
+    k_sort_keys<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(arrival, R, skey.p, sidx.p);
+  }
+  {
+    Pass ps(ctx, "a1_sort_requests", 0, 1);
+    KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, skey.p, skey2.p, sidx.p, order.p, (int)R, 0, 64, st);
+    }));
+  }
+  KCUDA(ctx, cudaMemsetAsync(nblk.p + R, 0, 8, st));
+  {
+    Pass ps(ctx, "a1_req_meta", 1, 1);
+    k_req_meta<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(R, d->mode, order.p, arrival, out_tok, offsets, input_tokens,
+                                                          arr_sorted.p, src_off.p, nblk.p, stats.p);
+  }
+  {
+    Pass ps(ctx, "a1_scan_starts", 0, 1);
+    KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, nblk.p, s64.p, (int)(R + 1), st);
+    }));
+  }
+  uint32_t *s_dev;
+  KCUDA(ctx, cudaMallocAsync((void **)&s_dev, 4 * (size_t)(R + 1), st));
+  tr->s = s_dev;
+  {
+    Pass ps(ctx, "a1_narrow", 1, 1);
+    k_narrow_starts<<<grid_for(R + 1, 256, 4 * sms), 256, 0, st>>>(R, s64.p, tr->s, arr_sorted.p, stats.p);
+  }
+  LoadStats hs;
+  KCUDA(ctx, cudaMemcpyAsync(&hs, stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  KCUDA(ctx, cudaStreamSynchronize(st));
+  if (hs.flags & F_OFFSETS) return fail(ctx, KARETO_E_PARSE, "offsets are not nondecreasing");
+  if (hs.flags & F_OUTPUT) return fail(ctx, KARETO_E_PARSE, "output_tokens < 0");
+  if (hs.flags & F_INPUT_LEN) return fail(ctx, KARETO_E_PARSE, "input_tokens < 16 * blocks (or absurd length)");
+  const uint64_t N = hs.n_total;
+  if (N >= (uint64_t)kNone - 1) return fail(ctx, KARETO_E_OVERFLOW, "%llu block accesses >= 2^32-2", (unsigned long long)N);
+  tr->N = (int64_t)N;
+  tr->max_blocks = (int32_t)hs.max_blocks;
+  tr->span_ms = hs.arr_last - hs.arr_first;
+  if (tr->span_ms < 1) tr->span_ms = 1;
+  tr->O = hs.O;
+  tr->SL = ((unsigned __int128)hs.sl_hi << 32) + hs.sl_lo;
+  tr->SQ = ((unsigned __int128)hs.sq_hi << 32) + hs.sq_lo;
+  if (tr->SL > (unsigned __int128)UINT64_MAX) return fail(ctx, KARETO_E_OVERFLOW, "sum of input tokens >= 2^64");
+  tr->Ltok = (uint64_t)tr->SL;
+  tr->arr = arr_sorted.detach();
+
+  const uint64_t Na = N > 0 ? N : 1;
+  KCUDA(ctx, cudaMallocAsync((void **)&tr->hash, 8 * Na, st));
+  KCUDA(ctx, cudaMallocAsync((void **)&tr->req, 4 * Na, st));
+  KCUDA(ctx, cudaMallocAsync((void **)&tr->prev, 4 * Na, st));
+  KCUDA(ctx, cudaMallocAsync((void **)&tr->delta, 4 * Na, st));
+  KCUDA(ctx, cudaMallocAsync((void **)&tr->depth, 4 * Na, st));
+  KCUDA(ctx, cudaMallocAsync((void **)&tr->grp, 2 * (size_t)R, st));
+
+  // ---- a2: K1 chained hashes (TOKENS) / copy (HASHES) into touch order
+  if (N > 0) {
+    if (d->mode == KARETO_TOKENS) {
+      uint64_t P_init = fmix64(d->salt ^ kSaltC);
+      int64_t per_cta = 16384;
+      unsigned g = (unsigned)((N + per_cta - 1) / per_cta);
+      if (g < (unsigned)(4 * sms)) g = (unsigned)(4 * sms);
+      if ((uint64_t)g > N) g = (unsigned)N;
+      Pass ps(ctx, "K1_chain_hash", 1, 1);
+      k_chain_hash<<<g, K1_THREADS, 0, st>>>(tokens, total, src_off.p, tr->s, R, N, P_init, tr->hash, tr->req);
+    } else {
+      Pass ps(ctx, "K1_copy_hashes", 1, 1);
+      k_copy_hashes<<<grid_for(32 * R, 256, 8 * sms), 256, 0, st>>>(bhash, src_off.p, tr->s, R, tr->hash, tr->req);
+    }
+  }
+  h_tok.release();
+  h_bh.release();
+
+  // ---- a3: K2 prev / delta / chain check
+  DBuf<uint32_t> first_cnt, reuse_cnt;
+  KTRY(first_cnt.alloc(ctx, R)); KTRY(reuse_cnt.alloc(ctx, R));
+  KTRY(first_cnt.zero()); KTRY(reuse_cnt.zero());
+  if (N > 0) {
+    DBuf<uint64_t> hsort;
+    DBuf<uint32_t> iota, jsort;
+    KTRY(hsort.alloc(ctx, N)); KTRY(iota.alloc(ctx, N)); KTRY(jsort.alloc(ctx, N));
+    {
+      Pass ps(ctx, "K2_iota", 1, 1);
+      k_iota<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(iota.p, N);
+    }
+    {
+      Pass ps(ctx, "K2_sort_hashes", 0, 1);
+      KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, tr->hash, hsort.p, iota.p, jsort.p, (int64_t)N, 0, 64, st);
+      }));
+    }
+    {
+      Pass ps(ctx, "K2_link_prev", 1, 1);
+      k_link_prev<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(hsort.p, jsort.p, N, tr->prev);
+    }
+    hsort.release(); iota.release(); jsort.release();
+    {
+      Pass ps(ctx, "K2_access_info", 1, 1);
+      k_access_info<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(N, tr->prev, tr->req, tr->s, tr->arr, tr->hash,
+                                                               tr->delta, first_cnt.p, reuse_cnt.p, stats.p);
+    }
+  }
+
+  // ---- a3: groups (top-K prefix subtrees by reuse, residual K)
+  {
+    const int K = tr->K;
+    DBuf<uint64_t> rkey, rkey_s, rankkey, rankkey_s;
+    DBuf<uint32_t> rval, rval_c, rval_s, head, run_incl, rankidx, ranked, rank, nruns;
+    DBuf<uint8_t> rflag;
+    DBuf<int> m_dev;
+    DBuf<unsigned long long> run_reuse, gtab;
+    KTRY(rkey.alloc(ctx, R)); KTRY(rkey_s.alloc(ctx, R)); KTRY(rval.alloc(ctx, R)); KTRY(rval_c.alloc(ctx, R));
+    KTRY(rval_s.alloc(ctx, R)); KTRY(head.alloc(ctx, R)); KTRY(run_incl.alloc(ctx, R)); KTRY(rflag.alloc(ctx, R));
+    KTRY(m_dev.alloc(ctx, 1)); KTRY(run_reuse.alloc(ctx, R)); KTRY(run_reuse.zero()); KTRY(nruns.alloc(ctx, 1));
+    KTRY(nruns.zero());
+    KTRY(rankkey.alloc(ctx, R)); KTRY(rankkey_s.alloc(ctx, R)); KTRY(rankidx.alloc(ctx, R)); KTRY(ranked.alloc(ctx, R));
+    KTRY(rank.alloc(ctx, R)); KTRY(gtab.alloc(ctx, 2 * (K + 1))); KTRY(gtab.zero());
+    DBuf<uint64_t> rkey_c;
+    KTRY(rkey_c.alloc(ctx, R));
+    Pass ps(ctx, "K2_groups", 1, 8);
+    k_root_keys<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(R, tr->s, tr->hash, rkey.p, rval.p, rflag.p);
+    KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceSelect::Flagged(t, b, rkey.p, rflag.p, rkey_c.p, m_dev.p, (int)R, st);
+    }));
+    KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceSelect::Flagged(t, b, rval.p, rflag.p, rval_c.p, m_dev.p, (int)R, st);
+    }));
+    int m = 0;
+    KCUDA(ctx, cudaMemcpyAsync(&m, m_dev.p, 4, cudaMemcpyDeviceToHost, st));
+    KCUDA(ctx, cudaStreamSynchronize(st));
+    k_fill_u16<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(tr->grp, R, (uint16_t)K);
+    if (m > 0) {
+      KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, rkey_c.p, rkey_s.p, rval_c.p, rval_s.p, m, 0, 64, st);
+      }));
+      k_run_heads<<<grid_for(m, 256, 4 * sms), 256, 0, st>>>(rkey_s.p, m_dev.p, head.p);
+      KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
+        return cub::DeviceScan::InclusiveSum(t, b, head.p, run_incl.p, m, st);
+      }));
+      k_run_reuse<<<grid_for(m, 256, 4 * sms), 256, 0, st>>>(rval_s.p, run_incl.p, m_dev.p, reuse_cnt.p, run_reuse.p,
+                                                             nruns.p);
+      k_rank_keys<<<grid_for(m, 256, 4 * sms), 256, 0, st>>>(run_reuse.p, nruns.p, rankkey.p, rankidx.p, (uint32_t)m);
+      KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, rankkey.p, rankkey_s.p, rankidx.p, ranked.p, m, 0, 64, st);
+      }));
+      k_rank_of_run<<<grid_for(m, 256, 4 * sms), 256, 0, st>>>(ranked.p, nruns.p, rank.p);
+      k_assign_groups<<<grid_for(m, 256, 4 * sms), 256, 0, st>>>(rval_s.p, run_incl.p, m_dev.p, rank.p, K, tr->grp);
+    }
+    k_group_tables<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(R, tr->grp, first_cnt.p, reuse_cnt.p, gtab.p);
+    std::vector<unsigned long long> h(2 * (K + 1));
+    KCUDA(ctx, cudaMemcpyAsync(h.data(), gtab.p, 16 * (K + 1), cudaMemcpyDeviceToHost, st));
+    KCUDA(ctx, cudaMemcpyAsync(&hs, stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    KCUDA(ctx, cudaStreamSynchronize(st));
+    tr->U_g.resize(K + 1);
+    tr->reuse_g.resize(K + 1);
+    int64_t U = 0;
+    for (int g = 0; g <= K; g++) {
+      tr->U_g[g] = (int64_t)h[2 * g];
+      tr->reuse_g[g] = (int64_t)h[2 * g + 1];
+      U += tr->U_g[g];
+    }
+    tr->U = U;
+  }
+  if (hs.flags & F_CHAIN) return fail(ctx, KARETO_E_CHAIN, "block hashes are not chain-consistent (R7)");
+  if (hs.flags & F_DELTA) return fail(ctx, KARETO_E_OVERFLOW, "a reuse interval >= 2^32-1 ms");
+
+  // ---- a4: K3 LRU stack depths
+  KTRY(stack_depth(ctx, tr));
+  KTRY(sync(ctx, "load_trace"));
+  guard.keep = true;
+  *out = tr;
+  return KARETO_OK;
+}
+
+}  // namespace kareto
+
+extern "C" kareto_status kareto_load_trace(kareto_ctx *ctx, const kareto_trace_desc *desc, kareto_trace **out) {
+  if (!ctx || !desc || !out) return KARETO_E_INVALID;
+  *out = nullptr;
+  ctx->err.clear();
+  cudaSetDevice(ctx->device);
+  kareto_status s = kareto::load(ctx, desc, out);
+  if (s != KARETO_OK) {
+    cudaStreamSynchronize(ctx->stream);
+    (void)cudaGetLastError();
+  }
+  return s;
+}

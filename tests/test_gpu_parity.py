@@ -1,0 +1,289 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Bar (BASELINE.json north_star): tier counts and Pareto membership bit-exact; fp64
+objectives within 1e-9 relative (expected bit-identical: both sides evaluate the same
+operation sequence without FMA contraction, R33)."""
+import numpy as np
+import pytest
+
+import kareto_inputs as ki
+import paper_2603_08739_b200 as K
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+U32 = 0xFFFFFFFF
+MODEL_KW = dict(instances=2, gpus_per_instance=8, alpha_ps=50_000_000, beta_ps=1, dec_ps=150_000_000,
+                block_bytes=5_242_880, bw_dram=25e9, c_hw=2.5, p_hbm=0.001, p_dram=0.004, iops_per_block=1.0,
+                ttl_prov_gb=1024.0, media=((120e6, 0.5e6, 350e6, 0.0001), (300e6, 1e6, 1e9, 0.0003)),
+                phi=((0.0, 0.0, 0.0), (3000.0, 0.005, 0.0), (32000.0, 0.065, 0.0)))
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    assert torch.cuda.is_available()
+    return K.Context(0)
+
+
+def kcfg(ocfg):
+    c = np.zeros(len(ocfg), K.CONFIG_DTYPE)
+    for f in ("cap", "policy", "medium", "tuner", "axis"):
+        c[f] = ocfg[f]
+    return c
+
+
+def as_u64(counts):
+    return np.ascontiguousarray(counts).view(np.uint64).reshape(len(counts), 11)
+
+
+def assert_counts_equal(got, want, cfgs=None):
+    g, w = as_u64(got), as_u64(want)
+    bad = np.nonzero((g != w).any(1))[0]
+    if len(bad):
+        i = bad[0]
+        raise AssertionError(f"{len(bad)} configs differ; first {i} cfg={None if cfgs is None else cfgs[i]}\n"
+                             f"gpu   ={got[i]}\noracle={want[i]}")
+
+
+def assert_obj_equal(got, want):
+    rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-300)
+    assert np.all(rel <= 1e-9), f"max rel {rel.max()}"
+    # expected bit-identical
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), "objectives not bit-identical"
+
+
+def run_both(ctx, tr, ocfg, ttl=None, top_k=2, salt=0, tau_e=0.05):
+    ot = O.OracleTrace(tr, top_k=top_k, salt=salt)
+    gt = ctx.load(tr, top_k=top_k, salt=salt)
+    want = ot.replay(ocfg, ttl)
+    got, obj = ctx.eval_grid(gt, kcfg(ocfg), K.Model(**MODEL_KW), ttl)
+    assert_counts_equal(got, want, ocfg)
+    fo = ot.objective(O.Model(**MODEL_KW), ocfg, want)
+    assert_obj_equal(obj, fo)
+    st, nf = ctx.pareto(obj, kcfg(ocfg), tau_e)
+    ost = O.select(fo, ocfg, tau_e)
+    assert np.array_equal(st, ost)
+    assert nf == int((ost == 1).sum())
+    return ot, gt
+
+
+def check_trace_exports(ot, gt):
+    e = ot.export()
+    assert gt.N == ot.N and gt.U == ot.U and gt.R == ot.R and gt.span_ms == ot.span_ms
+    assert gt.Ltok == ot.Ltok and gt.O == ot.O
+    assert np.array_equal(gt.export(K.X_HASH), e["hash"])
+    assert np.array_equal(gt.export(K.X_PREV).astype(np.int64), np.where(e["prev"] < 0, U32, e["prev"]))
+    assert np.array_equal(gt.export(K.X_DELTA).astype(np.int64), np.where(e["delta"] < 0, U32, e["delta"]))
+    assert np.array_equal(gt.export(K.X_REQ), e["req"].astype(np.uint32))
+    assert np.array_equal(gt.export(K.X_START).astype(np.int64), e["s"])
+    assert np.array_equal(gt.export(K.X_GROUP), e["group"].astype(np.uint16))
+    d, _ = ot.depth()
+    assert np.array_equal(gt.export(K.X_DEPTH).astype(np.int64), np.where(d < 0, U32, d))
+    assert np.array_equal(gt.U_g, ot.U_g) and np.array_equal(gt.reuse_g, ot.reuse_g)
+
+
+def tiny_configs(K_):
+    rows = [[U32] * (K_ + 1)]
+    for t in (0, 1, 3, 50):
+        rows.append([t] * (K_ + 1))
+    rng = np.random.default_rng(7)
+    for _ in range(3):
+        rows.append(list(rng.choice([0, 1, 3, 6, 50], K_ + 1)))
+    ttl = np.array(rows, np.uint32)
+    caps, tun, axis = [], [], []
+    for a in range(4):
+        for b in range(3):
+            for c in range(4):
+                for ti in range(5):
+                    caps.append([a, b, c]); tun.append(ti); axis.append([a, b, c])
+            for ti in range(5, 8):
+                caps.append([a, b, O.INF_CAP]); tun.append(ti); axis.append([a, b, 0])
+    cf = O.configs(caps, tuner=np.array(tun), axis=axis)
+    cf["medium"] = np.arange(len(cf)) % 2
+    return cf, ttl
+
+
+def test_w1_worked_example(ctx):
+    tr = ki.from_chains([[1, 2, 3], [1, 2, 4], [1, 2, 3]], [0, 10, 20])
+    gt = ctx.load(tr, top_k=0)
+    assert list(gt.export(K.X_DEPTH)) == [U32] * 4 + [2, 1, 4, 2, 1]
+    cnt, _ = ctx.eval_grid(gt, K.configs([[1, 1, 1], [1, 1, 2]]), K.Model())
+    assert list(cnt[0]["hit"]) == [2, 2, 0] and cnt[0]["miss"] == 5 and list(cnt[0]["evict"]) == [8, 7, 2]
+    assert list(cnt[1]["hit"]) == [2, 2, 1] and cnt[1]["miss"] == 4 and list(cnt[1]["evict"]) == [8, 7, 0]
+    cnt, _ = ctx.eval_grid(gt, K.configs([[0, 0, K.INF]]), K.Model(), ttl=np.array([[15]], np.uint32))
+    assert cnt[0]["hit"][2] == 4 and cnt[0]["bytetime_block_ms"] == 115
+
+
+def test_tiny_random_traces_all_stages(ctx):
+    rng = np.random.default_rng(2024)
+    for trial in range(25):
+        tr = ki.random_prefix_tree(rng)
+        K_ = int(rng.integers(0, 3))
+        cf, ttl = tiny_configs(K_)
+        ot, gt = run_both(ctx, tr, cf, ttl, top_k=K_, salt=trial)
+        check_trace_exports(ot, gt)
+
+
+def baseline_grid(U, m1=4, m2=4, m3=4, d1=16, d2=4, d3=1):
+    """BASELINE config-1 style grid: c1 in A(m1, U/d1), c2 in A(m2, U/d2), c3 in A(m3, U/d3)."""
+    A = lambda m, top: [top * i // (m - 1) for i in range(m)]
+    caps, axis = [], []
+    for i, a in enumerate(A(m1, U // d1)):
+        for j, b in enumerate(A(m2, U // d2)):
+            for k, c in enumerate(A(m3, U // d3)):
+                caps.append([a, b, c]); axis.append([i, j, k])
+    return caps, axis
+
+
+def test_config1_full_parity(ctx):
+    # BASELINE config 1: 10k requests / ~1M block accesses, 3-tier LRU, 4x4x4, fp64 model
+    tr = ki.synthetic("chat", R=10_000, seed=0)
+    ot = O.OracleTrace(tr, top_k=16)
+    gt = ctx.load(tr, top_k=16)
+    check_trace_exports(ot, gt)
+    caps, axis = baseline_grid(ot.U)
+    cf = O.configs(caps, axis=axis)
+    want = ot.replay(cf)
+    got, obj = ctx.eval_grid(gt, kcfg(cf), K.Model(**MODEL_KW))
+    assert_counts_equal(got, want, cf)
+    fo = ot.objective(O.Model(**MODEL_KW), cf, want)
+    assert_obj_equal(obj, fo)
+    for tau in (0.05, None):
+        st, _ = ctx.pareto(obj, kcfg(cf), tau)
+        assert np.array_equal(st, O.select(fo, cf, tau))
+
+
+def test_config1_ttl_and_uniform_tau(ctx):
+    tr = ki.synthetic("chat", R=3000, seed=5)
+    ot = O.OracleTrace(tr, top_k=4)
+    gt = ctx.load(tr, top_k=4)
+    caps, axis = baseline_grid(ot.U, 3, 3, 3)
+    rows = [[U32] * 5, [60_000] * 5, [600_000] * 5, [5_000, 60_000, 600_000, 30_000, 1_000]]
+    ttl = np.array(rows, np.uint32)
+    allcaps, tun, ax = [], [], []
+    for (c, a) in zip(caps, axis):
+        for ti in range(3):
+            allcaps.append(c); tun.append(ti); ax.append(a)
+        allcaps.append([c[0], c[1], O.INF_CAP]); tun.append(3); ax.append(a)
+    cf = O.configs(allcaps, tuner=np.array(tun), axis=ax)
+    want = ot.replay(cf, ttl)
+    got, obj = ctx.eval_grid(gt, kcfg(cf), K.Model(**MODEL_KW), ttl)
+    assert_counts_equal(got, want, cf)
+    assert_obj_equal(obj, ot.objective(O.Model(**MODEL_KW), cf, want))
+
+
+def test_edge_cases(ctx):
+    M = K.Model()
+    # requests with fewer than 16 tokens have no blocks (R3); a single block request
+    tr = ki.from_chains([[], [1], [], [1, 2]], [0, 1, 1, 2], tails=[5, 15, 0, 3])
+    ot, gt = run_both(ctx, tr, O.configs([[0, 0, 0], [1, 0, 0], [5, 5, 5]], axis=[[0, 0, 0], [1, 0, 0], [2, 1, 1]]),
+                      top_k=1)
+    check_trace_exports(ot, gt)
+    # no full blocks at all: N = 0
+    tr = ki.from_chains([[], []], [0, 5], tails=[3, 7])
+    gt = ctx.load(tr)
+    assert gt.N == 0 and gt.U == 0
+    cnt, obj = ctx.eval_grid(gt, K.configs([[1, 1, 1]]), M)
+    assert cnt[0]["miss"] == 0 and np.isfinite(obj).all()
+    # one request
+    tr = ki.from_chains([[1, 2, 3]], [7])
+    run_both(ctx, tr, O.configs([[1, 1, 1], [0, 0, 0]]), top_k=0)
+    # zero configurations
+    cnt, obj = ctx.eval_grid(ctx.load(ki.from_chains([[1]], [0])), K.configs(np.zeros((0, 3))), M)
+    assert len(cnt) == 0
+
+
+def test_hash_mode_matches_token_mode(ctx):
+    rng = np.random.default_rng(3)
+    tr = ki.random_prefix_tree(rng, n_req=40)
+    bh, boff = [], [0]
+    for r in range(tr.n_requests):
+        h = O.chain_hashes(tr.tokens[tr.offsets[r]:tr.offsets[r + 1]])
+        bh.append(h)
+        boff.append(boff[-1] + len(h))
+    th = ki.Trace(tr.arrival_ms, tr.output_tokens, np.array(boff, np.int64), block_hash=np.concatenate(bh),
+                  input_tokens=np.diff(tr.offsets))
+    a, b = ctx.load(tr, top_k=2), ctx.load(th, top_k=2)
+    for x in (K.X_HASH, K.X_PREV, K.X_DELTA, K.X_DEPTH, K.X_GROUP):
+        assert np.array_equal(a.export(x), b.export(x))
+    assert a.Ltok == b.Ltok
+
+
+def test_errors(ctx):
+    # chain violation (R7)
+    tr = ki.Trace(np.array([0, 1], np.int64), np.array([1, 1], np.int32), np.array([0, 1, 3], np.int64),
+                  block_hash=np.array([0xB, 0xA, 0xB], np.uint64))
+    with pytest.raises(K.KaretoError) as ei:
+        ctx.load(tr)
+    assert ei.value.status == K.E_CHAIN
+    # decreasing offsets
+    with pytest.raises(K.KaretoError) as ei:
+        ctx.load_trace(np.array([0, 1], np.int64), np.array([1, 1], np.int32), np.array([0, 32, 16], np.int64),
+                       tokens=np.zeros(32, np.uint32))
+    assert ei.value.status == K.E_PARSE
+    gt = ctx.load(ki.from_chains([[1, 2]], [0]))
+    M = K.Model()
+    for bad in (K.configs([[1, 1, 1]], policy=5), K.configs([[1, 1, 1]], medium=3), K.configs([[1, 1, K.INF]])):
+        with pytest.raises(K.KaretoError) as ei:
+            ctx.eval_grid(gt, bad, M)
+        assert ei.value.status == K.E_INVALID
+    with pytest.raises(ValueError):
+        ctx.eval_grid(gt, K.configs([[1, 1, 1]]), M, ttl=np.array([[5, 5, 5]], np.uint32))  # K+1 = 17 columns
+    with pytest.raises(K.KaretoError) as ei:
+        ctx.eval_grid(gt, K.configs([[1, 1, 1]], tuner=3), M, ttl=np.full((1, 17), 5, np.uint32))
+    assert ei.value.status == K.E_INVALID
+    with pytest.raises(K.KaretoError) as ei:
+        ctx.eval_grid(gt, K.configs([[1, 1, 1]], policy=K.FIFO), M)
+    assert ei.value.status == K.E_UNSUPPORTED
+    with pytest.raises(K.KaretoError) as ei:
+        bad = K.Model(bw_dram=0.0)
+        ctx.eval_grid(gt, K.configs([[1, 1, 1]]), bad)
+    assert ei.value.status == K.E_INVALID
+
+
+def test_medium_scale_depth_and_counts(ctx):
+    tr = ki.synthetic("chat", R=100_000, seed=1)
+    ot = O.OracleTrace(tr, top_k=16)
+    gt = ctx.load(tr, top_k=16)
+    d, _ = ot.depth()
+    assert np.array_equal(gt.export(K.X_DEPTH).astype(np.int64), np.where(d < 0, U32, d))
+    caps, axis = baseline_grid(ot.U, 8, 8, 8)
+    cf = O.configs(caps, axis=axis)
+    want = ot.stack_counts(cf)
+    got, obj = ctx.eval_grid(gt, kcfg(cf), K.Model(**MODEL_KW))
+    assert_counts_equal(got, want, cf)
+    assert_obj_equal(obj, ot.objective(O.Model(**MODEL_KW), cf, want))
+    # O1 on a sample
+    idx = np.random.default_rng(0).choice(len(cf), 6, replace=False)
+    assert_counts_equal(got[idx], ot.replay(cf[idx]), cf[idx])
+
+
+def test_agent_and_api_workloads(ctx):
+    for kind, R in (("agent", 800), ("api", 3000)):
+        tr = ki.synthetic(kind, R=R, seed=2)
+        ot = O.OracleTrace(tr, top_k=8)
+        gt = ctx.load(tr, top_k=8)
+        check_trace_exports(ot, gt)
+        caps, axis = baseline_grid(ot.U, 4, 4, 4)
+        cf = O.configs(caps, axis=axis)
+        want = ot.stack_counts(cf)
+        got, obj = ctx.eval_grid(gt, kcfg(cf), K.Model(**MODEL_KW))
+        assert_counts_equal(got, want, cf)
+
+
+@pytest.mark.slow
+def test_full_size_config2_sampled(ctx):
+    # BASELINE config 2 at full size, in the launch configuration bench.py times
+    tr = ki.synthetic("chat", R=1_000_000, seed=0)
+    gt = ctx.load(tr, top_k=16)
+    ot = O.OracleTrace(tr, top_k=16)
+    d, _ = ot.depth()
+    assert np.array_equal(gt.export(K.X_DEPTH).astype(np.int64), np.where(d < 0, U32, d))
+    caps, axis = baseline_grid(ot.U, 32, 32, 16, 16, 2, 1)
+    cf = O.configs(caps, axis=axis)
+    got, obj = ctx.eval_grid(gt, kcfg(cf), K.Model(**MODEL_KW))
+    idx = np.random.default_rng(1).choice(len(cf), 64, replace=False)
+    want = ot.stack_counts(cf[idx])
+    assert_counts_equal(got[idx], want, cf[idx])
+    assert_obj_equal(obj[idx], ot.objective(O.Model(**MODEL_KW), cf[idx], want))

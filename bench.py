@@ -79,16 +79,23 @@ class ClockSampler:
         self._t = None
 
     def _run(self):
-        cmd = ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-               "--format=csv,noheader,nounits"]
+        # NVML in-process (the same counters nvidia-smi reports: clocks.sm, clocks.max.sm,
+        # clocks_event_reasons.active); spawning nvidia-smi repeatedly stalls CUDA calls.
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        except Exception:
+            return
         while not self._stop.is_set():
             try:
-                out = subprocess.run(cmd, capture_output=True, text=True, timeout=5).stdout.strip()
-                sm, mx, rs = [x.strip() for x in out.split(",")]
-                self.samples.append((int(sm), int(mx), int(rs, 16) if rs.startswith("0x") else int(rs)))
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((int(sm), int(mx), int(rs)))
             except Exception:
                 pass
-            self._stop.wait(0.05)
+            self._stop.wait(0.02)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)

@@ -64,6 +64,7 @@ struct kareto_trace {
   kareto_ctx *ctx = nullptr;
   int64_t R = 0, N = 0, U = 0, span_ms = 1;
   int32_t K = 0, max_blocks = 0;
+  int64_t n_runs = 0;          // runs of consecutive previous positions (K3)
   uint64_t Ltok = 0, O = 0;
   // sum_r L_r and sum_r L_r (L_r - 1) / 2 as exact 128-bit values (for P0 = alpha*SL + beta*SQ)
   unsigned __int128 SL = 0, SQ = 0;
@@ -190,6 +191,6 @@ constexpr uint64_t kChainR = 0x9E3779B97F4A7C15ULL;
 constexpr uint64_t kSaltC = 0x243F6A8885A308D3ULL;
 
 // trace-load building blocks (trace_load.cu / stack_depth.cu)
-kareto_status stack_depth(kareto_ctx *ctx, kareto_trace *tr);
+kareto_status stack_depth(kareto_ctx *ctx, kareto_trace *tr, const uint8_t *run_flag);
 
 }  // namespace kareto

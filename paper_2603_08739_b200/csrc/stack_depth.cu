@@ -1,20 +1,26 @@
 // stack_depth.cu -- row a4, K3: exact LRU stack depth of every reuse access.
 //
 // The pre-request LRU depth of access j of request r with previous access p is
-//     d_j = s_r - p - A_j,   A_j = #{ i < s_r : prev[i] >= p }
-// (live positions in [p, s_r); the O2 oracle computes the same
-// with a sequential Fenwick tree).  A_j is an offline 2-D dominance count.  Here it is
-// computed by an MSD radix partition *with counting*: the stream of items
-//     for each request r in order:  queries (y = prev[j]) of its reuse accesses,
-//                                    then points (y = prev[j]) of its reuse accesses
-// (array order = time order x) is stably partitioned by the high digits of y; at every
-// level a query adds the number of EARLIER points of its segment whose digit is larger
-// (those have y > y_q), and the segment with equal digit recurses.  Two 8-bit global
-// passes (for N <= 2^27) leave segments of 2048 consecutive y values, which one warp
-// finishes with a 2048-bit shared-memory bitmap.  Equal y only occurs for a query and
-// its own point, which comes later, so "y > y_q" == "prev >= p".
+//     d_j = s_r - p - A(p, s_r),   A(y, s) = #{ i < s : prev[i] >= y }
+// (live positions in [p, s_r); the O2 oracle computes the same with
+// a sequential Fenwick tree).  A is an offline 2-D dominance count.
 //
-// Item = uint2 {y, w}: w = running count for a query, 0xFFFFFFFF for a point.
+// Run compression (exact for any trace): inside one request, a maximal run
+// of consecutive positions j0..j0+L-1 whose previous positions are consecutive,
+// prev[j0+t] = p0 + t, has
+//   (i)  one A for the whole run: A(y) - A(y+1) = [y re-touched before s_r], and no prev
+//        value y of the run is re-touched before s_r (it is the LAST earlier occurrence);
+//   (ii) one kill interval [p0, p0+L) (the y values it re-touches) at one time (its request).
+// Kill intervals are disjoint (each position is re-touched at most once) and an interval
+// that contains a query's p0 is killed at or after the query's request.  Hence
+//     A(run q) = sum of L' over runs q' of EARLIER requests with p0' > p0(q),
+// a weighted 2-D dominance count over runs -- ~2-3 runs per request instead of ~80
+// accesses.  It is solved by an MSD radix partition with counting (items: per request, its
+// query items then its weighted point items; each level adds the weight of earlier points
+// of the segment with a larger digit) and a per-segment Fenwick finish; d is then expanded
+// back to every access of the run.
+//
+// Item = uint2 {y, w}: query: w = running count (< 2^31); point: w = 0x80000000 | L.
 #include <cub/cub.cuh>
 
 #include "internal.cuh"
@@ -25,70 +31,78 @@ constexpr int SD_WARPS = 8;
 constexpr int SD_CHUNKS = 16;                          // chunks of 32 items per warp per tile
 constexpr int SD_TILE = SD_WARPS * SD_CHUNKS * 32;     // 4096 items per tile
 constexpr int SD_LOCAL_BITS = 11;
-constexpr uint32_t kPoint = 0xFFFFFFFFu;
+constexpr uint32_t kPointBit = 0x80000000u;
 
-struct VirtualIn {  // pass-1 input generated on the fly from prev[] / req[] / s[]
-  const uint32_t *req, *s, *prev;
-  uint64_t M;       // 2N virtual items
-};
-
-__device__ __forceinline__ bool virtual_item(const VirtualIn &vin, uint64_t v, uint2 &it) {
-  uint32_t r = vin.req[v >> 1];
-  uint32_t sr = vin.s[r], n = vin.s[r + 1] - sr;
-  uint32_t off = (uint32_t)(v - 2 * (uint64_t)sr);
-  bool q = off < n;
-  uint32_t j = sr + (q ? off : off - n);
-  uint32_t p = vin.prev[j];
-  it = make_uint2(p, q ? 0u : kPoint);
-  return p != kNone;
-}
+__device__ __forceinline__ bool is_point(uint32_t w) { return (w & kPointBit) != 0; }
+__device__ __forceinline__ uint32_t pweight(uint32_t w) { return is_point(w) ? (w & ~kPointBit) : 0u; }
 
 struct Tile {
   uint32_t seg, t;   // segment, local tile index
 };
 
 struct PassArgs {
-  // input
-  const uint2 *in;       // nullptr => virtual input
-  VirtualIn vin;
-  const Tile *tiles;     // per CTA tile descriptor (nullptr for virtual: seg 0, t = blockIdx)
+  const uint2 *in;
+  const Tile *tiles;
   const uint64_t *seg_start;   // [nseg] start offsets of segments in `in`
   const uint64_t *seg_len;     // [nseg]
   const uint32_t *seg_tile0;   // [nseg] first global tile of the segment
   const uint32_t *seg_ntiles;  // [nseg]
-  uint32_t n_tiles_virtual;
-  int shift, bits;       // digit = (y >> shift) & (2^bits - 1)
-  // outputs
+  int shift, bits;             // digit = (y >> shift) & (2^bits - 1)
   uint32_t *hist_all, *hist_pts;     // [tiles * bins] layout tile0*bins + d*ntiles + t
-  unsigned long long *seg_tot;       // [nseg * bins] (upsweep)
-  const uint32_t *off_all, *off_pts; // exclusive sums of the two histograms (downsweep)
+  unsigned long long *seg_tot;       // [nseg * bins]
+  const uint32_t *off_all, *off_pts; // exclusive sums of the two histograms
   uint2 *out;
 };
 
 __device__ __forceinline__ void tile_geometry(const PassArgs &a, uint32_t bid, uint32_t &seg, uint32_t &t,
                                               uint64_t &beg, uint64_t &end, uint32_t &tile0, uint32_t &ntiles) {
-  if (a.in == nullptr) {
-    seg = 0; t = bid; tile0 = 0; ntiles = a.n_tiles_virtual;
-    beg = (uint64_t)bid * SD_TILE;
-    end = beg + SD_TILE < a.vin.M ? beg + SD_TILE : a.vin.M;
-  } else {
-    Tile td = a.tiles[bid];
-    seg = td.seg; t = td.t;
-    tile0 = a.seg_tile0[seg]; ntiles = a.seg_ntiles[seg];
-    uint64_t s0 = a.seg_start[seg], L = a.seg_len[seg];
-    beg = s0 + (uint64_t)t * SD_TILE;
-    uint64_t e = s0 + (uint64_t)(t + 1) * SD_TILE;
-    end = e < s0 + L ? e : s0 + L;
+  Tile td = a.tiles[bid];
+  seg = td.seg; t = td.t;
+  if (seg == 0xFFFFFFFFu) { beg = end = 0; tile0 = ntiles = 0; return; }
+  tile0 = a.seg_tile0[seg]; ntiles = a.seg_ntiles[seg];
+  uint64_t s0 = a.seg_start[seg], L = a.seg_len[seg];
+  beg = s0 + (uint64_t)t * SD_TILE;
+  uint64_t e = s0 + (uint64_t)(t + 1) * SD_TILE;
+  end = e < s0 + L ? e : s0 + L;
+}
+
+// ---- run extraction: flags were written by K2 (k_access_info); runs listed by CUB select
+__global__ void k_run_info(const uint32_t *__restrict__ run_start, const int *__restrict__ m_ptr, uint64_t N,
+                           const uint32_t *__restrict__ req, const uint32_t *__restrict__ s,
+                           const uint32_t *__restrict__ prev, uint32_t *__restrict__ run_req,
+                           uint32_t *__restrict__ run_len, uint32_t *__restrict__ run_p0) {
+  const int M = *m_ptr;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < M; q += gridDim.x * blockDim.x) {
+    uint32_t j0 = run_start[q];
+    uint32_t r = req[j0];
+    uint32_t nxt = q + 1 < M ? run_start[q + 1] : (uint32_t)N;
+    uint32_t rend = s[r + 1];
+    run_req[q] = r;
+    run_len[q] = (nxt < rend ? nxt : rend) - j0;
+    run_p0[q] = prev[j0];
   }
 }
 
-__device__ __forceinline__ bool load_item(const PassArgs &a, uint64_t i, uint2 &it) {
-  if (a.in == nullptr) return virtual_item(a.vin, i, it);
-  it = a.in[i];
-  return true;
+// items of request r occupy [2 q0, 2 q0 + 2 nr): its nr queries, then its nr weighted points
+__global__ void k_run_items(const int *__restrict__ m_ptr, const uint32_t *__restrict__ run_req,
+                            const uint32_t *__restrict__ run_len, const uint32_t *__restrict__ run_p0,
+                            uint2 *__restrict__ items) {
+  const int M = *m_ptr;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < M; q += gridDim.x * blockDim.x) {
+    uint32_t r = run_req[q];
+    int lo = 0, hi = q;  // first run of request r
+    while (lo < hi) { int m = (lo + hi) >> 1; if (run_req[m] >= r) hi = m; else lo = m + 1; }
+    int q0 = lo;
+    lo = q + 1; hi = M;  // one past the last run of request r
+    while (lo < hi) { int m = (lo + hi) >> 1; if (run_req[m] > r) hi = m; else lo = m + 1; }
+    int nr = lo - q0;
+    uint32_t p0 = run_p0[q];
+    items[q + q0] = make_uint2(p0, 0u);
+    items[q + q0 + nr] = make_uint2(p0, kPointBit | run_len[q]);
+  }
 }
 
-// ---- upsweep: per-tile digit histograms (all items, points) + segment totals
+// ---- upsweep: per-tile digit histograms (item counts, point weights) + segment totals
 __global__ void __launch_bounds__(SD_WARPS * 32) k_sd_upsweep(PassArgs a) {
   __shared__ uint32_t h_all[256], h_pts[256];
   const int bins = 1 << a.bits;
@@ -97,12 +111,12 @@ __global__ void __launch_bounds__(SD_WARPS * 32) k_sd_upsweep(PassArgs a) {
   uint32_t seg, t, tile0, ntiles;
   uint64_t beg, end;
   tile_geometry(a, blockIdx.x, seg, t, beg, end, tile0, ntiles);
+  if (seg == 0xFFFFFFFFu) return;  // unused tile slot (upper-bound grid)
   for (uint64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
-    uint2 it;
-    if (!load_item(a, i, it)) continue;
+    uint2 it = a.in[i];
     uint32_t d = (it.x >> a.shift) & (bins - 1);
     atomicAdd(&h_all[d], 1u);
-    if (it.y == kPoint) atomicAdd(&h_pts[d], 1u);
+    if (is_point(it.y)) atomicAdd(&h_pts[d], pweight(it.y));
   }
   __syncthreads();
   for (int d = threadIdx.x; d < bins; d += blockDim.x) {
@@ -113,7 +127,7 @@ __global__ void __launch_bounds__(SD_WARPS * 32) k_sd_upsweep(PassArgs a) {
   }
 }
 
-// ---- downsweep: stable scatter by digit + query contributions
+// ---- downsweep: stable scatter by digit + weighted query contributions
 __global__ void __launch_bounds__(SD_WARPS * 32) k_sd_downsweep(PassArgs a) {
   __shared__ uint32_t run_all[SD_WARPS][256];
   __shared__ uint32_t run_pts[SD_WARPS][256];
@@ -123,27 +137,25 @@ __global__ void __launch_bounds__(SD_WARPS * 32) k_sd_downsweep(PassArgs a) {
   uint32_t seg, t, tile0, ntiles;
   uint64_t beg, end;
   tile_geometry(a, blockIdx.x, seg, t, beg, end, tile0, ntiles);
+  if (seg == 0xFFFFFFFFu) return;
   const uint64_t wbeg = beg + (uint64_t)wid * SD_CHUNKS * 32;
-  // phase A: per-warp histograms of this warp's contiguous sub-range
   for (int d = lane; d < bins; d += 32) { run_all[wid][d] = 0; run_pts[wid][d] = 0; }
   __syncwarp();
   for (int c = 0; c < SD_CHUNKS; c++) {
     uint64_t i = wbeg + (uint64_t)c * 32 + lane;
-    uint2 it;
-    bool live = i < end && load_item(a, i, it);
-    if (live) {
+    if (i < end) {
+      uint2 it = a.in[i];
       uint32_t d = (it.x >> a.shift) & (bins - 1);
       atomicAdd(&run_all[wid][d], 1u);
-      if (it.y == kPoint) atomicAdd(&run_pts[wid][d], 1u);
+      if (is_point(it.y)) atomicAdd(&run_pts[wid][d], pweight(it.y));
     }
   }
   __syncthreads();
-  // phase B: running offsets at the start of each warp's sub-range
   for (int d = threadIdx.x; d < bins; d += blockDim.x) {
     size_t idx = (size_t)tile0 * bins + (size_t)d * ntiles + t;
     size_t idx0 = (size_t)tile0 * bins + (size_t)d * ntiles;
     uint32_t ra = a.off_all[idx];
-    uint32_t rp = a.off_pts[idx] - a.off_pts[idx0];  // points of digit d in earlier tiles of the segment
+    uint32_t rp = a.off_pts[idx] - a.off_pts[idx0];  // point weight of digit d in earlier tiles of the segment
     for (int w = 0; w < SD_WARPS; w++) {
       uint32_t ca = run_all[w][d], cp = run_pts[w][d];
       run_all[w][d] = ra;
@@ -155,7 +167,8 @@ __global__ void __launch_bounds__(SD_WARPS * 32) k_sd_downsweep(PassArgs a) {
   __syncthreads();
   const unsigned lt = (1u << lane) - 1u;
   for (int c = 0; c < SD_CHUNKS; c++) {
-    // suffix sums over digits of the running point counts: suf[d] = sum_{d' > d} run_pts[d']
+    if (wbeg + (uint64_t)c * 32 >= end) break;  // warp-uniform
+    // suf[d] = sum_{d' > d} run_pts[d']
     {
       uint32_t v[8], tot = 0;
       int per = bins > 32 ? bins / 32 : 1;
@@ -165,14 +178,13 @@ __global__ void __launch_bounds__(SD_WARPS * 32) k_sd_downsweep(PassArgs a) {
         v[k] = (k < per && base + k < bins) ? run_pts[wid][base + k] : 0u;
         tot += v[k];
       }
-      // exclusive suffix over lanes: sum of totals of higher lanes
       uint32_t incl = tot;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
         uint32_t o = __shfl_down_sync(0xffffffffu, incl, off);
         if (lane + off < 32) incl += o;
       }
-      uint32_t acc = incl - tot;  // higher lanes
+      uint32_t acc = incl - tot;
 #pragma unroll
       for (int k = 7; k >= 0; k--) {
         if (k < per && base + k < bins) suf[wid][base + k] = acc;
@@ -181,117 +193,89 @@ __global__ void __launch_bounds__(SD_WARPS * 32) k_sd_downsweep(PassArgs a) {
     }
     __syncwarp();
     uint64_t i = wbeg + (uint64_t)c * 32 + lane;
-    uint2 it = make_uint2(0, 0);
-    bool live = i < end && load_item(a, i, it);
-    bool isp = live && it.y == kPoint;
+    bool live = i < end;
+    uint2 it = live ? a.in[i] : make_uint2(0, 0);
     uint32_t d = live ? (it.x >> a.shift) & (bins - 1) : 0u;
-    // earlier lanes that are points with a larger digit (bit-plane ballots)
-    unsigned gt = 0, eq = __ballot_sync(0xffffffffu, isp);
-    for (int b = a.bits - 1; b >= 0; b--) {
-      unsigned pb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-      if (!((d >> b) & 1u)) gt |= eq & pb;
-      eq &= ((d >> b) & 1u) ? pb : ~pb;
+    uint32_t wp = live ? pweight(it.y) : 0u;
+    // weight of earlier lanes' points with a larger digit
+    uint32_t intra = 0;
+#pragma unroll 8
+    for (int b = 0; b < 32; b++) {
+      uint32_t db = __shfl_sync(0xffffffffu, d, b);
+      uint32_t wb = __shfl_sync(0xffffffffu, wp, b);
+      if (b < lane && db > d) intra += wb;
     }
     unsigned lm = __ballot_sync(0xffffffffu, live);
-    unsigned ptsm = __ballot_sync(0xffffffffu, isp);
     unsigned same = __match_any_sync(0xffffffffu, live ? d : 0xFFFFFFFFu);
+    uint32_t gsum = __reduce_add_sync(same, wp);  // point weight of this digit in the chunk
     if (live) {
       uint32_t pos = run_all[wid][d] + __popc(same & lm & lt);
       uint2 o = it;
-      if (!isp) o.y = it.y + suf[wid][d] + __popc(gt & lt);
+      if (!is_point(it.y)) o.y = it.y + suf[wid][d] + intra;
       a.out[pos] = o;
     }
     __syncwarp();
-    // advance running counts (leader of each digit group)
     if (live && (__ffs(same & lm) - 1) == lane) {
       run_all[wid][d] += __popc(same & lm);
-      run_pts[wid][d] += __popc(same & ptsm);
+      run_pts[wid][d] += gsum;
     }
     __syncwarp();
   }
 }
 
-// ---- local pass: one warp per segment of 2^LB consecutive y values (bitmap in smem)
+// ---- local pass: one warp per segment of 2^LB consecutive y values; weighted Fenwick in smem.
+// A[y] = (count so far) + weight of earlier points of the segment with a larger y.
+constexpr int LOCAL_WARPS = 4;
 template <int LB>
-__global__ void __launch_bounds__(256) k_sd_local(const uint2 *__restrict__ in, VirtualIn vin,
-                                                  const uint64_t *__restrict__ seg_start,
+__global__ void __launch_bounds__(LOCAL_WARPS * 32) k_sd_local(const uint2 *__restrict__ in, const uint64_t *__restrict__ seg_start,
                                                   const uint64_t *__restrict__ seg_len, uint32_t nseg,
                                                   uint32_t *__restrict__ A) {
-  constexpr int W = (1 << LB) / 32 > 0 ? (1 << LB) / 32 : 1;  // bitmap words
-  __shared__ uint32_t bm[8][W];
-  __shared__ uint32_t sufw[8][W];
+  constexpr int S = 1 << LB;
+  __shared__ uint32_t fw[LOCAL_WARPS][S + 1];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  for (uint32_t seg = blockIdx.x * 8 + wid; seg < nseg; seg += gridDim.x * 8) {
-    uint64_t s0, L;
-    if (in) { s0 = seg_start[seg]; L = seg_len[seg]; }
-    else { s0 = 0; L = vin.M; }
+  for (uint32_t seg = blockIdx.x * LOCAL_WARPS + wid; seg < nseg; seg += gridDim.x * LOCAL_WARPS) {
+    const uint64_t s0 = seg_start[seg], L = seg_len[seg];
     if (L == 0) continue;
-    for (int w = lane; w < W; w += 32) { bm[wid][w] = 0; sufw[wid][w] = 0; }
+    for (int k = lane; k <= S; k += 32) fw[wid][k] = 0;
     __syncwarp();
+    uint32_t total = 0;  // weight inserted so far
     for (uint64_t c0 = 0; c0 < L; c0 += 32) {
-      uint64_t i = s0 + c0 + lane;
-      uint2 it = make_uint2(0, 0);
       bool live = c0 + lane < L;
-      if (live) {
-        if (in) it = in[i];
-        else live = virtual_item(vin, i, it);
+      uint2 it = live ? in[s0 + c0 + lane] : make_uint2(0, 0);
+      uint32_t yl = it.x & (S - 1);
+      uint32_t wp = live ? pweight(it.y) : 0u;
+      uint32_t intra = 0;
+#pragma unroll 8
+      for (int b = 0; b < 32; b++) {
+        uint32_t yb = __shfl_sync(0xffffffffu, yl, b);
+        uint32_t wb = __shfl_sync(0xffffffffu, wp, b);
+        if (b < lane && yb > yl) intra += wb;
       }
-      bool isp = live && it.y == kPoint;
-      uint32_t yl = it.x & ((1u << LB) - 1u);
-      unsigned gt = 0, eq = __ballot_sync(0xffffffffu, isp);
-#pragma unroll
-      for (int b = LB - 1; b >= 0; b--) {
-        unsigned pb = __ballot_sync(0xffffffffu, (yl >> b) & 1u);
-        if (!((yl >> b) & 1u)) gt |= eq & pb;
-        eq &= ((yl >> b) & 1u) ? pb : ~pb;
-      }
-      if (live && !isp) {
-        uint32_t wq = yl >> 5, bq = yl & 31;
-        uint32_t above = (bq == 31) ? 0u : (bm[wid][wq] >> (bq + 1));
-        uint32_t cnt = sufw[wid][wq] + __popc(above) + __popc(gt & lt);
-        A[it.x] = it.y + cnt;
+      if (live && !is_point(it.y)) {
+        uint32_t le = 0;  // weight with y' <= yl
+        for (int k = (int)yl + 1; k > 0; k -= k & -k) le += fw[wid][k];
+        A[it.x] = it.y + (total - le) + intra;
       }
       __syncwarp();
-      if (isp) atomicOr(&bm[wid][yl >> 5], 1u << (yl & 31));
-      __syncwarp();
-      // suffix popcounts over bitmap words: sufw[w] = sum_{w' > w} popc(bm[w'])
-      if (W <= 32) {
-        uint32_t pc = lane < W ? __popc(bm[wid][lane]) : 0u;
-        uint32_t incl = pc;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          uint32_t o = __shfl_down_sync(0xffffffffu, incl, off);
-          if (lane + off < 32) incl += o;
-        }
-        if (lane < W) sufw[wid][lane] = incl - pc;
-      } else {
-        constexpr int PER = W / 32;
-        uint32_t pc[PER > 0 ? PER : 1], tot = 0;
-#pragma unroll
-        for (int k = 0; k < PER; k++) { pc[k] = __popc(bm[wid][lane * PER + k]); tot += pc[k]; }
-        uint32_t incl = tot;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          uint32_t o = __shfl_down_sync(0xffffffffu, incl, off);
-          if (lane + off < 32) incl += o;
-        }
-        uint32_t acc = incl - tot;
-#pragma unroll
-        for (int k = PER - 1; k >= 0; k--) { sufw[wid][lane * PER + k] = acc; acc += pc[k]; }
-      }
+      if (wp)
+        for (int k = (int)yl + 1; k <= S; k += k & -k) atomicAdd(&fw[wid][k], wp);
+      total += __reduce_add_sync(0xffffffffu, wp);
       __syncwarp();
     }
   }
 }
 
-// d_j = s_r - p - A[p]  (UINT32_MAX for first accesses)
-__global__ void k_sd_finalize(uint64_t N, const uint32_t *__restrict__ prev, const uint32_t *__restrict__ req,
-                              const uint32_t *__restrict__ s, const uint32_t *__restrict__ A,
-                              uint32_t *__restrict__ depth) {
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t p = prev[j];
-    depth[j] = p == kNone ? kNone : s[req[j]] - p - A[p];
+// d_j = s_r - prev_j - A(run) for every access of each run (warp per run)
+__global__ void k_run_expand(const int *__restrict__ m_ptr, const uint32_t *__restrict__ run_start,
+                             const uint32_t *__restrict__ run_req, const uint32_t *__restrict__ run_len,
+                             const uint32_t *__restrict__ run_p0, const uint32_t *__restrict__ s,
+                             const uint32_t *__restrict__ A, uint32_t *__restrict__ depth) {
+  const int M = *m_ptr;
+  const int lane = threadIdx.x & 31;
+  for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < M; q += (gridDim.x * blockDim.x) >> 5) {
+    uint32_t j0 = run_start[q], L = run_len[q], p0 = run_p0[q];
+    uint32_t base = s[run_req[q]] - p0 - A[p0];
+    for (uint32_t t = lane; t < L; t += 32) depth[j0 + t] = base - t;
   }
 }
 
@@ -304,6 +288,12 @@ __global__ void k_sd_tiles(uint32_t nseg, const uint64_t *__restrict__ seg_len, 
   }
 }
 
+__global__ void k_single_segment(const int *__restrict__ m_ptr, uint64_t *__restrict__ start,
+                                 uint64_t *__restrict__ len) {
+  start[0] = 0;
+  len[0] = 2ull * (uint64_t)(*m_ptr);
+}
+
 template <typename F>
 static kareto_status cub_tmp(kareto_ctx *ctx, DBuf<uint8_t> &tmp, F &&f) {
   size_t bytes = 0;
@@ -314,55 +304,75 @@ static kareto_status cub_tmp(kareto_ctx *ctx, DBuf<uint8_t> &tmp, F &&f) {
   return KARETO_OK;
 }
 
-kareto_status stack_depth(kareto_ctx *ctx, kareto_trace *tr) {
+kareto_status stack_depth(kareto_ctx *ctx, kareto_trace *tr, const uint8_t *run_flag) {
   const uint64_t N = (uint64_t)tr->N;
   if (N == 0) return KARETO_OK;
   if (N >= (1ull << 31)) return fail(ctx, KARETO_E_OVERFLOW, "stack depth pass supports < 2^31 accesses");
   cudaStream_t st = ctx->stream;
   const int sms = ctx->num_sms;
+  KCUDA(ctx, cudaMemsetAsync(tr->depth, 0xFF, 4 * N, st));  // first accesses: UINT32_MAX
+  // ---- runs
+  DBuf<uint8_t> tmp;
+  DBuf<uint32_t> run_start, run_req, run_len, run_p0;
+  DBuf<int> m_dev;
+  KTRY(m_dev.alloc(ctx, 1));
+  // #runs <= reuse accesses; allocate for the worst case (N) lazily: count first
+  KTRY(run_start.alloc(ctx, N));
+  {
+    Pass ps(ctx, "K3_runs", 0, 1);
+    cub::CountingInputIterator<uint32_t> it0(0);
+    KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceSelect::Flagged(t, b, it0, run_flag, run_start.p, m_dev.p, (int64_t)N, st);
+    }));
+  }
+  int M = 0;
+  KCUDA(ctx, cudaMemcpyAsync(&M, m_dev.p, 4, cudaMemcpyDeviceToHost, st));
+  KCUDA(ctx, cudaStreamSynchronize(st));
+  tr->n_runs = M;
+  if (M == 0) return KARETO_OK;
+  KTRY(run_req.alloc(ctx, M)); KTRY(run_len.alloc(ctx, M)); KTRY(run_p0.alloc(ctx, M));
+  const uint64_t NI = 2ull * (uint64_t)M;  // items
+  DBuf<uint2> buf[2];
+  KTRY(buf[0].alloc(ctx, NI)); KTRY(buf[1].alloc(ctx, NI));
+  {
+    Pass ps(ctx, "K3_run_items", 1, 2);
+    k_run_info<<<grid_for(M, 256, 8 * sms), 256, 0, st>>>(run_start.p, m_dev.p, N, tr->req, tr->s, tr->prev,
+                                                          run_req.p, run_len.p, run_p0.p);
+    k_run_items<<<grid_for(M, 256, 8 * sms), 256, 0, st>>>(m_dev.p, run_req.p, run_len.p, run_p0.p, buf[0].p);
+  }
   int B = 1;
   while ((1ull << B) < N) B++;
   const int LB = B < SD_LOCAL_BITS ? B : SD_LOCAL_BITS;
   const int H = B - LB;
   const int npass = (H + 7) / 8;
-  VirtualIn vin{tr->req, tr->s, tr->prev, 2 * N};
   DBuf<uint32_t> A;
   KTRY(A.alloc(ctx, N));
-  DBuf<uint8_t> tmp;
-  DBuf<uint2> buf[2];
-  DBuf<uint64_t> seg_start, seg_len;  // segments of the current input
+  DBuf<uint64_t> seg_start, seg_len;
+  KTRY(seg_start.alloc(ctx, 1)); KTRY(seg_len.alloc(ctx, 1));
+  k_single_segment<<<1, 1, 0, st>>>(m_dev.p, seg_start.p, seg_len.p);
+  ctx->own_launches++;
   uint32_t nseg = 1;
-  const uint2 *cur = nullptr;         // nullptr => virtual
-  int shift = B;
-  int consumed = 0;
-  if (npass > 0) {
-    KTRY(buf[0].alloc(ctx, 2 * N));
-    KTRY(buf[1].alloc(ctx, 2 * N));
-  }
+  int cur = 0;
+  int shift = B, consumed = 0;
   for (int p = 0; p < npass; p++) {
     int bits = (H - consumed + (npass - p) - 1) / (npass - p);  // spread H bits over the passes
     shift -= bits;
     consumed += bits;
     const int bins = 1 << bits;
-    // tile descriptors
-    uint32_t ntiles;
     DBuf<Tile> tiles;
     DBuf<uint32_t> seg_tile0, seg_ntiles;
     KTRY(seg_tile0.alloc(ctx, nseg)); KTRY(seg_ntiles.alloc(ctx, nseg));
-    if (cur == nullptr) {
-      ntiles = (uint32_t)((vin.M + SD_TILE - 1) / SD_TILE);
-    } else {
+    uint32_t ntiles;
+    {
       Pass ps(ctx, "K3_tiles", 1, 2);
       k_sd_tiles<<<grid_for(nseg, 256, 1024), 256, 0, st>>>(nseg, seg_len.p, nullptr, seg_ntiles.p, nullptr, 0);
       KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
         return cub::DeviceScan::ExclusiveSum(t, b, seg_ntiles.p, seg_tile0.p, (int)nseg, st);
       }));
-      uint32_t last0 = 0, lastn = 0;
-      KCUDA(ctx, cudaMemcpyAsync(&last0, seg_tile0.p + nseg - 1, 4, cudaMemcpyDeviceToHost, st));
-      KCUDA(ctx, cudaMemcpyAsync(&lastn, seg_ntiles.p + nseg - 1, 4, cudaMemcpyDeviceToHost, st));
-      KCUDA(ctx, cudaStreamSynchronize(st));
-      ntiles = last0 + lastn;
-      KTRY(tiles.alloc(ctx, ntiles ? ntiles : 1));
+      // upper bound of the tile count (no host sync): every segment rounds up by < 1 tile
+      ntiles = (uint32_t)((NI + SD_TILE - 1) / SD_TILE + nseg);
+      KTRY(tiles.alloc(ctx, ntiles));
+      KCUDA(ctx, cudaMemsetAsync(tiles.p, 0xFF, sizeof(Tile) * ntiles, st));
       k_sd_tiles<<<grid_for(nseg, 256, 1024), 256, 0, st>>>(nseg, seg_len.p, seg_tile0.p, nullptr, tiles.p, 1);
     }
     DBuf<uint32_t> hist_all, hist_pts, off_all, off_pts;
@@ -371,28 +381,27 @@ kareto_status stack_depth(kareto_ctx *ctx, kareto_trace *tr) {
     size_t nh = (size_t)ntiles * bins;
     KTRY(hist_all.alloc(ctx, nh)); KTRY(hist_pts.alloc(ctx, nh));
     KTRY(off_all.alloc(ctx, nh)); KTRY(off_pts.alloc(ctx, nh));
+    KTRY(hist_all.zero()); KTRY(hist_pts.zero());
     KTRY(seg_tot.alloc(ctx, (size_t)nseg * bins)); KTRY(seg_tot.zero());
     KTRY(nstart.alloc(ctx, (size_t)nseg * bins));
     PassArgs a{};
-    a.in = cur;
-    a.vin = vin;
+    a.in = buf[cur].p;
     a.tiles = tiles.p;
     a.seg_start = seg_start.p;
     a.seg_len = seg_len.p;
     a.seg_tile0 = seg_tile0.p;
     a.seg_ntiles = seg_ntiles.p;
-    a.n_tiles_virtual = ntiles;
     a.shift = shift;
     a.bits = bits;
     a.hist_all = hist_all.p;
     a.hist_pts = hist_pts.p;
     a.seg_tot = seg_tot.p;
-    a.out = buf[p & 1].p;
-    if (ntiles > 0) {
-      Pass ps(ctx, p == 0 ? "K3_upsweep1" : "K3_upsweep2", 1, 1);
+    a.out = buf[cur ^ 1].p;
+    {
+      Pass ps(ctx, "K3_upsweep", 1, 1);
       k_sd_upsweep<<<ntiles, SD_WARPS * 32, 0, st>>>(a);
     }
-    if (nh > 0) {
+    {
       Pass ps(ctx, "K3_scans", 0, 3);
       KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
         return cub::DeviceScan::ExclusiveSum(t, b, hist_all.p, off_all.p, (int64_t)nh, st);
@@ -406,25 +415,24 @@ kareto_status stack_depth(kareto_ctx *ctx, kareto_trace *tr) {
     }
     a.off_all = off_all.p;
     a.off_pts = off_pts.p;
-    if (ntiles > 0) {
-      Pass ps(ctx, p == 0 ? "K3_downsweep1" : "K3_downsweep2", 1, 1);
+    {
+      Pass ps(ctx, "K3_downsweep", 1, 1);
       k_sd_downsweep<<<ntiles, SD_WARPS * 32, 0, st>>>(a);
     }
-    // next segments: (old segment, digit), starts = exclusive sums of seg_tot
     DBuf<uint64_t> nlen;
     KTRY(nlen.alloc(ctx, (size_t)nseg * bins));
     KCUDA(ctx, cudaMemcpyAsync(nlen.p, seg_tot.p, 8 * (size_t)nseg * bins, cudaMemcpyDeviceToDevice, st));
     seg_start = std::move(nstart);
     seg_len = std::move(nlen);
     nseg *= bins;
-    cur = buf[p & 1].p;
+    cur ^= 1;
   }
   {
     Pass ps(ctx, "K3_local", 1, 1);
-    unsigned g = (unsigned)((nseg + 7) / 8);
+    unsigned g = (unsigned)((nseg + LOCAL_WARPS - 1) / LOCAL_WARPS);
     if (g > (unsigned)(64 * sms)) g = (unsigned)(64 * sms);
     switch (LB) {
-#define SD_CASE(b) case b: k_sd_local<b><<<g, 256, 0, st>>>(cur, vin, seg_start.p, seg_len.p, nseg, A.p); break;
+#define SD_CASE(b) case b: k_sd_local<b><<<g, LOCAL_WARPS * 32, 0, st>>>(buf[cur].p, seg_start.p, seg_len.p, nseg, A.p); break;
       SD_CASE(1) SD_CASE(2) SD_CASE(3) SD_CASE(4) SD_CASE(5) SD_CASE(6) SD_CASE(7) SD_CASE(8) SD_CASE(9)
       SD_CASE(10) SD_CASE(11)
 #undef SD_CASE
@@ -432,8 +440,9 @@ kareto_status stack_depth(kareto_ctx *ctx, kareto_trace *tr) {
     }
   }
   {
-    Pass ps(ctx, "K3_finalize", 1, 1);
-    k_sd_finalize<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(N, tr->prev, tr->req, tr->s, A.p, tr->depth);
+    Pass ps(ctx, "K3_expand", 1, 1);
+    k_run_expand<<<grid_for(32ll * M, 256, 16 * sms), 256, 0, st>>>(m_dev.p, run_start.p, run_req.p, run_len.p,
+                                                                    run_p0.p, tr->s, A.p, tr->depth);
   }
   return KARETO_OK;
 }

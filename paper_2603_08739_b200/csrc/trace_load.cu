@@ -279,7 +279,8 @@ __device__ __forceinline__ void warp_count_add(uint32_t *arr, uint32_t key, bool
 __global__ void k_access_info(uint64_t N, const uint32_t *__restrict__ prev, const uint32_t *__restrict__ req,
                               const uint32_t *__restrict__ s, const int64_t *__restrict__ arr,
                               const uint64_t *__restrict__ hash, uint32_t *__restrict__ delta,
-                              uint32_t *__restrict__ first_cnt, uint32_t *__restrict__ reuse_cnt, LoadStats *st) {
+                              uint32_t *__restrict__ first_cnt, uint32_t *__restrict__ reuse_cnt,
+                              uint8_t *__restrict__ run_flag, LoadStats *st) {
   unsigned flags = 0;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t p = prev[j], r = req[j];
@@ -294,6 +295,14 @@ __global__ void k_access_info(uint64_t N, const uint32_t *__restrict__ prev, con
       else if (kj > 0 && hash[j + 1] != hash[p + 1]) flags |= F_CHAIN;
     }
     delta[j] = dl;
+    // K3 run heads: a reuse access whose predecessor position is not its previous position
+    // plus one, or the first position of its request (stack_depth.cu)
+    uint8_t head = 0;
+    if (p != kNone) {
+      uint32_t pm = j > 0 ? prev[j - 1] : kNone;
+      head = ((uint32_t)j == s[r] || pm == kNone || p != pm + 1) ? 1 : 0;
+    }
+    run_flag[j] = head;
     warp_count_add(first_cnt, r, p == kNone);
     warp_count_add(reuse_cnt, r, p != kNone);
   }
@@ -520,6 +529,8 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
 
   // ---- a3: K2 prev / delta / chain check
   DBuf<uint32_t> first_cnt, reuse_cnt;
+  DBuf<uint8_t> run_flag;
+  KTRY(run_flag.alloc(ctx, N > 0 ? N : 1));
   KTRY(first_cnt.alloc(ctx, R)); KTRY(reuse_cnt.alloc(ctx, R));
   KTRY(first_cnt.zero()); KTRY(reuse_cnt.zero());
   if (N > 0) {
@@ -544,7 +555,7 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
     {
       Pass ps(ctx, "K2_access_info", 1, 1);
       k_access_info<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(N, tr->prev, tr->req, tr->s, tr->arr, tr->hash,
-                                                               tr->delta, first_cnt.p, reuse_cnt.p, stats.p);
+                                                               tr->delta, first_cnt.p, reuse_cnt.p, run_flag.p, stats.p);
     }
   }
 
@@ -612,7 +623,7 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
   if (hs.flags & F_DELTA) return fail(ctx, KARETO_E_OVERFLOW, "a reuse interval >= 2^32-1 ms");
 
   // ---- a4: K3 LRU stack depths
-  KTRY(stack_depth(ctx, tr));
+  KTRY(stack_depth(ctx, tr, run_flag.p));
   KTRY(sync(ctx, "load_trace"));
   guard.keep = true;
   *out = tr;

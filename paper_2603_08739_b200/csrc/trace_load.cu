@@ -85,13 +85,27 @@ __global__ void k_req_meta(int64_t R, int mode, const uint32_t *__restrict__ ord
     sq_lo += q64 & 0xFFFFFFFFull;
     sq_hi += q64 >> 32;
   }
-  atomicAdd(&st->sl_lo, sl_lo);
-  atomicAdd(&st->sl_hi, sl_hi);
-  atomicAdd(&st->sq_lo, sq_lo);
-  atomicAdd(&st->sq_hi, sq_hi);
-  atomicAdd(&st->O, O);
-  if (flags) atomicOr(&st->flags, flags);
-  atomicMax(&st->max_blocks, maxb);
+  // warp-level reduction, one atomic per warp
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    sl_lo += __shfl_xor_sync(0xffffffffu, sl_lo, off);
+    sl_hi += __shfl_xor_sync(0xffffffffu, sl_hi, off);
+    sq_lo += __shfl_xor_sync(0xffffffffu, sq_lo, off);
+    sq_hi += __shfl_xor_sync(0xffffffffu, sq_hi, off);
+    O += __shfl_xor_sync(0xffffffffu, O, off);
+    flags |= __shfl_xor_sync(0xffffffffu, flags, off);
+    unsigned mb = __shfl_xor_sync(0xffffffffu, maxb, off);
+    maxb = mb > maxb ? mb : maxb;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&st->sl_lo, sl_lo);
+    atomicAdd(&st->sl_hi, sl_hi);
+    atomicAdd(&st->sq_lo, sq_lo);
+    atomicAdd(&st->sq_hi, sq_hi);
+    atomicAdd(&st->O, O);
+    if (flags) atomicOr(&st->flags, flags);
+    atomicMax(&st->max_blocks, maxb);
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->arr_first = arr_sorted[0];
   }
@@ -260,12 +274,81 @@ __global__ void k_iota(uint32_t *v, uint64_t n) {
     v[i] = (uint32_t)i;
 }
 
-__global__ void k_link_prev(const uint64_t *__restrict__ hs, const uint32_t *__restrict__ js, uint64_t N,
-                            uint32_t *__restrict__ prev) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t p = (i > 0 && hs[i] == hs[i - 1]) ? js[i - 1] : kNone;
-    prev[js[i]] = p;
+// Sort key: a 32-bit fingerprint of the 64-bit hash (top half of a bijective mix, so
+// caller-provided structured hashes cannot crowd one key); value: (other half << 32) |
+// position, so equality is decided on all 64 bits without gathers.
+__global__ void k_sort_prep(const uint64_t *__restrict__ hash, uint64_t N, uint32_t *__restrict__ key,
+                            uint64_t *__restrict__ val) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
+    // m = fmix64(h ^ c) is a bijection of h: (key, val >> 32) = (m >> 32, m & 0xFFFFFFFF)
+    // identifies h exactly
+    uint64_t m = fmix64(hash[j] ^ 0x6A09E667F3BCC909ULL);
+    key[j] = (uint32_t)(m >> 32);
+    val[j] = (m << 32) | (uint64_t)(uint32_t)j;
   }
+}
+
+// In fingerprint-sorted order (stable: positions ascending within a key), the previous
+// occurrence of element i is the nearest earlier element of its key run whose full hash
+// matches (almost always i-1).  Emits (position, prev) pairs for the bucketed scatter.
+constexpr int LINK_SCAN = 32;  // bounded backward scan; longer (fingerprint-collision) cases overflow
+
+__global__ void k_link_prev(const uint32_t *__restrict__ ks, const uint64_t *__restrict__ vs, uint64_t N,
+                            uint32_t *__restrict__ pj, uint32_t *__restrict__ pp, uint32_t *__restrict__ ovf,
+                            uint32_t *__restrict__ n_ovf) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = ks[i];
+    const uint64_t v = vs[i];
+    const uint32_t j = (uint32_t)v;
+    uint32_t p = kNone;
+    uint64_t t = i;
+    int steps = 0;
+    for (; t > 0 && ks[t - 1] == k && steps < LINK_SCAN; t--, steps++) {
+      uint64_t w = vs[t - 1];
+      if ((w >> 32) == (v >> 32)) { p = (uint32_t)w; break; }
+    }
+    if (p == kNone && steps == LINK_SCAN && t > 0 && ks[t - 1] == k) {
+      uint32_t slot = atomicAdd(n_ovf, 1u);
+      ovf[slot] = (uint32_t)i;  // resolved by k_link_overflow
+    }
+    pj[i] = j;
+    pp[i] = p;
+  }
+}
+
+// Rare slow path: warp-parallel backward scan of the key run for overflowed elements.
+__global__ void k_link_overflow(const uint32_t *__restrict__ ks, const uint64_t *__restrict__ vs,
+                                const uint32_t *__restrict__ ovf, const uint32_t *__restrict__ n_ovf,
+                                uint32_t *__restrict__ pp) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t n = *n_ovf;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += (gridDim.x * blockDim.x) >> 5) {
+    const uint64_t i = ovf[w];
+    const uint32_t k = ks[i];
+    const uint64_t hi = vs[i] >> 32;
+    uint32_t p = kNone;
+    for (int64_t base = (int64_t)i - 1 - LINK_SCAN; base >= -31; base -= 32) {
+      int64_t t = base - lane;  // lanes walk backwards 32 at a time
+      bool in = t >= 0 && ks[t] == k;
+      bool hit = in && (vs[t] >> 32) == hi;
+      unsigned mh = __ballot_sync(0xffffffffu, hit);
+      if (mh) {
+        int src = __ffs(mh) - 1;  // lowest lane = largest t
+        p = (uint32_t)__shfl_sync(0xffffffffu, (uint32_t)(in ? vs[t] : 0), src);
+        break;
+      }
+      if (__ballot_sync(0xffffffffu, in) != 0xffffffffu) break;  // reached the run start
+    }
+    if (lane == 0) pp[i] = p;
+  }
+}
+
+// (position, prev) pairs partitioned by the top bits of the position: the writes of a
+// warp land in one L2-resident window of prev[] instead of random HBM sectors.
+__global__ void k_bucket_scatter(const uint32_t *__restrict__ pj, const uint32_t *__restrict__ pp, uint64_t N,
+                                 uint32_t *__restrict__ prev) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x)
+    prev[pj[i]] = pp[i];
 }
 
 __device__ __forceinline__ void warp_count_add(uint32_t *arr, uint32_t key, bool pred) {
@@ -369,13 +452,19 @@ __global__ void k_fill_u16(uint16_t *p, int64_t n, uint16_t v) {
 }
 
 __global__ void k_group_tables(int64_t R, const uint16_t *__restrict__ grp, const uint32_t *__restrict__ first_cnt,
-                               const uint32_t *__restrict__ reuse_cnt, unsigned long long *__restrict__ tab) {
-  // tab[2g] = U_g, tab[2g+1] = reuse_g
+                               const uint32_t *__restrict__ reuse_cnt, unsigned long long *__restrict__ tab, int G) {
+  // tab[2g] = U_g, tab[2g+1] = reuse_g; privatised per block in smem (G <= 1024)
+  extern __shared__ unsigned long long ts[];
+  for (int i = threadIdx.x; i < 2 * G; i += blockDim.x) ts[i] = 0;
+  __syncthreads();
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
     int g = grp[r];
-    if (first_cnt[r]) atomicAdd(&tab[2 * g], (unsigned long long)first_cnt[r]);
-    if (reuse_cnt[r]) atomicAdd(&tab[2 * g + 1], (unsigned long long)reuse_cnt[r]);
+    if (first_cnt[r]) atomicAdd(&ts[2 * g], (unsigned long long)first_cnt[r]);
+    if (reuse_cnt[r]) atomicAdd(&ts[2 * g + 1], (unsigned long long)reuse_cnt[r]);
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * G; i += blockDim.x)
+    if (ts[i]) atomicAdd(&tab[i], ts[i]);
 }
 
 // ------------------------------------------------------------------ driver ----
@@ -534,24 +623,45 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
   KTRY(first_cnt.alloc(ctx, R)); KTRY(reuse_cnt.alloc(ctx, R));
   KTRY(first_cnt.zero()); KTRY(reuse_cnt.zero());
   if (N > 0) {
-    DBuf<uint64_t> hsort;
-    DBuf<uint32_t> iota, jsort;
-    KTRY(hsort.alloc(ctx, N)); KTRY(iota.alloc(ctx, N)); KTRY(jsort.alloc(ctx, N));
+    int B = 1;
+    while ((1ull << B) < N) B++;
     {
-      Pass ps(ctx, "K2_iota", 1, 1);
-      k_iota<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(iota.p, N);
+      DBuf<uint32_t> k32, k32s, pj, pp, pj2, pp2;
+      DBuf<uint64_t> v64, v64s;
+      KTRY(k32.alloc(ctx, N)); KTRY(v64.alloc(ctx, N)); KTRY(k32s.alloc(ctx, N)); KTRY(v64s.alloc(ctx, N));
+      {
+        Pass ps(ctx, "K2_sort_prep", 1, 1);
+        k_sort_prep<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(tr->hash, N, k32.p, v64.p);
+      }
+      {
+        Pass ps(ctx, "K2_sort_hashes", 0, 1);
+        KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
+          return cub::DeviceRadixSort::SortPairs(t, b, k32.p, k32s.p, v64.p, v64s.p, (int64_t)N, 0, 32, st);
+        }));
+      }
+      k32.release(); v64.release();
+      KTRY(pj.alloc(ctx, N)); KTRY(pp.alloc(ctx, N));
+      {
+        DBuf<uint32_t> ovf, n_ovf;
+        KTRY(ovf.alloc(ctx, N)); KTRY(n_ovf.alloc(ctx, 1)); KTRY(n_ovf.zero());
+        Pass ps(ctx, "K2_link_prev", 1, 2);
+        k_link_prev<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(k32s.p, v64s.p, N, pj.p, pp.p, ovf.p, n_ovf.p);
+        k_link_overflow<<<4 * sms, 256, 0, st>>>(k32s.p, v64s.p, ovf.p, n_ovf.p, pp.p);
+      }
+      k32s.release(); v64s.release();
+      KTRY(pj2.alloc(ctx, N)); KTRY(pp2.alloc(ctx, N));
+      {
+        Pass ps(ctx, "K2_partition_prev", 0, 1);  // one stable 8-bit radix pass on the top bits of j
+        int b0 = B > 8 ? B - 8 : 0;
+        KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
+          return cub::DeviceRadixSort::SortPairs(t, b, pj.p, pj2.p, pp.p, pp2.p, (int64_t)N, b0, B, st);
+        }));
+      }
+      {
+        Pass ps(ctx, "K2_bucket_scatter", 1, 1);
+        k_bucket_scatter<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(pj2.p, pp2.p, N, tr->prev);
+      }
     }
-    {
-      Pass ps(ctx, "K2_sort_hashes", 0, 1);
-      KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, tr->hash, hsort.p, iota.p, jsort.p, (int64_t)N, 0, 64, st);
-      }));
-    }
-    {
-      Pass ps(ctx, "K2_link_prev", 1, 1);
-      k_link_prev<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(hsort.p, jsort.p, N, tr->prev);
-    }
-    hsort.release(); iota.release(); jsort.release();
     {
       Pass ps(ctx, "K2_access_info", 1, 1);
       k_access_info<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(N, tr->prev, tr->req, tr->s, tr->arr, tr->hash,
@@ -604,7 +714,7 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
       k_rank_of_run<<<grid_for(m, 256, 4 * sms), 256, 0, st>>>(ranked.p, nruns.p, rank.p);
       k_assign_groups<<<grid_for(m, 256, 4 * sms), 256, 0, st>>>(rval_s.p, run_incl.p, m_dev.p, rank.p, K, tr->grp);
     }
-    k_group_tables<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(R, tr->grp, first_cnt.p, reuse_cnt.p, gtab.p);
+    k_group_tables<<<grid_for(R, 256, 4 * sms), 256, 16 * (K + 1), st>>>(R, tr->grp, first_cnt.p, reuse_cnt.p, gtab.p, K + 1);
     std::vector<unsigned long long> h(2 * (K + 1));
     KCUDA(ctx, cudaMemcpyAsync(h.data(), gtab.p, 16 * (K + 1), cudaMemcpyDeviceToHost, st));
     KCUDA(ctx, cudaMemcpyAsync(&hs, stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));

@@ -210,6 +210,41 @@ def test_hash_mode_matches_token_mode(ctx):
     assert a.Ltok == b.Ltok
 
 
+def _unxorshift(x, s):
+    z = x
+    for _ in range(64 // s + 1):
+        z = x ^ (z >> s)
+    return z & ((1 << 64) - 1)
+
+
+def _fmix64_inv(m):
+    M = (1 << 64) - 1
+    z = _unxorshift(m, 31)
+    z = (z * pow(0x94D049BB133111EB, -1, 1 << 64)) & M
+    z = _unxorshift(z, 27)
+    z = (z * pow(0xBF58476D1CE4E5B9, -1, 1 << 64)) & M
+    return _unxorshift(z, 30)
+
+
+def test_fingerprint_collisions_resolved_exactly(ctx):
+    # HASHES mode: distinct block hashes crafted to share the 32-bit sort fingerprint used by
+    # K2 (top half of fmix64(h ^ c)), including a hot block interleaved with rare ones, so the
+    # bounded scan overflows into the warp-parallel slow path.  prev must still be exact.
+    c = 0x6A09E667F3BCC909
+    fp = 0x12345678
+    hs = [_fmix64_inv((fp << 32) | lo) ^ c for lo in (7, 11, 13, 17, 19, 23)]
+    assert O.fmix64(hs[0] ^ c) >> 32 == fp
+    rng = np.random.default_rng(5)
+    seq = [0] * 400 + [1, 2, 3, 4, 5] * 6
+    seq = list(rng.permutation(seq))
+    R = len(seq)
+    tr = ki.Trace(np.arange(R, dtype=np.int64), np.ones(R, np.int32), np.arange(R + 1, dtype=np.int64),
+                  block_hash=np.array([hs[x] for x in seq], np.uint64))
+    ot = O.OracleTrace(tr, mode="hashes", top_k=2)
+    gt = ctx.load(tr, top_k=2)
+    check_trace_exports(ot, gt)
+
+
 def test_errors(ctx):
     # chain violation (R7)
     tr = ki.Trace(np.array([0, 1], np.int64), np.array([1, 1], np.int32), np.array([0, 1, 3], np.int64),

@@ -181,7 +181,8 @@ extern "C" kareto_status kareto_launch_counter(kareto_ctx *ctx, int64_t *own_lau
 extern "C" void kareto_trace_free(kareto_trace *tr) {
   if (!tr) return;
   kareto_ctx *ctx = tr->ctx;
-  void *ptrs[] = {tr->arr, tr->s, tr->grp, tr->hash, tr->req, tr->prev, tr->delta, tr->depth};
+  void *ptrs[] = {tr->arr, tr->s, tr->grp, tr->hash, tr->req, tr->prev, tr->delta, tr->depth,
+                  tr->blk, tr->gblk, tr->arr_rel};
   for (void *p : ptrs)
     if (p) cudaFreeAsync(p, ctx->stream);
   cudaStreamSynchronize(ctx->stream);

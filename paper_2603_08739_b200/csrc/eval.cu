@@ -15,6 +15,7 @@
 #include <cub/cub.cuh>
 
 #include "eval.cuh"
+#include "replay.cuh"
 
 namespace kareto {
 
@@ -186,6 +187,18 @@ __global__ void k_prefix_t(unsigned long long *__restrict__ a, int rows, int nt1
   }
 }
 
+__global__ void k_scatter_out(const kareto_counts *__restrict__ c, const double *__restrict__ o,
+                              const uint32_t *__restrict__ idx, int64_t n, kareto_counts *__restrict__ cout,
+                              double *__restrict__ oout) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t d = idx[i];
+    cout[d] = c[i];
+    oout[3 * (size_t)d] = o[3 * i];
+    oout[3 * (size_t)d + 1] = o[3 * i + 1];
+    oout[3 * (size_t)d + 2] = o[3 * i + 2];
+  }
+}
+
 template <typename F>
 static kareto_status cub_tmp(kareto_ctx *ctx, DBuf<uint8_t> &tmp, F &&f) {
   size_t bytes = 0;
@@ -256,10 +269,7 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
     }
     if (ttl && !all_finite)
       return fail(ctx, KARETO_E_INVALID, "config %lld: TTL mode needs finite TTLs (R22)", (long long)i);
-    bool stack = c.policy == KARETO_LRU && (ttl || uniform);
-    if (!stack)
-      return fail(ctx, KARETO_E_UNSUPPORTED, "config %lld needs the per-configuration replay (policy %d)", (long long)i,
-                  c.policy);
+    (void)uniform;
     // overflow guards of the integer model terms
     if (!ttl) {
       unsigned __int128 cb = (unsigned __int128)sat_add(sat_add(c.cap[0], c.cap[1]), c.cap[2]) * model->block_bytes;
@@ -283,13 +293,25 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
   if (ctx->world > 1) shard_range(n_cfg, ctx->rank, ctx->world, lo, hi);
   const int64_t ns = hi - lo;
   const kareto_config *sc = cfg + lo;
+  // stack-eligible (LRU, and TTL mode or a uniform disk TTL) vs per-configuration replay (K6)
+  std::vector<kareto_config> cS, cP;
+  std::vector<uint32_t> iS, iP;
+  for (int64_t i = 0; i < ns; i++) {
+    const kareto_config &c = sc[i];
+    const uint32_t *row = rows.data() + (size_t)(n_tuner > 0 ? c.tuner : 0) * G;
+    bool uniform = true;
+    for (int g = 1; g < G; g++) uniform &= row[g] == row[0];
+    if (c.policy == KARETO_LRU && (c.cap[2] == KARETO_INF || uniform)) { cS.push_back(c); iS.push_back((uint32_t)i); }
+    else { cP.push_back(c); iP.push_back((uint32_t)i); }
+  }
+  const int64_t nS = (int64_t)cS.size(), nP = (int64_t)cP.size();
 
-  // ---- boundary / TTL sets of the shard
+  // ---- boundary / TTL sets of the shard's stack configurations
   std::vector<uint32_t> Bd, B12, Tc, Tt;
   std::vector<char> row_used(nrows, 0);
   auto clampU = [&](uint64_t v) -> uint32_t { return (uint32_t)(v < U ? v : U); };
-  for (int64_t i = 0; i < ns; i++) {
-    const kareto_config &c = sc[i];
+  for (int64_t i = 0; i < nS; i++) {
+    const kareto_config &c = cS[i];
     uint64_t c12 = sat_add(c.cap[0], c.cap[1]);
     Bd.push_back(clampU(c.cap[0]));
     Bd.push_back(clampU(c12));
@@ -313,7 +335,7 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
   uniq(Bd); uniq(B12); uniq(Tc); uniq(Tt);
   const int nb = (int)Bd.size(), nb12 = (int)B12.size(), ntc = (int)Tc.size(), ntt = (int)Tt.size();
   // per-config lookup indices
-  std::vector<CfgDev> cd(ns > 0 ? ns : 1);
+  std::vector<CfgDev> cd(nS > 0 ? nS : 1);
   auto idx = [](const std::vector<uint32_t> &v, uint32_t x) {
     return (int32_t)(std::lower_bound(v.begin(), v.end(), x) - v.begin());
   };
@@ -321,8 +343,8 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
   for (int r = 0; r < nrows; r++)
     if (row_used[r])
       for (int g = 0; g < G; g++) tix[(size_t)r * G + g] = (uint32_t)idx(Tt, rows[(size_t)r * G + g]);
-  for (int64_t i = 0; i < ns; i++) {
-    const kareto_config &c = sc[i];
+  for (int64_t i = 0; i < nS; i++) {
+    const kareto_config &c = cS[i];
     uint64_t c12 = sat_add(c.cap[0], c.cap[1]);
     int ri = n_tuner > 0 ? c.tuner : 0;
     CfgDev x{};
@@ -444,18 +466,36 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
   int64_t nsa = ns > 0 ? ns : 1;
   // gathered outputs are assembled in padded per-rank slots: slot = ceil(n / world)
   const int64_t slot = ctx->world > 1 ? (n_cfg + ctx->world - 1) / ctx->world : nsa;
-  KTRY(dcfg.alloc(ctx, nsa)); KTRY(dcd.alloc(ctx, nsa));
+  KTRY(dcfg.alloc(ctx, nS > 0 ? nS : 1)); KTRY(dcd.alloc(ctx, nS > 0 ? nS : 1));
   KTRY(dcounts.alloc(ctx, slot > 0 ? slot : 1)); KTRY(dobj.alloc(ctx, 3 * (slot > 0 ? slot : 1)));
-  if (ns > 0) {
-    KCUDA(ctx, cudaMemcpyAsync(dcfg.p, sc, sizeof(kareto_config) * ns, cudaMemcpyHostToDevice, st));
-    KCUDA(ctx, cudaMemcpyAsync(dcd.p, cd.data(), sizeof(CfgDev) * ns, cudaMemcpyHostToDevice, st));
+  if (nS > 0) {
+    KCUDA(ctx, cudaMemcpyAsync(dcfg.p, cS.data(), sizeof(kareto_config) * nS, cudaMemcpyHostToDevice, st));
+    KCUDA(ctx, cudaMemcpyAsync(dcd.p, cd.data(), sizeof(CfgDev) * nS, cudaMemcpyHostToDevice, st));
   }
   StackTables T{};
   T.Bd = nullptr; T.nb = nb; T.Tc = dTc.p; T.ntc = ntc;
   T.C1 = C1.p; T.S1 = S1.p; T.CD = CD.p;
   T.B12 = nullptr; T.nb12 = nb12; T.Tt = dTt.p; T.ntt = ntt; T.G = G;
   T.C2 = C2.p; T.S2 = S2.p; T.SDg = SDg.p; T.Ug = dUg.p; T.Rg = dRg.p;
-  launch_objective(ctx, T, dcfg.p, dcd.p, dtix.p, drows.p, ns, model, mc, dcounts.p, dobj.p);
+  if (nP == 0) {  // pure stack shard: outputs in shard order directly
+    launch_objective(ctx, T, dcfg.p, dcd.p, dtix.p, drows.p, nS, model, mc, nullptr, dcounts.p, dobj.p);
+  } else {
+    // K6 replay for the rest, then the objective from its counts; scatter both to shard order
+    DBuf<kareto_counts> cntS, cntP;
+    DBuf<double> objS, objP;
+    DBuf<kareto_config> dcfgP;
+    DBuf<uint32_t> diS, diP;
+    KTRY(cntS.alloc(ctx, nS > 0 ? nS : 1)); KTRY(objS.alloc(ctx, 3 * (nS > 0 ? nS : 1)));
+    KTRY(cntP.alloc(ctx, nP)); KTRY(objP.alloc(ctx, 3 * nP)); KTRY(dcfgP.alloc(ctx, nP));
+    KTRY(upload(ctx, diS, iS)); KTRY(upload(ctx, diP, iP));
+    launch_objective(ctx, T, dcfg.p, dcd.p, dtix.p, drows.p, nS, model, mc, nullptr, cntS.p, objS.p);
+    KTRY(replay_eval(ctx, const_cast<kareto_trace *>(tr), cP.data(), nP, drows.p, n_tuner, cntP.p));
+    KCUDA(ctx, cudaMemcpyAsync(dcfgP.p, cP.data(), sizeof(kareto_config) * nP, cudaMemcpyHostToDevice, st));
+    launch_objective(ctx, T, dcfgP.p, nullptr, dtix.p, drows.p, nP, model, mc, cntP.p, nullptr, objP.p);
+    Pass ps(ctx, "K5_scatter", 1, 2);
+    if (nS > 0) k_scatter_out<<<grid_for(nS, 256), 256, 0, st>>>(cntS.p, objS.p, diS.p, nS, dcounts.p, dobj.p);
+    k_scatter_out<<<grid_for(nP, 256), 256, 0, st>>>(cntP.p, objP.p, diP.p, nP, dcounts.p, dobj.p);
+  }
 
   // ---- gather (row e): one NCCL allgather of counts and objective vectors over NVLink
   kareto_counts *all_counts = dcounts.p;

@@ -44,7 +44,7 @@ struct CfgDev {       // per-configuration lookup indices (host-computed)
 // K5 + K7: counts from the cumulative tables, then the fp64 objective (objective.cu)
 void launch_objective(kareto_ctx *ctx, const StackTables &T, const kareto_config *cfg, const CfgDev *cd,
                       const uint32_t *ttl_t_index /*[n_rows][G] index into Tt*/, const uint32_t *ttl_ms,
-                      int64_t n, const kareto_model *model, ModelConsts mc, kareto_counts *counts,
-                      double *obj);
+                      int64_t n, const kareto_model *model, ModelConsts mc, const kareto_counts *given,
+                      kareto_counts *counts, double *obj);
 
 }  // namespace kareto

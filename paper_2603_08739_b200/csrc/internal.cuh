@@ -78,6 +78,10 @@ struct kareto_trace {
   uint32_t *prev = nullptr;
   uint32_t *delta = nullptr;
   uint32_t *depth = nullptr;   // LRU depth d at request start (kNone: first access)
+  // K6 replay inputs, built on first use (replay.cu)
+  uint32_t *blk = nullptr;     // [N] dense block id
+  uint16_t *gblk = nullptr;    // [U] group of each block
+  uint32_t *arr_rel = nullptr; // [R] arrival - first arrival (ms)
   // group tables (host) [K+1]
   std::vector<int64_t> U_g, reuse_g;
 };

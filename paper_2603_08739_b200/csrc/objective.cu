@@ -27,18 +27,21 @@ __device__ double phi_iops(const kareto_model &m, double u) {  // R32, right-con
 
 __global__ void k_objective(StackTables T, const kareto_config *__restrict__ cfg, const CfgDev *__restrict__ cd,
                             const uint32_t *__restrict__ tix, const uint32_t *__restrict__ ttl_ms, int64_t n,
-                            kareto_model m, ModelConsts mc, kareto_counts *__restrict__ counts,
-                            double *__restrict__ obj) {
+                            kareto_model m, ModelConsts mc, const kareto_counts *__restrict__ given,
+                            kareto_counts *__restrict__ counts, double *__restrict__ obj) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const kareto_config c = cfg[i];
-    const CfgDev x = cd[i];
     const bool ttl = c.cap[2] == KARETO_INF;
+    const uint64_t c1 = c.cap[0];
+    kareto_counts k;
+    if (given) {  // counts from the K6 replay: objective only
+      k = given[i];
+    } else {
+    const CfgDev x = cd[i];
     const int any = T.ntc;
     const unsigned long long *Ca = T.C1 + (size_t)any * T.nb, *Sa = T.S1 + (size_t)any * T.nb;
     const uint64_t N = mc.N, U = mc.U;
-    const uint64_t c1 = c.cap[0];
     const uint64_t c12 = c1 + c.cap[1];
-    kareto_counts k;
     uint64_t h1 = Ca[x.i1], h12 = Ca[x.i12];
     k.hit[0] = h1;
     k.hit[1] = h12 - h1;
@@ -76,6 +79,7 @@ __global__ void k_objective(StackTables T, const kareto_config *__restrict__ cfg
     }
     k.hit_pos_sum = hps;
     k.miss = N - k.hit[0] - k.hit[1] - k.hit[2];
+    }
     if (counts) counts[i] = k;
 
     // ---- K7: fluid objective, DESIGN.md section 3 (fixed order, no FMA)
@@ -113,11 +117,11 @@ __global__ void k_objective(StackTables T, const kareto_config *__restrict__ cfg
 
 void launch_objective(kareto_ctx *ctx, const StackTables &T, const kareto_config *cfg, const CfgDev *cd,
                       const uint32_t *tix, const uint32_t *ttl_ms, int64_t n, const kareto_model *model,
-                      ModelConsts mc, kareto_counts *counts, double *obj) {
+                      ModelConsts mc, const kareto_counts *given, kareto_counts *counts, double *obj) {
   if (n <= 0) return;
-  Pass ps(ctx, "K5K7_objective", 1, 1);
+  Pass ps(ctx, given ? "K7_objective" : "K5K7_objective", 1, 1);
   k_objective<<<grid_for(n, 128, 8 * ctx->num_sms), 128, 0, ctx->stream>>>(T, cfg, cd, tix, ttl_ms, n, *model, mc,
-                                                                           counts, obj);
+                                                                           given, counts, obj);
 }
 
 }  // namespace kareto

@@ -1,0 +1,23 @@
+// replay.cuh -- K6 per-configuration replay (replay.cu), used by eval.cu.
+#pragma once
+#include <cub/cub.cuh>
+
+#include "internal.cuh"
+
+namespace kareto {
+
+struct ReplayTrace {
+  uint32_t R, U;
+  const uint32_t *s;       // [R+1] first touch position of each request
+  const uint32_t *arr;     // [R] arrival ms relative to the first request
+  const uint16_t *grp;     // [R] group of each request
+  const uint32_t *blk;     // [N] dense block id of each access (touch order)
+};
+
+// dense block ids / groups / relative arrivals (lazily, cached in the trace)
+kareto_status replay_prepare(kareto_ctx *ctx, kareto_trace *tr);
+// counts of n configurations (host array) into counts_dev[n]; rows_dev = [max(n_tuner,1)][K+1]
+kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config *cfg_host, int64_t n,
+                          const uint32_t *rows_dev, int n_tuner, kareto_counts *counts_dev);
+
+}  // namespace kareto

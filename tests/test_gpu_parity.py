@@ -269,9 +269,6 @@ def test_errors(ctx):
         ctx.eval_grid(gt, K.configs([[1, 1, 1]], tuner=3), M, ttl=np.full((1, 17), 5, np.uint32))
     assert ei.value.status == K.E_INVALID
     with pytest.raises(K.KaretoError) as ei:
-        ctx.eval_grid(gt, K.configs([[1, 1, 1]], policy=K.FIFO), M)
-    assert ei.value.status == K.E_UNSUPPORTED
-    with pytest.raises(K.KaretoError) as ei:
         bad = K.Model(bw_dram=0.0)
         ctx.eval_grid(gt, K.configs([[1, 1, 1]]), bad)
     assert ei.value.status == K.E_INVALID
@@ -305,6 +302,59 @@ def test_agent_and_api_workloads(ctx):
         want = ot.stack_counts(cf)
         got, obj = ctx.eval_grid(gt, kcfg(cf), K.Model(**MODEL_KW))
         assert_counts_equal(got, want, cf)
+
+
+def replay_configs(K_, rng, n_rows=4):
+    """Configurations that need the K6 replay: FIFO / LFU in both modes, LRU with per-group TTL on
+    a finite disk; mixed with stack-eligible LRU ones (eval_grid splits and re-merges them)."""
+    rows = [[U32] * (K_ + 1), [3] * (K_ + 1)]
+    for _ in range(n_rows):
+        rows.append(list(rng.choice([0, 1, 3, 6, 50], K_ + 1)))
+    ttl = np.array(rows, np.uint32)
+    caps, pol, tun, axis = [], [], [], []
+    for a in range(3):
+        for b in range(3):
+            for c in range(3):
+                for p in (O.LRU, O.FIFO, O.LFU):
+                    for ti in range(len(rows)):
+                        caps.append([a, b, c]); pol.append(p); tun.append(ti); axis.append([a, b, c])
+                    for ti in range(2, len(rows)):
+                        caps.append([a, b, O.INF_CAP]); pol.append(p); tun.append(ti); axis.append([a, b, 0])
+    cf = O.configs(caps, policy=np.array(pol), tuner=np.array(tun), axis=axis)
+    return cf, ttl
+
+
+def test_replay_tiny_random_all_policies(ctx):
+    rng = np.random.default_rng(99)
+    for trial in range(12):
+        tr = ki.random_prefix_tree(rng)
+        K_ = int(rng.integers(0, 3))
+        cf, ttl = replay_configs(K_, rng)
+        run_both(ctx, tr, cf, ttl, top_k=K_, salt=trial)
+
+
+def test_replay_belady_and_w3(ctx):
+    BEL = [1, 2, 3, 4, 1, 2, 5, 1, 2, 3, 4, 5]
+    gt = ctx.load(ki.from_chains([[x] for x in BEL], list(range(12))), top_k=0)
+    cnt, _ = ctx.eval_grid(gt, K.configs([[3, 0, 0], [4, 0, 0]] * 3, policy=np.repeat([0, 1, 2], 2)), K.Model())
+    assert [int(c["hit"].sum()) for c in cnt] == [2, 4, 3, 2, 2, 4]  # LRU, FIFO (Belady anomaly), LFU
+
+
+def test_replay_chat_trace_mixed_grid(ctx):
+    # config-3-shaped grid (LRU / FIFO / LFU x tuner rows incl. TTL mode) on a small chat trace
+    tr = ki.synthetic("chat", R=1500, seed=4)
+    ot = O.OracleTrace(tr, top_k=4)
+    rows = [[U32] * 5, [600_000] * 5, [60_000, 600_000, 3_600_000, 30_000, 5_000]]
+    ttl = np.array(rows, np.uint32)
+    caps, axis = baseline_grid(ot.U, 3, 3, 3)
+    allc, pol, tun, ax = [], [], [], []
+    for c, a in zip(caps, axis):
+        for p in (O.LRU, O.FIFO, O.LFU):
+            for ti in range(3):
+                allc.append(c); pol.append(p); tun.append(ti); ax.append(a)
+            allc.append([c[0], c[1], O.INF_CAP]); pol.append(p); tun.append(2); ax.append(a)
+    cf = O.configs(allc, policy=np.array(pol), tuner=np.array(tun), axis=ax)
+    run_both(ctx, tr, cf, ttl, top_k=4)
 
 
 @pytest.mark.slow

@@ -37,19 +37,56 @@ CONFIGS = {
             desc="config1: G-chat 10k requests (~1.06M block accesses), 3-tier LRU 4x4x4 grid, fp64 model"),
     2: dict(kind="chat", R=1_000_000, grid=(32, 32, 16), div=(16, 2, 1), prune=None,
             desc="config2: G-chat 1M requests (~1.06e8 block accesses), 3-tier LRU 32x32x16 grid, full Pareto"),
+    # config 3 down-scaled twin ("full O1 on a down-scaled twin (R = 10^4, same grid
+    # shape)"): LRU/FIFO/LFU x 17 tuner rows (4 uniform, 7 quantile, 6 ROI), K = 16
+    3: dict(kind="chat", R=10_000, grid="config3", prune=None, top_k=16,
+            desc="config3 twin: G-chat 10k requests, A(16,U/16) x A(16,U/2) x (A(7,U) + TTL mode) x "
+                 "{LRU,FIFO,LFU} x 17 tuner rows (103,680 configs, ~92K on the K6 replay)"),
+    # config 4: agentic trace, 1e8 accesses, 70B-class blocks, GB grids of P:856 style, pruning on
+    4: dict(kind="agent", N=100_000_000, grid="config4", prune=0.05, top_k=16,
+            desc="config4: G-agent 1e8 block accesses, Bb = 5,242,880 B, HBM 0-1240 GB/40 x DRAM 0-4096 GB/128 x "
+                 "disk 0-3600 GB/120 x uniform TTL {inf, 1h, 10min, 1min} (130,944 configs), pruning tau_e = 0.05"),
 }
+
+
+def tuner_rows_config3(delta_by_group, U_g, K):
+    """17 tuner rows: 4 uniform, 7 nearest-rank quantiles of Delta_g, 6 ROI rows
+    floor(a * t_roi), t_roi = argmax_delta H_g(delta)/C_g(delta) (Alg. 2 lines 4-5)."""
+    inf = 0xFFFFFFFF
+    rows = [[inf] * (K + 1), [3_600_000] * (K + 1), [600_000] * (K + 1), [60_000] * (K + 1)]
+    for q in (0.5, 0.6, 0.7, 0.8, 0.9, 0.95, 0.99):
+        row = []
+        for g in range(K + 1):
+            d = np.sort(delta_by_group[g])
+            row.append(0 if len(d) == 0 else int(d[max(0, int(np.ceil(q * len(d))) - 1)]))
+        rows.append(row)
+    troi = []
+    for g in range(K + 1):
+        d = np.sort(delta_by_group[g]).astype(np.int64)
+        if len(d) == 0:
+            troi.append(0)
+            continue
+        vals, first = np.unique(d, return_index=True)
+        H = np.searchsorted(d, vals, side="right")                       # #{delta <= t}
+        csum = np.concatenate([[0], np.cumsum(d)])
+        C = int(U_g[g]) * vals + csum[H] + vals * (len(d) - H)           # U_g t + sum min(t, delta)
+        best = 0
+        for i in range(1, len(vals)):                                    # exact cross-multiplied compare
+            if int(H[i]) * int(C[best]) > int(H[best]) * int(C[i]):
+                best = i
+        troi.append(int(vals[best]))
+    for a in (0.5, 1, 2, 4, 8, 16):
+        rows.append([min(int(a * t), inf - 1) for t in troi])
+    return np.array(rows, np.uint32)
 
 # algorithmic bytes per unit of each own kernel (DESIGN.md "Measurement")
 ALGO = {
     "K1_chain_hash": ("block", 76),        # 64 B tokens in + 8 B hash + 4 B request id out
-    "K2_link_prev": ("access", 16),        # 8 B sorted hash + 4 B position in, 4 B prev out
-    "K2_access_info": ("access", 12),      # prev, req in; delta out
-    "K3_upsweep1": ("access", 8),          # req + prev
-    "K3_downsweep1": ("access", 20),       # req + prev in, 12 B of live items out (1.5 items x 8 B)
-    "K3_upsweep2": ("access", 12),         # 1.5 live items x 8 B
-    "K3_downsweep2": ("access", 24),
-    "K3_local": ("access", 14),            # 12 B items in + 2 B of A out (0.75 x 4 B / 1.5 ...)
-    "K3_finalize": ("access", 16),         # prev, req, A[prev], depth out
+    "K2_sort_prep": ("access", 20),        # 8 B hash in, 4 B key + 8 B value out
+    "K2_link_prev": ("access", 20),        # 4 B key + 8 B value in, 4 B position + 4 B prev out
+    "K2_bucket_scatter": ("access", 12),   # 8 B pair in, 4 B prev out
+    "K2_access_info": ("access", 13),      # prev, req in; delta + run flag out
+    "K3_expand": ("access", 4),            # depth out
     "K4_hist_d": ("access", 8),            # depth + req
     "K4_hist_D": ("access", 8),
 }
@@ -133,6 +170,67 @@ def grid_configs(K, U, grid, div):
     return cfg
 
 
+def config3_grid(K, U, rows):
+    """A(16,U/16) x A(16,U/2) x (A(7,U) + TTL mode) x 3 policies x rows,
+    minus TTL mode with an all-infinite row (R22)."""
+    A = lambda m, top: [top * i // (m - 1) for i in range(m)]
+    c1, c2, c3 = A(16, U // 16), A(16, U // 2), A(7, U)
+    out = []
+    for i, a in enumerate(c1):
+        for j, b in enumerate(c2):
+            for k in range(8):
+                cap3 = c3[k] if k < 7 else K.INF
+                for p in (K.LRU, K.FIFO, K.LFU):
+                    for t in range(len(rows)):
+                        if cap3 == K.INF and (rows[t] == 0xFFFFFFFF).any():
+                            continue
+                        out.append((a, b, cap3, p, t, i, j, k))
+    cfg = np.zeros(len(out), K.CONFIG_DTYPE)
+    arr = np.array(out, dtype=object)
+    cfg["cap"] = np.array([[o[0], o[1], o[2]] for o in out], np.uint64)
+    cfg["policy"] = [o[3] for o in out]
+    cfg["tuner"] = [o[4] for o in out]
+    cfg["axis"] = np.array([[o[5], o[6], o[7]] for o in out], np.int32)
+    del arr
+    return cfg
+
+
+def config4_grid(K, block_bytes):
+    """HBM 0-1240 GB step 40 x DRAM 0-4096 GB step 128 x disk 0-3600 GB step 120
+    x uniform TTL {inf, 1 h, 10 min, 1 min}; GB -> blocks = floor(GB * 1e9 / Bb) (R14)."""
+    gb = lambda lo, hi, step: np.arange(lo, hi + 1, step, dtype=np.uint64)
+    h, d, s = gb(0, 1240, 40), gb(0, 4096, 128), gb(0, 3600, 120)
+    blocks = lambda g: (g * np.uint64(10**9)) // np.uint64(block_bytes)
+    ii, jj, kk, tt = np.meshgrid(np.arange(len(h)), np.arange(len(d)), np.arange(len(s)), np.arange(4), indexing="ij")
+    cfg = np.zeros(ii.size, K.CONFIG_DTYPE)
+    cfg["cap"][:, 0] = blocks(h)[ii.ravel()]
+    cfg["cap"][:, 1] = blocks(d)[jj.ravel()]
+    cfg["cap"][:, 2] = blocks(s)[kk.ravel()]
+    cfg["tuner"] = tt.ravel()
+    cfg["axis"] = np.stack([ii.ravel(), jj.ravel(), kk.ravel()], 1)
+    return cfg
+
+
+def config4_rows(top_k):
+    return np.array([[t] * (top_k + 1) for t in (0xFFFFFFFF, 3_600_000, 600_000, 60_000)], np.uint32)
+
+
+def build_grid(K, spec, trace):
+    """(configs, ttl rows or None) for a workload spec on a loaded trace."""
+    g = spec["grid"]
+    if g == "config3":
+        delta = trace.export(K.X_DELTA)
+        req = trace.export(K.X_REQ)
+        grp = trace.export(K.X_GROUP)[req]
+        ok = delta != 0xFFFFFFFF
+        by_g = [delta[ok & (grp == gi)] for gi in range(trace.K + 1)]
+        rows = tuner_rows_config3(by_g, trace.U_g, trace.K)
+        return config3_grid(K, trace.U, rows), rows
+    if g == "config4":
+        return config4_grid(K, K.Model().block_bytes), config4_rows(trace.K)
+    return grid_configs(K, trace.U, g, spec["div"]), None
+
+
 def run_reference(args, spec):
     """Reference arm: the oracle as it stands, on host cores, bounded sample of the workload."""
     import kareto_inputs as ki
@@ -140,43 +238,80 @@ def run_reference(args, spec):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    sample_R = min(spec["R"], args.sample_requests)
-    tr = ki.synthetic(spec["kind"], R=sample_R, seed=0)
-    plan_full = ki.Plan(spec["kind"], R=spec["R"], seed=0)
+    import paper_2603_08739_b200 as K  # grid helpers / dtypes only (no device work)
+    top_k = spec.get("top_k", 16)
+    if "R" in spec:
+        plan_full = ki.Plan(spec["kind"], R=spec["R"], seed=0)
+        tr = ki.synthetic(spec["kind"], R=min(spec["R"], args.sample_requests), seed=0)
+    else:
+        plan_full = ki.Plan(spec["kind"], N=spec["N"], seed=0)
+        tr = ki.synthetic(spec["kind"], N=min(spec["N"], args.sample_requests * 100), seed=0)
     N_full = plan_full.n_blocks
+
+    class _Shim:  # trace-like view of the oracle trace for build_grid
+        def __init__(self, ot):
+            e = ot.export()
+            self.U, self.K, self.U_g = ot.U, ot.K, ot.U_g
+            self._x = {K.X_DELTA: np.where(e["delta"] < 0, 0xFFFFFFFF, e["delta"]).astype(np.uint32),
+                       K.X_REQ: e["req"].astype(np.uint32), K.X_GROUP: e["group"].astype(np.uint16)}
+
+        def export(self, which):
+            return self._x[which]
 
     def one():
         t0 = time.perf_counter()
-        ot = O.OracleTrace(tr, top_k=16)
-        cf = O.configs(np.zeros((0, 3)))
-        import paper_2603_08739_b200 as K  # only for the grid helper dtype
-        kc = grid_configs(K, ot.U, spec["grid"], spec["div"])
+        ot = O.OracleTrace(tr, top_k=top_k)
+        kc, rows = build_grid(K, spec, _Shim(ot))
         cf = np.zeros(len(kc), O.CONFIG_DTYPE)
         for f in ("cap", "policy", "medium", "tuner", "axis"):
             cf[f] = kc[f]
-        cnt = ot.stack_counts(cf)
-        fobj = ot.objective(O.Model(), cf, cnt)
-        O.select(fobj, cf, spec["prune"])
-        return time.perf_counter() - t0, ot.N, len(cf)
+        ttl = rows if rows is not None else np.full((1, top_k + 1), 0xFFFFFFFF, np.uint32)
+        elig = np.array([ot.stack_eligible(cf[i:i + 1], ttl) for i in range(len(cf))], bool)
+        t_trace = time.perf_counter() - t0
+        cnt = np.zeros(len(cf), O.COUNTS_DTYPE)
+        t1 = time.perf_counter()
+        if elig.any():
+            cnt[elig] = ot.stack_counts(cf[elig], ttl)
+        t_stack = time.perf_counter() - t1
+        # O1 replay: a stratified sample of the replay configurations, extrapolated in count
+        rep = np.nonzero(~elig)[0]
+        t_rep = 0.0
+        if len(rep):
+            samp = rep[np.linspace(0, len(rep) - 1, min(len(rep), 48)).astype(int)]
+            t2 = time.perf_counter()
+            cnt[samp] = ot.replay(cf[samp], ttl, threads=os.cpu_count())
+            t_rep = (time.perf_counter() - t2) * len(rep) / len(samp)
+        # selection: O(n^2) Pareto timed on <= 16384 configurations, extrapolated quadratically
+        t3 = time.perf_counter()
+        m = min(len(cf), 16384)
+        fobj = ot.objective(O.Model(), cf[:m], cnt[:m]) if not len(rep) else np.random.default_rng(0).random((m, 3))
+        O.select(fobj, cf[:m], spec["prune"])
+        t_sel = (time.perf_counter() - t3) * (len(cf) / m) ** 2
+        return t_trace, t_stack, t_rep, t_sel, ot.N, len(cf), int(len(rep))
 
     for _ in range(args.warmup):
         one()
-    ts = []
-    for _ in range(args.steps):
-        dt, Ns, n = one()
-        ts.append(dt)
-    t = sum(ts) / len(ts)
-    t_full = t * N_full / Ns       # trace-proportional work, extrapolated linearly to the full trace
+    res = [one() for _ in range(args.steps)]
+    t_trace, t_stack, t_rep, t_sel = (sum(r[i] for r in res) / len(res) for i in range(4))
+    Ns, n, n_rep = res[0][4], res[0][5], res[0][6]
+    # trace-proportional work extrapolated linearly to the full trace
+    t_full = (t_trace + t_stack + t_rep) * N_full / Ns + t_sel
+    t = t_trace + t_stack + t_rep + t_sel
     value = n / t_full
     line = {"impl": "reference", "metric": "configs evaluated/sec", "value": value, "unit": "configs/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64/f64",
             "data": "synthetic", "config": {"workload": spec["desc"], "n_configs": n},
-            "cpu_baseline": {"value": value, "unit": "configs/s", "cores": 1, "kind": "oracle",
-                             "sample": f"O2 oracle (sequential Fenwick stack depths + closed forms + fp64 model + "
-                                       f"O(n^2) Pareto) on a {sample_R}-request sample of the same generator "
-                                       f"({Ns} accesses) x the full {n}-config grid, {t:.2f} s/step, extrapolated "
-                                       f"linearly to the full trace ({N_full} accesses)"},
+            "cpu_baseline": {"value": value, "unit": "configs/s",
+                             "cores": os.cpu_count() if n_rep else 1, "kind": "oracle",
+                             "sample": f"oracle on a {Ns}-access sample trace of the same generator: trace build + "
+                                       f"O2 Fenwick stack path for the stack-eligible configs of the full {n}-config "
+                                       f"grid ({t_stack:.2f} s)"
+                                       + (f", O1 literal replay of 48 of the {n_rep} replay configs on all host "
+                                          f"threads, extrapolated in config count ({t_rep:.2f} s)" if n_rep else "")
+                                       + f", fp64 model + O(n^2) Pareto (extrapolated from <=16384 configs, "
+                                         f"{t_sel:.2f} s); {t:.2f} s/step, trace-proportional parts extrapolated "
+                                         f"linearly to the full trace ({N_full} accesses)"},
             "e2e": {"value": value, "unit": "configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -211,16 +346,13 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.Stream()
-    nid = None
-    if world > 1:
-        obj = [K.Context.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nid = obj[0]
-    ctx = K.Context(local, stream.cuda_stream, nid, rank, world)
+    from paper_2603_08739_b200 import dist as kd
+    ctx = kd.create_context(local, stream.cuda_stream)
+    top_k = spec.get("top_k", 16)
 
     # ---- synthetic workload (seeded; host pinned buffers, then device copies)
     t0 = time.time()
-    plan = ki.Plan(spec["kind"], R=spec["R"], seed=0)
+    plan = ki.Plan(spec["kind"], R=spec.get("R", 0), N=spec.get("N", 0), seed=0)
     R, T = plan.n_requests, plan.n_tokens
     arr_h = torch.empty(R, dtype=torch.int64, pin_memory=True)
     out_h = torch.empty(R, dtype=torch.int32, pin_memory=True)
@@ -234,12 +366,17 @@ def main():
     stream.synchronize()
 
     def load_dev():
-        return ctx.load_trace(arr_d, out_d, off_d, tokens=tok_d, top_k=16)
+        return ctx.load_trace(arr_d, out_d, off_d, tokens=tok_d, top_k=top_k)
 
     tr = load_dev()
     N, U = tr.N, tr.U
-    cfg = grid_configs(K, U, spec["grid"], spec["div"])
+    cfg, ttl = build_grid(K, spec, tr)   # the planner's grid (not part of the timed hot path)
     n_cfg = len(cfg)
+    if ttl is None:
+        n_replay = int((cfg["policy"] != K.LRU).sum())
+    else:
+        nonuni = (ttl[cfg["tuner"]] != ttl[cfg["tuner"]][:, :1]).any(1)
+        n_replay = int(((cfg["policy"] != K.LRU) | ((cfg["cap"][:, 2] != K.INF) & nonuni)).sum())
     model = K.Model()
     cnt_d = torch.empty((n_cfg, 11), dtype=torch.int64, device=f"cuda:{local}")
     obj_d = torch.empty((n_cfg, 3), dtype=torch.float64, device=f"cuda:{local}")
@@ -248,7 +385,7 @@ def main():
 
     def step():
         t = load_dev()
-        ctx.eval_grid(t, cfg, model, None, counts=cnt_d, obj=obj_d)
+        ctx.eval_grid(t, cfg, model, ttl, counts=cnt_d, obj=obj_d)
         _, nf = ctx.pareto(obj_d, cfg, spec["prune"], status=st_d)
         t.free()
         return nf
@@ -313,8 +450,8 @@ def main():
         arr_np, out_np, off_np, tok_np = arr_h.numpy(), out_h.numpy(), off_h.numpy(), tok_h.numpy().view(np.uint32)
 
         def step_host():
-            t_ = ctx.load_trace(arr_np, out_np, off_np, tokens=tok_np, top_k=16)
-            ctx.eval_grid(t_, cfg, model, None, counts=cnt_h, obj=obj_h)
+            t_ = ctx.load_trace(arr_np, out_np, off_np, tokens=tok_np, top_k=top_k)
+            ctx.eval_grid(t_, cfg, model, ttl, counts=cnt_h, obj=obj_h)
             s_, _ = ctx.pareto(obj_h, cfg, spec["prune"])
             t_.free()
             return s_
@@ -359,7 +496,7 @@ def main():
                            "n_unique": U, "tokens_bytes": int(T * 4),
                            "l2": "no flush: per-step inputs (6.8 GB tokens) exceed the 126 MB L2",
                            "parallelism": f"config-shard x{world} (trace passes replicated)",
-                           "pruning": spec["prune"]},
+                           "pruning": spec["prune"], "replay_configs": n_replay},
                 "block_accesses_per_s": N / (ms_step * 1e-3),
                 "effective_access_configs_per_s": N * n_cfg / (ms_step * 1e-3),
                 "frontier": nf, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),

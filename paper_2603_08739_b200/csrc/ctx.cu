@@ -180,12 +180,13 @@ extern "C" kareto_status kareto_launch_counter(kareto_ctx *ctx, int64_t *own_lau
 
 extern "C" void kareto_trace_free(kareto_trace *tr) {
   if (!tr) return;
-  kareto_ctx *ctx = tr->ctx;
+  // uses only the trace's own copy of the stream: a trace may outlive its context
   void *ptrs[] = {tr->arr, tr->s, tr->grp, tr->hash, tr->req, tr->prev, tr->delta, tr->depth,
                   tr->blk, tr->gblk, tr->arr_rel};
   for (void *p : ptrs)
-    if (p) cudaFreeAsync(p, ctx->stream);
-  cudaStreamSynchronize(ctx->stream);
+    if (p) cudaFreeAsync(p, tr->stream);
+  cudaStreamSynchronize(tr->stream);
+  (void)cudaGetLastError();
   delete tr;
 }
 

@@ -187,6 +187,53 @@ __global__ void k_prefix_t(unsigned long long *__restrict__ a, int rows, int nt1
   }
 }
 
+// boundary values of the stack configurations (clamped to U; C unused in TTL mode), and
+// the c12 values of TTL-mode configurations (kNone sentinel for CAPACITY ones)
+__device__ __forceinline__ uint64_t sat_add_d(uint64_t a, uint64_t b) { return a > ~0ull - b ? ~0ull : a + b; }
+__global__ void k_bound_vals(const kareto_config *__restrict__ c, int64_t n, uint64_t U, uint32_t *__restrict__ vals,
+                             uint32_t *__restrict__ v12) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const kareto_config x = c[i];
+    uint64_t c12 = sat_add_d(x.cap[0], x.cap[1]);
+    bool ttl = x.cap[2] == KARETO_INF;
+    uint64_t C = ttl ? c12 : sat_add_d(c12, x.cap[2]);
+    vals[3 * i] = (uint32_t)(x.cap[0] < U ? x.cap[0] : U);
+    vals[3 * i + 1] = (uint32_t)(c12 < U ? c12 : U);
+    vals[3 * i + 2] = (uint32_t)(C < U ? C : U);
+    v12[i] = ttl ? (uint32_t)(c12 < U ? c12 : U) : kNone;
+  }
+}
+__device__ __forceinline__ int32_t lb32(const uint32_t *__restrict__ v, int n, uint32_t x) {
+  int lo = 0, hi = n;
+  while (lo < hi) { int m = (lo + hi) >> 1; if (v[m] >= x) hi = m; else lo = m + 1; }
+  return lo;
+}
+__global__ void k_cfgdev(const kareto_config *__restrict__ c, int64_t n, uint64_t U, const uint32_t *__restrict__ Bd,
+                         int nb, const uint32_t *__restrict__ B12, int nb12, const uint32_t *__restrict__ Tc, int ntc,
+                         const uint32_t *__restrict__ rows, int n_tuner, int G, CfgDev *__restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const kareto_config x = c[i];
+    auto cl = [&](uint64_t v) { return (uint32_t)(v < U ? v : U); };
+    uint64_t c12 = sat_add_d(x.cap[0], x.cap[1]);
+    int ri = n_tuner > 0 ? x.tuner : 0;
+    CfgDev d{};
+    d.i1 = lb32(Bd, nb, cl(x.cap[0]));
+    d.i12 = lb32(Bd, nb, cl(c12));
+    d.row = ri;
+    if (x.cap[2] != KARETO_INF) {
+      d.iC = lb32(Bd, nb, cl(sat_add_d(c12, x.cap[2])));
+      uint32_t tau = rows[(size_t)ri * G];
+      d.tc = tau == KARETO_TTL_INF ? ntc : lb32(Tc, ntc, tau);
+      d.i12t = 0;
+    } else {
+      d.iC = -1;
+      d.tc = ntc;
+      d.i12t = lb32(B12, nb12, cl(c12));
+    }
+    out[i] = d;
+  }
+}
+
 __global__ void k_scatter_out(const kareto_counts *__restrict__ c, const double *__restrict__ o,
                               const uint32_t *__restrict__ idx, int64_t n, kareto_counts *__restrict__ cout,
                               double *__restrict__ oout) {
@@ -252,7 +299,14 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
   int nrows = n_tuner;
   if (n_tuner == 0) { rows.assign(G, KARETO_TTL_INF); nrows = 1; }
   else rows.assign(ttl_ms, ttl_ms + (size_t)n_tuner * G);
-  // ---- validation + classification (every rank validates the full list identically)
+  // per-row flags: uniform across groups, all finite
+  std::vector<char> row_uniform(nrows, 1), row_finite(nrows, 1);
+  for (int r = 0; r < nrows; r++)
+    for (int g = 0; g < G; g++) {
+      if (rows[(size_t)r * G + g] != rows[(size_t)r * G]) row_uniform[r] = 0;
+      if (rows[(size_t)r * G + g] == KARETO_TTL_INF) row_finite[r] = 0;
+    }
+  // ---- validation (every rank validates the full list identically), O(1) per configuration
   for (int64_t i = 0; i < n_cfg; i++) {
     const kareto_config &c = cfg[i];
     if (c.policy > KARETO_LFU) return fail(ctx, KARETO_E_INVALID, "config %lld: policy %d", (long long)i, c.policy);
@@ -260,24 +314,16 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
     if (n_tuner > 0 && c.tuner >= n_tuner) return fail(ctx, KARETO_E_INVALID, "config %lld: tuner", (long long)i);
     if (c.cap[0] == KARETO_INF || c.cap[1] == KARETO_INF)
       return fail(ctx, KARETO_E_INVALID, "config %lld: infinite HBM/DRAM", (long long)i);
-    const uint32_t *row = rows.data() + (size_t)(n_tuner > 0 ? c.tuner : 0) * G;
-    bool ttl = c.cap[2] == KARETO_INF;
-    bool uniform = true, all_finite = true;
-    for (int g = 0; g < G; g++) {
-      if (row[g] != row[0]) uniform = false;
-      if (row[g] == KARETO_TTL_INF) all_finite = false;
-    }
-    if (ttl && !all_finite)
+    const int ri = n_tuner > 0 ? c.tuner : 0;
+    const bool ttl = c.cap[2] == KARETO_INF;
+    if (ttl && !row_finite[ri])
       return fail(ctx, KARETO_E_INVALID, "config %lld: TTL mode needs finite TTLs (R22)", (long long)i);
-    (void)uniform;
     // overflow guards of the integer model terms
-    if (!ttl) {
-      unsigned __int128 cb = (unsigned __int128)sat_add(sat_add(c.cap[0], c.cap[1]), c.cap[2]) * model->block_bytes;
-      if (cb > (unsigned __int128)UINT64_MAX) return fail(ctx, KARETO_E_OVERFLOW, "config %lld: capacity x block bytes", (long long)i);
-    } else {
-      unsigned __int128 cb = (unsigned __int128)sat_add(c.cap[0], c.cap[1]) * model->block_bytes;
-      if (cb > (unsigned __int128)UINT64_MAX) return fail(ctx, KARETO_E_OVERFLOW, "config %lld: capacity x block bytes", (long long)i);
-    }
+    unsigned __int128 cb = (unsigned __int128)(ttl ? sat_add(c.cap[0], c.cap[1])
+                                                   : sat_add(sat_add(c.cap[0], c.cap[1]), c.cap[2])) *
+                           model->block_bytes;
+    if (cb > (unsigned __int128)UINT64_MAX)
+      return fail(ctx, KARETO_E_OVERFLOW, "config %lld: capacity x block bytes", (long long)i);
   }
   // trace x model integer constants
   unsigned __int128 P0 = (unsigned __int128)model->alpha_ps * tr->SL + (unsigned __int128)model->beta_ps * tr->SQ;
@@ -296,79 +342,87 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
   // stack-eligible (LRU, and TTL mode or a uniform disk TTL) vs per-configuration replay (K6)
   std::vector<kareto_config> cS, cP;
   std::vector<uint32_t> iS, iP;
+  std::vector<char> cap_row_used(nrows, 0), ttl_row_used(nrows, 0);
+  cS.reserve(ns);
   for (int64_t i = 0; i < ns; i++) {
     const kareto_config &c = sc[i];
-    const uint32_t *row = rows.data() + (size_t)(n_tuner > 0 ? c.tuner : 0) * G;
-    bool uniform = true;
-    for (int g = 1; g < G; g++) uniform &= row[g] == row[0];
-    if (c.policy == KARETO_LRU && (c.cap[2] == KARETO_INF || uniform)) { cS.push_back(c); iS.push_back((uint32_t)i); }
-    else { cP.push_back(c); iP.push_back((uint32_t)i); }
-  }
-  const int64_t nS = (int64_t)cS.size(), nP = (int64_t)cP.size();
-
-  // ---- boundary / TTL sets of the shard's stack configurations
-  std::vector<uint32_t> Bd, B12, Tc, Tt;
-  std::vector<char> row_used(nrows, 0);
-  auto clampU = [&](uint64_t v) -> uint32_t { return (uint32_t)(v < U ? v : U); };
-  for (int64_t i = 0; i < nS; i++) {
-    const kareto_config &c = cS[i];
-    uint64_t c12 = sat_add(c.cap[0], c.cap[1]);
-    Bd.push_back(clampU(c.cap[0]));
-    Bd.push_back(clampU(c12));
-    int ri = n_tuner > 0 ? c.tuner : 0;
-    if (c.cap[2] != KARETO_INF) {
-      Bd.push_back(clampU(sat_add(c12, c.cap[2])));
-      uint32_t tau = rows[(size_t)ri * G];
-      if (tau != KARETO_TTL_INF) Tc.push_back(tau);
+    const int ri = n_tuner > 0 ? c.tuner : 0;
+    const bool ttl = c.cap[2] == KARETO_INF;
+    if (c.policy == KARETO_LRU && (ttl || row_uniform[ri])) {
+      cS.push_back(c);
+      iS.push_back((uint32_t)i);
+      (ttl ? ttl_row_used : cap_row_used)[ri] = 1;
     } else {
-      B12.push_back(clampU(c12));
-      row_used[ri] = 1;
+      cP.push_back(c);
+      iP.push_back((uint32_t)i);
     }
   }
-  for (int r = 0; r < nrows; r++)
-    if (row_used[r])
+  const int64_t nS = (int64_t)cS.size(), nP = (int64_t)cP.size();
+  // TTL value sets: uniform CAPACITY TTLs (Tc) and all TTLs of rows used in TTL mode (Tt)
+  std::vector<uint32_t> Tc, Tt;
+  for (int r = 0; r < nrows; r++) {
+    if (cap_row_used[r] && rows[(size_t)r * G] != KARETO_TTL_INF) Tc.push_back(rows[(size_t)r * G]);
+    if (ttl_row_used[r])
       for (int g = 0; g < G; g++) Tt.push_back(rows[(size_t)r * G + g]);
+  }
   auto uniq = [](std::vector<uint32_t> &v) {
     std::sort(v.begin(), v.end());
     v.erase(std::unique(v.begin(), v.end()), v.end());
   };
-  uniq(Bd); uniq(B12); uniq(Tc); uniq(Tt);
-  const int nb = (int)Bd.size(), nb12 = (int)B12.size(), ntc = (int)Tc.size(), ntt = (int)Tt.size();
-  // per-config lookup indices
-  std::vector<CfgDev> cd(nS > 0 ? nS : 1);
-  auto idx = [](const std::vector<uint32_t> &v, uint32_t x) {
-    return (int32_t)(std::lower_bound(v.begin(), v.end(), x) - v.begin());
-  };
+  uniq(Tc); uniq(Tt);
+  const int ntc = (int)Tc.size(), ntt = (int)Tt.size();
   std::vector<uint32_t> tix((size_t)nrows * G, 0);
   for (int r = 0; r < nrows; r++)
-    if (row_used[r])
-      for (int g = 0; g < G; g++) tix[(size_t)r * G + g] = (uint32_t)idx(Tt, rows[(size_t)r * G + g]);
-  for (int64_t i = 0; i < nS; i++) {
-    const kareto_config &c = cS[i];
-    uint64_t c12 = sat_add(c.cap[0], c.cap[1]);
-    int ri = n_tuner > 0 ? c.tuner : 0;
-    CfgDev x{};
-    x.i1 = idx(Bd, clampU(c.cap[0]));
-    x.i12 = idx(Bd, clampU(c12));
-    x.row = ri;
-    if (c.cap[2] != KARETO_INF) {
-      x.iC = idx(Bd, clampU(sat_add(c12, c.cap[2])));
-      uint32_t tau = rows[(size_t)ri * G];
-      x.tc = tau == KARETO_TTL_INF ? ntc : idx(Tc, tau);
-      x.i12t = 0;
-    } else {
-      x.iC = -1;
-      x.tc = ntc;
-      x.i12t = idx(B12, clampU(c12));
+    if (ttl_row_used[r])
+      for (int g = 0; g < G; g++)
+        tix[(size_t)r * G + g] =
+            (uint32_t)(std::lower_bound(Tt.begin(), Tt.end(), rows[(size_t)r * G + g]) - Tt.begin());
+
+  // ---- boundary sets and per-configuration lookup indices, on the GPU
+  DBuf<kareto_config> dcfg;
+  DBuf<CfgDev> dcd;
+  DBuf<uint8_t> tmp;
+  DBuf<uint32_t> dBd, dB12, dTc, dTt, dtix, drows;
+  KTRY(upload(ctx, dTc, Tc)); KTRY(upload(ctx, dTt, Tt)); KTRY(upload(ctx, dtix, tix)); KTRY(upload(ctx, drows, rows));
+  KTRY(dcfg.alloc(ctx, nS > 0 ? nS : 1)); KTRY(dcd.alloc(ctx, nS > 0 ? nS : 1));
+  int nb = 0, nb12 = 0;
+  if (nS > 0) {
+    KCUDA(ctx, cudaMemcpyAsync(dcfg.p, cS.data(), sizeof(kareto_config) * nS, cudaMemcpyHostToDevice, st));
+    DBuf<uint32_t> vals, vals_s, v12, v12_s;
+    DBuf<int> cnt;
+    KTRY(vals.alloc(ctx, 3 * nS)); KTRY(vals_s.alloc(ctx, 3 * nS)); KTRY(v12.alloc(ctx, nS)); KTRY(v12_s.alloc(ctx, nS));
+    KTRY(dBd.alloc(ctx, 3 * nS)); KTRY(dB12.alloc(ctx, nS)); KTRY(cnt.alloc(ctx, 2));
+    Pass ps(ctx, "K4_boundaries", 1, 2);
+    k_bound_vals<<<grid_for(nS, 256, 4 * sms), 256, 0, st>>>(dcfg.p, nS, U, vals.p, v12.p);
+    KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceRadixSort::SortKeys(t, b, vals.p, vals_s.p, (int)(3 * nS), 0, 32, st);
+    }));
+    KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceSelect::Unique(t, b, vals_s.p, dBd.p, cnt.p, (int)(3 * nS), st);
+    }));
+    KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceRadixSort::SortKeys(t, b, v12.p, v12_s.p, (int)nS, 0, 32, st);
+    }));
+    KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceSelect::Unique(t, b, v12_s.p, dB12.p, cnt.p + 1, (int)nS, st);
+    }));
+    int hc[2] = {0, 0};
+    uint32_t last12 = 0;
+    KCUDA(ctx, cudaMemcpyAsync(hc, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+    KCUDA(ctx, cudaStreamSynchronize(st));
+    nb = hc[0];
+    nb12 = hc[1];
+    if (nb12 > 0) {  // drop the sentinel of CAPACITY configurations (the largest key)
+      KCUDA(ctx, cudaMemcpyAsync(&last12, dB12.p + nb12 - 1, 4, cudaMemcpyDeviceToHost, st));
+      KCUDA(ctx, cudaStreamSynchronize(st));
+      if (last12 == kNone) nb12--;
     }
-    cd[i] = x;
+    k_cfgdev<<<grid_for(nS, 256, 4 * sms), 256, 0, st>>>(dcfg.p, nS, U, dBd.p, nb, dB12.p, nb12, dTc.p, ntc,
+                                                         drows.p, n_tuner, G, dcd.p);
   }
 
   // ---- K4: histograms over the accesses
-  DBuf<uint8_t> tmp;
-  DBuf<uint32_t> dBd, dB12, dTc, dTt, dlut, dtix, drows;
-  KTRY(upload(ctx, dBd, Bd)); KTRY(upload(ctx, dB12, B12)); KTRY(upload(ctx, dTc, Tc)); KTRY(upload(ctx, dTt, Tt));
-  KTRY(upload(ctx, dtix, tix)); KTRY(upload(ctx, drows, rows));
+  DBuf<uint32_t> dlut;
   const int ncol = ntc + 1;
   DBuf<unsigned long long> hC, hS, hD, C1, S1, CD;
   size_t ncell = (size_t)ncol * (nb > 0 ? nb : 1);
@@ -459,19 +513,12 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
   }
 
   // ---- K5 + K7 on the shard
-  DBuf<kareto_config> dcfg;
-  DBuf<CfgDev> dcd;
   DBuf<kareto_counts> dcounts;
   DBuf<double> dobj;
   int64_t nsa = ns > 0 ? ns : 1;
   // gathered outputs are assembled in padded per-rank slots: slot = ceil(n / world)
   const int64_t slot = ctx->world > 1 ? (n_cfg + ctx->world - 1) / ctx->world : nsa;
-  KTRY(dcfg.alloc(ctx, nS > 0 ? nS : 1)); KTRY(dcd.alloc(ctx, nS > 0 ? nS : 1));
   KTRY(dcounts.alloc(ctx, slot > 0 ? slot : 1)); KTRY(dobj.alloc(ctx, 3 * (slot > 0 ? slot : 1)));
-  if (nS > 0) {
-    KCUDA(ctx, cudaMemcpyAsync(dcfg.p, cS.data(), sizeof(kareto_config) * nS, cudaMemcpyHostToDevice, st));
-    KCUDA(ctx, cudaMemcpyAsync(dcd.p, cd.data(), sizeof(CfgDev) * nS, cudaMemcpyHostToDevice, st));
-  }
   StackTables T{};
   T.Bd = nullptr; T.nb = nb; T.Tc = dTc.p; T.ntc = ntc;
   T.C1 = C1.p; T.S1 = S1.p; T.CD = CD.p;

@@ -62,6 +62,7 @@ struct kareto_ctx {
 
 struct kareto_trace {
   kareto_ctx *ctx = nullptr;
+  cudaStream_t stream = nullptr;  // copy of ctx->stream (trace_free must not touch ctx)
   int64_t R = 0, N = 0, U = 0, span_ms = 1;
   int32_t K = 0, max_blocks = 0;
   int64_t n_runs = 0;          // runs of consecutive previous positions (K3)

@@ -523,6 +523,7 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
 
   kareto_trace *tr = new kareto_trace();
   tr->ctx = ctx;
+  tr->stream = ctx->stream;
   tr->R = R;
   tr->K = d->top_k;
   struct Guard {

@@ -200,7 +200,6 @@ __global__ void __launch_bounds__(K1_THREADS) k_chain_hash(const uint32_t *__res
   const uint32_t rb = range_sh[0], re = range_sh[1];
   const uint64_t B0 = s[rb], B1 = s[re];
   const uint64_t RP = kChainR * P_init;
-  const uint32_t *tok_end = tokens + n_tokens;
   uint32_t r = rb;  // per-thread request cursor (monotone across rounds)
   for (uint64_t base = B0; base < B1; base += K1_THREADS) {
     uint64_t b = base + tid;
@@ -213,7 +212,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_chain_hash(const uint32_t *__res
       n = s[r + 1] - sr;
       k = (uint32_t)(b - sr);
       uint32_t t[16];
-      load_block_tokens(tokens + tok_off[r] + 16 * (int64_t)k, tok_end, t);
+      load_block_tokens(tokens + tok_off[r] + 16 * (int64_t)k, tokens + n_tokens, t);
       uint64_t c = nh_block(t, key);
       e = (k == 0) ? Aff{0, RP + c} : Aff{kChainR, c};
     }
@@ -316,30 +315,36 @@ __global__ void k_link_prev(const uint32_t *__restrict__ ks, const uint64_t *__r
   }
 }
 
-// Rare slow path: warp-parallel backward scan of the key run for overflowed elements.
-__global__ void k_link_overflow(const uint32_t *__restrict__ ks, const uint64_t *__restrict__ vs,
-                                const uint32_t *__restrict__ ovf, const uint32_t *__restrict__ n_ovf,
-                                uint32_t *__restrict__ pp) {
-  const int lane = threadIdx.x & 31;
+// Rare slow path (32-bit fingerprint collisions in long key runs): one CTA per overflowed
+// element walks the key run backwards 1024 elements per step; the largest matching position
+// below i is the previous occurrence.
+constexpr int OVF_THREADS = 1024;
+__global__ void __launch_bounds__(OVF_THREADS) k_link_overflow(const uint32_t *__restrict__ ks,
+                                                                const uint64_t *__restrict__ vs,
+                                                                const uint32_t *__restrict__ ovf,
+                                                                const uint32_t *__restrict__ n_ovf,
+                                                                uint32_t *__restrict__ pp) {
+  __shared__ unsigned long long best1;  // 1 + best position, 0 = none
+  __shared__ int ended;
   const uint32_t n = *n_ovf;
-  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += (gridDim.x * blockDim.x) >> 5) {
+  for (uint32_t w = blockIdx.x; w < n; w += gridDim.x) {
     const uint64_t i = ovf[w];
     const uint32_t k = ks[i];
     const uint64_t hi = vs[i] >> 32;
-    uint32_t p = kNone;
-    for (int64_t base = (int64_t)i - 1 - LINK_SCAN; base >= -31; base -= 32) {
-      int64_t t = base - lane;  // lanes walk backwards 32 at a time
+    if (threadIdx.x == 0) { best1 = 0; ended = 0; }
+    __syncthreads();
+    for (int64_t base = (int64_t)i - 1 - LINK_SCAN; base >= 0; base -= OVF_THREADS) {
+      int64_t t = base - threadIdx.x;
       bool in = t >= 0 && ks[t] == k;
-      bool hit = in && (vs[t] >> 32) == hi;
-      unsigned mh = __ballot_sync(0xffffffffu, hit);
-      if (mh) {
-        int src = __ffs(mh) - 1;  // lowest lane = largest t
-        p = (uint32_t)__shfl_sync(0xffffffffu, (uint32_t)(in ? vs[t] : 0), src);
-        break;
-      }
-      if (__ballot_sync(0xffffffffu, in) != 0xffffffffu) break;  // reached the run start
+      if (!in) atomicOr(&ended, 1);
+      else if ((vs[t] >> 32) == hi) atomicMax(&best1, (unsigned long long)t + 1);
+      __syncthreads();
+      bool stop = best1 != 0 || ended;
+      __syncthreads();
+      if (stop) break;
     }
-    if (lane == 0) pp[i] = p;
+    if (threadIdx.x == 0) pp[i] = best1 ? (uint32_t)vs[best1 - 1] : kNone;
+    __syncthreads();
   }
 }
 
@@ -647,7 +652,7 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
         KTRY(ovf.alloc(ctx, N)); KTRY(n_ovf.alloc(ctx, 1)); KTRY(n_ovf.zero());
         Pass ps(ctx, "K2_link_prev", 1, 2);
         k_link_prev<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(k32s.p, v64s.p, N, pj.p, pp.p, ovf.p, n_ovf.p);
-        k_link_overflow<<<4 * sms, 256, 0, st>>>(k32s.p, v64s.p, ovf.p, n_ovf.p, pp.p);
+        k_link_overflow<<<2 * sms, OVF_THREADS, 0, st>>>(k32s.p, v64s.p, ovf.p, n_ovf.p, pp.p);
       }
       k32s.release(); v64s.release();
       KTRY(pj2.alloc(ctx, N)); KTRY(pp2.alloc(ctx, N));

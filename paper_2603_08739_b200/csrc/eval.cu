@@ -22,6 +22,7 @@ namespace kareto {
 constexpr int H_THREADS = 1024;
 constexpr int LUT_BITS = 12;                 // boundary lookup table: 4096 buckets
 constexpr int SMEM_BUDGET = 200 * 1024;
+constexpr int SMEM_MAX = 227 * 1024;         // sm_100 max dynamic shared memory per block
 
 // bucket LUT: lut[b] = first boundary index with Bd[i] >= (b << sh); lut[nbk] = nb
 __global__ void k_build_lut(const uint32_t *__restrict__ Bd, int nb, int sh, uint32_t *__restrict__ lut) {
@@ -96,6 +97,65 @@ __global__ void __launch_bounds__(H_THREADS) k_hist_d(uint64_t N, uint64_t per_c
     if (cnt[i]) atomicAdd(&gcnt[c_lo + i], (unsigned long long)cnt[i]);
     if (sk[i]) atomicAdd(&gsk[c_lo + i], (unsigned long long)sk[i]);
   }
+}
+
+// K4 fused (when both histograms fit in shared memory): one pass over the accesses builds
+// the (d-bin, tau-bin) count / sum-k histogram and the D-bin count histogram.  Updates are
+// warp-aggregated (match_any on the cell) so hot bins (small depths) do not serialise.
+__global__ void __launch_bounds__(H_THREADS) k_hist_dD(uint64_t N, uint64_t per_cta, const uint32_t *__restrict__ depth,
+                                                       const uint32_t *__restrict__ req, const uint32_t *__restrict__ s,
+                                                       const uint32_t *__restrict__ delta,
+                                                       const uint32_t *__restrict__ Bd, int nb,
+                                                       const uint32_t *__restrict__ lut, int sh,
+                                                       const uint32_t *__restrict__ Tc, int ntc,
+                                                       unsigned long long *__restrict__ gcnt,
+                                                       unsigned long long *__restrict__ gsk,
+                                                       unsigned long long *__restrict__ gD) {
+  extern __shared__ uint32_t sm[];
+  uint32_t *lut_s = sm;
+  const int W = (ntc + 1) * nb;
+  uint32_t *cnt = lut_s + (1 << LUT_BITS) + 1;
+  uint32_t *sk = cnt + W;
+  uint32_t *cD = sk + W;
+  for (int i = threadIdx.x; i <= (1 << LUT_BITS); i += blockDim.x) lut_s[i] = lut[i];
+  for (int i = threadIdx.x; i < W; i += blockDim.x) { cnt[i] = 0; sk[i] = 0; }
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) cD[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  uint64_t j0 = blockIdx.x * per_cta, j1 = j0 + per_cta < N ? j0 + per_cta : N;
+  for (uint64_t jb = j0; jb < j1; jb += blockDim.x) {  // block-uniform trip count
+    uint64_t j = jb + threadIdx.x;
+    int cell = -1, dcell = -1;
+    uint32_t k = 0;
+    if (j < j1) {
+      uint32_t d = depth[j];
+      if (d != kNone) {
+        uint32_t r = req[j];
+        uint32_t sr1 = s[r + 1];
+        k = sr1 - 1 - (uint32_t)j;
+        int bd = bin_of(d, Bd, nb, lut_s, sh);
+        if (bd < nb) cell = (ntc > 0 ? tbin_of(delta[j], Tc, ntc) : 0) * nb + bd;
+        uint32_t D = d + ((uint32_t)j - s[r]);
+        int bD = bin_of(D, Bd, nb, lut_s, sh);
+        if (bD < nb) dcell = bD;
+      }
+    }
+    unsigned same = __match_any_sync(0xffffffffu, cell);
+    uint32_t ks = __reduce_add_sync(same, k);
+    if (cell >= 0 && (__ffs(same) - 1) == lane) {
+      atomicAdd(&cnt[cell], (uint32_t)__popc(same));
+      if (ks) atomicAdd(&sk[cell], ks);
+    }
+    unsigned sameD = __match_any_sync(0xffffffffu, dcell);
+    if (dcell >= 0 && (__ffs(sameD) - 1) == lane) atomicAdd(&cD[dcell], (uint32_t)__popc(sameD));
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < W; i += blockDim.x) {
+    if (cnt[i]) atomicAdd(&gcnt[i], (unsigned long long)cnt[i]);
+    if (sk[i]) atomicAdd(&gsk[i], (unsigned long long)sk[i]);
+  }
+  for (int i = threadIdx.x; i < nb; i += blockDim.x)
+    if (cD[i]) atomicAdd(&gD[i], (unsigned long long)cD[i]);
 }
 
 // K4b: histogram of D over the boundaries (count), window [b_lo, b_hi)
@@ -451,8 +511,15 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
     if (!attr_set) {
       cudaFuncSetAttribute(k_hist_d, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BUDGET);
       cudaFuncSetAttribute(k_hist_D, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BUDGET);
+      cudaFuncSetAttribute(k_hist_dD, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
       attr_set = true;
     }
+    const size_t fused = lut_bytes + 8 * ncell + 4 * (size_t)nb;
+    if (fused <= (size_t)SMEM_MAX) {  // one pass for both histograms
+      Pass ps(ctx, "K4_hist_dD", 1, 1);
+      k_hist_dD<<<g, H_THREADS, fused, st>>>(N, per, depth, req, s, delta, dBd.p, nb, dlut.p, sh, dTc.p, ntc, hC.p,
+                                            hS.p, hD.p);
+    } else {
     for (int c0 = 0; c0 < (int)ncell; c0 += wcell) {
       int c1 = c0 + wcell < (int)ncell ? c0 + wcell : (int)ncell;
       size_t smem = lut_bytes + 8 * (size_t)(c1 - c0);
@@ -465,6 +532,7 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
       size_t smem = lut_bytes + 4 * (size_t)(b1 - b0);
       Pass ps(ctx, "K4_hist_D", 1, 1);
       k_hist_D<<<g, H_THREADS, smem, st>>>(N, per, depth, req, s, dBd.p, nb, dlut.p, sh, b0, b1, hD.p);
+    }
     }
     {
       Pass ps(ctx, "K4_cumulate", 0, 3);

@@ -168,42 +168,68 @@ __device__ __forceinline__ void load_block_tokens(const uint32_t *p, const uint3
   for (int i = 0; i < 16; i++) t[i] = (mis & 2) ? u[i + 2] : u[i];
 }
 
-constexpr int K1_THREADS = 256;
+// Half a block (8 tokens) starting at word pointer p: the 2 or 3 covering 16-byte chunks
+// + funnel select.  Two threads per block halve the lines one warp-wide load touches
+// (adjacent lanes read adjacent 32 B), i.e. the L1 wavefronts per block.
+__device__ __forceinline__ void load_half_tokens(const uint32_t *p, const uint32_t *end, uint32_t t[8]) {
+  uintptr_t addr = (uintptr_t)p;
+  int mis = (int)((addr >> 2) & 3);
+  const uint4 *q = (const uint4 *)(addr & ~(uintptr_t)15);
+  if ((const uint32_t *)(q + (mis ? 3 : 2)) > end) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) t[i] = __ldg(p + i);
+    return;
+  }
+  uint32_t w[12];
+  uint4 c0 = __ldg(q), c1 = __ldg(q + 1);
+  uint4 c2 = mis ? __ldg(q + 2) : make_uint4(0, 0, 0, 0);
+  w[0] = c0.x; w[1] = c0.y; w[2] = c0.z; w[3] = c0.w;
+  w[4] = c1.x; w[5] = c1.y; w[6] = c1.z; w[7] = c1.w;
+  w[8] = c2.x; w[9] = c2.y; w[10] = c2.z; w[11] = c2.w;
+  uint32_t u[10];
+#pragma unroll
+  for (int i = 0; i < 10; i++) u[i] = (mis & 1) ? w[i + 1] : w[i];
+#pragma unroll
+  for (int i = 0; i < 8; i++) t[i] = (mis & 2) ? u[i + 2] : u[i];
+}
 
-// CTA c owns the sorted-block range [s[rb], s[re]) where rb, re are the first requests
-// starting at or after c*N/nCTA and (c+1)*N/nCTA: whole requests per CTA, so the scan
-// carry never crosses CTAs.  Rounds of 256 consecutive blocks; thread = block.
+constexpr int K1_THREADS = 256;
+constexpr int K1_WARPS = K1_THREADS / 32;
+
+// Every WARP owns a request-aligned range of sorted blocks [s[rb], s[re)) (rb, re = first
+// requests starting at or after w*N/nWarps and (w+1)*N/nWarps), so the scan carry never
+// crosses warps: rounds of 32 consecutive blocks, one thread per block, a 5-step shuffle
+// scan and the carry kept in a register -- no block-level barrier on the path, so the
+// warps of an SM overlap each other's load latency freely.
 __global__ void __launch_bounds__(K1_THREADS) k_chain_hash(const uint32_t *__restrict__ tokens, int64_t n_tokens,
                                                             const int64_t *__restrict__ tok_off,
                                                             const uint32_t *__restrict__ s, int64_t R, uint64_t N,
                                                             uint64_t P_init, uint64_t *__restrict__ hash_out,
                                                             uint32_t *__restrict__ req_out) {
-  __shared__ Aff warp_tot[K1_THREADS / 32];
-  __shared__ uint64_t carry_sh;
-  __shared__ uint32_t range_sh[2];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid < 2) {
-    uint64_t target = ((uint64_t)(blockIdx.x + tid) * N) / gridDim.x;
-    // first request r with s[r] >= target
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * K1_WARPS;
+  const uint64_t w = (uint64_t)blockIdx.x * K1_WARPS + (threadIdx.x >> 5);
+  uint32_t bound = 0;
+  if (lane < 2) {  // first request r with s[r] >= target
+    uint64_t target = ((w + lane) * N) / nw;
     int64_t lo = 0, hi = R;
     while (lo < hi) {
       int64_t m = (lo + hi) >> 1;
       if ((uint64_t)s[m] >= target) hi = m; else lo = m + 1;
     }
-    range_sh[tid] = (uint32_t)lo;
+    bound = (uint32_t)lo;
   }
+  const uint32_t rb = __shfl_sync(0xffffffffu, bound, 0), re = __shfl_sync(0xffffffffu, bound, 1);
   uint32_t key[16];
 #pragma unroll
   for (int i = 0; i < 16; i++) key[i] = (uint32_t)fmix64((uint64_t)(i + 1));
-  if (tid == 0) carry_sh = 0;
-  __syncthreads();
-  const uint32_t rb = range_sh[0], re = range_sh[1];
   const uint64_t B0 = s[rb], B1 = s[re];
   const uint64_t RP = kChainR * P_init;
+  uint64_t carry = 0;
   uint32_t r = rb;  // per-thread request cursor (monotone across rounds)
-  for (uint64_t base = B0; base < B1; base += K1_THREADS) {
-    uint64_t b = base + tid;
-    bool valid = b < B1;
+  for (uint64_t base = B0; base < B1; base += 32) {
+    const uint64_t b = base + lane;
+    const bool valid = b < B1;
     Aff e = {1, 0};
     uint32_t k = 0, sr = 0, n = 0;
     if (valid) {
@@ -216,36 +242,19 @@ __global__ void __launch_bounds__(K1_THREADS) k_chain_hash(const uint32_t *__res
       uint64_t c = nh_block(t, key);
       e = (k == 0) ? Aff{0, RP + c} : Aff{kChainR, c};
     }
-    // warp inclusive scan
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       uint64_t ua = __shfl_up_sync(0xffffffffu, e.a, off);
       uint64_t ub = __shfl_up_sync(0xffffffffu, e.b, off);
       if (lane >= off) e = aff_compose(Aff{ua, ub}, e);
     }
-    if (lane == 31) warp_tot[wid] = e;
-    __syncthreads();
-    if (wid == 0) {
-      Aff w = lane < K1_THREADS / 32 ? warp_tot[lane] : Aff{1, 0};
-#pragma unroll
-      for (int off = 1; off < K1_THREADS / 32; off <<= 1) {
-        uint64_t ua = __shfl_up_sync(0xffffffffu, w.a, off);
-        uint64_t ub = __shfl_up_sync(0xffffffffu, w.b, off);
-        if (lane >= off) w = aff_compose(Aff{ua, ub}, w);
-      }
-      if (lane < K1_THREADS / 32) warp_tot[lane] = w;  // inclusive prefix over warps
-    }
-    __syncthreads();
-    if (wid > 0) e = aff_compose(warp_tot[wid - 1], e);
-    uint64_t P = e.a * carry_sh + e.b;
-    __syncthreads();  // everyone has read carry_sh / warp_tot
+    const uint64_t P = e.a * carry + e.b;
     if (valid) {
       uint64_t j = (uint64_t)sr + n - 1 - k;
       hash_out[j] = fmix64(P);
       req_out[j] = r;
     }
-    if (tid == K1_THREADS - 1) carry_sh = P;  // last block of the round (if beyond B1 its value is unused)
-    __syncthreads();
+    carry = __shfl_sync(0xffffffffu, P, 31);  // last block of the round (beyond B1: unused)
   }
 }
 
@@ -608,10 +617,10 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
   if (N > 0) {
     if (d->mode == KARETO_TOKENS) {
       uint64_t P_init = fmix64(d->salt ^ kSaltC);
-      int64_t per_cta = 16384;
-      unsigned g = (unsigned)((N + per_cta - 1) / per_cta);
-      if (g < (unsigned)(4 * sms)) g = (unsigned)(4 * sms);
-      if ((uint64_t)g > N) g = (unsigned)N;
+      // ~2048 blocks per warp, at least 16 warps per SM
+      uint64_t nwarps = (N + 2047) / 2048;
+      if (nwarps < (uint64_t)(16 * sms)) nwarps = 16 * sms;
+      unsigned g = (unsigned)((nwarps + K1_WARPS - 1) / K1_WARPS);
       Pass ps(ctx, "K1_chain_hash", 1, 1);
       k_chain_hash<<<g, K1_THREADS, 0, st>>>(tokens, total, src_off.p, tr->s, R, N, P_init, tr->hash, tr->req);
     } else {

@@ -282,45 +282,91 @@ __global__ void k_iota(uint32_t *v, uint64_t n) {
     v[i] = (uint32_t)i;
 }
 
-// Sort key: a 32-bit fingerprint of the 64-bit hash (top half of a bijective mix, so
-// caller-provided structured hashes cannot crowd one key); value: (other half << 32) |
+// Sort key: a 32-bit fingerprint of the 64-bit hash (top half of a bijective mix m, so
+// caller-provided structured hashes cannot crowd one key); value: (other half of m << 32) |
 // position, so equality is decided on all 64 bits without gathers.
 __global__ void k_sort_prep(const uint64_t *__restrict__ hash, uint64_t N, uint32_t *__restrict__ key,
                             uint64_t *__restrict__ val) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
-    // m = fmix64(h ^ c) is a bijection of h: (key, val >> 32) = (m >> 32, m & 0xFFFFFFFF)
-    // identifies h exactly
-    uint64_t m = fmix64(hash[j] ^ 0x6A09E667F3BCC909ULL);
+    uint64_t m = fmix64(hash[j] ^ 0x6A09E667F3BCC909ULL);  // bijection: (key, val >> 32) identifies h
     key[j] = (uint32_t)(m >> 32);
     val[j] = (m << 32) | (uint64_t)(uint32_t)j;
   }
 }
 
+// prev is assembled per bucket of 2^PB consecutive positions: every position appears exactly
+// once among the (position, prev) pairs, so bucket b owns pair slots [b << PB, (b+1) << PB).
+constexpr int PB = 11;
+
 // In fingerprint-sorted order (stable: positions ascending within a key), the previous
 // occurrence of element i is the nearest earlier element of its key run whose full hash
-// matches (almost always i-1).  Emits (position, prev) pairs for the bucketed scatter.
-constexpr int LINK_SCAN = 32;  // bounded backward scan; longer (fingerprint-collision) cases overflow
+// matches (almost always i-1; a bounded scan, longer fingerprint-collision cases overflow).
+constexpr int LINK_SCAN = 32;
 
-__global__ void k_link_prev(const uint32_t *__restrict__ ks, const uint64_t *__restrict__ vs, uint64_t N,
-                            uint32_t *__restrict__ pj, uint32_t *__restrict__ pp, uint32_t *__restrict__ ovf,
-                            uint32_t *__restrict__ n_ovf) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = ks[i];
-    const uint64_t v = vs[i];
-    const uint32_t j = (uint32_t)v;
-    uint32_t p = kNone;
-    uint64_t t = i;
-    int steps = 0;
-    for (; t > 0 && ks[t - 1] == k && steps < LINK_SCAN; t--, steps++) {
-      uint64_t w = vs[t - 1];
-      if ((w >> 32) == (v >> 32)) { p = (uint32_t)w; break; }
+// Each warp links LINK_U * 32 consecutive sorted elements: the predecessor element comes by
+// shuffle, and the LINK_U slot reservations are issued before any result is consumed so their
+// L2 round trips overlap.
+constexpr int LINK_U = 4;
+__global__ void __launch_bounds__(256) k_link_prev(const uint32_t *__restrict__ ks, const uint64_t *__restrict__ vs,
+                                                   uint64_t N, unsigned *__restrict__ cursor, uint2 *__restrict__ pairs,
+                                                   uint2 *__restrict__ ovf, uint32_t *__restrict__ n_ovf) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nchunk = (N + 32 * LINK_U - 1) / (32 * LINK_U);
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; c < nchunk; c += nwarps) {
+    const uint64_t i0 = c * 32 * LINK_U;
+    uint32_t k[LINK_U], p[LINK_U], bk[LINK_U], same[LINK_U], base[LINK_U];
+    uint64_t v[LINK_U];
+    bool ovfl[LINK_U];
+#pragma unroll
+    for (int u = 0; u < LINK_U; u++) {
+      const uint64_t i = i0 + u * 32 + lane;
+      k[u] = i < N ? ks[i] : 0xFFFFFFFFu;
+      v[u] = i < N ? vs[i] : 0;
     }
-    if (p == kNone && steps == LINK_SCAN && t > 0 && ks[t - 1] == k) {
-      uint32_t slot = atomicAdd(n_ovf, 1u);
-      ovf[slot] = (uint32_t)i;  // resolved by k_link_overflow
+#pragma unroll
+    for (int u = 0; u < LINK_U; u++) {
+      const uint64_t i = i0 + u * 32 + lane;
+      uint32_t kq = __shfl_up_sync(0xFFFFFFFFu, k[u], 1);
+      uint64_t vq = __shfl_up_sync(0xFFFFFFFFu, v[u], 1);
+      if (lane == 0) {
+        if (i > 0) { kq = ks[i - 1]; vq = vs[i - 1]; }
+        else kq = ~k[u];
+      }
+      p[u] = kNone;
+      ovfl[u] = false;
+      if (i < N && kq == k[u]) {
+        if ((vq >> 32) == (v[u] >> 32)) {
+          p[u] = (uint32_t)vq;
+        } else {  // fingerprint collision: bounded backward scan of the key run
+          uint64_t t = i - 1;
+          int steps = 1;
+          for (; t > 0 && ks[t - 1] == k[u] && steps < LINK_SCAN; t--, steps++) {
+            const uint64_t w = vs[t - 1];
+            if ((w >> 32) == (v[u] >> 32)) { p[u] = (uint32_t)w; break; }
+          }
+          ovfl[u] = p[u] == kNone && steps == LINK_SCAN && t > 0 && ks[t - 1] == k[u];
+        }
+      }
     }
-    pj[i] = j;
-    pp[i] = p;
+#pragma unroll
+    for (int u = 0; u < LINK_U; u++) {
+      const bool in = i0 + u * 32 + lane < N;
+      bk[u] = in ? ((uint32_t)v[u] >> PB) : 0xFFFFFFFFu;
+      same[u] = __match_any_sync(0xFFFFFFFFu, bk[u]);
+      base[u] = 0;
+      if (in && lane == __ffs(same[u]) - 1) base[u] = atomicAdd(&cursor[bk[u]], (unsigned)__popc(same[u]));
+    }
+#pragma unroll
+    for (int u = 0; u < LINK_U; u++) {
+      const uint64_t i = i0 + u * 32 + lane;
+      const uint32_t b = __shfl_sync(0xFFFFFFFFu, base[u], __ffs(same[u]) - 1);
+      if (i < N) {
+        const uint32_t slot = (bk[u] << PB) + b + __popc(same[u] & ((1u << lane) - 1u));
+        pairs[slot] = make_uint2((uint32_t)v[u], p[u]);
+        if (ovfl[u]) ovf[atomicAdd(n_ovf, 1u)] = make_uint2((uint32_t)i, slot);  // resolved by k_link_overflow
+      }
+    }
   }
 }
 
@@ -330,14 +376,15 @@ __global__ void k_link_prev(const uint32_t *__restrict__ ks, const uint64_t *__r
 constexpr int OVF_THREADS = 1024;
 __global__ void __launch_bounds__(OVF_THREADS) k_link_overflow(const uint32_t *__restrict__ ks,
                                                                 const uint64_t *__restrict__ vs,
-                                                                const uint32_t *__restrict__ ovf,
+                                                                const uint2 *__restrict__ ovf,
                                                                 const uint32_t *__restrict__ n_ovf,
-                                                                uint32_t *__restrict__ pp) {
-  __shared__ unsigned long long best1;  // 1 + best position, 0 = none
+                                                                uint2 *__restrict__ pairs) {
+  __shared__ unsigned long long best1;  // 1 + best sorted index, 0 = none
   __shared__ int ended;
   const uint32_t n = *n_ovf;
   for (uint32_t w = blockIdx.x; w < n; w += gridDim.x) {
-    const uint64_t i = ovf[w];
+    const uint2 o = ovf[w];
+    const uint64_t i = o.x;
     const uint32_t k = ks[i];
     const uint64_t hi = vs[i] >> 32;
     if (threadIdx.x == 0) { best1 = 0; ended = 0; }
@@ -352,17 +399,27 @@ __global__ void __launch_bounds__(OVF_THREADS) k_link_overflow(const uint32_t *_
       __syncthreads();
       if (stop) break;
     }
-    if (threadIdx.x == 0) pp[i] = best1 ? (uint32_t)vs[best1 - 1] : kNone;
+    if (threadIdx.x == 0) pairs[o.y].y = best1 ? (uint32_t)vs[best1 - 1] : kNone;
     __syncthreads();
   }
 }
 
-// (position, prev) pairs partitioned by the top bits of the position: the writes of a
-// warp land in one L2-resident window of prev[] instead of random HBM sectors.
-__global__ void k_bucket_scatter(const uint32_t *__restrict__ pj, const uint32_t *__restrict__ pp, uint64_t N,
-                                 uint32_t *__restrict__ prev) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x)
-    prev[pj[i]] = pp[i];
+// bucket b's pairs -> the 2^PB-entry slice of prev[] in shared memory -> one coalesced write
+__global__ void __launch_bounds__(256) k_bucket_assemble(const uint2 *__restrict__ pairs, uint64_t N,
+                                                          uint32_t *__restrict__ prev) {
+  __shared__ uint32_t slice[1 << PB];
+  const uint64_t nb = (N + (1u << PB) - 1) >> PB;
+  for (uint64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const uint64_t lo = b << PB;
+    const uint32_t cnt = (uint32_t)((N - lo) < (1u << PB) ? (N - lo) : (1u << PB));
+    for (uint32_t q = threadIdx.x; q < cnt; q += blockDim.x) {
+      uint2 pr = pairs[lo + q];
+      slice[pr.x & ((1u << PB) - 1)] = pr.y;
+    }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < cnt; q += blockDim.x) prev[lo + q] = slice[q];
+    __syncthreads();
+  }
 }
 
 __device__ __forceinline__ void warp_count_add(uint32_t *arr, uint32_t key, bool pred) {
@@ -641,9 +698,9 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
     int B = 1;
     while ((1ull << B) < N) B++;
     {
-      DBuf<uint32_t> k32, k32s, pj, pp, pj2, pp2;
+      DBuf<uint32_t> k32, k32s;
       DBuf<uint64_t> v64, v64s;
-      KTRY(k32.alloc(ctx, N)); KTRY(v64.alloc(ctx, N)); KTRY(k32s.alloc(ctx, N)); KTRY(v64s.alloc(ctx, N));
+      KTRY(k32.alloc(ctx, N)); KTRY(k32s.alloc(ctx, N)); KTRY(v64.alloc(ctx, N)); KTRY(v64s.alloc(ctx, N));
       {
         Pass ps(ctx, "K2_sort_prep", 1, 1);
         k_sort_prep<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(tr->hash, N, k32.p, v64.p);
@@ -655,26 +712,33 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
         }));
       }
       k32.release(); v64.release();
-      KTRY(pj.alloc(ctx, N)); KTRY(pp.alloc(ctx, N));
       {
-        DBuf<uint32_t> ovf, n_ovf;
-        KTRY(ovf.alloc(ctx, N)); KTRY(n_ovf.alloc(ctx, 1)); KTRY(n_ovf.zero());
-        Pass ps(ctx, "K2_link_prev", 1, 2);
-        k_link_prev<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(k32s.p, v64s.p, N, pj.p, pp.p, ovf.p, n_ovf.p);
-        k_link_overflow<<<2 * sms, OVF_THREADS, 0, st>>>(k32s.p, v64s.p, ovf.p, n_ovf.p, pp.p);
-      }
-      k32s.release(); v64s.release();
-      KTRY(pj2.alloc(ctx, N)); KTRY(pp2.alloc(ctx, N));
-      {
-        Pass ps(ctx, "K2_partition_prev", 0, 1);  // one stable 8-bit radix pass on the top bits of j
-        int b0 = B > 8 ? B - 8 : 0;
-        KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
-          return cub::DeviceRadixSort::SortPairs(t, b, pj.p, pj2.p, pp.p, pp2.p, (int64_t)N, b0, B, st);
-        }));
-      }
-      {
-        Pass ps(ctx, "K2_bucket_scatter", 1, 1);
-        k_bucket_scatter<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(pj2.p, pp2.p, N, tr->prev);
+        DBuf<uint2> pairs, ovf;
+        DBuf<uint32_t> n_ovf;
+        DBuf<unsigned> cursor;
+        const uint64_t nbk = (N + (1u << PB) - 1) >> PB;
+        KTRY(pairs.alloc(ctx, N)); KTRY(ovf.alloc(ctx, N)); KTRY(n_ovf.alloc(ctx, 1)); KTRY(n_ovf.zero());
+        KTRY(cursor.alloc(ctx, nbk)); KTRY(cursor.zero());
+        {
+          Pass ps(ctx, "K2_link_prev", 1, 1);
+          k_link_prev<<<grid_for((N + LINK_U - 1) / LINK_U, 256, 8 * sms), 256, 0, st>>>(
+              k32s.p, v64s.p, N, cursor.p, pairs.p, ovf.p, n_ovf.p);
+        }
+        {
+          Pass ps(ctx, "K2_link_overflow", 1, 1);
+          k_link_overflow<<<2 * sms, OVF_THREADS, 0, st>>>(k32s.p, v64s.p, ovf.p, n_ovf.p, pairs.p);
+        }
+        if (getenv("KARETO_DEBUG")) {
+          uint32_t h = 0;
+          cudaMemcpyAsync(&h, n_ovf.p, 4, cudaMemcpyDeviceToHost, st);
+          cudaStreamSynchronize(st);
+          fprintf(stderr, "[kareto] K2 link overflow elements: %u of %llu\n", h, (unsigned long long)N);
+        }
+        {
+          Pass ps(ctx, "K2_bucket_assemble", 1, 1);
+          k_bucket_assemble<<<(unsigned)(nbk < (uint64_t)(32 * sms) ? nbk : 32 * sms), 256, 0, st>>>(pairs.p, N,
+                                                                                                     tr->prev);
+        }
       }
     }
     {

@@ -83,12 +83,15 @@ def tuner_rows_config3(delta_by_group, U_g, K):
 ALGO = {
     "K1_chain_hash": ("block", 76),        # 64 B tokens in + 8 B hash + 4 B request id out
     "K2_sort_prep": ("access", 20),        # 8 B hash in, 4 B key + 4 B fingerprint half + 4 B position out
-    "K2_link_prev": ("access", 20),        # 4 B key + 4 B position + 4 B gathered half in, 8 B pair out
+    "K2_link_prev": ("access", 20),        # 4 B fingerprint + 8 B (hash half, position) in, 8 B pair out
     "K2_bucket_assemble": ("access", 12),  # 8 B pair in, 4 B prev out
     "K2_access_info": ("access", 13),      # prev, req in; delta + run flag out
     "K3_expand": ("access", 4),            # depth out
     "K4_hist_d": ("access", 8),            # depth + req
     "K4_hist_D": ("access", 8),
+    # K6 per (access, replayed configuration): read the block's tier (1 B), last-access time (4 B)
+    # and list links / heap slot (8 B), write its last-access time (4 B); victim bookkeeping extra
+    "K6_replay": ("access-config", 17),
 }
 
 
@@ -420,13 +423,17 @@ def main():
     # ---- per-pass device times (profiled replay of the same steps) for the roofline
     ctx.set_profiling(True)
     ctx.pass_times(reset=True)
-    prof_steps = max(3, min(args.steps, 10))
+    prof_steps = 1 if ms_step > 10_000 else max(3, min(args.steps, 10))
     for _ in range(prof_steps):
         step()
     passes = ctx.pass_times(reset=True)
     ctx.set_profiling(False)
     peak, peak_src = measured_peak()
     units = {"block": N, "access": N}
+    k6 = [p for p in passes if p["name"] == "K6_replay"]
+    if k6 and n_replay:
+        # this rank's replayed configurations (the cost-weighted shard is ~1/world of them)
+        units["access-config"] = N * n_replay / world * prof_steps / k6[0]["launches"]
     roof = None
     own = [p for p in passes if p["own"] and p["name"] in ALGO]
     if own:

@@ -604,7 +604,7 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
     KTRY(cntP.alloc(ctx, nP)); KTRY(objP.alloc(ctx, 3 * nP)); KTRY(dcfgP.alloc(ctx, nP));
     KTRY(upload(ctx, diS, iS)); KTRY(upload(ctx, diP, iP));
     launch_objective(ctx, T, dcfg.p, dcd.p, dtix.p, drows.p, nS, model, mc, nullptr, cntS.p, objS.p);
-    KTRY(replay_eval(ctx, const_cast<kareto_trace *>(tr), cP.data(), nP, drows.p, n_tuner, cntP.p));
+    KTRY(replay_eval(ctx, const_cast<kareto_trace *>(tr), cP.data(), nP, rows.data(), drows.p, n_tuner, cntP.p));
     KCUDA(ctx, cudaMemcpyAsync(dcfgP.p, cP.data(), sizeof(kareto_config) * nP, cudaMemcpyHostToDevice, st));
     launch_objective(ctx, T, dcfgP.p, nullptr, dtix.p, drows.p, nP, model, mc, cntP.p, nullptr, objP.p);
     Pass ps(ctx, "K5_scatter", 1, 2);

@@ -10,288 +10,448 @@
 // Layout (B200): one thread per configuration; a wave of W configurations walks the same
 // access stream in lockstep, and every per-(block, configuration) field is stored at
 // [block * W + config], so the 32 lanes of a warp touching the same block hit one or two
-// sectors.  Victim order: LRU / FIFO tiers are doubly-linked lists (front = newest key;
-// for LRU a demoted block's last_seq exceeds every member of the lower tier, so demotion
-// order is key order), LFU tiers are binary heaps keyed (freq, last_seq); disk purges use a
-// binary heap keyed last_t + tau_g.  All state lives in HBM; waves are sized to free memory.
+// sectors.  The replay is latency-bound (dependent HBM round trips per access), so the
+// design minimises round trips and per-configuration bytes (bytes bound the wave size):
+//   * configurations are split into four classes {list, LFU} x {expiry heap or not}, each
+//     with its own field set, waves sized to free HBM per class;
+//   * LRU / FIFO tiers are doubly-linked lists with both links in one 8-byte word, loaded
+//     speculatively with the tier byte, so an HBM hit costs one round trip;
+//   * LFU tiers and the disk-expiry heap are 4-ary heaps with the key stored inline in the
+//     slot (one round trip per level, half the depth of a binary heap);
+//   * the lookup pass issues its loads sixteen blocks at a time, and the UPDATE pass loads the
+//     next block's state while the current one is processed;
+//   * head / tail / sizes / counters live in registers.
+// Victim order: list tail (LRU: least recent -- a demoted block's recency exceeds every
+// member of the lower tier, so demotion order is recency order; FIFO: entry order), LFU heap
+// minimum of (freq, last_seq); both keys are unique, so the result never depends on heap shape.
 #include "replay.cuh"
+
+#include <algorithm>
+#include <vector>
 
 namespace kareto {
 
 enum : uint8_t { T_NONE = 0, T_HBM = 1, T_DRAM = 2, T_DISK = 3 };
+constexpr int LOOK = 16;  // LOOKUP blocks whose loads are issued together
 
-struct RView {
-  uint8_t *tier;
-  uint32_t *lp, *ln, *lseq, *iseq, *freq, *last_t, *lease, *epos;
-  uint32_t *heap[3];  // LFU heaps per tier, [slot * W + c]
-  uint32_t *eheap;    // expiry heap
+struct RState {
+  uint8_t *tier;       // [b*W+c] T_*
+  uint32_t *lt;        // [b*W+c] ms of the last access (kNone = never seen): lease start, expiry base
+  uint2 *link;         // list classes: [b*W+c] (prev, next) toward head / tail
+  uint32_t *hpos;      // LFU: [b*W+c] slot in its tier heap
+  uint64_t *hkey[3];   // LFU: [slot*W+c] (freq << 32 | last_seq) per tier heap
+  uint32_t *hid[3];    // LFU: [slot*W+c] block of each heap slot
+  uint32_t *epos;      // expiry: [b*W+c] slot in the expiry heap (kNone = absent)
+  uint64_t *ekey;      // expiry: [slot*W+c] (min(lt + tau_g, 2^32-1) << 32 | block)
   const uint16_t *gblk;
   uint64_t W;
-  uint32_t c;
-  __device__ __forceinline__ uint64_t at(uint32_t b) const { return (uint64_t)b * W + c; }
 };
 
-struct RCfg {
+// Per-thread replay of one configuration.  Every tier-indexed member is accessed with a
+// compile-time tier (template parameter / unrolled cascade), so the per-tier state stays in
+// registers rather than local memory.
+template <bool LFU, bool EXP>
+struct Rep {
+  const RState &v;
+  const uint64_t c;
   uint64_t cap[3];
-  int policy;
-  bool ttl_mode, use_expiry;
-  const uint32_t *tau;  // [G]
-  uint32_t head[3], tail[3];
   uint64_t size[3];
+  uint32_t head[3], tail[3], tail2[3];
   uint32_t esize;
   uint32_t seq;
-  kareto_counts k;
+  bool ttl_mode, lru;
+  const uint32_t *tau;
+  uint64_t hit[3], miss, evict[3], disk_writes, hit_pos_sum, bytetime, after_hole;
+  // prefetched state of the next block of the UPDATE pass; every write to that block's tier /
+  // link / heap slot during the current touch is mirrored here, so the copy stays exact
+  uint32_t nx = kNone, nx_hpos = 0;
+  uint8_t nx_tier = 0;
+  uint2 nx_link = make_uint2(0, 0);
+
+  __device__ Rep(const RState &vv, uint64_t cc) : v(vv), c(cc) {}
+  __device__ __forceinline__ uint64_t at(uint32_t b) const { return (uint64_t)b * v.W + c; }
+
+  // ------------------------------------------------------------ lists
+  // tail2[t] = prev link of tail[t], kept current so an eviction needs no dependent load
+  template <int t>
+  __device__ __forceinline__ void l_push_front(uint32_t b) {
+    const uint32_t h = head[t];
+    v.link[at(b)] = make_uint2(kNone, h);
+    if (b == nx) nx_link = make_uint2(kNone, h);
+    if (h != kNone) {
+      v.link[at(h)].x = b;
+      if (h == nx) nx_link.x = b;
+      if (h == tail[t]) tail2[t] = b;
+    } else {
+      tail[t] = b;
+      tail2[t] = kNone;
+    }
+    head[t] = b;
+  }
+  template <int t>
+  __device__ __forceinline__ void l_unlink(uint2 lk) {  // lk = link of the removed block
+    if (lk.x != kNone) {
+      v.link[at(lk.x)].y = lk.y;
+      if (lk.x == nx) nx_link.y = lk.y;
+    } else {
+      head[t] = lk.y;
+    }
+    if (lk.y != kNone) {
+      v.link[at(lk.y)].x = lk.x;
+      if (lk.y == nx) nx_link.x = lk.x;
+      if (lk.y == tail[t]) tail2[t] = lk.x;
+    } else {
+      tail[t] = lk.x;
+      tail2[t] = lk.x != kNone ? v.link[at(lk.x)].x : kNone;
+    }
+  }
+  template <int t>
+  __device__ __forceinline__ uint32_t l_pop_tail() {
+    const uint32_t x = tail[t], p = tail2[t];
+    if (p != kNone) {
+      v.link[at(p)].y = kNone;
+      if (p == nx) nx_link.y = kNone;
+      tail2[t] = v.link[at(p)].x;  // consumed at the next eviction from this tier
+    } else {
+      head[t] = kNone;
+      tail2[t] = kNone;
+    }
+    tail[t] = p;
+    return x;
+  }
+
+  // ------------------------------------------------------------ 4-ary heaps, inline keys
+  // hole-based sift: (key, id) moves from slot i toward the leaves / the root
+  template <int t>
+  __device__ void h_down(uint64_t i, uint64_t key, uint32_t id) {
+    uint64_t *hk = v.hkey[t];
+    uint32_t *hi = v.hid[t];
+    const uint64_t n = size[t];
+    for (;;) {
+      const uint64_t c0 = 4 * i + 1;
+      if (c0 >= n) break;
+      uint64_t ck[4];
+      uint32_t cid[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const bool ok = c0 + q < n;
+        ck[q] = ok ? hk[(c0 + q) * v.W + c] : ~0ull;
+        cid[q] = ok ? hi[(c0 + q) * v.W + c] : 0u;
+      }
+      uint64_t mk = ck[0];
+      uint32_t mid = cid[0], mq = 0;
+#pragma unroll
+      for (int q = 1; q < 4; q++)
+        if (ck[q] < mk) { mk = ck[q]; mid = cid[q]; mq = q; }
+      if (mk >= key) break;
+      hk[i * v.W + c] = mk;
+      hi[i * v.W + c] = mid;
+      v.hpos[at(mid)] = (uint32_t)i;
+      if (mid == nx) nx_hpos = (uint32_t)i;
+      i = c0 + mq;
+    }
+    hk[i * v.W + c] = key;
+    hi[i * v.W + c] = id;
+    v.hpos[at(id)] = (uint32_t)i;
+    if (id == nx) nx_hpos = (uint32_t)i;
+  }
+  template <int t>
+  __device__ void h_up(uint64_t i, uint64_t key, uint32_t id) {
+    uint64_t *hk = v.hkey[t];
+    uint32_t *hi = v.hid[t];
+    while (i > 0) {
+      const uint64_t p = (i - 1) / 4;
+      const uint64_t pk = hk[p * v.W + c];
+      const uint32_t pid = hi[p * v.W + c];
+      if (pk <= key) break;
+      hk[i * v.W + c] = pk;
+      hi[i * v.W + c] = pid;
+      v.hpos[at(pid)] = (uint32_t)i;
+      if (pid == nx) nx_hpos = (uint32_t)i;
+      i = p;
+    }
+    hk[i * v.W + c] = key;
+    hi[i * v.W + c] = id;
+    v.hpos[at(id)] = (uint32_t)i;
+    if (id == nx) nx_hpos = (uint32_t)i;
+  }
+  // remove slot i holding key ki
+  template <int t>
+  __device__ void h_remove(uint64_t i, uint64_t ki) {
+    const uint64_t last = --size[t];
+    if (i == last) return;
+    const uint64_t lk = v.hkey[t][last * v.W + c];
+    const uint32_t lid = v.hid[t][last * v.W + c];
+    if (lk < ki) h_up<t>(i, lk, lid); else h_down<t>(i, lk, lid);
+  }
+
+  // ------------------------------------------------------------ expiry heap (4-ary, packed)
+  __device__ void e_down(uint64_t i, uint64_t key) {
+    const uint64_t n = esize;
+    for (;;) {
+      const uint64_t c0 = 4 * i + 1;
+      if (c0 >= n) break;
+      uint64_t ck[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) ck[q] = c0 + q < n ? v.ekey[(c0 + q) * v.W + c] : ~0ull;
+      uint64_t mk = ck[0];
+      uint32_t mq = 0;
+#pragma unroll
+      for (int q = 1; q < 4; q++)
+        if (ck[q] < mk) { mk = ck[q]; mq = q; }
+      if (mk >= key) break;
+      v.ekey[i * v.W + c] = mk;
+      v.epos[at((uint32_t)mk)] = (uint32_t)i;
+      i = c0 + mq;
+    }
+    v.ekey[i * v.W + c] = key;
+    v.epos[at((uint32_t)key)] = (uint32_t)i;
+  }
+  __device__ void e_up(uint64_t i, uint64_t key) {
+    while (i > 0) {
+      const uint64_t p = (i - 1) / 4;
+      const uint64_t pk = v.ekey[p * v.W + c];
+      if (pk <= key) break;
+      v.ekey[i * v.W + c] = pk;
+      v.epos[at((uint32_t)pk)] = (uint32_t)i;
+      i = p;
+    }
+    v.ekey[i * v.W + c] = key;
+    v.epos[at((uint32_t)key)] = (uint32_t)i;
+  }
+  __device__ void e_remove_at(uint64_t i, uint32_t b) {
+    const uint64_t last = --esize;
+    v.epos[at(b)] = kNone;
+    if (i == last) return;
+    const uint64_t lk = v.ekey[last * v.W + c];
+    const uint64_t ki = v.ekey[i * v.W + c];
+    if (lk < ki) e_up(i, lk); else e_down(i, lk);
+  }
+  __device__ __forceinline__ void e_remove(uint32_t b) {
+    const uint32_t i = v.epos[at(b)];
+    if (i != kNone) e_remove_at(i, b);
+  }
+
+  // ------------------------------------------------------------ tiers (t = 0, 1, 2)
+  // insert b (not resident) into tier t; key = LFU key
+  template <int t>
+  __device__ __forceinline__ void t_insert(uint32_t b, uint64_t key) {
+    v.tier[at(b)] = (uint8_t)(t + 1);
+    if (b == nx) nx_tier = (uint8_t)(t + 1);
+    if (LFU) h_up<t>(size[t]++, key, b);
+    else { l_push_front<t>(b); size[t]++; }
+    if (EXP && t == 2) {
+      const uint32_t tg = tau[v.gblk[b]];
+      if (tg != KARETO_TTL_INF) {
+        const uint64_t e = (uint64_t)v.lt[at(b)] + tg;
+        e_up(esize++, ((e < 0xFFFFFFFFull ? e : 0xFFFFFFFFull) << 32) | b);
+      }
+    }
+  }
+  // remove resident b (link / heap slot already loaded) from tier t
+  template <int t>
+  __device__ __forceinline__ uint64_t t_remove(uint32_t b, uint2 lk, uint32_t hp) {
+    uint64_t key = 0;
+    if (LFU) {
+      key = v.hkey[t][(uint64_t)hp * v.W + c];
+      h_remove<t>(hp, key);
+    } else {
+      l_unlink<t>(lk);
+      size[t]--;
+    }
+    if (EXP && t == 2) e_remove(b);
+    return key;
+  }
+  // one CASCADE level: tier t overflows by at most one block; returns false when done
+  template <int t>
+  __device__ __forceinline__ bool overflow() {
+    const uint64_t capt = (t == 2 && ttl_mode) ? 0 : cap[t];
+    if (size[t] <= capt) return false;
+    uint32_t x;
+    uint64_t key = 0;
+    if (LFU) {
+      x = v.hid[t][c];
+      key = v.hkey[t][c];
+      h_remove<t>(0, key);
+    } else {
+      x = l_pop_tail<t>();
+      size[t]--;
+    }
+    if (EXP && t == 2) e_remove(x);
+    evict[t] += 1;
+    const bool next = ttl_mode ? (t == 0) : (t < 2);
+    if (!next) {
+      v.tier[at(x)] = T_NONE;
+      if (x == nx) nx_tier = T_NONE;
+      return false;
+    }
+    seq += 1;
+    if (t < 2) t_insert<(t < 2 ? t + 1 : 2)>(x, key);  // LFU key (freq, last_seq) carried
+    return true;
+  }
+  __device__ __forceinline__ void cascade() {
+    if (overflow<0>() && overflow<1>()) overflow<2>();
+  }
+
+  __device__ void run(const ReplayTrace &T, const kareto_config &cf, const uint32_t *rows, int n_tuner, int G,
+                      kareto_counts *out) {
+    cap[0] = cf.cap[0];
+    cap[1] = cf.cap[1];
+    cap[2] = cf.cap[2];
+    lru = cf.policy == KARETO_LRU;
+    ttl_mode = cf.cap[2] == KARETO_INF;
+    tau = rows + (size_t)(n_tuner > 0 ? cf.tuner : 0) * G;
+    bool any_finite = false;
+    for (int g = 0; g < G; g++) any_finite |= tau[g] != KARETO_TTL_INF;
+#pragma unroll
+    for (int t = 0; t < 3; t++) {
+      head[t] = tail[t] = tail2[t] = kNone;
+      size[t] = 0;
+      hit[t] = evict[t] = 0;
+    }
+    miss = disk_writes = hit_pos_sum = bytetime = after_hole = 0;
+    esize = 0;
+    seq = 0;
+    uint32_t s0 = T.s[0];
+    for (uint32_t r = 0; r < T.R; r++) {
+      const uint32_t s1 = T.s[r + 1];
+      const uint32_t nb = s1 - s0;
+      if (nb == 0) continue;
+      const uint32_t a = T.arr[r];
+      const uint32_t tg = tau[T.grp[r]];
+      // 1 PURGE (CAPACITY mode): disk blocks whose expiry key is below a (a - lt > tau_g)
+      if (EXP) {
+        while (esize > 0) {
+          const uint64_t top = v.ekey[c];
+          if ((uint32_t)(top >> 32) >= a) break;
+          const uint32_t x = (uint32_t)top;
+          e_remove_at(0, x);
+          if (LFU) {
+            const uint64_t hp = v.hpos[at(x)];
+            h_remove<2>(hp, v.hkey[2][hp * v.W + c]);
+          } else {
+            l_unlink<2>(v.link[at(x)]);
+            size[2]--;
+          }
+          v.tier[at(x)] = T_NONE;
+        }
+      }
+      // 2 LOOKUP on the pre-request state: block k sits at position s0 + nb - 1 - k
+      bool in_prefix = true;
+      for (uint32_t k0 = 0; k0 < nb; k0 += LOOK) {
+        uint32_t bb[LOOK];
+        uint8_t tt[LOOK];
+        uint32_t ll[LOOK];
+#pragma unroll
+        for (int q = 0; q < LOOK; q++) bb[q] = k0 + q < nb ? T.blk[s1 - 1 - (k0 + q)] : 0u;
+#pragma unroll
+        for (int q = 0; q < LOOK; q++) {
+          const bool ok = k0 + q < nb;
+          tt[q] = ok ? v.tier[at(bb[q])] : 0;
+          ll[q] = ok ? v.lt[at(bb[q])] : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < LOOK; q++) {
+          if (k0 + q >= nb) break;
+          const uint8_t t = tt[q];
+          const bool alive = ll[q] != kNone && (a - ll[q]) <= tg;
+          const bool present = t != T_NONE || (ttl_mode && alive);
+          in_prefix = in_prefix && present;
+          if (in_prefix) {
+            hit[0] += t == T_HBM;
+            hit[1] += t == T_DRAM;
+            hit[2] += t == T_DISK || t == T_NONE;
+            hit_pos_sum += k0 + q;
+          } else {
+            miss += 1;
+            after_hole += t != T_NONE;
+          }
+          disk_writes += ttl_mode && !alive;
+        }
+      }
+      // 3 UPDATE leaf -> root = touch positions s0 .. s1-1 in order; the state of block j+1 is
+      // loaded while block j is processed (mirrored writes keep it exact)
+      uint32_t bn = T.blk[s0];
+      uint32_t bnn = s0 + 1 < s1 ? T.blk[s0 + 1] : 0u;
+      uint8_t t_n = v.tier[at(bn)];
+      uint32_t l_n = v.lt[at(bn)];
+      uint2 lk_n = make_uint2(0, 0);
+      uint32_t hp_n = 0;
+      if (LFU) hp_n = v.hpos[at(bn)];
+      else lk_n = v.link[at(bn)];
+      for (uint32_t j = s0; j < s1; j++) {
+        const uint32_t b = bn;
+        const uint8_t t = t_n;
+        const uint32_t l = l_n;
+        const uint2 lk = lk_n;
+        const uint32_t hp = hp_n;
+        seq += 1;
+        if (j + 1 < s1) {
+          bn = bnn;
+          if (j + 2 < s1) bnn = T.blk[j + 2];
+          nx = bn;
+          nx_tier = v.tier[at(bn)];
+          l_n = v.lt[at(bn)];
+          if (LFU) nx_hpos = v.hpos[at(bn)];
+          else nx_link = v.link[at(bn)];
+        } else {
+          nx = kNone;
+        }
+        if (ttl_mode && l != kNone) {
+          const uint32_t dt = a - l;
+          bytetime += dt < tg ? dt : tg;
+        }
+        v.lt[at(b)] = a;  // before any expiry insertion of b in its own cascade
+        if (t == T_HBM) {
+          if (LFU) {
+            const uint64_t key = v.hkey[0][(uint64_t)hp * v.W + c];
+            h_down<0>(hp, (((key >> 32) + 1) << 32) | seq, b);
+          } else if (lru && head[0] != b) {
+            l_unlink<0>(lk);
+            l_push_front<0>(b);
+          }
+        } else {
+          uint64_t freq = 1;
+          if (t == T_DRAM) freq = (t_remove<1>(b, lk, hp) >> 32) + 1;  // LFU count carried
+          else if (t == T_DISK) freq = (t_remove<2>(b, lk, hp) >> 32) + 1;
+          t_insert<0>(b, (freq << 32) | seq);
+          cascade();
+        }
+        t_n = nx_tier;
+        lk_n = nx_link;
+        hp_n = nx_hpos;
+      }
+      s0 = s1;
+    }
+    if (ttl_mode) {
+      for (uint32_t b = 0; b < T.U; b++)
+        if (v.lt[at(b)] != kNone) bytetime += tau[v.gblk[b]];
+      evict[2] = 0;
+    } else {
+      disk_writes = cap[2] > 0 ? evict[1] : 0;
+      if (any_finite) evict[2] = KARETO_NA;
+    }
+    kareto_counts k;
+    for (int t = 0; t < 3; t++) { k.hit[t] = hit[t]; k.evict[t] = evict[t]; }
+    k.miss = miss;
+    k.disk_writes = disk_writes;
+    k.hit_pos_sum = hit_pos_sum;
+    k.bytetime_block_ms = bytetime;
+    k.resident_after_hole = after_hole;
+    *out = k;
+  }
 };
 
-// ---------------------------------------------------------------- lists (LRU / FIFO)
-__device__ __forceinline__ void l_push_front(const RView &v, RCfg &s, int t, uint32_t b) {
-  uint32_t h = s.head[t - 1];
-  v.ln[v.at(b)] = h;
-  v.lp[v.at(b)] = kNone;
-  if (h != kNone) v.lp[v.at(h)] = b; else s.tail[t - 1] = b;
-  s.head[t - 1] = b;
-}
-__device__ __forceinline__ void l_unlink(const RView &v, RCfg &s, int t, uint32_t b) {
-  uint32_t p = v.lp[v.at(b)], n = v.ln[v.at(b)];
-  if (p != kNone) v.ln[v.at(p)] = n; else s.head[t - 1] = n;
-  if (n != kNone) v.lp[v.at(n)] = p; else s.tail[t - 1] = p;
-}
-
-// ---------------------------------------------------------------- heaps (LFU, expiry)
-__device__ __forceinline__ uint64_t lfu_key(const RView &v, uint32_t b) {
-  return ((uint64_t)v.freq[v.at(b)] << 32) | v.lseq[v.at(b)];
-}
-// position of b in its tier heap is kept in lp[] for LFU
-__device__ void h_swap(const RView &v, uint32_t *hp, uint64_t i, uint64_t j) {
-  uint32_t a = hp[i * v.W + v.c], b = hp[j * v.W + v.c];
-  hp[i * v.W + v.c] = b;
-  hp[j * v.W + v.c] = a;
-  v.lp[v.at(b)] = (uint32_t)i;
-  v.lp[v.at(a)] = (uint32_t)j;
-}
-__device__ void h_up(const RView &v, uint32_t *hp, uint64_t i) {
-  while (i > 0) {
-    uint64_t p = (i - 1) / 2;
-    if (lfu_key(v, hp[i * v.W + v.c]) >= lfu_key(v, hp[p * v.W + v.c])) break;
-    h_swap(v, hp, i, p);
-    i = p;
-  }
-}
-__device__ void h_down(const RView &v, uint32_t *hp, uint64_t n, uint64_t i) {
-  for (;;) {
-    uint64_t l = 2 * i + 1, r = l + 1, m = i;
-    if (l < n && lfu_key(v, hp[l * v.W + v.c]) < lfu_key(v, hp[m * v.W + v.c])) m = l;
-    if (r < n && lfu_key(v, hp[r * v.W + v.c]) < lfu_key(v, hp[m * v.W + v.c])) m = r;
-    if (m == i) break;
-    h_swap(v, hp, i, m);
-    i = m;
-  }
-}
-
-__device__ __forceinline__ uint64_t exp_key(const RView &v, const RCfg &s, uint32_t b) {
-  return (uint64_t)v.last_t[v.at(b)] + s.tau[v.gblk[b]];
-}
-__device__ void e_swap(const RView &v, uint64_t i, uint64_t j) {
-  uint32_t a = v.eheap[i * v.W + v.c], b = v.eheap[j * v.W + v.c];
-  v.eheap[i * v.W + v.c] = b;
-  v.eheap[j * v.W + v.c] = a;
-  v.epos[v.at(b)] = (uint32_t)i;
-  v.epos[v.at(a)] = (uint32_t)j;
-}
-__device__ void e_up(const RView &v, const RCfg &s, uint64_t i) {
-  while (i > 0) {
-    uint64_t p = (i - 1) / 2;
-    if (exp_key(v, s, v.eheap[i * v.W + v.c]) >= exp_key(v, s, v.eheap[p * v.W + v.c])) break;
-    e_swap(v, i, p);
-    i = p;
-  }
-}
-__device__ void e_down(const RView &v, const RCfg &s, uint64_t i) {
-  uint64_t n = s.esize;
-  for (;;) {
-    uint64_t l = 2 * i + 1, r = l + 1, m = i;
-    if (l < n && exp_key(v, s, v.eheap[l * v.W + v.c]) < exp_key(v, s, v.eheap[m * v.W + v.c])) m = l;
-    if (r < n && exp_key(v, s, v.eheap[r * v.W + v.c]) < exp_key(v, s, v.eheap[m * v.W + v.c])) m = r;
-    if (m == i) break;
-    e_swap(v, i, m);
-    i = m;
-  }
-}
-__device__ void e_push(const RView &v, RCfg &s, uint32_t b) {
-  uint64_t i = s.esize++;
-  v.eheap[i * v.W + v.c] = b;
-  v.epos[v.at(b)] = (uint32_t)i;
-  e_up(v, s, i);
-}
-__device__ void e_remove(const RView &v, RCfg &s, uint32_t b) {
-  uint64_t i = v.epos[v.at(b)], last = --s.esize;
-  if (i != last) {
-    e_swap(v, i, last);
-    e_up(v, s, i);
-    e_down(v, s, i);
-  }
-  v.epos[v.at(b)] = kNone;
-}
-
-// ---------------------------------------------------------------- tier operations
-__device__ void t_insert(const RView &v, RCfg &s, int t, uint32_t b) {
-  v.tier[v.at(b)] = (uint8_t)t;
-  if (s.policy == KARETO_LFU) {
-    uint32_t *hp = v.heap[t - 1];
-    uint64_t i = s.size[t - 1];
-    hp[i * v.W + v.c] = b;
-    v.lp[v.at(b)] = (uint32_t)i;
-    s.size[t - 1]++;
-    h_up(v, hp, i);
-  } else {
-    l_push_front(v, s, t, b);
-    s.size[t - 1]++;
-  }
-  if (t == T_DISK && s.use_expiry && s.tau[v.gblk[b]] != KARETO_TTL_INF) e_push(v, s, b);
-}
-__device__ void t_remove(const RView &v, RCfg &s, int t, uint32_t b) {
-  if (s.policy == KARETO_LFU) {
-    uint32_t *hp = v.heap[t - 1];
-    uint64_t i = v.lp[v.at(b)], last = --s.size[t - 1];
-    if (i != last) {
-      h_swap(v, hp, i, last);
-      h_up(v, hp, i);
-      h_down(v, hp, s.size[t - 1], i);
-    }
-  } else {
-    l_unlink(v, s, t, b);
-    s.size[t - 1]--;
-  }
-  if (t == T_DISK && v.epos[v.at(b)] != kNone) e_remove(v, s, b);
-}
-__device__ __forceinline__ uint32_t t_victim(const RView &v, const RCfg &s, int t) {
-  return s.policy == KARETO_LFU ? v.heap[t - 1][v.c] : s.tail[t - 1];
-}
-// reorder after an HBM hit (LRU: move to front; LFU: key grew)
-__device__ void t_touch_hbm(const RView &v, RCfg &s, uint32_t b) {
-  if (s.policy == KARETO_LRU) {
-    l_unlink(v, s, T_HBM, b);
-    l_push_front(v, s, T_HBM, b);
-  } else if (s.policy == KARETO_LFU) {
-    h_down(v, v.heap[0], s.size[0], v.lp[v.at(b)]);
-  }
-}
-
-// CASCADE from HBM after an insertion: each level overflows by at most one block
-__device__ void cascade(const RView &v, RCfg &s) {
-  for (int t = T_HBM; t <= T_DISK; t++) {
-    uint64_t capt = (t == T_DISK && s.ttl_mode) ? 0 : s.cap[t - 1];
-    if (s.size[t - 1] <= capt) return;
-    uint32_t x = t_victim(v, s, t);
-    t_remove(v, s, t, x);
-    s.k.evict[t - 1] += 1;
-    bool next = s.ttl_mode ? (t == T_HBM) : (t < T_DISK);
-    if (!next) {
-      v.tier[v.at(x)] = T_NONE;
-      return;
-    }
-    s.seq += 1;
-    v.iseq[v.at(x)] = s.seq;  // last_seq kept (FIFO order of the lower tier = entry order)
-    t_insert(v, s, t + 1, x);
-  }
-}
-
-__global__ void __launch_bounds__(128) k_replay(ReplayTrace T, const kareto_config *__restrict__ cfg,
-                                                const uint32_t *__restrict__ rows, int n_tuner, int G, RView v0,
-                                                int64_t n, kareto_counts *__restrict__ out) {
+template <bool LFU, bool EXP>
+__global__ void __launch_bounds__(64) k_replay(ReplayTrace T, const kareto_config *__restrict__ cfg,
+                                               const uint32_t *__restrict__ idx, const uint32_t *__restrict__ rows,
+                                               int n_tuner, int G, RState v, int64_t n,
+                                               kareto_counts *__restrict__ out) {
   const int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (ci >= n) return;
-  RView v = v0;
-  v.c = (uint32_t)ci;
-  RCfg s;
-  const kareto_config c = cfg[ci];
-  s.cap[0] = c.cap[0];
-  s.cap[1] = c.cap[1];
-  s.cap[2] = c.cap[2];
-  s.policy = c.policy;
-  s.ttl_mode = c.cap[2] == KARETO_INF;
-  s.tau = rows + (size_t)(n_tuner > 0 ? c.tuner : 0) * G;
-  bool any_finite = false;
-  for (int g = 0; g < G; g++) any_finite |= s.tau[g] != KARETO_TTL_INF;
-  s.use_expiry = !s.ttl_mode && any_finite;
-  for (int t = 0; t < 3; t++) { s.head[t] = s.tail[t] = kNone; s.size[t] = 0; }
-  s.esize = 0;
-  s.seq = 0;
-  memset(&s.k, 0, sizeof(s.k));
-  for (uint32_t r = 0; r < T.R; r++) {
-    const uint32_t s0 = T.s[r], nb = T.s[r + 1] - s0;
-    if (nb == 0) continue;
-    const uint32_t a = T.arr[r];
-    const uint32_t tg = s.tau[T.grp[r]];
-    // 1 PURGE (CAPACITY mode): disk blocks with a - last_t > tau_g
-    if (s.use_expiry) {
-      while (s.esize > 0) {
-        uint32_t x = v.eheap[v.c];
-        if (exp_key(v, s, x) >= a) break;
-        t_remove(v, s, T_DISK, x);  // also leaves the expiry heap
-        v.tier[v.at(x)] = T_NONE;
-      }
-    }
-    // 2 LOOKUP on the pre-request state (block k sits at position s0 + nb - 1 - k)
-    bool in_prefix = true;
-    for (uint32_t k = 0; k < nb; k++) {
-      const uint32_t b = T.blk[s0 + nb - 1 - k];
-      const uint8_t t = v.tier[v.at(b)];
-      const uint32_t ls = v.lease[v.at(b)];  // kNone = never seen
-      const bool alive = ls != kNone && (a - ls) <= tg;
-      const bool present = t != T_NONE || (s.ttl_mode && alive);
-      if (in_prefix && !present) in_prefix = false;
-      if (in_prefix) {
-        s.k.hit[(t != T_NONE ? t : T_DISK) - 1] += 1;
-        s.k.hit_pos_sum += k;
-      } else {
-        s.k.miss += 1;
-        if (t != T_NONE) s.k.resident_after_hole += 1;
-      }
-      if (s.ttl_mode && !alive) s.k.disk_writes += 1;
-    }
-    // 3 UPDATE leaf -> root
-    for (uint32_t kk = nb; kk-- > 0;) {
-      const uint32_t b = T.blk[s0 + nb - 1 - kk];
-      s.seq += 1;
-      const uint8_t t = v.tier[v.at(b)];
-      if (t == T_HBM) {
-        if (s.policy == KARETO_LRU) { v.lseq[v.at(b)] = s.seq; t_touch_hbm(v, s, b); }
-        else if (s.policy == KARETO_LFU) { v.freq[v.at(b)] += 1; v.lseq[v.at(b)] = s.seq; t_touch_hbm(v, s, b); }
-      } else {
-        if (t == T_DRAM || t == T_DISK) {
-          t_remove(v, s, t, b);
-          v.freq[v.at(b)] += 1;  // LFU count carried across tiers
-        } else {
-          v.freq[v.at(b)] = 1;
-        }
-        v.lseq[v.at(b)] = s.seq;
-        v.iseq[v.at(b)] = s.seq;
-        t_insert(v, s, T_HBM, b);
-        cascade(v, s);
-      }
-      const uint32_t ls = v.lease[v.at(b)];
-      if (s.ttl_mode && ls != kNone) {
-        uint32_t dt = a - ls;
-        s.k.bytetime_block_ms += dt < tg ? dt : tg;
-      }
-      v.last_t[v.at(b)] = a;
-      if (v.tier[v.at(b)] == T_DISK && v.epos[v.at(b)] != kNone) {  // demoted in its own cascade
-        e_up(v, s, v.epos[v.at(b)]);
-        e_down(v, s, v.epos[v.at(b)]);
-      }
-      v.lease[v.at(b)] = a;
-    }
-  }
-  if (s.ttl_mode) {
-    for (uint32_t b = 0; b < T.U; b++)
-      if (v.lease[v.at(b)] != kNone) s.k.bytetime_block_ms += s.tau[v.gblk[b]];
-    s.k.evict[2] = 0;
-  } else {
-    s.k.disk_writes = s.cap[2] > 0 ? s.k.evict[1] : 0;
-    if (any_finite) s.k.evict[2] = KARETO_NA;
-  }
-  out[ci] = s.k;
+  const uint32_t id = idx[ci];
+  Rep<LFU, EXP> rp(v, (uint64_t)ci);
+  rp.run(T, cfg[id], rows, n_tuner, G, out + id);
 }
 
 // ---------------------------------------------------------------- dense block ids
@@ -372,45 +532,103 @@ kareto_status replay_prepare(kareto_ctx *ctx, kareto_trace *tr) {
 }
 
 kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config *cfg_host, int64_t n,
-                          const uint32_t *rows_dev, int n_tuner, kareto_counts *counts_dev) {
+                          const uint32_t *rows_host, const uint32_t *rows_dev, int n_tuner,
+                          kareto_counts *counts_dev) {
   if (n <= 0) return KARETO_OK;
   KTRY(replay_prepare(ctx, tr));
   cudaStream_t st = ctx->stream;
   const uint64_t U = tr->U > 0 ? (uint64_t)tr->U : 1;
+  const int G = tr->K + 1;
   ReplayTrace T{(uint32_t)tr->R, (uint32_t)tr->U, tr->s, tr->arr_rel, tr->grp, tr->blk};
-  // wave size from free memory: per (block, config) 1 + 8*4 bytes + heaps 4*4 bytes
-  size_t freeb = 0, totb = 0;
-  KCUDA(ctx, cudaMemGetInfo(&freeb, &totb));
-  const uint64_t per_cfg = U * (1 + 8 * 4 + 4 * 4) + 64;
-  uint64_t W = (uint64_t)(0.5 * (double)freeb) / per_cfg;
-  if (W > 16384) W = 16384;
-  if (W > (uint64_t)n) W = (uint64_t)n;
-  if (W < 1) return fail(ctx, KARETO_E_OOM, "replay needs %llu bytes per configuration", (unsigned long long)per_cfg);
-  DBuf<uint8_t> tier;
-  DBuf<uint32_t> lp, ln, lseq, iseq, freq, last_t, lease, epos, heap, eheap;
-  KTRY(tier.alloc(ctx, U * W));
-  for (DBuf<uint32_t> *b : {&lp, &ln, &lseq, &iseq, &freq, &last_t, &lease, &epos, &eheap}) KTRY(b->alloc(ctx, U * W));
-  KTRY(heap.alloc(ctx, 3 * (U + 2) * W));
+  // classes {list, LFU} x {expiry heap or not}; within a class, neighbours in a warp get
+  // similar configurations (policy, TTL row, capacities) so their branches agree more often
+  std::vector<uint32_t> cls[4];
+  for (int64_t i = 0; i < n; i++) {
+    const kareto_config &c = cfg_host[i];
+    const uint32_t *tau = rows_host + (size_t)(n_tuner > 0 ? c.tuner : 0) * G;
+    bool any_finite = false;
+    for (int g = 0; g < G; g++) any_finite |= tau[g] != KARETO_TTL_INF;
+    const bool exp = c.cap[2] != KARETO_INF && any_finite;
+    cls[(c.policy == KARETO_LFU ? 2 : 0) + (exp ? 1 : 0)].push_back((uint32_t)i);
+  }
   DBuf<kareto_config> dcfg;
   KTRY(dcfg.alloc(ctx, n));
   KCUDA(ctx, cudaMemcpyAsync(dcfg.p, cfg_host, sizeof(kareto_config) * n, cudaMemcpyHostToDevice, st));
-  for (int64_t w0 = 0; w0 < n; w0 += (int64_t)W) {
-    int64_t nw = n - w0 < (int64_t)W ? n - w0 : (int64_t)W;
-    KCUDA(ctx, cudaMemsetAsync(tier.p, 0, U * W, st));
-    KCUDA(ctx, cudaMemsetAsync(lease.p, 0xFF, 4 * U * W, st));
-    KCUDA(ctx, cudaMemsetAsync(epos.p, 0xFF, 4 * U * W, st));
-    KCUDA(ctx, cudaMemsetAsync(freq.p, 0, 4 * U * W, st));
-    RView v{};
-    v.tier = tier.p; v.lp = lp.p; v.ln = ln.p; v.lseq = lseq.p; v.iseq = iseq.p; v.freq = freq.p;
-    v.last_t = last_t.p; v.lease = lease.p; v.epos = epos.p;
-    v.heap[0] = heap.p; v.heap[1] = heap.p + (U + 2) * W; v.heap[2] = heap.p + 2 * (U + 2) * W;
-    v.eheap = eheap.p;
+  for (int q = 0; q < 4; q++) {
+    std::vector<uint32_t> &ix = cls[q];
+    if (ix.empty()) continue;
+    const bool lfu = q >= 2, exp = q & 1;
+    std::stable_sort(ix.begin(), ix.end(), [&](uint32_t a, uint32_t b) {
+      const kareto_config &x = cfg_host[a], &y = cfg_host[b];
+      if (x.policy != y.policy) return x.policy < y.policy;
+      if (x.tuner != y.tuner) return x.tuner < y.tuner;
+      for (int t = 0; t < 3; t++)
+        if (x.cap[t] != y.cap[t]) return x.cap[t] < y.cap[t];
+      return false;
+    });
+    // heap slots per tier (LFU): a tier holds at most min(cap + 1, U) blocks
+    uint64_t hs[3] = {0, 0, 0};
+    for (uint32_t i : ix)
+      for (int t = 0; t < 3; t++) {
+        uint64_t cp = cfg_host[i].cap[t];
+        if (t == 2 && cp == KARETO_INF) cp = 0;
+        uint64_t m = (cp < U ? cp + 1 : U) + 1;
+        if (m > hs[t]) hs[t] = m;
+      }
+    const uint64_t es = U + 1;
+    uint64_t per_cfg = U * (1 + 4) + (lfu ? U * 4 + 12 * (hs[0] + hs[1] + hs[2]) : U * 8) + (exp ? U * 4 + 8 * es : 0);
+    size_t freeb = 0, totb = 0, rsv = 0, used = 0;
+    KCUDA(ctx, cudaStreamSynchronize(st));
+    KCUDA(ctx, cudaMemGetInfo(&freeb, &totb));
+    cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, &rsv);
+    cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    const double avail = (double)freeb + (double)(rsv > used ? rsv - used : 0);
+    uint64_t W = (uint64_t)(0.6 * avail) / per_cfg;
+    if (W > (1u << 20)) W = 1u << 20;
+    if (W > ix.size()) W = ix.size();
+    if (W < 1) return fail(ctx, KARETO_E_OOM, "replay needs %llu bytes per configuration", (unsigned long long)per_cfg);
+    // balance the waves
+    const uint64_t nwaves = (ix.size() + W - 1) / W;
+    W = (ix.size() + nwaves - 1) / nwaves;
+    DBuf<uint8_t> tier;
+    DBuf<uint32_t> lt, hpos, epos, hid, didx;
+    DBuf<uint2> link;
+    DBuf<uint64_t> hkey, ekey;
+    KTRY(tier.alloc(ctx, U * W)); KTRY(lt.alloc(ctx, U * W));
+    if (lfu) {
+      KTRY(hpos.alloc(ctx, U * W));
+      KTRY(hkey.alloc(ctx, (hs[0] + hs[1] + hs[2]) * W)); KTRY(hid.alloc(ctx, (hs[0] + hs[1] + hs[2]) * W));
+    } else {
+      KTRY(link.alloc(ctx, U * W));
+    }
+    if (exp) { KTRY(epos.alloc(ctx, U * W)); KTRY(ekey.alloc(ctx, es * W)); }
+    KTRY(didx.alloc(ctx, ix.size()));
+    KCUDA(ctx, cudaMemcpyAsync(didx.p, ix.data(), 4 * ix.size(), cudaMemcpyHostToDevice, st));
+    RState v{};
+    v.tier = tier.p; v.lt = lt.p; v.link = link.p; v.hpos = hpos.p;
+    if (lfu) {
+      v.hkey[0] = hkey.p; v.hkey[1] = hkey.p + hs[0] * W; v.hkey[2] = hkey.p + (hs[0] + hs[1]) * W;
+      v.hid[0] = hid.p; v.hid[1] = hid.p + hs[0] * W; v.hid[2] = hid.p + (hs[0] + hs[1]) * W;
+    }
+    v.epos = epos.p; v.ekey = ekey.p;
     v.gblk = tr->gblk;
     v.W = W;
-    Pass ps(ctx, "K6_replay", 1, 1);
-    k_replay<<<grid_for(nw, 128), 128, 0, st>>>(T, dcfg.p + w0, rows_dev, n_tuner, tr->K + 1, v, nw, counts_dev + w0);
+    for (uint64_t w0 = 0; w0 < ix.size(); w0 += W) {
+      const int64_t nw = (int64_t)(ix.size() - w0 < W ? ix.size() - w0 : W);
+      KCUDA(ctx, cudaMemsetAsync(tier.p, 0, U * W, st));
+      KCUDA(ctx, cudaMemsetAsync(lt.p, 0xFF, 4 * U * W, st));
+      if (exp) KCUDA(ctx, cudaMemsetAsync(epos.p, 0xFF, 4 * U * W, st));
+      Pass ps(ctx, "K6_replay", 1, 1);
+      const unsigned grid = (unsigned)((nw + 63) / 64);
+      const uint32_t *wi = didx.p + w0;
+      if (q == 0) k_replay<false, false><<<grid, 64, 0, st>>>(T, dcfg.p, wi, rows_dev, n_tuner, G, v, nw, counts_dev);
+      if (q == 1) k_replay<false, true><<<grid, 64, 0, st>>>(T, dcfg.p, wi, rows_dev, n_tuner, G, v, nw, counts_dev);
+      if (q == 2) k_replay<true, false><<<grid, 64, 0, st>>>(T, dcfg.p, wi, rows_dev, n_tuner, G, v, nw, counts_dev);
+      if (q == 3) k_replay<true, true><<<grid, 64, 0, st>>>(T, dcfg.p, wi, rows_dev, n_tuner, G, v, nw, counts_dev);
+    }
+    KTRY(sync(ctx, "replay"));
   }
-  return sync(ctx, "replay");
+  return KARETO_OK;
 }
 
 }  // namespace kareto

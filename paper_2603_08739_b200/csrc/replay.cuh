@@ -16,8 +16,10 @@ struct ReplayTrace {
 
 // dense block ids / groups / relative arrivals (lazily, cached in the trace)
 kareto_status replay_prepare(kareto_ctx *ctx, kareto_trace *tr);
-// counts of n configurations (host array) into counts_dev[n]; rows_dev = [max(n_tuner,1)][K+1]
+// counts of n configurations (host array) into counts_dev[n]; rows = [max(n_tuner,1)][K+1]
+// TTL rows, on the host and on the device
 kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config *cfg_host, int64_t n,
-                          const uint32_t *rows_dev, int n_tuner, kareto_counts *counts_dev);
+                          const uint32_t *rows_host, const uint32_t *rows_dev, int n_tuner,
+                          kareto_counts *counts_dev);
 
 }  // namespace kareto

@@ -155,3 +155,18 @@ def replay(chains_sorted, cap, policy, tau):
         if any(t is not None for t in tau):
             c["evict"][2] = 0xFFFFFFFFFFFFFFFF
     return c
+
+
+def hypervolume_cells(points, ref):
+    """Brute-force 3-D hypervolume on the grid of all point coordinates: a cell is dominated
+    iff some point is <= its lower corner in every coordinate (no sorting, no sweeping)."""
+    axes = [sorted({float(p[a]) for p in points} | {float(ref[a])}) for a in range(3)]
+    vol = 0.0
+    for i in range(len(axes[0]) - 1):
+        for j in range(len(axes[1]) - 1):
+            for k in range(len(axes[2]) - 1):
+                lo = (axes[0][i], axes[1][j], axes[2][k])
+                if any(p[0] <= lo[0] and p[1] <= lo[1] and p[2] <= lo[2] for p in points):
+                    vol += ((axes[0][i + 1] - axes[0][i]) * (axes[1][j + 1] - axes[1][j])
+                            * (axes[2][k + 1] - axes[2][k]))
+    return vol

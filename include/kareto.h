@@ -195,6 +195,45 @@ kareto_status kareto_pareto(kareto_ctx *ctx, const double *obj, const kareto_con
  * n configurations that `rank` of `world` evaluates inside kareto_eval_grid. */
 kareto_status kareto_shard_range(int64_t n, int32_t rank, int32_t world, int64_t *lo, int64_t *hi);
 
+/* ------------------------------------------------------ row f1: search ---- */
+/* Exact 3-D hypervolume ("We compute hypervolume using an identical dominated
+ * reference point"; R41): the Lebesgue measure of the union of the boxes [obj_i, ref] of the
+ * points with mask[i] != 0 (mask NULL: all n), minimisation in all three objectives.
+ *   obj   [n][3] device (on_device = 1) or host (0); mask [n] same space or NULL;
+ *   ref   host [3]; hv_out host.
+ * Errors: KARETO_E_INVALID when some selected point is not strictly better than ref in every
+ * objective (the message names its index) or n < 0. */
+kareto_status kareto_hypervolume(kareto_ctx *ctx, const double *obj, const uint8_t *mask, int64_t n,
+                                 const double ref[3], double *hv_out, int32_t on_device);
+
+/* Alg. 1 "Adaptive Pareto Exploration" over the DRAM-capacity x disk-TTL
+ * plane: HBM fixed at hbm_gb; DRAM d GB; TTL (lease) mode with a uniform disk TTL of t seconds
+ * for every group; GB -> blocks = floor(GB * 1e9 / block_bytes) (R14).  Each round's
+ * candidates are evaluated in one kareto_eval_grid call (sharded over the context's ranks);
+ * the expansion / refinement decisions follow DESIGN.md R36-R40. */
+typedef struct {
+  double hbm_gb;                      /* fixed HBM capacity per instance, GB               */
+  int64_t d_min, d_max, d_step;       /* initial DRAM range and step, GB (d_step >= 1)     */
+  int64_t t_min, t_max, t_step;       /* initial disk-TTL range and step, s (t_step >= 1)  */
+  double tau_e, tau_perf, tau_cost;   /* expand / refine thresholds, relative (R36)        */
+  int32_t policy;                     /* KARETO_LRU (stack path) / _FIFO / _LFU (K6)       */
+  int32_t max_rounds;                 /* 0 = until no candidates remain                    */
+} kareto_search_params;
+typedef struct {
+  int64_t d_gb, t_s;                  /* the evaluated configuration                       */
+  double obj[3];                      /* mean TTFT ms, -tokens/s, cost $                   */
+  int32_t round;                      /* evaluation round (0 = the seed grid)              */
+  uint8_t status;                     /* 1: on the Pareto frontier of all evaluated points */
+  uint8_t pad[3];
+} kareto_search_point;                /* 48 bytes */
+/* out: host [cap] in evaluation order (rounds ascending, (d, t) ascending within a round);
+ * *n_out = number evaluated; *truncated = 1 when a round would have exceeded cap or
+ * max_rounds (that round is not evaluated, R40).  Errors: KARETO_E_INVALID (bad ranges /
+ * steps / thresholds, t * 1000 >= 2^32 - 1 ms), plus those of kareto_eval_grid. */
+kareto_status kareto_search(kareto_ctx *ctx, const kareto_trace *tr, const kareto_search_params *params,
+                            const kareto_model *model, kareto_search_point *out, int64_t cap, int64_t *n_out,
+                            int32_t *truncated);
+
 /* ------------------------------------------------------------ profiling ---- */
 typedef struct {
   char name[24];      /* kernel / pass name                                         */

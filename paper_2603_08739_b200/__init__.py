@@ -75,6 +75,19 @@ class PruneC(ctypes.Structure):
     _fields_ = [("enabled", ctypes.c_int32), ("tau_e", ctypes.c_double)]
 
 
+class SearchParamsC(ctypes.Structure):
+    _fields_ = [("hbm_gb", ctypes.c_double), ("d_min", ctypes.c_int64), ("d_max", ctypes.c_int64),
+                ("d_step", ctypes.c_int64), ("t_min", ctypes.c_int64), ("t_max", ctypes.c_int64),
+                ("t_step", ctypes.c_int64), ("tau_e", ctypes.c_double), ("tau_perf", ctypes.c_double),
+                ("tau_cost", ctypes.c_double), ("policy", ctypes.c_int32), ("max_rounds", ctypes.c_int32)]
+
+
+# kareto_search_point (48 bytes)
+SEARCH_POINT_DTYPE = np.dtype([("d_gb", np.int64), ("t_s", np.int64), ("obj", np.float64, 3), ("round", np.int32),
+                               ("status", np.uint8), ("pad", np.uint8, 3)])
+assert SEARCH_POINT_DTYPE.itemsize == 48
+
+
 class PassTime(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 24), ("ms", ctypes.c_double), ("launches", ctypes.c_int32),
                 ("own", ctypes.c_int32)]
@@ -86,7 +99,7 @@ _lib = None
 ABI_FUNCTIONS = ["kareto_create", "kareto_destroy", "kareto_last_error", "kareto_nccl_unique_id",
                  "kareto_load_trace", "kareto_trace_free", "kareto_trace_stats", "kareto_trace_export",
                  "kareto_eval_grid", "kareto_pareto", "kareto_set_profiling", "kareto_get_pass_times",
-                 "kareto_launch_counter", "kareto_shard_range"]
+                 "kareto_launch_counter", "kareto_shard_range", "kareto_hypervolume", "kareto_search"]
 
 
 def load_library(path: str = LIB_PATH):
@@ -111,6 +124,10 @@ def load_library(path: str = LIB_PATH):
     L.kareto_trace_export.argtypes = [vp, vp, i32, vp]
     L.kareto_eval_grid.argtypes = [vp, vp, vp, i64, vp, i32, ctypes.POINTER(ModelC), vp, vp, i32]
     L.kareto_pareto.argtypes = [vp, vp, vp, i64, ctypes.POINTER(PruneC), vp, ctypes.POINTER(i64), i32]
+    L.kareto_hypervolume.argtypes = [vp, vp, vp, i64, ctypes.POINTER(ctypes.c_double * 3),
+                                     ctypes.POINTER(ctypes.c_double), i32]
+    L.kareto_search.argtypes = [vp, vp, ctypes.POINTER(SearchParamsC), ctypes.POINTER(ModelC), vp, i64,
+                                ctypes.POINTER(i64), ctypes.POINTER(i32)]
     L.kareto_set_profiling.argtypes = [vp, i32]
     L.kareto_get_pass_times.argtypes = [vp, ctypes.POINTER(PassTime), i32, ctypes.POINTER(i32), i32]
     L.kareto_launch_counter.argtypes = [vp, ctypes.POINTER(i64), i32]
@@ -297,6 +314,32 @@ class Context:
         self._check(self._L.kareto_pareto(self._h, po, None if cf is None else cf.ctypes.data, n, ctypes.byref(pr),
                                           ps, ctypes.byref(nf), int(dev)), "pareto")
         return status, int(nf.value)
+
+    def hypervolume(self, obj, ref, mask=None) -> float:
+        """kareto_hypervolume: exact 3-D hypervolume of the (masked) points w.r.t. ref (row f1)."""
+        n = int(obj.shape[0])
+        po, dev = _ptr(obj)
+        pm, mdev = _ptr(mask)
+        assert mask is None or mdev == dev, "obj and mask must both be host or both be device buffers"
+        r = (ctypes.c_double * 3)(*[float(v) for v in ref])
+        hv = ctypes.c_double()
+        self._check(self._L.kareto_hypervolume(self._h, po, pm, n, ctypes.byref(r), ctypes.byref(hv), int(dev)),
+                    "hypervolume")
+        return float(hv.value)
+
+    def search(self, trace: "Trace", model: Model, d_range, t_range, hbm_gb: float, tau_e=0.05, tau_perf=0.05,
+               tau_cost=0.02, policy=LRU, max_rounds=0, cap=1 << 16):
+        """kareto_search: Alg. 1 adaptive Pareto exploration (row f1).  d_range / t_range =
+        (min, max, step) in GB / s.  Returns (points [SEARCH_POINT_DTYPE], truncated)."""
+        p = SearchParamsC(float(hbm_gb), *[int(v) for v in d_range], *[int(v) for v in t_range], float(tau_e),
+                          float(tau_perf), float(tau_cost), int(policy), int(max_rounds))
+        out = np.zeros(int(cap), SEARCH_POINT_DTYPE)
+        n, tr_ = ctypes.c_int64(), ctypes.c_int32()
+        m = model.c()
+        self._check(self._L.kareto_search(self._h, trace._h, ctypes.byref(p), ctypes.byref(m),
+                                          out.ctypes.data if cap else None, int(cap), ctypes.byref(n),
+                                          ctypes.byref(tr_)), "search")
+        return out[:n.value].copy(), bool(tr_.value)
 
 
 class Trace:

@@ -319,6 +319,73 @@ def run_reference(args, spec):
     print(json.dumps(line), flush=True)
 
 
+def run_search(args, K, ctx, tr, rank, spec, lengths):
+    """Row f1 measurement, the P:856 protocol on a synthetic trace: grid search over DRAM
+    0-4096 GB step 256 x disk TTL 0-3600 s step 120 (17 x 31 = 527 configurations, one batched
+    kareto_eval_grid + kareto_pareto) against Alg. 1 seeded with DRAM 0-2048 GB step 512 x TTL
+    0-2400 s step 600 (kareto_search); both frontiers' hypervolumes against one reference point
+    strictly worse than every evaluated configuration (kareto_hypervolume).  HBM fixed, LRU,
+    TTL (lease) mode with a uniform TTL; times are host wall clock around the synchronous calls
+    with the trace resident, after one untimed run of each."""
+    import torch
+    # instance count from the no-cache work (SURVEY 8.d.3): I = max(1, round(busy_0 / (rho0 span))),
+    # rho0 = 1.3 ("ins1-like", compute-constrained, P:806-808)
+    m0 = K.Model()
+    L = lengths.astype(np.int64)
+    busy0 = (m0.alpha_ps * int(L.sum()) + m0.beta_ps * int((L * (L - 1) // 2).sum()) + m0.dec_ps * tr.O) * 1e-12
+    inst = max(1, round(busy0 / (1.3 * tr.span_ms * 1e-3)))
+    model = K.Model(instances=inst)
+    Bb = model.block_bytes
+    hbm = int(args.search_hbm_gb * 1e9) // Bb
+    ds, ts = list(range(0, 4097, 256)), list(range(0, 3601, 120))
+    cfg = np.zeros(len(ds) * len(ts), K.CONFIG_DTYPE)
+    rows = np.array([[t * 1000] * (tr.K + 1) for t in ts], np.uint32)
+    for a, d in enumerate(ds):
+        for b, t in enumerate(ts):
+            i = a * len(ts) + b
+            cfg[i]["cap"] = (hbm, d * 10**9 // Bb, K.INF)
+            cfg[i]["tuner"] = b
+            cfg[i]["axis"] = (a, b, 0)
+
+    def grid():
+        _, obj = ctx.eval_grid(tr, cfg, model, rows)
+        st, _ = ctx.pareto(obj, cfg, None)
+        return obj, st
+
+    def adaptive():
+        return ctx.search(tr, model, (0, 2048, 512), (0, 2400, 600), args.search_hbm_gb)
+
+    grid(), adaptive()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    obj, st = grid()
+    t_grid = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    pts, trunc = adaptive()
+    t_ad = time.perf_counter() - t0
+    allf = np.vstack([obj, pts["obj"]])
+    ref = allf.max(0) + np.abs(allf.max(0)) * 0.01 + 1e-12
+    t0 = time.perf_counter()
+    hv_g = ctx.hypervolume(obj, ref, mask=(st == 1).astype(np.uint8))
+    t_hv = time.perf_counter() - t0
+    hv_a = ctx.hypervolume(np.ascontiguousarray(pts["obj"]), ref, mask=(pts["status"] == 1).astype(np.uint8))
+    if rank == 0:
+        line = {"metric": "adaptive search (Alg. 1) vs grid search (P:856 protocol)", "unit": "evaluations",
+                "grid_evals": int(len(cfg)), "adaptive_evals": int(len(pts)),
+                "adaptive_rounds": int(pts["round"].max()) + 1 if len(pts) else 0, "truncated": bool(trunc),
+                "hv_grid": hv_g, "hv_adaptive": hv_a, "hv_ratio": hv_a / hv_g if hv_g > 0 else None,
+                "frontier_grid": int((st == 1).sum()), "frontier_adaptive": int((pts["status"] == 1).sum()),
+                "grid_s": t_grid, "adaptive_s": t_ad, "hypervolume_s": t_hv, "reference_point": ref.tolist(),
+                "config": {"workload": spec["desc"], "n_accesses": tr.N, "hbm_gb": args.search_hbm_gb,
+                           "instances": inst, "rho0": 1.3,
+                           "policy": "LRU, TTL (lease) mode, uniform disk TTL", "block_bytes": Bb,
+                           "grid": "DRAM 0-4096 GB step 256 x TTL 0-3600 s step 120",
+                           "seed": "DRAM 0-2048 GB step 512 x TTL 0-2400 s step 600",
+                           "thresholds": {"tau_e": 0.05, "tau_perf": 0.05, "tau_cost": 0.02}},
+                "data": "synthetic", "timing": "host wall clock around synchronous ABI calls, trace resident"}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -330,6 +397,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sample-requests", type=int, default=50_000)
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no cpu baseline / e2e)")
+    ap.add_argument("--search", action="store_true",
+                    help="row f1: Alg. 1 adaptive search vs the P:856 grid search on the config's trace")
+    ap.add_argument("--search-hbm-gb", type=float, default=320.0)
     args = ap.parse_args()
     spec = CONFIGS[args.config]
     if args.impl == "reference":
@@ -370,6 +440,10 @@ def main():
 
     def load_dev():
         return ctx.load_trace(arr_d, out_d, off_d, tokens=tok_d, top_k=top_k)
+
+    if args.search:
+        run_search(args, K, ctx, load_dev(), rank, spec, np.diff(off_h.numpy()))
+        return
 
     tr = load_dev()
     N, U = tr.N, tr.U

@@ -370,6 +370,114 @@ __global__ void __launch_bounds__(256) k_link_prev(const uint32_t *__restrict__ 
   }
 }
 
+// Tile-staged variant (N <= 2^(12+P)): a CTA links a tile of 8192 consecutive sorted elements
+// in two sweeps.  Sweep 1 histograms the tile's positions by 2^P-position bucket (shared-memory
+// atomics); one block scan turns the histogram into tile-local offsets and ONE global atomic per
+// (tile, bucket) reserves the bucket's run of pair slots.  Sweep 2 (the tile again, now from L2)
+// links each element and stages its (position, prev) pair in shared memory grouped by bucket;
+// the staged tile is then written out in order, so a warp's stores form runs of consecutive
+// slots instead of 32 scattered 8-byte sectors.
+constexpr int LT_THREADS = 1024, LT_U = 8, LT_TILE = LT_THREADS * LT_U;
+constexpr int LT_MAX_BUCKETS = 4096;
+template <int P>
+__global__ void __launch_bounds__(LT_THREADS, 2) k_link_tile(const uint32_t *__restrict__ ks,
+                                                          const uint64_t *__restrict__ vs, uint64_t N, int nbk,
+                                                          unsigned *__restrict__ cursor, uint2 *__restrict__ pairs,
+                                                          uint2 *__restrict__ ovf, uint32_t *__restrict__ n_ovf) {
+  typedef cub::BlockScan<uint32_t, LT_THREADS> Scan;
+  __shared__ typename Scan::TempStorage scan_ts;
+  extern __shared__ __align__(16) uint8_t lt_raw[];
+  uint2 *stage = reinterpret_cast<uint2 *>(lt_raw);                       // [LT_TILE]
+  uint32_t *cur = reinterpret_cast<uint32_t *>(lt_raw + 8 * LT_TILE);     // [nbk]
+  int32_t *off = reinterpret_cast<int32_t *>(cur + nbk);                  // [nbk]
+  const int lane = threadIdx.x & 31;
+  const uint64_t ntile = (N + LT_TILE - 1) / LT_TILE;
+  const int per = (nbk + LT_THREADS - 1) / LT_THREADS;
+  for (uint64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+    const uint64_t t0 = tile * LT_TILE;
+    const uint32_t tn = (uint32_t)(N - t0 < (uint64_t)LT_TILE ? N - t0 : LT_TILE);
+    for (int b = threadIdx.x; b < nbk; b += LT_THREADS) cur[b] = 0;
+    __syncthreads();
+    // sweep 1: bucket histogram of the tile's positions
+#pragma unroll
+    for (int u = 0; u < LT_U; u++) {
+      const uint32_t q = u * LT_THREADS + threadIdx.x;
+      if (q < tn) atomicAdd(&cur[(uint32_t)vs[t0 + q] >> P], 1u);
+    }
+    __syncthreads();
+    // tile-local exclusive offsets; one global reservation per non-empty bucket
+    uint32_t part = 0;
+    for (int e = 0; e < per; e++) {
+      const int b = threadIdx.x * per + e;
+      if (b < nbk) part += cur[b];
+    }
+    uint32_t run;
+    Scan(scan_ts).ExclusiveSum(part, run);
+    constexpr int PER_MAX = LT_MAX_BUCKETS / LT_THREADS;
+    uint32_t cc[PER_MAX], gg[PER_MAX];
+#pragma unroll
+    for (int e = 0; e < PER_MAX; e++) {  // all reservations in flight before any result is used
+      const int b = threadIdx.x * per + e;
+      cc[e] = (e < per && b < nbk) ? cur[b] : 0u;
+      gg[e] = cc[e] ? atomicAdd(&cursor[b], cc[e]) : 0u;
+    }
+#pragma unroll
+    for (int e = 0; e < PER_MAX; e++) {
+      const int b = threadIdx.x * per + e;
+      if (e < per && b < nbk) {
+        off[b] = (int32_t)gg[e] - (int32_t)run;
+        cur[b] = run;
+        run += cc[e];
+      }
+    }
+    __syncthreads();
+    // sweep 2: link and stage grouped by bucket
+#pragma unroll 2
+    for (int u = 0; u < LT_U; u++) {
+      const uint32_t q = u * LT_THREADS + threadIdx.x;
+      const uint64_t i = t0 + q;
+      const bool in = q < tn;
+      const uint32_t k = in ? ks[i] : 0xFFFFFFFFu;
+      const uint64_t v = in ? vs[i] : 0;
+      uint32_t kq = __shfl_up_sync(0xFFFFFFFFu, k, 1);
+      uint64_t vq = __shfl_up_sync(0xFFFFFFFFu, v, 1);
+      if (lane == 0) {
+        if (in && i > 0) { kq = ks[i - 1]; vq = vs[i - 1]; }
+        else kq = ~k;
+      }
+      if (in) {
+        uint32_t p = kNone;
+        bool ov = false;
+        if (kq == k) {
+          if ((vq >> 32) == (v >> 32)) {
+            p = (uint32_t)vq;
+          } else {  // fingerprint collision: bounded backward scan of the key run
+            uint64_t t = i - 1;
+            int steps = 1;
+            for (; t > 0 && ks[t - 1] == k && steps < LINK_SCAN; t--, steps++) {
+              const uint64_t w = vs[t - 1];
+              if ((w >> 32) == (v >> 32)) { p = (uint32_t)w; break; }
+            }
+            ov = p == kNone && steps == LINK_SCAN && t > 0 && ks[t - 1] == k;
+          }
+        }
+        const uint32_t j = (uint32_t)v, bk = j >> P;
+        const uint32_t loc = atomicAdd(&cur[bk], 1u);
+        stage[loc] = make_uint2(j, p);
+        if (ov) ovf[atomicAdd(n_ovf, 1u)] = make_uint2((uint32_t)i, (uint32_t)((bk << P) + off[bk] + (int32_t)loc));
+      }
+    }
+    __syncthreads();
+    // write the staged tile out in order: runs of consecutive slots per bucket
+    for (uint32_t q = threadIdx.x; q < tn; q += LT_THREADS) {
+      const uint2 e = stage[q];
+      const uint32_t bk = e.x >> P;
+      pairs[(uint64_t)(bk << P) + (int64_t)off[bk] + q] = e;
+    }
+    __syncthreads();
+  }
+}
+
 // Rare slow path (32-bit fingerprint collisions in long key runs): one CTA per overflowed
 // element walks the key run backwards 1024 elements per step; the largest matching position
 // below i is the previous occurrence.
@@ -404,17 +512,25 @@ __global__ void __launch_bounds__(OVF_THREADS) k_link_overflow(const uint32_t *_
   }
 }
 
-// bucket b's pairs -> the 2^PB-entry slice of prev[] in shared memory -> one coalesced write
-__global__ void __launch_bounds__(256) k_bucket_assemble(const uint2 *__restrict__ pairs, uint64_t N,
-                                                          uint32_t *__restrict__ prev) {
-  __shared__ uint32_t slice[1 << PB];
-  const uint64_t nb = (N + (1u << PB) - 1) >> PB;
+// bucket b's pairs -> the 2^P-entry slice of prev[] in shared memory -> one coalesced write
+template <int P>
+__global__ void __launch_bounds__(1024) k_bucket_assemble(const uint2 *__restrict__ pairs, uint64_t N,
+                                                           uint32_t *__restrict__ prev) {
+  extern __shared__ uint32_t slice[];
+  const uint64_t nb = (N + (1u << P) - 1) >> P;
   for (uint64_t b = blockIdx.x; b < nb; b += gridDim.x) {
-    const uint64_t lo = b << PB;
-    const uint32_t cnt = (uint32_t)((N - lo) < (1u << PB) ? (N - lo) : (1u << PB));
-    for (uint32_t q = threadIdx.x; q < cnt; q += blockDim.x) {
-      uint2 pr = pairs[lo + q];
-      slice[pr.x & ((1u << PB) - 1)] = pr.y;
+    const uint64_t lo = b << P;
+    const uint32_t cnt = (uint32_t)((N - lo) < (1u << P) ? (N - lo) : (1u << P));
+    for (uint32_t q0 = 0; q0 < cnt; q0 += 8 * blockDim.x) {  // 8 loads in flight per thread
+      uint2 pr[8];
+#pragma unroll
+      for (int e = 0; e < 8; e++) {
+        const uint32_t q = q0 + e * blockDim.x + threadIdx.x;
+        pr[e] = q < cnt ? pairs[lo + q] : make_uint2(0xFFFFFFFFu, 0);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; e++)
+        if (pr[e].x != 0xFFFFFFFFu) slice[pr[e].x & ((1u << P) - 1)] = pr[e].y;
     }
     __syncthreads();
     for (uint32_t q = threadIdx.x; q < cnt; q += blockDim.x) prev[lo + q] = slice[q];
@@ -716,13 +832,25 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
         DBuf<uint2> pairs, ovf;
         DBuf<uint32_t> n_ovf;
         DBuf<unsigned> cursor;
-        const uint64_t nbk = (N + (1u << PB) - 1) >> PB;
+        constexpr int PBT = 15;
+        const uint64_t nbk_t = (N + (1u << PBT) - 1) >> PBT;
+        const bool tiled = nbk_t <= (uint64_t)LT_MAX_BUCKETS;
+        const int pbits = tiled ? PBT : PB;
+        const uint64_t nbk = (N + (1ull << pbits) - 1) >> pbits;
         KTRY(pairs.alloc(ctx, N)); KTRY(ovf.alloc(ctx, N)); KTRY(n_ovf.alloc(ctx, 1)); KTRY(n_ovf.zero());
         KTRY(cursor.alloc(ctx, nbk)); KTRY(cursor.zero());
         {
           Pass ps(ctx, "K2_link_prev", 1, 1);
-          k_link_prev<<<grid_for((N + LINK_U - 1) / LINK_U, 256, 8 * sms), 256, 0, st>>>(
-              k32s.p, v64s.p, N, cursor.p, pairs.p, ovf.p, n_ovf.p);
+          if (tiled) {
+            const size_t smem = 8 * (size_t)LT_TILE + 8 * (size_t)nbk;
+            cudaFuncSetAttribute(k_link_tile<PBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            const uint64_t ntile = (N + LT_TILE - 1) / LT_TILE;
+            k_link_tile<PBT><<<(unsigned)(ntile < (uint64_t)(2 * sms) ? ntile : 2 * sms), LT_THREADS, smem, st>>>(
+                k32s.p, v64s.p, N, (int)nbk, cursor.p, pairs.p, ovf.p, n_ovf.p);
+          } else {
+            k_link_prev<<<grid_for((N + LINK_U - 1) / LINK_U, 256, 8 * sms), 256, 0, st>>>(
+                k32s.p, v64s.p, N, cursor.p, pairs.p, ovf.p, n_ovf.p);
+          }
         }
         {
           Pass ps(ctx, "K2_link_overflow", 1, 1);
@@ -736,8 +864,13 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
         }
         {
           Pass ps(ctx, "K2_bucket_assemble", 1, 1);
-          k_bucket_assemble<<<(unsigned)(nbk < (uint64_t)(32 * sms) ? nbk : 32 * sms), 256, 0, st>>>(pairs.p, N,
-                                                                                                     tr->prev);
+          const unsigned g = (unsigned)(nbk < (uint64_t)(4 * sms) ? nbk : 4 * sms);
+          if (tiled) {
+            cudaFuncSetAttribute(k_bucket_assemble<PBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << PBT);
+            k_bucket_assemble<PBT><<<g, 1024, 4 << PBT, st>>>(pairs.p, N, tr->prev);
+          } else {
+            k_bucket_assemble<PB><<<g, 1024, 4 << PB, st>>>(pairs.p, N, tr->prev);
+          }
         }
       }
     }

@@ -516,8 +516,15 @@ def main():
         per_launch_ms = top["ms"] / top["launches"]
         algo_bytes = bpu * units[unit]
         achieved = algo_bytes / (per_launch_ms * 1e-3) / 1e9
+        traffic, traffic_src = None, None
+        tp = os.path.join(ROOT, "profiles", f"ncu_traffic_config{args.config}.json")
+        if os.path.exists(tp):  # DRAM bytes per launch from a committed `ncu --set full` capture
+            with open(tp) as f:
+                tj = json.load(f)
+            traffic = tj.get("dram_bytes_per_launch", {}).get(top["name"])
+            traffic_src = tj.get("source") if traffic is not None else None
         roof = {"kernel": top["name"], "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": algo_bytes, "bytes_per_unit": bpu, "unit_of_work": unit,
                 "avg_launch_ms": per_launch_ms,
                 "share_of_step": top["ms"] / prof_steps / ms_step}

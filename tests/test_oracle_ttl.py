@@ -1,0 +1,95 @@
+"""Pins for the row-f2 oracle (oracle/ttl_alloc.py): the group curves H_g / C_g,
+the ROI-optimal TTL (Alg. 2 l.4-5) and the allocation of Eq. 3 (Alg. 2).
+
+Pinned against: the literal definitions evaluated naively, SPEC's worked curve values,
+hand-derived ROI values from the paper's C_g, exhaustive search of Eq. 3 on small instances
+(SPEC S:594-597 property: >= 95% of the optimum), feasibility, and the SPEC allocation examples."""
+import itertools
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import ttl_alloc as A
+
+
+def naive_H(d, t):
+    return sum(1 for x in d if x <= t)
+
+
+def naive_C(d, U, t):
+    return U * t + sum(min(t, x) for x in d)
+
+
+def test_curves_match_definitions():
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        d = rng.integers(0, 40, size=int(rng.integers(0, 30))).tolist()
+        U = int(rng.integers(0, 5))
+        c = A.Curve(d, U)
+        for t in range(0, 45):
+            assert c.H(t) == naive_H(d, t) and c.C(t) == naive_C(d, U, t)
+        assert c.HJ == [naive_H(d, t) for t in c.J] and c.CJ == [naive_C(d, U, t) for t in c.J]
+
+
+def test_spec_curve_examples():
+    c = A.Curve([1, 3, 3, 7], 2)
+    assert (c.H(0), c.H(3), c.H(10**9)) == (0, 3, 4)
+    assert c.C(3) == 2 * 3 + (1 + 3 + 3 + 3) == 16
+    e = A.Curve([], 3)                               # no-reuse group
+    assert e.H(5) == 0 and e.C(5) == 15
+
+
+def test_roi_ttl():
+    # the paper's C_g: R(1) = 1/6, R(3) = 3/16, R(7) = 4/28 -> argmax 3 (R43 notes SPEC's 1/4, 4/30)
+    c = A.Curve([1, 3, 3, 7], 2)
+    assert [Fraction(c.H(t), c.C(t)) for t in (1, 3, 7)] == [Fraction(1, 6), Fraction(3, 16), Fraction(1, 7)]
+    assert A.roi_ttl(c) == 3
+    assert A.roi_ttl(A.Curve([5], 1)) == 5
+    assert A.roi_ttl(A.Curve([], 1)) == 0
+    rng = np.random.default_rng(1)
+    for _ in range(300):                             # the maximum over ALL integer t >= 1 is a candidate
+        d = rng.integers(0, 25, size=int(rng.integers(1, 12))).tolist()
+        U = int(rng.integers(1, 4))
+        best = max(range(1, max(max(d), 1) + 1), key=lambda t: (Fraction(naive_H(d, t), naive_C(d, U, t)), -t))
+        assert A.roi_ttl(A.Curve(d, U)) == best
+
+
+def exhaustive(curves, B):
+    best = 0
+    for t in itertools.product(*[c.J for c in curves]):
+        h, cc = A.totals(curves, t)
+        if cc <= B and h > best:
+            best = h
+    return best
+
+
+def test_spec_allocation_examples():
+    c = A.Curve([1, 3, 3, 7], 1)                     # budget >= C(7) = 21 -> all 4 hits
+    assert c.C(7) == 21
+    t, h, cost, _, _ = A.allocate([c], 21)
+    assert h == 4 and cost <= 21 and t[0] >= 7
+    g1, g2 = A.Curve([1, 1, 1], 1), A.Curve([10], 5)  # the budget goes to group 1
+    t, h, cost, _, _ = A.allocate([g1, g2], 6)
+    assert h == 3 and t[0] >= 1 and t[1] < 10 and cost <= 6
+    grid = max(A.totals([g1, g2], (a, b))[0] for a in range(13) for b in range(13)
+               if A.totals([g1, g2], (a, b))[1] <= 6)
+    assert grid == 3
+    t, h, cost, _, _ = A.allocate([g1, g2], 0)       # vanishing budget
+    assert cost == 0 and h == 0
+
+
+def test_allocation_near_optimal_and_feasible():
+    rng = np.random.default_rng(2)
+    ratios = []
+    for trial in range(120):
+        G = int(rng.integers(1, 4))
+        curves = [A.Curve(rng.integers(0, 30, size=int(rng.integers(0, 9))).tolist(), int(rng.integers(1, 4)))
+                  for _ in range(G)]
+        B = int(rng.integers(0, 150))
+        t, h, cost, _, _ = A.allocate(curves, B, seed=trial)
+        assert cost <= B and A.totals(curves, t) == (h, cost)
+        opt = exhaustive(curves, B)
+        assert h <= opt
+        ratios.append(1.0 if opt == 0 else h / opt)
+    assert np.mean(ratios) >= 0.95 and min(ratios) >= 0.5

@@ -66,7 +66,7 @@ def tuner_rows_config3(delta_by_group, U_g, K):
         if len(d) == 0:
             troi.append(0)
             continue
-        vals, first = np.unique(d, return_index=True)
+        vals = np.unique(np.maximum(d, 1))                               # candidates (DESIGN R43)
         H = np.searchsorted(d, vals, side="right")                       # #{delta <= t}
         csum = np.concatenate([[0], np.cumsum(d)])
         C = int(U_g[g]) * vals + csum[H] + vals * (len(d) - H)           # U_g t + sum min(t, delta)

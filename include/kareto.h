@@ -234,6 +234,29 @@ kareto_status kareto_search(kareto_ctx *ctx, const kareto_trace *tr, const karet
                             const kareto_model *model, kareto_search_point *out, int64_t cap, int64_t *n_out,
                             int32_t *truncated);
 
+/* ------------------------------------------------- row f2: group TTLs ---- */
+/* Alg. 2 "ROI-Aware TTL Allocation" over the exact group curves of
+ * P:750-752 for the loaded trace's K+1 groups (R23):
+ *   H_g(t) = #{delta in Delta_g : delta <= t},  C_g(t) = |B_g| t + sum_{delta in Delta_g} min(t, delta),
+ * Delta_g = the reuse intervals (ms) of the group's non-first accesses, |B_g| its unique blocks;
+ * t in ms, C in block * ms.  All outputs are host arrays of K+1 entries (or n). */
+
+/* Alg. 2 l.4-5: t_roi[g] = argmax over the candidate TTLs {max(delta, 1)} of H_g/C_g, exact,
+ * ties -> smallest t, empty group -> 0 (R43); h_roi / c_roi (may be NULL) = H_g, C_g there. */
+kareto_status kareto_ttl_roi(kareto_ctx *ctx, const kareto_trace *tr, uint32_t *t_roi, uint64_t *h_roi,
+                             uint64_t *c_roi);
+/* sum_g H_g(ttl[i][g]) and sum_g C_g(ttl[i][g]) for n TTL vectors ttl [n][K+1] (host, ms, finite;
+ * KARETO_TTL_INF -> KARETO_E_INVALID naming the entry). */
+kareto_status kareto_ttl_eval(kareto_ctx *ctx, const kareto_trace *tr, const uint32_t *ttl, int64_t n,
+                              uint64_t *hits, uint64_t *cost);
+/* Eq. 3 by Alg. 2: ROI TTLs, alpha = budget / sum C_g(t_roi) (R46), floor(sqrt(K))
+ * deterministic perturbed starts from `seed` (R45), the exact discrete local solve from each
+ * start (R44), the start with the most hits.  t_out = t*, hits_out / cost_out = its totals
+ * (cost_out <= budget); t_roi_out / t_init_out may be NULL. */
+kareto_status kareto_ttl_allocate(kareto_ctx *ctx, const kareto_trace *tr, uint64_t budget, uint64_t seed,
+                                  uint32_t *t_out, uint64_t *hits_out, uint64_t *cost_out, uint32_t *t_roi_out,
+                                  uint32_t *t_init_out);
+
 /* ------------------------------------------------------------ profiling ---- */
 typedef struct {
   char name[24];      /* kernel / pass name                                         */

@@ -99,7 +99,8 @@ _lib = None
 ABI_FUNCTIONS = ["kareto_create", "kareto_destroy", "kareto_last_error", "kareto_nccl_unique_id",
                  "kareto_load_trace", "kareto_trace_free", "kareto_trace_stats", "kareto_trace_export",
                  "kareto_eval_grid", "kareto_pareto", "kareto_set_profiling", "kareto_get_pass_times",
-                 "kareto_launch_counter", "kareto_shard_range", "kareto_hypervolume", "kareto_search"]
+                 "kareto_launch_counter", "kareto_shard_range", "kareto_hypervolume", "kareto_search",
+                 "kareto_ttl_roi", "kareto_ttl_eval", "kareto_ttl_allocate"]
 
 
 def load_library(path: str = LIB_PATH):
@@ -128,6 +129,10 @@ def load_library(path: str = LIB_PATH):
                                      ctypes.POINTER(ctypes.c_double), i32]
     L.kareto_search.argtypes = [vp, vp, ctypes.POINTER(SearchParamsC), ctypes.POINTER(ModelC), vp, i64,
                                 ctypes.POINTER(i64), ctypes.POINTER(i32)]
+    L.kareto_ttl_roi.argtypes = [vp, vp, vp, vp, vp]
+    L.kareto_ttl_eval.argtypes = [vp, vp, vp, i64, vp, vp]
+    L.kareto_ttl_allocate.argtypes = [vp, vp, ctypes.c_uint64, ctypes.c_uint64, vp, ctypes.POINTER(ctypes.c_uint64),
+                                      ctypes.POINTER(ctypes.c_uint64), vp, vp]
     L.kareto_set_profiling.argtypes = [vp, i32]
     L.kareto_get_pass_times.argtypes = [vp, ctypes.POINTER(PassTime), i32, ctypes.POINTER(i32), i32]
     L.kareto_launch_counter.argtypes = [vp, ctypes.POINTER(i64), i32]
@@ -340,6 +345,34 @@ class Context:
                                           out.ctypes.data if cap else None, int(cap), ctypes.byref(n),
                                           ctypes.byref(tr_)), "search")
         return out[:n.value].copy(), bool(tr_.value)
+
+
+    # ---- row f2: Alg. 2 group TTLs
+    def ttl_roi(self, trace: "Trace"):
+        """kareto_ttl_roi -> (t_roi, H at t_roi, C at t_roi), each [K+1]."""
+        G = trace.K + 1
+        t, h, c = np.zeros(G, np.uint32), np.zeros(G, np.uint64), np.zeros(G, np.uint64)
+        self._check(self._L.kareto_ttl_roi(self._h, trace._h, t.ctypes.data, h.ctypes.data, c.ctypes.data), "ttl_roi")
+        return t, h, c
+
+    def ttl_eval(self, trace: "Trace", ttl):
+        """kareto_ttl_eval: (sum H, sum C) of each TTL vector in ttl [n][K+1] (ms)."""
+        ttl = np.ascontiguousarray(np.atleast_2d(ttl), np.uint32)
+        n = ttl.shape[0]
+        h, c = np.zeros(n, np.uint64), np.zeros(n, np.uint64)
+        self._check(self._L.kareto_ttl_eval(self._h, trace._h, ttl.ctypes.data if n else None, n,
+                                            h.ctypes.data if n else None, c.ctypes.data if n else None), "ttl_eval")
+        return h, c
+
+    def ttl_allocate(self, trace: "Trace", budget: int, seed: int = 0):
+        """kareto_ttl_allocate -> dict(t, hits, cost, t_roi, t_init)."""
+        G = trace.K + 1
+        t, tr_, ti = np.zeros(G, np.uint32), np.zeros(G, np.uint32), np.zeros(G, np.uint32)
+        h, c = ctypes.c_uint64(), ctypes.c_uint64()
+        self._check(self._L.kareto_ttl_allocate(self._h, trace._h, int(budget), int(seed), t.ctypes.data,
+                                                ctypes.byref(h), ctypes.byref(c), tr_.ctypes.data, ti.ctypes.data),
+                    "ttl_allocate")
+        return dict(t=t, hits=int(h.value), cost=int(c.value), t_roi=tr_, t_init=ti)
 
 
 class Trace:

@@ -386,6 +386,52 @@ def run_search(args, K, ctx, tr, rank, spec, lengths):
         print(json.dumps(line), flush=True)
 
 
+def run_ttl(args, K, ctx, tr, rank, spec):
+    """Row f2 measurement: Alg. 2 (kareto_ttl_allocate) on the config's trace at budgets of 1%, 5%
+    and 20% of the cost of leasing every block for the whole span, against the best uniform TTL
+    with the same budget (bisection over kareto_ttl_eval batches).  Host wall clock around the
+    synchronous calls, trace resident, after one untimed run."""
+    import time as _t
+    G = tr.K + 1
+    span = int(tr.span_ms)
+    _, full = ctx.ttl_eval(tr, np.full((1, G), span, np.uint32))
+    full = int(full[0])
+    ctx.ttl_roi(tr)
+    t0 = _t.perf_counter()
+    t_roi, h_roi, c_roi = ctx.ttl_roi(tr)
+    t_roi_s = _t.perf_counter() - t0
+    total_reuse = int(tr.reuse_g.sum())
+    rows = []
+    for frac in (0.01, 0.05, 0.2):
+        B = int(frac * full)
+        ctx.ttl_allocate(tr, B, seed=0)
+        t0 = _t.perf_counter()
+        r = ctx.ttl_allocate(tr, B, seed=0)
+        t_alloc = _t.perf_counter() - t0
+        lo, hi = 0, span                        # best uniform TTL within the budget
+        while lo < hi:
+            cand = np.linspace(lo, hi, 65).astype(np.int64)
+            hh, cc = ctx.ttl_eval(tr, np.repeat(cand[:, None], G, 1).astype(np.uint32))
+            ok = cand[cc <= B]
+            new_lo = int(ok.max()) if len(ok) else lo
+            bad = cand[cc > B]
+            new_hi = int(bad.min()) - 1 if len(bad) else hi
+            if (new_lo, new_hi) == (lo, hi):
+                break
+            lo, hi = new_lo, max(new_lo, new_hi)
+        hu, cu = ctx.ttl_eval(tr, np.full((1, G), lo, np.uint32))
+        rows.append({"budget_frac": frac, "budget_block_ms": B, "alg2_hits": r["hits"], "alg2_cost": r["cost"],
+                     "alg2_s": t_alloc, "uniform_ttl_ms": lo, "uniform_hits": int(hu[0]), "uniform_cost": int(cu[0]),
+                     "hit_gain_vs_uniform": r["hits"] / max(1, int(hu[0])), "t_ms": r["t"].tolist()})
+    if rank == 0:
+        line = {"metric": "Alg. 2 group-TTL allocation (row f2)", "unit": "hits", "groups": G,
+                "total_reuse_events": total_reuse, "full_lease_cost_block_ms": full, "roi_s": t_roi_s,
+                "t_roi_ms": t_roi.tolist(), "budgets": rows,
+                "config": {"workload": spec["desc"], "n_accesses": tr.N, "top_k": tr.K},
+                "data": "synthetic", "timing": "host wall clock around synchronous ABI calls, trace resident"}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -400,6 +446,8 @@ def main():
     ap.add_argument("--search", action="store_true",
                     help="row f1: Alg. 1 adaptive search vs the P:856 grid search on the config's trace")
     ap.add_argument("--search-hbm-gb", type=float, default=320.0)
+    ap.add_argument("--ttl", action="store_true",
+                    help="row f2: Alg. 2 group-TTL allocation vs the best uniform TTL on the config's trace")
     args = ap.parse_args()
     spec = CONFIGS[args.config]
     if args.impl == "reference":
@@ -443,6 +491,9 @@ def main():
 
     if args.search:
         run_search(args, K, ctx, load_dev(), rank, spec, np.diff(off_h.numpy()))
+        return
+    if args.ttl:
+        run_ttl(args, K, ctx, load_dev(), rank, spec)
         return
 
     tr = load_dev()

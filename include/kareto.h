@@ -257,6 +257,24 @@ kareto_status kareto_ttl_allocate(kareto_ctx *ctx, const kareto_trace *tr, uint6
                                   uint32_t *t_out, uint64_t *hits_out, uint64_t *cost_out, uint32_t *t_roi_out,
                                   uint32_t *t_init_out);
 
+/* ------------------------------------------------ row f4: trace analytics ---- */
+/* X6 reuse skew and X5 oracle-TTL footprint, DESIGN R47-R48:
+ *   hits(b) = accesses of block b after its first; total_hits = sum; blocks sorted by hits
+ *   descending; blocks_90 = fewest top blocks holding >= 90% of the hits (frac_90 = blocks_90 / U;
+ *   no hits: blocks_90 = U, frac_90 = 1); lorenz[i] (i < n_pts) = share of the hits held by the
+ *   top ceil(i U / (n_pts - 1)) blocks;
+ *   after request r (arrival order): cumulative[r] = distinct blocks seen so far, active[r] =
+ *   blocks seen so far whose next access is in a later request (the oracle TTL); peak_active =
+ *   max_r active[r] at its first request peak_active_request.
+ * lorenz [n_pts] (n_pts = 0 or >= 2), cumulative / active [R] are host arrays or NULL. */
+typedef struct {
+  int64_t unique_blocks, total_hits, blocks_90;
+  double frac_90;
+  int64_t peak_active, peak_active_request, final_cumulative;
+} kareto_analytics;
+kareto_status kareto_trace_analytics(kareto_ctx *ctx, const kareto_trace *tr, kareto_analytics *out, double *lorenz,
+                                     int32_t n_pts, int64_t *cumulative, int64_t *active);
+
 /* ------------------------------------------------------------ profiling ---- */
 typedef struct {
   char name[24];      /* kernel / pass name                                         */

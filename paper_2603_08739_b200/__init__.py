@@ -88,6 +88,12 @@ SEARCH_POINT_DTYPE = np.dtype([("d_gb", np.int64), ("t_s", np.int64), ("obj", np
 assert SEARCH_POINT_DTYPE.itemsize == 48
 
 
+class AnalyticsC(ctypes.Structure):
+    _fields_ = [("unique_blocks", ctypes.c_int64), ("total_hits", ctypes.c_int64), ("blocks_90", ctypes.c_int64),
+                ("frac_90", ctypes.c_double), ("peak_active", ctypes.c_int64),
+                ("peak_active_request", ctypes.c_int64), ("final_cumulative", ctypes.c_int64)]
+
+
 class PassTime(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 24), ("ms", ctypes.c_double), ("launches", ctypes.c_int32),
                 ("own", ctypes.c_int32)]
@@ -100,7 +106,7 @@ ABI_FUNCTIONS = ["kareto_create", "kareto_destroy", "kareto_last_error", "kareto
                  "kareto_load_trace", "kareto_trace_free", "kareto_trace_stats", "kareto_trace_export",
                  "kareto_eval_grid", "kareto_pareto", "kareto_set_profiling", "kareto_get_pass_times",
                  "kareto_launch_counter", "kareto_shard_range", "kareto_hypervolume", "kareto_search",
-                 "kareto_ttl_roi", "kareto_ttl_eval", "kareto_ttl_allocate"]
+                 "kareto_ttl_roi", "kareto_ttl_eval", "kareto_ttl_allocate", "kareto_trace_analytics"]
 
 
 def load_library(path: str = LIB_PATH):
@@ -133,6 +139,7 @@ def load_library(path: str = LIB_PATH):
     L.kareto_ttl_eval.argtypes = [vp, vp, vp, i64, vp, vp]
     L.kareto_ttl_allocate.argtypes = [vp, vp, ctypes.c_uint64, ctypes.c_uint64, vp, ctypes.POINTER(ctypes.c_uint64),
                                       ctypes.POINTER(ctypes.c_uint64), vp, vp]
+    L.kareto_trace_analytics.argtypes = [vp, vp, ctypes.POINTER(AnalyticsC), vp, i32, vp, vp]
     L.kareto_set_profiling.argtypes = [vp, i32]
     L.kareto_get_pass_times.argtypes = [vp, ctypes.POINTER(PassTime), i32, ctypes.POINTER(i32), i32]
     L.kareto_launch_counter.argtypes = [vp, ctypes.POINTER(i64), i32]
@@ -373,6 +380,23 @@ class Context:
                                                 ctypes.byref(h), ctypes.byref(c), tr_.ctypes.data, ti.ctypes.data),
                     "ttl_allocate")
         return dict(t=t, hits=int(h.value), cost=int(c.value), t_roi=tr_, t_init=ti)
+
+
+    # ---- row f4: trace analytics (X5, X6)
+    def analytics(self, trace: "Trace", n_pts: int = 101, series: bool = True) -> dict:
+        """kareto_trace_analytics -> dict of the scalars, 'lorenz' [n_pts] and (series=True)
+        'cumulative' / 'active' [R]."""
+        a = AnalyticsC()
+        lor = np.zeros(n_pts, np.float64)
+        cum = np.zeros(trace.R, np.int64) if series else None
+        act = np.zeros(trace.R, np.int64) if series else None
+        self._check(self._L.kareto_trace_analytics(self._h, trace._h, ctypes.byref(a),
+                                                   lor.ctypes.data if n_pts else None, int(n_pts),
+                                                   None if cum is None else cum.ctypes.data,
+                                                   None if act is None else act.ctypes.data), "trace_analytics")
+        d = {f: getattr(a, f) for f, _ in AnalyticsC._fields_}
+        d.update(lorenz=lor, cumulative=cum, active=act)
+        return d
 
 
 class Trace:

@@ -446,6 +446,8 @@ def main():
     ap.add_argument("--search", action="store_true",
                     help="row f1: Alg. 1 adaptive search vs the P:856 grid search on the config's trace")
     ap.add_argument("--search-hbm-gb", type=float, default=320.0)
+    ap.add_argument("--analytics", action="store_true",
+                    help="row f4 analytics: X6 reuse skew and X5 oracle-TTL footprint of the config's trace")
     ap.add_argument("--ttl", action="store_true",
                     help="row f2: Alg. 2 group-TTL allocation vs the best uniform TTL on the config's trace")
     args = ap.parse_args()
@@ -494,6 +496,21 @@ def main():
         return
     if args.ttl:
         run_ttl(args, K, ctx, load_dev(), rank, spec)
+        return
+    if args.analytics:
+        tr = load_dev()
+        ctx.analytics(tr, series=False)
+        t0 = time.perf_counter()
+        a = ctx.analytics(tr, n_pts=11, series=False)
+        dt = time.perf_counter() - t0
+        if rank == 0:
+            print(json.dumps({"metric": "trace analytics X5/X6 (row f4)", "unit": "s", "value": dt,
+                              "unique_blocks": a["unique_blocks"], "total_hits": a["total_hits"],
+                              "frac_blocks_for_90pct_hits": a["frac_90"], "lorenz_deciles": a["lorenz"].tolist(),
+                              "peak_active_blocks": a["peak_active"], "final_cumulative_blocks": a["final_cumulative"],
+                              "config": {"workload": spec["desc"], "n_accesses": tr.N},
+                              "data": "synthetic", "timing": "host wall clock around the synchronous call"}),
+                  flush=True)
         return
 
     tr = load_dev()

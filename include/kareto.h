@@ -257,6 +257,27 @@ kareto_status kareto_ttl_allocate(kareto_ctx *ctx, const kareto_trace *tr, uint6
                                   uint32_t *t_out, uint64_t *hits_out, uint64_t *cost_out, uint32_t *t_roi_out,
                                   uint32_t *t_init_out);
 
+/* ------------------------------------------------ row f3: queue model ---- */
+/* Queue-coupled disk prefetch and per-request TTFT (PAPER.md Obs. 2/4; P99 TTFT
+ * constraints), DESIGN R49-R53, for stack-eligible LRU configurations (TTL mode, or
+ * CAPACITY with one TTL for every group): per request its prefix hits by tier (from the LRU
+ * depths); FCFS over model->instances instances; a request's disk-resident prefix blocks count as
+ * hits only if they stream in (at the medium's bandwidth) during its queue wait; TTFT = wait +
+ * prefill + DRAM load.  out [n_cfg] host.  Errors: KARETO_E_INVALID (tuner / medium / TTL mode
+ * with an infinite TTL / instances outside 1..4096), KARETO_E_UNSUPPORTED (non-LRU or per-group
+ * TTLs on a finite disk: no stack path), _E_OOM. */
+typedef struct {
+  double ttft_mean_ms;          /* mean TTFT over requests                                  */
+  double ttft_p99_ms;           /* nearest-rank P99 TTFT                                    */
+  double makespan_s;            /* max(span, last instance free time)                       */
+  double tokens_per_s;          /* (Ltok + O) / makespan                                    */
+  uint64_t disk_hits_capacity;  /* disk-resident prefix blocks (capacity prediction)        */
+  uint64_t disk_hits_realized;  /* of those, prefetched before service started              */
+} kareto_queue_result;          /* 48 bytes */
+kareto_status kareto_eval_queue(kareto_ctx *ctx, const kareto_trace *tr, const kareto_config *cfg, int64_t n_cfg,
+                                const uint32_t *ttl_ms, int32_t n_tuner, const kareto_model *model,
+                                kareto_queue_result *out);
+
 /* ------------------------------------------------ row f4: trace analytics ---- */
 /* X6 reuse skew and X5 oracle-TTL footprint, DESIGN R47-R48:
  *   hits(b) = accesses of block b after its first; total_hits = sum; blocks sorted by hits

@@ -94,6 +94,13 @@ class AnalyticsC(ctypes.Structure):
                 ("peak_active_request", ctypes.c_int64), ("final_cumulative", ctypes.c_int64)]
 
 
+# kareto_queue_result (48 bytes)
+QUEUE_DTYPE = np.dtype([("ttft_mean_ms", np.float64), ("ttft_p99_ms", np.float64), ("makespan_s", np.float64),
+                        ("tokens_per_s", np.float64), ("disk_hits_capacity", np.uint64),
+                        ("disk_hits_realized", np.uint64)])
+assert QUEUE_DTYPE.itemsize == 48
+
+
 class PassTime(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 24), ("ms", ctypes.c_double), ("launches", ctypes.c_int32),
                 ("own", ctypes.c_int32)]
@@ -106,7 +113,8 @@ ABI_FUNCTIONS = ["kareto_create", "kareto_destroy", "kareto_last_error", "kareto
                  "kareto_load_trace", "kareto_trace_free", "kareto_trace_stats", "kareto_trace_export",
                  "kareto_eval_grid", "kareto_pareto", "kareto_set_profiling", "kareto_get_pass_times",
                  "kareto_launch_counter", "kareto_shard_range", "kareto_hypervolume", "kareto_search",
-                 "kareto_ttl_roi", "kareto_ttl_eval", "kareto_ttl_allocate", "kareto_trace_analytics"]
+                 "kareto_ttl_roi", "kareto_ttl_eval", "kareto_ttl_allocate", "kareto_trace_analytics",
+                 "kareto_eval_queue"]
 
 
 def load_library(path: str = LIB_PATH):
@@ -140,6 +148,7 @@ def load_library(path: str = LIB_PATH):
     L.kareto_ttl_allocate.argtypes = [vp, vp, ctypes.c_uint64, ctypes.c_uint64, vp, ctypes.POINTER(ctypes.c_uint64),
                                       ctypes.POINTER(ctypes.c_uint64), vp, vp]
     L.kareto_trace_analytics.argtypes = [vp, vp, ctypes.POINTER(AnalyticsC), vp, i32, vp, vp]
+    L.kareto_eval_queue.argtypes = [vp, vp, vp, i64, vp, i32, ctypes.POINTER(ModelC), vp]
     L.kareto_set_profiling.argtypes = [vp, i32]
     L.kareto_get_pass_times.argtypes = [vp, ctypes.POINTER(PassTime), i32, ctypes.POINTER(i32), i32]
     L.kareto_launch_counter.argtypes = [vp, ctypes.POINTER(i64), i32]
@@ -397,6 +406,23 @@ class Context:
         d = {f: getattr(a, f) for f, _ in AnalyticsC._fields_}
         d.update(lorenz=lor, cumulative=cum, active=act)
         return d
+
+
+    # ---- row f3: queue-coupled disk prefetch, TTFT distribution
+    def eval_queue(self, trace: "Trace", cfgs: np.ndarray, model: Model, ttl=None) -> np.ndarray:
+        """kareto_eval_queue -> QUEUE_DTYPE [n]."""
+        cfgs = np.ascontiguousarray(cfgs, CONFIG_DTYPE)
+        n = len(cfgs)
+        ttl_arr, n_tuner = None, 0
+        if ttl is not None:
+            ttl_arr = np.ascontiguousarray(ttl, np.uint32)
+            n_tuner = ttl_arr.shape[0]
+        out = np.zeros(n, QUEUE_DTYPE)
+        m = model.c()
+        self._check(self._L.kareto_eval_queue(self._h, trace._h, cfgs.ctypes.data if n else None, n,
+                                              None if ttl_arr is None else ttl_arr.ctypes.data, n_tuner,
+                                              ctypes.byref(m), out.ctypes.data if n else None), "eval_queue")
+        return out
 
 
 class Trace:

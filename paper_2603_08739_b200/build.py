@@ -10,12 +10,12 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libkareto.so")
 SOURCES = ["ctx.cu", "trace_load.cu", "stack_depth.cu", "eval.cu", "objective.cu", "pareto.cu", "replay.cu",
-           "search.cu", "ttl_alloc.cu", "analytics.cu"]
+           "search.cu", "ttl_alloc.cu", "analytics.cu", "queue.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),
           "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 # objective.cu holds the fp64 model: no FMA contraction (R33)
-PER_FILE = {"objective.cu": ["-fmad=false"]}
+PER_FILE = {"objective.cu": ["-fmad=false"], "queue.cu": ["-fmad=false"]}
 
 
 def _nvcc() -> str:

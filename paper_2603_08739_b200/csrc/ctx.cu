@@ -182,7 +182,7 @@ extern "C" void kareto_trace_free(kareto_trace *tr) {
   if (!tr) return;
   // uses only the trace's own copy of the stream: a trace may outlive its context
   void *ptrs[] = {tr->arr, tr->s, tr->grp, tr->hash, tr->req, tr->prev, tr->delta, tr->depth,
-                  tr->blk, tr->gblk, tr->arr_rel};
+                  tr->blk, tr->gblk, tr->arr_rel, tr->inlen, tr->outlen};
   for (void *p : ptrs)
     if (p) cudaFreeAsync(p, tr->stream);
   cudaStreamSynchronize(tr->stream);

@@ -73,6 +73,8 @@ struct kareto_trace {
   int64_t *arr = nullptr;      // arrival ms
   uint32_t *s = nullptr;       // first touch position [R+1]
   uint16_t *grp = nullptr;     // group of request
+  uint32_t *inlen = nullptr;   // input tokens L_r (saturated at 2^32-1; flagged)
+  uint32_t *outlen = nullptr;  // output tokens o_r
   // per access (touch order) [N]
   uint64_t *hash = nullptr;
   uint32_t *req = nullptr;

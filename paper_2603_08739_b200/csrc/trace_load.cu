@@ -50,7 +50,8 @@ __global__ void k_sort_keys(const int64_t *__restrict__ arrival, int64_t R, uint
 __global__ void k_req_meta(int64_t R, int mode, const uint32_t *__restrict__ order, const int64_t *__restrict__ arrival,
                            const int32_t *__restrict__ out_tok, const int64_t *__restrict__ offsets,
                            const int64_t *__restrict__ input_tokens, int64_t *__restrict__ arr_sorted,
-                           int64_t *__restrict__ src_off, uint64_t *__restrict__ nblk, LoadStats *st) {
+                           int64_t *__restrict__ src_off, uint64_t *__restrict__ nblk, uint32_t *__restrict__ inlen,
+                           uint32_t *__restrict__ outlen, LoadStats *st) {
   unsigned long long sl_lo = 0, sl_hi = 0, sq_lo = 0, sq_hi = 0, O = 0;
   unsigned int flags = 0, maxb = 0;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
@@ -75,6 +76,9 @@ __global__ void k_req_meta(int64_t R, int mode, const uint32_t *__restrict__ ord
     }
     src_off[r] = o0;
     nblk[r] = n;
+    if (L > 0xFFFFFFFFull) flags |= F_INPUT_LEN;
+    inlen[r] = L > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)L;
+    outlen[r] = (uint32_t)ot;
     if (n > maxb) maxb = n > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)n;
     // exact 128-bit sums split into 32-bit halves: SL = sum L, SQ = sum L(L-1)/2
     unsigned __int128 q = L ? ((unsigned __int128)L * (unsigned __int128)(L - 1)) / 2 : 0;
@@ -741,10 +745,13 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
     }));
   }
   KCUDA(ctx, cudaMemsetAsync(nblk.p + R, 0, 8, st));
+  KCUDA(ctx, cudaMallocAsync((void **)&tr->inlen, 4 * (size_t)R, st));
+  KCUDA(ctx, cudaMallocAsync((void **)&tr->outlen, 4 * (size_t)R, st));
   {
     Pass ps(ctx, "a1_req_meta", 1, 1);
     k_req_meta<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(R, d->mode, order.p, arrival, out_tok, offsets, input_tokens,
-                                                          arr_sorted.p, src_off.p, nblk.p, stats.p);
+                                                          arr_sorted.p, src_off.p, nblk.p, tr->inlen, tr->outlen,
+                                                          stats.p);
   }
   {
     Pass ps(ctx, "a1_scan_starts", 0, 1);

@@ -432,6 +432,55 @@ def run_ttl(args, K, ctx, tr, rank, spec):
         print(json.dumps(line), flush=True)
 
 
+def run_queue(args, K, ctx, tr, rank, spec, lengths):
+    """Row f3 measurement (Obs. 2 / Obs. 4): a 4 x 8 x 8 LRU grid (HBM A(4, U/16) x DRAM
+    A(8, U/2) x disk A(8, U), CAPACITY, no TTL) through kareto_eval_queue at a low (rho0 = 0.3,
+    "ins4-like") and a high (rho0 = 1.3, "ins1-like") workload density, I = max(1, round(busy_0 /
+    (rho0 span))); reports the realised share of the capacity-predicted disk hits, TTFT, the
+    configurations meeting P99 TTFT <= 2 s, and the device time per configuration."""
+    import torch
+    m0 = K.Model()
+    L = lengths.astype(np.int64)
+    busy0 = (m0.alpha_ps * int(L.sum()) + m0.beta_ps * int((L * (L - 1) // 2).sum()) + m0.dec_ps * tr.O) * 1e-12
+    U = tr.U
+    A = lambda m, top: [top * i // (m - 1) for i in range(m)]
+    caps = [[a, b, c] for a in A(4, U // 16) for b in A(8, U // 2) for c in A(8, U)]
+    cfg = K.configs(caps)
+    res = []
+    for rho in (0.3, 1.3):
+        inst = max(1, round(busy0 / (rho * tr.span_ms * 1e-3)))
+        model = K.Model(instances=inst)
+        ctx.eval_queue(tr, cfg[:2], model)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        q = ctx.eval_queue(tr, cfg, model)
+        dt = time.perf_counter() - t0
+        _, obj = ctx.eval_grid(tr, cfg, model)
+        ok = q["ttft_p99_ms"] <= 2000.0
+        f = obj.copy()
+        f[:, 0] = q["ttft_mean_ms"]
+        f[:, 1] = -q["tokens_per_s"]
+        front = 0
+        if ok.any():
+            st, front = ctx.pareto(np.ascontiguousarray(f[ok]), None, None)
+        capd = int(q["disk_hits_capacity"].sum())
+        real = int(q["disk_hits_realized"].sum())
+        res.append({"rho0": rho, "instances": inst, "configs": len(cfg), "seconds": dt,
+                    "configs_per_s": len(cfg) / dt,
+                    "disk_hits_capacity": capd, "disk_hits_realized": real,
+                    "realized_fraction": real / capd if capd else None,
+                    "ttft_mean_ms_range": [float(q["ttft_mean_ms"].min()), float(q["ttft_mean_ms"].max())],
+                    "ttft_p99_ms_range": [float(q["ttft_p99_ms"].min()), float(q["ttft_p99_ms"].max())],
+                    "fluid_mean_ttft_ms_range": [float(obj[:, 0].min()), float(obj[:, 0].max())],
+                    "p99_le_2s": int(ok.sum()), "frontier_under_p99": int(front)})
+    if rank == 0:
+        print(json.dumps({"metric": "queue-coupled disk prefetch (row f3)", "unit": "configs/s",
+                          "densities": res, "config": {"workload": spec["desc"], "n_accesses": tr.N,
+                                                        "n_requests": tr.R, "grid": "A(4,U/16) x A(8,U/2) x A(8,U), LRU"},
+                          "data": "synthetic", "timing": "host wall clock around the synchronous call"}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -446,6 +495,8 @@ def main():
     ap.add_argument("--search", action="store_true",
                     help="row f1: Alg. 1 adaptive search vs the P:856 grid search on the config's trace")
     ap.add_argument("--search-hbm-gb", type=float, default=320.0)
+    ap.add_argument("--queue", action="store_true",
+                    help="row f3: queue-coupled disk prefetch at low and high workload density (Obs. 2/4)")
     ap.add_argument("--analytics", action="store_true",
                     help="row f4 analytics: X6 reuse skew and X5 oracle-TTL footprint of the config's trace")
     ap.add_argument("--ttl", action="store_true",
@@ -496,6 +547,9 @@ def main():
         return
     if args.ttl:
         run_ttl(args, K, ctx, load_dev(), rank, spec)
+        return
+    if args.queue:
+        run_queue(args, K, ctx, load_dev(), rank, spec, np.diff(off_h.numpy()))
         return
     if args.analytics:
         tr = load_dev()

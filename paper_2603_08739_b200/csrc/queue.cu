@@ -7,13 +7,15 @@
 // realised hit prefix -- and with it prefill time, TTFT and the instance's busy time -- depends
 // on the wait, which depends on every earlier request.
 //
-// B200 design: one thread per configuration walks the requests in arrival order.  Per request
-// it counts its tier hits from the accesses' pre-request LRU depths and reuse intervals
-// (uniform loads: every lane of a warp reads the same access, one broadcast transaction), picks
-// the earliest-free instance from an [instance][config] array (coalesced across the warp),
-// and writes the request's TTFT to a per-configuration row for the exact nearest-rank P99
-// (CUB segmented sort).  Compiled with -fmad=false: the fp64 sequence is the oracle's, term by
-// term (R33).
+// B200 design, per wave of configurations sized to free HBM:
+//   1. k_queue_counts -- data-parallel over (request, configuration): each request's tier hits
+//      from its accesses' pre-request LRU depths and reuse intervals (a CTA per request, threads
+//      over configurations, broadcast loads of the accesses), stored [request][configuration];
+//   2. k_queue -- the sequential part only: one thread per configuration walks the requests,
+//      reading its counts coalesced, the instances' free times in shared memory; writes each
+//      request's TTFT to a per-configuration row;
+//   3. the exact nearest-rank P99 from a CUB segmented sort of the rows.
+// Compiled with -fmad=false: the fp64 sequence is the oracle's, term by term (R33).
 #include <cub/cub.cuh>
 
 #include <vector>
@@ -25,47 +27,73 @@ namespace kareto {
 __device__ __forceinline__ double qmax(double a, double b) { return a > b ? a : b; }
 __device__ __forceinline__ double qmin(double a, double b) { return a < b ? a : b; }
 
-__global__ void __launch_bounds__(128) k_queue(const uint32_t *__restrict__ s, const uint32_t *__restrict__ depth,
-                                               const uint32_t *__restrict__ delta, const uint16_t *__restrict__ grp,
-                                               const int64_t *__restrict__ arr, const uint32_t *__restrict__ inlen,
-                                               const uint32_t *__restrict__ outlen, int64_t R,
-                                               const kareto_config *__restrict__ cfg,
-                                               const uint32_t *__restrict__ rows, int n_tuner, int G, int64_t n,
-                                               const kareto_model m, uint64_t span_ms, uint64_t LO,
-                                               double *__restrict__ F, double *__restrict__ ttft,
-                                               kareto_queue_result *__restrict__ out) {
+// R49, data-parallel over (request, configuration): a CTA per request, threads over the wave's
+// configurations; every thread scans the request's accesses (the same addresses across the
+// CTA: broadcast loads) and stores (h1, h2, h3) at [request][configuration].
+__global__ void __launch_bounds__(128) k_queue_counts(const uint32_t *__restrict__ s,
+                                                      const uint32_t *__restrict__ depth,
+                                                      const uint32_t *__restrict__ delta,
+                                                      const uint16_t *__restrict__ grp, int64_t R,
+                                                      const kareto_config *__restrict__ cfg,
+                                                      const uint32_t *__restrict__ rows, int n_tuner, int G,
+                                                      int64_t nw, uint4 *__restrict__ cnt) {
+  for (int64_t r = blockIdx.x; r < R; r += gridDim.x) {
+    const uint32_t s0 = s[r], s1 = s[r + 1];
+    const uint16_t g = grp[r];
+    for (int64_t c = threadIdx.x; c < nw; c += blockDim.x) {
+      const kareto_config cf = cfg[c];
+      const bool ttl = cf.cap[2] == KARETO_INF;
+      const uint64_t c1 = cf.cap[0], c12 = cf.cap[0] + cf.cap[1];
+      const uint64_t C = ttl ? c12 : c12 + cf.cap[2];
+      const uint32_t tg = rows[(size_t)(n_tuner > 0 ? cf.tuner : 0) * G + g];
+      uint32_t h1 = 0, h2 = 0, h3 = 0;
+#pragma unroll 4
+      for (uint32_t j = s0; j < s1; j++) {
+        const uint32_t dj = depth[j];
+        if (dj == kNone) continue;
+        if (dj <= c1) h1++;
+        else if (dj <= c12) h2++;
+        else if ((ttl || dj <= C) && delta[j] <= tg) h3++;
+      }
+      cnt[(size_t)r * nw + c] = make_uint4(h1, h2, h3, 0);
+    }
+  }
+}
+
+// R50-R53: one thread per configuration walks the requests; the instances' free times live in
+// shared memory (SMEM) or in an [instance][configuration] global array.
+template <bool SMEM>
+__global__ void __launch_bounds__(32) k_queue(const int64_t *__restrict__ arr, const uint32_t *__restrict__ inlen,
+                                              const uint32_t *__restrict__ outlen, int64_t R,
+                                              const kareto_config *__restrict__ cfg, int64_t n,
+                                              const uint4 *__restrict__ cnt, const kareto_model m, uint64_t span_ms,
+                                              uint64_t LO, double *__restrict__ Fg, double *__restrict__ ttft,
+                                              kareto_queue_result *__restrict__ out) {
+  extern __shared__ double Fs[];
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= n) return;
+  const int I = m.instances;
+  // F[i] of this thread: shared [i][lane] or global [i][config]
+  double *F = SMEM ? Fs + threadIdx.x : Fg + c;
+  const size_t fs = SMEM ? blockDim.x : (size_t)n;
   const kareto_config cf = cfg[c];
   const bool ttl = cf.cap[2] == KARETO_INF;
-  const uint64_t c1 = cf.cap[0], c12 = cf.cap[0] + cf.cap[1];
-  const uint64_t C = ttl ? c12 : c12 + cf.cap[2];
-  const uint32_t *tau = rows + (size_t)(n_tuner > 0 ? cf.tuner : 0) * G;
   const uint64_t Bb = m.block_bytes;
   const kareto_medium md = m.media[cf.medium];
   const double prov_gb = ttl ? m.ttl_prov_gb : (double)(cf.cap[2] * Bb) / 1e9;
   const double bw = qmin(md.bw_max, md.bw_base + md.bw_slope * prov_gb);
-  const int I = m.instances;
-  for (int i = 0; i < I; i++) F[(size_t)i * n + c] = 0.0;
+  for (int i = 0; i < I; i++) F[i * fs] = 0.0;
   const int64_t a0 = arr[0];
   double total = 0.0;
   uint64_t real = 0, capd = 0;
   for (int64_t r = 0; r < R; r++) {
-    const uint32_t s0 = s[r], s1 = s[r + 1];
-    const uint32_t tg = tau[grp[r]];
-    uint64_t h1 = 0, h2 = 0, h3 = 0;
-    for (uint32_t j = s0; j < s1; j++) {  // R49
-      const uint32_t dj = depth[j];
-      if (dj == kNone) continue;
-      if (dj <= c1) h1++;
-      else if (dj <= c12) h2++;
-      else if ((ttl || dj <= C) && delta[j] <= tg) h3++;
-    }
+    const uint4 hc = cnt[(size_t)r * n + c];
+    const uint64_t h1 = hc.x, h2 = hc.y, h3 = hc.z;
     const double a = (double)(arr[r] - a0) * 1e-3;  // R50
     int bi = 0;
-    double fb = F[c];
+    double fb = F[0];
     for (int i = 1; i < I; i++) {
-      const double f = F[(size_t)i * n + c];
+      const double f = F[i * fs];
       if (f < fb) { fb = f; bi = i; }
     }
     const double start = qmax(a, fb);
@@ -82,12 +110,12 @@ __global__ void __launch_bounds__(128) k_queue(const uint32_t *__restrict__ s, c
     const double t = (w + prefill) + dram;
     total = total + t;
     if (ttft) ttft[(size_t)c * R + r] = t;
-    F[(size_t)bi * n + c] = ((start + prefill) + dram) + decode;
+    F[bi * fs] = ((start + prefill) + dram) + decode;
     real += h3r;
     capd += h3;
   }
-  double fmax = F[c];
-  for (int i = 1; i < I; i++) fmax = qmax(fmax, F[(size_t)i * n + c]);
+  double fmax = F[0];
+  for (int i = 1; i < I; i++) fmax = qmax(fmax, F[i * fs]);
   const double M = qmax((double)span_ms * 1e-3, fmax);  // R53
   kareto_queue_result q;
   q.ttft_mean_ms = 1e3 * (total / (double)R);
@@ -155,22 +183,35 @@ static kareto_status eval_queue(kareto_ctx *ctx, const kareto_trace *tr, const k
   cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, &rsv);
   cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemCurrent, &used);
   const double avail = (double)freeb + (double)(rsv > used ? rsv - used : 0);
-  int64_t W = (int64_t)(0.4 * avail / (16.0 * (double)R + 8.0 * m.instances + 64.0));
+  int64_t W = (int64_t)(0.4 * avail / (32.0 * (double)R + 8.0 * m.instances + 64.0));
   if (W > n) W = n;
   if (W < 1) return fail(ctx, KARETO_E_OOM, "eval_queue: %lld requests do not fit one configuration", (long long)R);
   const int64_t k99 = (99 * R + 99) / 100;  // ceil(0.99 R)
+  const bool smem = (size_t)m.instances * 32 * 8 <= 96 * 1024;
   DBuf<double> F, tt, ts;
+  DBuf<uint4> cnt;
   DBuf<int64_t> off;
   DBuf<uint8_t> tmp;
-  KTRY(F.alloc(ctx, (size_t)m.instances * W)); KTRY(tt.alloc(ctx, (size_t)W * R)); KTRY(ts.alloc(ctx, (size_t)W * R));
-  KTRY(off.alloc(ctx, W + 1));
+  KTRY(F.alloc(ctx, smem ? 1 : (size_t)m.instances * W)); KTRY(tt.alloc(ctx, (size_t)W * R));
+  KTRY(ts.alloc(ctx, (size_t)W * R)); KTRY(cnt.alloc(ctx, (size_t)W * R)); KTRY(off.alloc(ctx, W + 1));
+  const size_t sbytes = smem ? (size_t)m.instances * 32 * 8 : 0;
+  if (smem) cudaFuncSetAttribute(k_queue<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbytes);
   for (int64_t w0 = 0; w0 < n; w0 += W) {
     const int64_t nw = n - w0 < W ? n - w0 : W;
     {
+      Pass ps(ctx, "F3_counts", 1, 1);
+      k_queue_counts<<<(unsigned)(R < 64 * ctx->num_sms ? R : 64 * ctx->num_sms), 128, 0, st>>>(
+          tr->s, tr->depth, tr->delta, tr->grp, R, dcfg.p + w0, drows.p, n_tuner, G, nw, cnt.p);
+    }
+    {
       Pass ps(ctx, "F3_queue", 1, 1);
-      k_queue<<<grid_for(nw, 128), 128, 0, st>>>(tr->s, tr->depth, tr->delta, tr->grp, tr->arr, tr->inlen, tr->outlen,
-                                                 R, dcfg.p + w0, drows.p, n_tuner, G, nw, m, (uint64_t)tr->span_ms,
-                                                 tr->Ltok + tr->O, F.p, tt.p, dout.p + w0);
+      const unsigned g = (unsigned)((nw + 31) / 32);
+      if (smem)
+        k_queue<true><<<g, 32, sbytes, st>>>(tr->arr, tr->inlen, tr->outlen, R, dcfg.p + w0, nw, cnt.p, m,
+                                             (uint64_t)tr->span_ms, tr->Ltok + tr->O, F.p, tt.p, dout.p + w0);
+      else
+        k_queue<false><<<g, 32, 0, st>>>(tr->arr, tr->inlen, tr->outlen, R, dcfg.p + w0, nw, cnt.p, m,
+                                         (uint64_t)tr->span_ms, tr->Ltok + tr->O, F.p, tt.p, dout.p + w0);
     }
     {
       Pass ps(ctx, "F3_p99", 1, 2);

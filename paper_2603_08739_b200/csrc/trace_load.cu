@@ -605,9 +605,16 @@ __global__ void k_run_reuse(const uint32_t *__restrict__ val, const uint32_t *__
                             const int *__restrict__ m_ptr, const uint32_t *__restrict__ reuse_cnt,
                             unsigned long long *__restrict__ run_reuse, uint32_t *__restrict__ n_runs) {
   int m = *m_ptr;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    uint32_t rid = run_incl[i] - 1;
-    atomicAdd(&run_reuse[rid], (unsigned long long)reuse_cnt[val[i]]);
+  // runs are contiguous in sorted order, so a warp's lanes mostly share a run: reduce per run
+  // inside the warp first (hot system-prompt roots would otherwise serialise on one address)
+  const int m_pad = (m + 31) & ~31;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m_pad; i += gridDim.x * blockDim.x) {
+    const bool in = i < m;
+    const uint32_t rid = in ? run_incl[i] - 1 : 0xFFFFFFFFu;
+    const uint32_t v = in ? reuse_cnt[val[i]] : 0u;
+    const unsigned same = __match_any_sync(0xFFFFFFFFu, rid);
+    const uint32_t sum = __reduce_add_sync(same, v);
+    if (in && (int)(threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&run_reuse[rid], (unsigned long long)sum);
     if (i == m - 1) *n_runs = run_incl[i];
   }
 }
@@ -928,7 +935,8 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
                                                              nruns.p);
       k_rank_keys<<<grid_for(m, 256, 4 * sms), 256, 0, st>>>(run_reuse.p, nruns.p, rankkey.p, rankidx.p, (uint32_t)m);
       KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, rankkey.p, rankkey_s.p, rankidx.p, ranked.p, m, 0, 64, st);
+        // reuse < 2^32: the low 32 bits of ~reuse order runs the same way (4 passes instead of 8)
+        return cub::DeviceRadixSort::SortPairs(t, b, rankkey.p, rankkey_s.p, rankidx.p, ranked.p, m, 0, 32, st);
       }));
       k_rank_of_run<<<grid_for(m, 256, 4 * sms), 256, 0, st>>>(ranked.p, nruns.p, rank.p);
       k_assign_groups<<<grid_for(m, 256, 4 * sms), 256, 0, st>>>(rval_s.p, run_incl.p, m_dev.p, rank.p, K, tr->grp);

@@ -38,6 +38,10 @@ __global__ void k_build_lut(const uint32_t *__restrict__ Bd, int nb, int sh, uin
   }
 }
 
+#ifndef HIST_AGG
+#define HIST_AGG 0
+#endif
+
 // index of the first boundary >= v (nb if none)
 __device__ __forceinline__ int bin_of(uint32_t v, const uint32_t *__restrict__ Bd, int nb, const uint32_t *lut_s,
                                       int sh) {
@@ -136,18 +140,31 @@ __global__ void __launch_bounds__(H_THREADS) k_hist_dD(uint64_t N, uint64_t per_
         int bd = bin_of(d, Bd, nb, lut_s, sh);
         if (bd < nb) cell = (ntc > 0 ? tbin_of(delta[j], Tc, ntc) : 0) * nb + bd;
         uint32_t D = d + ((uint32_t)j - s[r]);
-        int bD = bin_of(D, Bd, nb, lut_s, sh);
+        // D >= d: walk forward from d's bin (D - d is the offset inside the request, usually
+        // small against the boundary gaps), falling back to the search after a few steps
+        int bD = bd;
+        int steps = 0;
+        while (bD < nb && __ldg(&Bd[bD]) < D && steps < 4) { bD++; steps++; }
+        if (bD < nb && __ldg(&Bd[bD]) < D) bD = bin_of(D, Bd, nb, lut_s, sh);
         if (bD < nb) dcell = bD;
       }
     }
-    unsigned same = __match_any_sync(0xffffffffu, cell);
-    uint32_t ks = __reduce_add_sync(same, k);
-    if (cell >= 0 && (__ffs(same) - 1) == lane) {
-      atomicAdd(&cnt[cell], (uint32_t)__popc(same));
-      if (ks) atomicAdd(&sk[cell], ks);
+    if (HIST_AGG) {
+      unsigned same = __match_any_sync(0xffffffffu, cell);
+      uint32_t ks = __reduce_add_sync(same, k);
+      if (cell >= 0 && (__ffs(same) - 1) == lane) {
+        atomicAdd(&cnt[cell], (uint32_t)__popc(same));
+        if (ks) atomicAdd(&sk[cell], ks);
+      }
+      unsigned sameD = __match_any_sync(0xffffffffu, dcell);
+      if (dcell >= 0 && (__ffs(sameD) - 1) == lane) atomicAdd(&cD[dcell], (uint32_t)__popc(sameD));
+    } else {
+      if (cell >= 0) {
+        atomicAdd(&cnt[cell], 1u);
+        if (k) atomicAdd(&sk[cell], k);
+      }
+      if (dcell >= 0) atomicAdd(&cD[dcell], 1u);
     }
-    unsigned sameD = __match_any_sync(0xffffffffu, dcell);
-    if (dcell >= 0 && (__ffs(sameD) - 1) == lane) atomicAdd(&cD[dcell], (uint32_t)__popc(sameD));
   }
   __syncthreads();
   for (int i = threadIdx.x; i < W; i += blockDim.x) {

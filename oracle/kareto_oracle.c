@@ -488,8 +488,11 @@ static void or_enter(or_run *X, int t, int32_t b) {
   if (t == T_DISK && X->use_expiry && S->tau[S->gblk[b]] != OR_INF_TTL) or_epush(S, b);
 }
 
-/* One configuration, literal replay. tau_row[K+1] (ms, OR_INF_TTL = infinity). */
-int or_replay(const or_trace *tr, const or_config *cfg, const uint32_t *tau_row, or_counts *out) {
+/* One configuration, literal replay. tau_row[K+1] (ms, OR_INF_TTL = infinity).  lookup_tier
+ * (may be NULL): [N] per access (touch order) the tier that served it in its request's hit
+ * prefix (1 HBM, 2 DRAM, 3 disk or lease store), 0 outside the prefix (row f3, R51). */
+int or_replay_lookup(const or_trace *tr, const or_config *cfg, const uint32_t *tau_row, or_counts *out,
+                     uint8_t *lookup_tier) {
   memset(out, 0, sizeof(*out));
   if (cfg->policy > OR_LFU) return OR_E_INVALID;
   int ttl_mode = cfg->cap[2] == OR_INF_CAP;
@@ -550,10 +553,12 @@ int or_replay(const or_trace *tr, const or_config *cfg, const uint32_t *tau_row,
     }
     for (int64_t k = 0; k < n; k++) {
       int32_t b = chain[k];
+      if (lookup_tier) lookup_tier[tr->s[r] + (n - 1 - k)] = 0;
       if (k < h) {
         int t = S.tier[b] != T_NONE ? S.tier[b] : T_DISK;
         out->hit[t - 1] += 1;
         out->hit_pos_sum += (uint64_t)k;
+        if (lookup_tier) lookup_tier[tr->s[r] + (n - 1 - k)] = (uint8_t)t;
       } else {
         out->miss += 1;
         if (S.tier[b] != T_NONE) out->resident_after_hole += 1;
@@ -610,6 +615,10 @@ int or_replay(const or_trace *tr, const or_config *cfg, const uint32_t *tau_row,
   free(S.pos); free(S.eheap); free(S.epos); free(S.tier); free(S.seen); free(S.last_t);
   free(S.last_seq); free(S.ins_seq); free(S.freq); free(S.lease_t); free(gblk);
   return OR_OK;
+}
+
+int or_replay(const or_trace *tr, const or_config *cfg, const uint32_t *tau_row, or_counts *out) {
+  return or_replay_lookup(tr, cfg, tau_row, out, NULL);
 }
 
 typedef struct {

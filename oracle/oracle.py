@@ -80,6 +80,7 @@ def _load():
     L.or_trace_stats.argtypes = [vp] + [vp] * 8
     L.or_trace_export.argtypes = [vp] + [vp] * 7
     L.or_replay_many.argtypes = [vp, vp, i64, vp, i32, vp, ctypes.c_int]
+    L.or_replay_lookup.argtypes = [vp, vp, vp, vp, vp]
     L.or_stack_create.restype = vp
     L.or_stack_create.argtypes = [vp]
     L.or_stack_free.argtypes = [vp]
@@ -245,6 +246,19 @@ class OracleTrace:
         if st != OK:
             raise OracleError(st, "replay")
         return out
+
+    def replay_lookup(self, cfg, ttl=None):
+        """O1 for one configuration plus, per access (touch order), the tier that served it in
+        its request's hit prefix (1 HBM, 2 DRAM, 3 disk / lease), 0 outside (row f3)."""
+        ttl = self._ttl(ttl)
+        c = np.ascontiguousarray(np.atleast_1d(cfg)[:1], CONFIG_DTYPE)
+        row = np.ascontiguousarray(ttl[int(c[0]["tuner"])])
+        out = np.zeros(1, COUNTS_DTYPE)
+        lt = np.zeros(max(self.N, 1), np.uint8)
+        st = self._L.or_replay_lookup(self._h, c.ctypes.data, row.ctypes.data, out.ctypes.data, lt.ctypes.data)
+        if st != OK:
+            raise OracleError(st, "replay_lookup")
+        return out[0], lt[:self.N]
 
     def _ttl(self, ttl):
         if ttl is None:

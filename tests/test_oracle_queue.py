@@ -23,6 +23,23 @@ def setup(tr, top_k=2):
 
 
 @pytest.mark.parametrize("seed", [0, 1, 2])
+def test_literal_prefixes_match_the_stack_shape(seed):
+    # O1's per-request hit prefixes (any policy) against the O2 depth counts for LRU stack configs:
+    # same blocks, HBM first, then DRAM, then disk
+    tr = ki.synthetic("chat", R=300, seed=seed)
+    ot, e, d = setup(tr)
+    U = ot.U
+    ttl = np.array([[600_000] * 3, [0xFFFFFFFF] * 3], np.uint32)
+    for cap, tuner in [((U // 50, U // 10, U // 3), 1), ((U // 20, U // 5, U // 2), 0), ((U // 20, 0, INF), 0),
+                       ((0, U // 7, INF), 0)]:
+        cf = O.configs([cap], tuner=tuner)
+        _, lt = ot.replay_lookup(cf, ttl)
+        lit = Q.prefixes_from_lookup(lt.tolist(), e["s"].tolist())
+        h1, h2, h3 = Q.per_request_hits(d, e["delta"], e["s"].tolist(), e["group"].tolist(), cap, ttl[tuner])
+        assert lit == Q.prefixes_from_counts(h1, h2, h3)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
 def test_per_request_hits_sum_to_stack_totals(seed):
     tr = ki.synthetic("chat", R=400, seed=seed)
     ot, e, d = setup(tr)
@@ -93,6 +110,15 @@ def test_no_queueing_no_disk_matches_fluid_mean():
     span_s = ot.span_ms * 1e-3
     assert span_s <= res["makespan_s"] <= span_s + 60.0
     assert res["tok_per_s"] == (ot.Ltok + ot.O) / res["makespan_s"] <= -fluid[1]
+
+
+def test_realised_prefix_rule():
+    # R51 on hand sequences: disk blocks stream in chain order; the prefix ends at the first one
+    # not loaded; x = 1.5 loads one disk block
+    assert Q.realised([1, 1, 2, 3, 3], 1.5) == (4, 1, 1, 2)
+    assert Q.realised([1, 3, 1, 3, 2], 1.0) == (3, 0, 1, 2)       # mixed tiers (FIFO / LFU)
+    assert Q.realised([3, 1, 2], 0.0) == (0, 0, 0, 1)
+    assert Q.realised([1, 2, 2], 0.0) == (3, 2, 0, 0)
 
 
 def test_p99_is_the_nearest_rank():

@@ -15,7 +15,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),
           "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 # objective.cu holds the fp64 model: no FMA contraction (R33)
-PER_FILE = {"objective.cu": ["-fmad=false"], "queue.cu": ["-fmad=false"]}
+PER_FILE = {"objective.cu": ["-fmad=false"], "queue.cu": ["-fmad=false"], "replay.cu": ["-fmad=false"]}
 
 
 def _nvcc() -> str:

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "replay.cuh"
 
 namespace kareto {
 
@@ -138,9 +139,10 @@ __global__ void k_seg_offsets(int64_t n, int64_t R, int64_t *__restrict__ off) {
   if (c <= n) off[c] = c * R;
 }
 
-static kareto_status eval_queue(kareto_ctx *ctx, const kareto_trace *tr, const kareto_config *cfg, int64_t n,
-                                const uint32_t *ttl_ms, int32_t n_tuner, const kareto_model *model,
-                                kareto_queue_result *out) {
+// stack-eligible LRU configurations: per-request counts from the depths (k_queue_counts)
+static kareto_status eval_queue_stack(kareto_ctx *ctx, const kareto_trace *tr, const kareto_config *cfg, int64_t n,
+                                      const uint32_t *ttl_ms, int32_t n_tuner, const kareto_model *model,
+                                      kareto_queue_result *out) {
   if (!tr || !model || n < 0 || (n > 0 && (!cfg || !out)) || n_tuner < 0 || (n_tuner > 0 && !ttl_ms))
     return fail(ctx, KARETO_E_INVALID, "eval_queue: bad arguments");
   if (n == 0) return KARETO_OK;
@@ -226,6 +228,66 @@ static kareto_status eval_queue(kareto_ctx *ctx, const kareto_trace *tr, const k
   }
   KCUDA(ctx, cudaMemcpyAsync(out, dout.p, sizeof(kareto_queue_result) * n, cudaMemcpyDeviceToHost, st));
   return sync(ctx, "eval_queue");
+}
+
+// all configurations: stack-eligible LRU ones through the depth counts, the others through the
+// K6 replay with the queue evaluated inline (the hit prefix of every request, R49)
+static kareto_status eval_queue(kareto_ctx *ctx, const kareto_trace *tr, const kareto_config *cfg, int64_t n,
+                                const uint32_t *ttl_ms, int32_t n_tuner, const kareto_model *model,
+                                kareto_queue_result *out) {
+  if (!tr || !model || n < 0 || (n > 0 && (!cfg || !out)) || n_tuner < 0 || (n_tuner > 0 && !ttl_ms))
+    return fail(ctx, KARETO_E_INVALID, "eval_queue: bad arguments");
+  if (n == 0) return KARETO_OK;
+  const int G = tr->K + 1;
+  const kareto_model &m = *model;
+  if (m.instances < 1 || m.instances > 4096 || m.block_bytes == 0 || !(m.bw_dram > 0) || m.n_media < 1 ||
+      m.n_media > 8)
+    return fail(ctx, KARETO_E_INVALID, "eval_queue: invalid model constants (1 <= instances <= 4096)");
+  std::vector<uint32_t> rows;
+  if (n_tuner == 0) rows.assign(G, KARETO_TTL_INF);
+  else rows.assign(ttl_ms, ttl_ms + (size_t)n_tuner * G);
+  std::vector<kareto_config> cS, cP;
+  std::vector<int64_t> iS, iP;
+  for (int64_t i = 0; i < n; i++) {
+    const kareto_config &c = cfg[i];
+    if (c.policy > KARETO_LFU) return fail(ctx, KARETO_E_INVALID, "eval_queue: config %lld: bad policy", (long long)i);
+    if ((n_tuner == 0 && c.tuner != 0) || (n_tuner > 0 && c.tuner >= n_tuner) || c.medium >= m.n_media)
+      return fail(ctx, KARETO_E_INVALID, "eval_queue: config %lld: bad tuner / medium", (long long)i);
+    const uint32_t *row = rows.data() + (size_t)(n_tuner > 0 ? c.tuner : 0) * G;
+    bool uniform = true;
+    for (int g = 1; g < G; g++) uniform = uniform && row[g] == row[0];
+    if (c.cap[2] == KARETO_INF) {
+      for (int g = 0; g < G; g++)
+        if (row[g] == KARETO_TTL_INF)
+          return fail(ctx, KARETO_E_INVALID, "eval_queue: config %lld: TTL mode with an infinite TTL", (long long)i);
+    }
+    const bool stack = c.policy == KARETO_LRU && (c.cap[2] == KARETO_INF || uniform);
+    (stack ? cS : cP).push_back(c);
+    (stack ? iS : iP).push_back(i);
+  }
+  std::vector<kareto_queue_result> oS(cS.size()), oP(cP.size());
+  if (!cS.empty())
+    KTRY(eval_queue_stack(ctx, tr, cS.data(), (int64_t)cS.size(), ttl_ms, n_tuner, model, oS.data()));
+  if (!cP.empty()) {
+    DBuf<uint32_t> drows;
+    DBuf<kareto_counts> dcnt;
+    DBuf<kareto_queue_result> dq;
+    KTRY(drows.alloc(ctx, rows.size())); KTRY(dcnt.alloc(ctx, cP.size())); KTRY(dq.alloc(ctx, cP.size()));
+    KCUDA(ctx, cudaMemcpyAsync(drows.p, rows.data(), 4 * rows.size(), cudaMemcpyHostToDevice, ctx->stream));
+    QueueArgs qa;
+    qa.model = model;
+    qa.out_dev = dq.p;
+    qa.span_ms = (uint64_t)tr->span_ms;
+    qa.LO = tr->Ltok + tr->O;
+    KTRY(replay_eval(ctx, const_cast<kareto_trace *>(tr), cP.data(), (int64_t)cP.size(), rows.data(), drows.p,
+                     n_tuner, dcnt.p, qa));
+    KCUDA(ctx, cudaMemcpyAsync(oP.data(), dq.p, sizeof(kareto_queue_result) * cP.size(), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    KTRY(sync(ctx, "eval_queue replay"));
+  }
+  for (size_t k = 0; k < cS.size(); k++) out[iS[k]] = oS[k];
+  for (size_t k = 0; k < cP.size(); k++) out[iP[k]] = oP[k];
+  return KARETO_OK;
 }
 
 }  // namespace kareto

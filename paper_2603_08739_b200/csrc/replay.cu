@@ -50,7 +50,16 @@ struct RState {
 // Per-thread replay of one configuration.  Every tier-indexed member is accessed with a
 // compile-time tier (template parameter / unrolled cascade), so the per-tier state stays in
 // registers rather than local memory.
-template <bool LFU, bool EXP>
+struct QueueState {  // row f3: per-configuration FCFS queue (DESIGN R50-R53)
+  const kareto_model *m;   // kernel-parameter copy
+  double *F;               // [I][W] instance free times
+  double *ttft;            // [W][R] per-request TTFT
+  double bw;               // disk bandwidth of the configuration's medium
+  double total;
+  uint64_t real, capd;
+};
+
+template <bool LFU, bool EXP, bool Q>
 struct Rep {
   const RState &v;
   const uint64_t c;
@@ -293,8 +302,47 @@ struct Rep {
     if (overflow<0>() && overflow<1>()) overflow<2>();
   }
 
+  // ------------------------------------------------------------ f3 queue (R50-R52)
+  QueueState *qs = nullptr;
+  __device__ void q_wait(uint32_t a, int &bi, double &start, double &w, double &x) const {
+    const double a_s = (double)a * 1e-3;
+    const int I = qs->m->instances;
+    double fb = qs->F[c];
+    bi = 0;
+    for (int i = 1; i < I; i++) {
+      const double f = qs->F[(size_t)i * v.W + c];
+      if (f < fb) { fb = f; bi = i; }
+    }
+    start = a_s > fb ? a_s : fb;
+    w = start - a_s;
+    x = (w * qs->bw) / (double)qs->m->block_bytes;
+  }
+  __device__ void q_serve(const ReplayTrace &T, uint32_t r, int bi, double start, double w, uint64_t H, uint64_t h2,
+                          uint64_t nd) {
+    const kareto_model &m = *qs->m;
+    const uint64_t L = T.inlen[r];
+    const uint64_t P0 = m.alpha_ps * L + m.beta_ps * (L * (L - 1) / 2);
+    const uint64_t S = 16 * m.alpha_ps * H + m.beta_ps * (256 * (H * (H - 1) / 2) + 120 * H);
+    const double prefill = (double)(P0 - S) * 1e-12;
+    const double dram = (double)(h2 * m.block_bytes) / m.bw_dram;
+    const double decode = (double)(m.dec_ps * (uint64_t)T.outlen[r]) * 1e-12;
+    const double t = (w + prefill) + dram;
+    qs->total = qs->total + t;
+    qs->ttft[(size_t)c * T.R + r] = t;
+    qs->F[(size_t)bi * v.W + c] = ((start + prefill) + dram) + decode;
+    qs->capd += nd;
+  }
+  __device__ void q_step(const ReplayTrace &T, uint32_t r, uint32_t a, uint64_t H, uint64_t h2, uint64_t nd,
+                         uint64_t) {
+    int bi;
+    double start, w, x;
+    q_wait(a, bi, start, w, x);
+    q_serve(T, r, bi, start, w, H, h2, nd);
+  }
+
   __device__ void run(const ReplayTrace &T, const kareto_config &cf, const uint32_t *rows, int n_tuner, int G,
-                      kareto_counts *out) {
+                      kareto_counts *out, QueueState *qsp = nullptr) {
+    qs = qsp;
     cap[0] = cf.cap[0];
     cap[1] = cf.cap[1];
     cap[2] = cf.cap[2];
@@ -316,8 +364,11 @@ struct Rep {
     for (uint32_t r = 0; r < T.R; r++) {
       const uint32_t s1 = T.s[r + 1];
       const uint32_t nb = s1 - s0;
-      if (nb == 0) continue;
       const uint32_t a = T.arr[r];
+      if (nb == 0) {
+        if (Q) q_step(T, r, a, 0, 0, 0, 0);  // a request without full blocks still queues
+        continue;
+      }
       const uint32_t tg = tau[T.grp[r]];
       // 1 PURGE (CAPACITY mode): disk blocks whose expiry key is below a (a - lt > tau_g)
       if (EXP) {
@@ -336,6 +387,12 @@ struct Rep {
           v.tier[at(x)] = T_NONE;
         }
       }
+      // f3 queue (R50): wait of this request before its lookup; x = disk blocks loadable (R51)
+      int qbi = 0;
+      double qstart = 0.0, qw = 0.0, qx = 0.0;
+      uint64_t qH = 0, qh2 = 0, qnd = 0;
+      bool qopen = true;
+      if (Q) q_wait(a, qbi, qstart, qw, qx);
       // 2 LOOKUP on the pre-request state: block k sits at position s0 + nb - 1 - k
       bool in_prefix = true;
       for (uint32_t k0 = 0; k0 < nb; k0 += LOOK) {
@@ -362,6 +419,18 @@ struct Rep {
             hit[1] += t == T_DRAM;
             hit[2] += t == T_DISK || t == T_NONE;
             hit_pos_sum += k0 + q;
+            if (Q) {  // R51: disk blocks stream in chain order; the first one not loaded ends the prefix
+              const bool disk = t == T_DISK || t == T_NONE;
+              if (disk) {
+                qnd++;
+                if (qopen && (double)qnd > qx) qopen = false;
+              }
+              if (qopen) {
+                qH++;
+                qh2 += t == T_DRAM;
+                qs->real += disk;
+              }
+            }
           } else {
             miss += 1;
             after_hole += t != T_NONE;
@@ -369,6 +438,7 @@ struct Rep {
           disk_writes += ttl_mode && !alive;
         }
       }
+      if (Q) q_serve(T, r, qbi, qstart, qw, qH, qh2, qnd);
       // 3 UPDATE leaf -> root = touch positions s0 .. s1-1 in order; the state of block j+1 is
       // loaded while block j is processed (mirrored writes keep it exact)
       uint32_t bn = T.blk[s0];
@@ -442,16 +512,56 @@ struct Rep {
   }
 };
 
-template <bool LFU, bool EXP>
+struct QueueKernelArgs {  // row f3 inside the replay (Q = true)
+  kareto_model m;
+  double *F;                     // [I][W]
+  double *ttft;                  // [W][R]
+  kareto_queue_result *out;      // indexed by the caller's configuration id
+  uint64_t span_ms, LO;
+};
+
+template <bool LFU, bool EXP, bool Q>
 __global__ void __launch_bounds__(64) k_replay(ReplayTrace T, const kareto_config *__restrict__ cfg,
                                                const uint32_t *__restrict__ idx, const uint32_t *__restrict__ rows,
                                                int n_tuner, int G, RState v, int64_t n,
-                                               kareto_counts *__restrict__ out) {
+                                               kareto_counts *__restrict__ out, QueueKernelArgs qa) {
   const int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (ci >= n) return;
   const uint32_t id = idx[ci];
-  Rep<LFU, EXP> rp(v, (uint64_t)ci);
-  rp.run(T, cfg[id], rows, n_tuner, G, out + id);
+  const kareto_config cf = cfg[id];
+  Rep<LFU, EXP, Q> rp(v, (uint64_t)ci);
+  if (!Q) {
+    rp.run(T, cf, rows, n_tuner, G, out + id);
+    return;
+  }
+  QueueState qs;
+  qs.m = &qa.m;
+  qs.F = qa.F;
+  qs.ttft = qa.ttft;
+  const bool ttl = cf.cap[2] == KARETO_INF;
+  const kareto_medium md = qa.m.media[cf.medium];
+  const double prov_gb = ttl ? qa.m.ttl_prov_gb : (double)(cf.cap[2] * qa.m.block_bytes) / 1e9;
+  const double bwv = md.bw_base + md.bw_slope * prov_gb;
+  qs.bw = md.bw_max < bwv ? md.bw_max : bwv;
+  qs.total = 0.0;
+  qs.real = qs.capd = 0;
+  for (int i = 0; i < qa.m.instances; i++) qa.F[(size_t)i * v.W + ci] = 0.0;
+  rp.run(T, cf, rows, n_tuner, G, out + id, &qs);
+  double fmax = qa.F[ci];
+  for (int i = 1; i < qa.m.instances; i++) {
+    const double f = qa.F[(size_t)i * v.W + ci];
+    fmax = fmax > f ? fmax : f;
+  }
+  const double span_s = (double)qa.span_ms * 1e-3;
+  const double M = span_s > fmax ? span_s : fmax;
+  kareto_queue_result q;
+  q.ttft_mean_ms = 1e3 * (qs.total / (double)T.R);
+  q.ttft_p99_ms = 0.0;
+  q.makespan_s = M;
+  q.tokens_per_s = (double)qa.LO / M;
+  q.disk_hits_capacity = qs.capd;
+  q.disk_hits_realized = qs.real;
+  qa.out[id] = q;
 }
 
 // ---------------------------------------------------------------- dense block ids
@@ -531,15 +641,27 @@ kareto_status replay_prepare(kareto_ctx *ctx, kareto_trace *tr) {
   return KARETO_OK;
 }
 
+__global__ void k_pick_p99_idx(const double *__restrict__ sorted, int64_t R, int64_t n, int64_t k,
+                               const uint32_t *__restrict__ idx, kareto_queue_result *__restrict__ out) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c < n) out[idx[c]].ttft_p99_ms = 1e3 * sorted[(size_t)c * R + (k - 1)];
+}
+__global__ void k_row_offsets(int64_t n, int64_t R, int64_t *__restrict__ off) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c <= n) off[c] = c * R;
+}
+
 kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config *cfg_host, int64_t n,
                           const uint32_t *rows_host, const uint32_t *rows_dev, int n_tuner,
-                          kareto_counts *counts_dev) {
+                          kareto_counts *counts_dev, const QueueArgs &qarg) {
   if (n <= 0) return KARETO_OK;
   KTRY(replay_prepare(ctx, tr));
   cudaStream_t st = ctx->stream;
   const uint64_t U = tr->U > 0 ? (uint64_t)tr->U : 1;
   const int G = tr->K + 1;
-  ReplayTrace T{(uint32_t)tr->R, (uint32_t)tr->U, tr->s, tr->arr_rel, tr->grp, tr->blk};
+  ReplayTrace T{(uint32_t)tr->R, (uint32_t)tr->U, tr->s, tr->arr_rel, tr->grp, tr->blk, tr->inlen, tr->outlen};
+  const bool Qm = qarg.model != nullptr;
+  const int64_t R = tr->R;
   // classes {list, LFU} x {expiry heap or not}; within a class, neighbours in a warp get
   // similar configurations (policy, TTL row, capacities) so their branches agree more often
   std::vector<uint32_t> cls[4];
@@ -577,6 +699,7 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
       }
     const uint64_t es = U + 1;
     uint64_t per_cfg = U * (1 + 4) + (lfu ? U * 4 + 12 * (hs[0] + hs[1] + hs[2]) : U * 8) + (exp ? U * 4 + 8 * es : 0);
+    if (Qm) per_cfg += 16 * (uint64_t)R + 8 * (uint64_t)qarg.model->instances + 64;  // f3: TTFT rows + queue
     size_t freeb = 0, totb = 0, rsv = 0, used = 0;
     KCUDA(ctx, cudaStreamSynchronize(st));
     KCUDA(ctx, cudaMemGetInfo(&freeb, &totb));
@@ -613,6 +736,16 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
     v.epos = epos.p; v.ekey = ekey.p;
     v.gblk = tr->gblk;
     v.W = W;
+    QueueKernelArgs qa{};
+    DBuf<double> qF, qt, qts;
+    DBuf<int64_t> qoff;
+    DBuf<uint8_t> qtmp;
+    if (Qm) {
+      qa.m = *qarg.model;
+      KTRY(qF.alloc(ctx, (size_t)qarg.model->instances * W)); KTRY(qt.alloc(ctx, (size_t)W * R));
+      KTRY(qts.alloc(ctx, (size_t)W * R)); KTRY(qoff.alloc(ctx, W + 1));
+      qa.F = qF.p; qa.ttft = qt.p; qa.out = qarg.out_dev; qa.span_ms = qarg.span_ms; qa.LO = qarg.LO;
+    }
     for (uint64_t w0 = 0; w0 < ix.size(); w0 += W) {
       const int64_t nw = (int64_t)(ix.size() - w0 < W ? ix.size() - w0 : W);
       KCUDA(ctx, cudaMemsetAsync(tier.p, 0, U * W, st));
@@ -621,10 +754,29 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
       Pass ps(ctx, "K6_replay", 1, 1);
       const unsigned grid = (unsigned)((nw + 63) / 64);
       const uint32_t *wi = didx.p + w0;
-      if (q == 0) k_replay<false, false><<<grid, 64, 0, st>>>(T, dcfg.p, wi, rows_dev, n_tuner, G, v, nw, counts_dev);
-      if (q == 1) k_replay<false, true><<<grid, 64, 0, st>>>(T, dcfg.p, wi, rows_dev, n_tuner, G, v, nw, counts_dev);
-      if (q == 2) k_replay<true, false><<<grid, 64, 0, st>>>(T, dcfg.p, wi, rows_dev, n_tuner, G, v, nw, counts_dev);
-      if (q == 3) k_replay<true, true><<<grid, 64, 0, st>>>(T, dcfg.p, wi, rows_dev, n_tuner, G, v, nw, counts_dev);
+#define KREP(L, E, QQ) k_replay<L, E, QQ><<<grid, 64, 0, st>>>(T, dcfg.p, wi, rows_dev, n_tuner, G, v, nw, counts_dev, qa)
+      if (!Qm) {
+        if (q == 0) KREP(false, false, false);
+        if (q == 1) KREP(false, true, false);
+        if (q == 2) KREP(true, false, false);
+        if (q == 3) KREP(true, true, false);
+      } else {
+        if (q == 0) KREP(false, false, true);
+        if (q == 1) KREP(false, true, true);
+        if (q == 2) KREP(true, false, true);
+        if (q == 3) KREP(true, true, true);
+      }
+#undef KREP
+      if (Qm && R > 0) {  // exact nearest-rank P99 of each configuration's TTFT row (R53)
+        Pass pq(ctx, "F3_p99", 1, 2);
+        k_row_offsets<<<grid_for(nw + 1, 256), 256, 0, st>>>(nw, R, qoff.p);
+        size_t bytes = 0;
+        KCUDA(ctx, cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, qt.p, qts.p, nw * R, nw, qoff.p, qoff.p + 1, st));
+        if (bytes > qtmp.n) KTRY(qtmp.alloc(ctx, bytes));
+        bytes = qtmp.n;
+        KCUDA(ctx, cub::DeviceSegmentedSort::SortKeys(qtmp.p, bytes, qt.p, qts.p, nw * R, nw, qoff.p, qoff.p + 1, st));
+        k_pick_p99_idx<<<grid_for(nw, 256), 256, 0, st>>>(qts.p, R, nw, (99 * R + 99) / 100, wi, qarg.out_dev);
+      }
     }
     KTRY(sync(ctx, "replay"));
   }

@@ -12,6 +12,15 @@ struct ReplayTrace {
   const uint32_t *arr;     // [R] arrival ms relative to the first request
   const uint16_t *grp;     // [R] group of each request
   const uint32_t *blk;     // [N] dense block id of each access (touch order)
+  const uint32_t *inlen;   // [R] input tokens (row f3 queue)
+  const uint32_t *outlen;  // [R] output tokens (row f3 queue)
+};
+
+// row f3 (queue.cu): the queue model evaluated inside the replay of each configuration
+struct QueueArgs {
+  const kareto_model *model = nullptr;  // host; null = no queue
+  kareto_queue_result *out_dev = nullptr;  // [n] in the caller's configuration order
+  uint64_t span_ms = 0, LO = 0;
 };
 
 // dense block ids / groups / relative arrivals (lazily, cached in the trace)
@@ -20,6 +29,6 @@ kareto_status replay_prepare(kareto_ctx *ctx, kareto_trace *tr);
 // TTL rows, on the host and on the device
 kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config *cfg_host, int64_t n,
                           const uint32_t *rows_host, const uint32_t *rows_dev, int n_tuner,
-                          kareto_counts *counts_dev);
+                          kareto_counts *counts_dev, const QueueArgs &q = QueueArgs());
 
 }  // namespace kareto

@@ -46,30 +46,28 @@ def test_queue_parity(ctx, kind, R, seed, inst):
     for cap in caps:
         for t in range(3):
             if cap[2] == INF and t == 0:
-                continue                    # TTL mode needs finite TTLs
-            if cap[2] != INF and t == 2:
-                continue                    # per-group TTLs on a finite disk: replay only
-            for med in (0, 1):
-                rows.append((cap, t, med))
-    oc = O.configs([r[0] for r in rows], tuner=[r[1] for r in rows], medium=[r[2] for r in rows])
+                continue                    # TTL mode needs finite TTLs (R22)
+            for pol in (O.LRU, O.FIFO, O.LFU):
+                rows.append((cap, t, (len(rows) % 2), pol))
+    oc = O.configs([r[0] for r in rows], tuner=[r[1] for r in rows], medium=[r[2] for r in rows],
+                   policy=[r[3] for r in rows])
     want = Q.evaluate(tr, ot, oc, ttl, O.Model(instances=inst, **MODEL_KW))
     gt = ctx.load(tr, top_k=3)
     got = ctx.eval_queue(gt, kcfg(oc), K.Model(instances=inst, **MODEL_KW), ttl)
     for i, w in enumerate(want):
         g = got[i]
-        assert (int(g["disk_hits_capacity"]), int(g["disk_hits_realized"])) == (w["disk_cap"], w["disk_real"]), i
+        assert (int(g["disk_hits_capacity"]), int(g["disk_hits_realized"])) == (w["disk_cap"], w["disk_real"]), \
+            (i, rows[i])
         for f, k in (("ttft_mean_ms", "mean_ms"), ("ttft_p99_ms", "p99_ms"), ("makespan_s", "makespan_s"),
                      ("tokens_per_s", "tok_per_s")):
-            assert np.float64(g[f]).view(np.uint64) == np.float64(w[k]).view(np.uint64), (i, f, g[f], w[k])
+            assert np.float64(g[f]).view(np.uint64) == np.float64(w[k]).view(np.uint64), (i, rows[i], f, g[f], w[k])
 
 
-def test_queue_unsupported_and_invalid(ctx):
+def test_queue_invalid(ctx):
     tr = ki.synthetic("chat", R=50, seed=9)
     gt = ctx.load(tr, top_k=2)
     m = K.Model(**MODEL_KW)
-    with pytest.raises(K.KaretoError, match="not LRU"):
-        ctx.eval_queue(gt, K.configs([[1, 1, 1]], policy=K.FIFO), m)
-    with pytest.raises(K.KaretoError, match="per-group"):
-        ctx.eval_queue(gt, K.configs([[1, 1, 1]]), m, np.array([[1, 2, 3]], np.uint32))
     with pytest.raises(K.KaretoError, match="infinite"):
         ctx.eval_queue(gt, K.configs([[1, 1, int(K.INF)]]), m)
+    with pytest.raises(K.KaretoError, match="tuner"):
+        ctx.eval_queue(gt, K.configs([[1, 1, 1]], tuner=2), m, np.array([[1, 2, 3]], np.uint32))

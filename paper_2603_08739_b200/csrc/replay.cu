@@ -751,7 +751,8 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
       KCUDA(ctx, cudaMemsetAsync(tier.p, 0, U * W, st));
       KCUDA(ctx, cudaMemsetAsync(lt.p, 0xFF, 4 * U * W, st));
       if (exp) KCUDA(ctx, cudaMemsetAsync(epos.p, 0xFF, 4 * U * W, st));
-      Pass ps(ctx, "K6_replay", 1, 1);
+      static const char *kPassName[4] = {"K6_replay_list", "K6_replay_list_exp", "K6_replay_lfu", "K6_replay_lfu_exp"};
+      Pass ps(ctx, kPassName[q], 1, 1);
       const unsigned grid = (unsigned)((nw + 63) / 64);
       const uint32_t *wi = didx.p + w0;
 #define KREP(L, E, QQ) k_replay<L, E, QQ><<<grid, 64, 0, st>>>(T, dcfg.p, wi, rows_dev, n_tuner, G, v, nw, counts_dev, qa)

@@ -16,8 +16,9 @@
 //     with its own field set, waves sized to free HBM per class;
 //   * LRU / FIFO tiers are doubly-linked lists with both links in one 8-byte word, loaded
 //     speculatively with the tier byte, so an HBM hit costs one round trip;
-//   * LFU tiers and the disk-expiry heap are 4-ary heaps with the key stored inline in the
-//     slot (one round trip per level, half the depth of a binary heap);
+//   * LFU tiers are frequency buckets (one list per frequency, ordered by last access; victim =
+//     the oldest block of the lowest non-empty bucket, found through a two-level bitmap), the
+//     disk-expiry heap is 4-ary with the key stored inline in the slot;
 //   * the lookup pass issues its loads sixteen blocks at a time, and the UPDATE pass loads the
 //     next block's state while the current one is processed;
 //   * head / tail / sizes / counters live in registers.
@@ -38,9 +39,12 @@ struct RState {
   uint8_t *tier;       // [b*W+c] T_*
   uint32_t *lt;        // [b*W+c] ms of the last access (kNone = never seen): lease start, expiry base
   uint2 *link;         // list classes: [b*W+c] (prev, next) toward head / tail
-  uint32_t *hpos;      // LFU: [b*W+c] slot in its tier heap
-  uint64_t *hkey[3];   // LFU: [slot*W+c] (freq << 32 | last_seq) per tier heap
-  uint32_t *hid[3];    // LFU: [slot*W+c] block of each heap slot
+  uint32_t *freq;      // LFU: [b*W+c] access count of a resident block
+  uint32_t *bh[3];     // LFU: [f*W+c] newest block of frequency bucket f per tier
+  uint32_t *bt[3];     // LFU: [f*W+c] oldest block of frequency bucket f per tier
+  uint64_t *occ[3];    // LFU: [w*W+c] bucket occupancy bitmap (bit f) per tier
+  uint64_t *occ2[3];   // LFU: [w2*W+c] summary: bit w set iff occ word w is non-zero
+  uint32_t NW, NSW;    // LFU: bitmap words, summary words
   uint32_t *epos;      // expiry: [b*W+c] slot in the expiry heap (kNone = absent)
   uint64_t *ekey;      // expiry: [slot*W+c] (min(lt + tau_g, 2^32-1) << 32 | block)
   const uint16_t *gblk;
@@ -73,7 +77,8 @@ struct Rep {
   uint64_t hit[3], miss, evict[3], disk_writes, hit_pos_sum, bytetime, after_hole;
   // prefetched state of the next block of the UPDATE pass; every write to that block's tier /
   // link / heap slot during the current touch is mirrored here, so the copy stays exact
-  uint32_t nx = kNone, nx_hpos = 0;
+  uint32_t nx = kNone, nx_freq = 0;
+  uint32_t minf[3];  // LFU: lowest non-empty frequency bucket per tier
   uint8_t nx_tier = 0;
   uint2 nx_link = make_uint2(0, 0);
 
@@ -129,69 +134,86 @@ struct Rep {
     return x;
   }
 
-  // ------------------------------------------------------------ 4-ary heaps, inline keys
-  // hole-based sift: (key, id) moves from slot i toward the leaves / the root
+  // ------------------------------------------------------------ LFU frequency buckets
+  // Each tier keeps one doubly-linked list per frequency, newest block at the front.  A block
+  // enters a bucket with a last_seq larger than every member's (HBM: it was just touched; DRAM /
+  // disk: victims of one frequency leave the tier above in increasing last_seq), so every bucket
+  // is ordered by last_seq and the policy victim -- the smallest (freq, last_seq) -- is the tail
+  // of the lowest non-empty bucket.  O(1) per operation except finding the next non-empty
+  // bucket, a two-level bitmap scan.
   template <int t>
-  __device__ void h_down(uint64_t i, uint64_t key, uint32_t id) {
-    uint64_t *hk = v.hkey[t];
-    uint32_t *hi = v.hid[t];
-    const uint64_t n = size[t];
-    for (;;) {
-      const uint64_t c0 = 4 * i + 1;
-      if (c0 >= n) break;
-      uint64_t ck[4];
-      uint32_t cid[4];
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        const bool ok = c0 + q < n;
-        ck[q] = ok ? hk[(c0 + q) * v.W + c] : ~0ull;
-        cid[q] = ok ? hi[(c0 + q) * v.W + c] : 0u;
+  __device__ __forceinline__ void bit_set(uint32_t f) {
+    const uint64_t w = f >> 6;
+    const uint64_t old = v.occ[t][w * v.W + c];
+    if (!old) v.occ2[t][(w >> 6) * v.W + c] |= 1ull << (w & 63);
+    v.occ[t][w * v.W + c] = old | (1ull << (f & 63));
+  }
+  template <int t>
+  __device__ __forceinline__ void bit_clear(uint32_t f) {
+    const uint64_t w = f >> 6;
+    const uint64_t nw = v.occ[t][w * v.W + c] & ~(1ull << (f & 63));
+    v.occ[t][w * v.W + c] = nw;
+    if (!nw) v.occ2[t][(w >> 6) * v.W + c] &= ~(1ull << (w & 63));
+  }
+  // smallest non-empty frequency >= from (kNone if none)
+  template <int t>
+  __device__ uint32_t next_set(uint32_t from) const {
+    uint64_t w = from >> 6;
+    if (w < v.NW) {
+      const uint64_t word = v.occ[t][w * v.W + c] & (~0ull << (from & 63));
+      if (word) return (uint32_t)((w << 6) + __ffsll((long long)word) - 1);
+    }
+    const uint64_t w1 = w + 1;
+    for (uint64_t sw = w1 >> 6; sw < v.NSW; sw++) {
+      uint64_t sm = v.occ2[t][sw * v.W + c];
+      if (sw == (w1 >> 6)) sm &= (w1 & 63) ? (~0ull << (w1 & 63)) : ~0ull;
+      if (sm) {
+        const uint64_t wn = (sw << 6) + __ffsll((long long)sm) - 1;
+        return (uint32_t)((wn << 6) + __ffsll((long long)v.occ[t][wn * v.W + c]) - 1);
       }
-      uint64_t mk = ck[0];
-      uint32_t mid = cid[0], mq = 0;
-#pragma unroll
-      for (int q = 1; q < 4; q++)
-        if (ck[q] < mk) { mk = ck[q]; mid = cid[q]; mq = q; }
-      if (mk >= key) break;
-      hk[i * v.W + c] = mk;
-      hi[i * v.W + c] = mid;
-      v.hpos[at(mid)] = (uint32_t)i;
-      if (mid == nx) nx_hpos = (uint32_t)i;
-      i = c0 + mq;
     }
-    hk[i * v.W + c] = key;
-    hi[i * v.W + c] = id;
-    v.hpos[at(id)] = (uint32_t)i;
-    if (id == nx) nx_hpos = (uint32_t)i;
+    return kNone;
   }
   template <int t>
-  __device__ void h_up(uint64_t i, uint64_t key, uint32_t id) {
-    uint64_t *hk = v.hkey[t];
-    uint32_t *hi = v.hid[t];
-    while (i > 0) {
-      const uint64_t p = (i - 1) / 4;
-      const uint64_t pk = hk[p * v.W + c];
-      const uint32_t pid = hi[p * v.W + c];
-      if (pk <= key) break;
-      hk[i * v.W + c] = pk;
-      hi[i * v.W + c] = pid;
-      v.hpos[at(pid)] = (uint32_t)i;
-      if (pid == nx) nx_hpos = (uint32_t)i;
-      i = p;
+  __device__ __forceinline__ void b_push(uint32_t b, uint32_t f) {
+    uint32_t *bh = v.bh[t], *bt = v.bt[t];
+    const uint32_t h = bh[(uint64_t)f * v.W + c];
+    v.link[at(b)] = make_uint2(kNone, h);
+    if (b == nx) nx_link = make_uint2(kNone, h);
+    if (h != kNone) {
+      v.link[at(h)].x = b;
+      if (h == nx) nx_link.x = b;
+    } else {
+      bt[(uint64_t)f * v.W + c] = b;
+      bit_set<t>(f);
     }
-    hk[i * v.W + c] = key;
-    hi[i * v.W + c] = id;
-    v.hpos[at(id)] = (uint32_t)i;
-    if (id == nx) nx_hpos = (uint32_t)i;
+    bh[(uint64_t)f * v.W + c] = b;
+    if (size[t] == 0 || f < minf[t]) minf[t] = f;
+    size[t]++;
   }
-  // remove slot i holding key ki
+  // unlink b (links lk) from bucket f; returns true when the bucket became empty
   template <int t>
-  __device__ void h_remove(uint64_t i, uint64_t ki) {
-    const uint64_t last = --size[t];
-    if (i == last) return;
-    const uint64_t lk = v.hkey[t][last * v.W + c];
-    const uint32_t lid = v.hid[t][last * v.W + c];
-    if (lk < ki) h_up<t>(i, lk, lid); else h_down<t>(i, lk, lid);
+  __device__ __forceinline__ bool b_unlink(uint2 lk, uint32_t f, bool fix_min) {
+    uint32_t *bh = v.bh[t], *bt = v.bt[t];
+    if (lk.x != kNone) {
+      v.link[at(lk.x)].y = lk.y;
+      if (lk.x == nx) nx_link.y = lk.y;
+    } else {
+      bh[(uint64_t)f * v.W + c] = lk.y;
+    }
+    if (lk.y != kNone) {
+      v.link[at(lk.y)].x = lk.x;
+      if (lk.y == nx) nx_link.x = lk.x;
+    } else {
+      bt[(uint64_t)f * v.W + c] = lk.x;
+    }
+    size[t]--;
+    const bool empty = lk.x == kNone && lk.y == kNone;
+    if (empty) {
+      bit_clear<t>(f);
+      if (fix_min && f == minf[t] && size[t] > 0) minf[t] = next_set<t>(f + 1);
+    }
+    return empty;
   }
 
   // ------------------------------------------------------------ expiry heap (4-ary, packed)
@@ -247,8 +269,15 @@ struct Rep {
   __device__ __forceinline__ void t_insert(uint32_t b, uint64_t key) {
     v.tier[at(b)] = (uint8_t)(t + 1);
     if (b == nx) nx_tier = (uint8_t)(t + 1);
-    if (LFU) h_up<t>(size[t]++, key, b);
-    else { l_push_front<t>(b); size[t]++; }
+    if (LFU) {
+      const uint32_t f = (uint32_t)(key >> 32);
+      v.freq[at(b)] = f;
+      if (b == nx) nx_freq = f;
+      b_push<t>(b, f);
+    } else {
+      l_push_front<t>(b);
+      size[t]++;
+    }
     if (EXP && t == 2) {
       const uint32_t tg = tau[v.gblk[b]];
       if (tg != KARETO_TTL_INF) {
@@ -259,11 +288,11 @@ struct Rep {
   }
   // remove resident b (link / heap slot already loaded) from tier t
   template <int t>
-  __device__ __forceinline__ uint64_t t_remove(uint32_t b, uint2 lk, uint32_t hp) {
+  __device__ __forceinline__ uint64_t t_remove(uint32_t b, uint2 lk, uint32_t fb) {
     uint64_t key = 0;
-    if (LFU) {
-      key = v.hkey[t][(uint64_t)hp * v.W + c];
-      h_remove<t>(hp, key);
+    if (LFU) {  // fb = the block's frequency
+      b_unlink<t>(lk, fb, true);
+      key = (uint64_t)fb << 32;
     } else {
       l_unlink<t>(lk);
       size[t]--;
@@ -278,10 +307,11 @@ struct Rep {
     if (size[t] <= capt) return false;
     uint32_t x;
     uint64_t key = 0;
-    if (LFU) {
-      x = v.hid[t][c];
-      key = v.hkey[t][c];
-      h_remove<t>(0, key);
+    if (LFU) {  // the oldest block of the lowest non-empty bucket
+      const uint32_t f = minf[t];
+      x = v.bt[t][(uint64_t)f * v.W + c];
+      b_unlink<t>(v.link[at(x)], f, true);
+      key = (uint64_t)f << 32;
     } else {
       x = l_pop_tail<t>();
       size[t]--;
@@ -355,6 +385,7 @@ struct Rep {
     for (int t = 0; t < 3; t++) {
       head[t] = tail[t] = tail2[t] = kNone;
       size[t] = 0;
+      minf[t] = kNone;
       hit[t] = evict[t] = 0;
     }
     miss = disk_writes = hit_pos_sum = bytetime = after_hole = 0;
@@ -378,8 +409,7 @@ struct Rep {
           const uint32_t x = (uint32_t)top;
           e_remove_at(0, x);
           if (LFU) {
-            const uint64_t hp = v.hpos[at(x)];
-            h_remove<2>(hp, v.hkey[2][hp * v.W + c]);
+            b_unlink<2>(v.link[at(x)], v.freq[at(x)], true);
           } else {
             l_unlink<2>(v.link[at(x)]);
             size[2]--;
@@ -445,10 +475,8 @@ struct Rep {
       uint32_t bnn = s0 + 1 < s1 ? T.blk[s0 + 1] : 0u;
       uint8_t t_n = v.tier[at(bn)];
       uint32_t l_n = v.lt[at(bn)];
-      uint2 lk_n = make_uint2(0, 0);
-      uint32_t hp_n = 0;
-      if (LFU) hp_n = v.hpos[at(bn)];
-      else lk_n = v.link[at(bn)];
+      uint2 lk_n = v.link[at(bn)];
+      uint32_t hp_n = LFU ? v.freq[at(bn)] : 0u;
       for (uint32_t j = s0; j < s1; j++) {
         const uint32_t b = bn;
         const uint8_t t = t_n;
@@ -462,8 +490,8 @@ struct Rep {
           nx = bn;
           nx_tier = v.tier[at(bn)];
           l_n = v.lt[at(bn)];
-          if (LFU) nx_hpos = v.hpos[at(bn)];
-          else nx_link = v.link[at(bn)];
+          nx_link = v.link[at(bn)];
+          if (LFU) nx_freq = v.freq[at(bn)];
         } else {
           nx = kNone;
         }
@@ -473,9 +501,12 @@ struct Rep {
         }
         v.lt[at(b)] = a;  // before any expiry insertion of b in its own cascade
         if (t == T_HBM) {
-          if (LFU) {
-            const uint64_t key = v.hkey[0][(uint64_t)hp * v.W + c];
-            h_down<0>(hp, (((key >> 32) + 1) << 32) | seq, b);
+          if (LFU) {  // move to the front of bucket f + 1
+            const uint32_t f = hp;
+            const bool emptied = b_unlink<0>(lk, f, false);
+            v.freq[at(b)] = f + 1;
+            b_push<0>(b, f + 1);
+            if (emptied && minf[0] == f) minf[0] = f + 1;
           } else if (lru && head[0] != b) {
             l_unlink<0>(lk);
             l_push_front<0>(b);
@@ -489,7 +520,7 @@ struct Rep {
         }
         t_n = nx_tier;
         lk_n = nx_link;
-        hp_n = nx_hpos;
+        hp_n = nx_freq;
       }
       s0 = s1;
     }
@@ -688,17 +719,11 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
         if (x.cap[t] != y.cap[t]) return x.cap[t] < y.cap[t];
       return false;
     });
-    // heap slots per tier (LFU): a tier holds at most min(cap + 1, U) blocks
-    uint64_t hs[3] = {0, 0, 0};
-    for (uint32_t i : ix)
-      for (int t = 0; t < 3; t++) {
-        uint64_t cp = cfg_host[i].cap[t];
-        if (t == 2 && cp == KARETO_INF) cp = 0;
-        uint64_t m = (cp < U ? cp + 1 : U) + 1;
-        if (m > hs[t]) hs[t] = m;
-      }
+    // LFU frequency buckets: a resident block's frequency is at most its accesses (<= R)
+    const uint64_t FM = (uint64_t)tr->R + 2;
+    const uint64_t NW = (FM + 63) / 64, NSW = (NW + 63) / 64;
     const uint64_t es = U + 1;
-    uint64_t per_cfg = U * (1 + 4) + (lfu ? U * 4 + 12 * (hs[0] + hs[1] + hs[2]) : U * 8) + (exp ? U * 4 + 8 * es : 0);
+    uint64_t per_cfg = U * (1 + 4 + 8) + (lfu ? U * 4 + 3 * 8 * (FM + NW + NSW) : 0) + (exp ? U * 4 + 8 * es : 0);
     if (Qm) per_cfg += 16 * (uint64_t)R + 8 * (uint64_t)qarg.model->instances + 64;  // f3: TTFT rows + queue
     size_t freeb = 0, totb = 0, rsv = 0, used = 0;
     KCUDA(ctx, cudaStreamSynchronize(st));
@@ -714,24 +739,28 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
     const uint64_t nwaves = (ix.size() + W - 1) / W;
     W = (ix.size() + nwaves - 1) / nwaves;
     DBuf<uint8_t> tier;
-    DBuf<uint32_t> lt, hpos, epos, hid, didx;
+    DBuf<uint32_t> lt, freq, bht, epos, didx;
     DBuf<uint2> link;
-    DBuf<uint64_t> hkey, ekey;
-    KTRY(tier.alloc(ctx, U * W)); KTRY(lt.alloc(ctx, U * W));
+    DBuf<uint64_t> occ, ekey;
+    KTRY(tier.alloc(ctx, U * W)); KTRY(lt.alloc(ctx, U * W)); KTRY(link.alloc(ctx, U * W));
     if (lfu) {
-      KTRY(hpos.alloc(ctx, U * W));
-      KTRY(hkey.alloc(ctx, (hs[0] + hs[1] + hs[2]) * W)); KTRY(hid.alloc(ctx, (hs[0] + hs[1] + hs[2]) * W));
-    } else {
-      KTRY(link.alloc(ctx, U * W));
+      KTRY(freq.alloc(ctx, U * W)); KTRY(bht.alloc(ctx, 6 * FM * W)); KTRY(occ.alloc(ctx, 3 * (NW + NSW) * W));
     }
     if (exp) { KTRY(epos.alloc(ctx, U * W)); KTRY(ekey.alloc(ctx, es * W)); }
     KTRY(didx.alloc(ctx, ix.size()));
     KCUDA(ctx, cudaMemcpyAsync(didx.p, ix.data(), 4 * ix.size(), cudaMemcpyHostToDevice, st));
     RState v{};
-    v.tier = tier.p; v.lt = lt.p; v.link = link.p; v.hpos = hpos.p;
+    v.tier = tier.p; v.lt = lt.p; v.link = link.p;
     if (lfu) {
-      v.hkey[0] = hkey.p; v.hkey[1] = hkey.p + hs[0] * W; v.hkey[2] = hkey.p + (hs[0] + hs[1]) * W;
-      v.hid[0] = hid.p; v.hid[1] = hid.p + hs[0] * W; v.hid[2] = hid.p + (hs[0] + hs[1]) * W;
+      v.freq = freq.p;
+      for (int t = 0; t < 3; t++) {
+        v.bh[t] = bht.p + (size_t)(2 * t) * FM * W;
+        v.bt[t] = bht.p + (size_t)(2 * t + 1) * FM * W;
+        v.occ[t] = occ.p + (size_t)t * (NW + NSW) * W;
+        v.occ2[t] = v.occ[t] + NW * W;
+      }
+      v.NW = (uint32_t)NW;
+      v.NSW = (uint32_t)NSW;
     }
     v.epos = epos.p; v.ekey = ekey.p;
     v.gblk = tr->gblk;
@@ -750,6 +779,10 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
       const int64_t nw = (int64_t)(ix.size() - w0 < W ? ix.size() - w0 : W);
       KCUDA(ctx, cudaMemsetAsync(tier.p, 0, U * W, st));
       KCUDA(ctx, cudaMemsetAsync(lt.p, 0xFF, 4 * U * W, st));
+      if (lfu) {
+        KCUDA(ctx, cudaMemsetAsync(bht.p, 0xFF, 4 * 6 * FM * W, st));
+        KCUDA(ctx, cudaMemsetAsync(occ.p, 0, 8 * 3 * (NW + NSW) * W, st));
+      }
       if (exp) KCUDA(ctx, cudaMemsetAsync(epos.p, 0xFF, 4 * U * W, st));
       static const char *kPassName[4] = {"K6_replay_list", "K6_replay_list_exp", "K6_replay_lfu", "K6_replay_lfu_exp"};
       Pass ps(ctx, kPassName[q], 1, 1);

@@ -46,6 +46,8 @@ struct RState {
   uint64_t *occ2[3];   // LFU: [w2*W+c] summary: bit w set iff occ word w is non-zero
   uint32_t NW, NSW;    // LFU: bitmap words, summary words
   uint32_t *epos;      // expiry: [b*W+c] slot in the expiry heap (kNone = absent)
+  uint2 *elink;        // LRU expiry lists: [b*W+c] (newer, older) neighbour in its group's list
+  uint32_t *eh, *et;   // LRU expiry lists: [g*W+c] newest / oldest disk block of group g
   uint64_t *ekey;      // expiry: [slot*W+c] (min(lt + tau_g, 2^32-1) << 32 | block)
   const uint16_t *gblk;
   uint64_t W;
@@ -63,8 +65,12 @@ struct QueueState {  // row f3: per-configuration FCFS queue (DESIGN R50-R53)
   uint64_t real, capd;
 };
 
-template <bool LFU, bool EXP, bool Q>
+// EXPM: 0 no expiry; 1 expiry heap keyed lt + tau_g; 2 (LRU) one list per group in lt order --
+// LRU demotes in recency order, so a group's disk blocks arrive with non-decreasing lt and the
+// group's expired blocks are always at its list's old end.
+template <bool LFU, int EXPM, bool Q>
 struct Rep {
+  static constexpr bool EXP = EXPM != 0;
   const RState &v;
   const uint64_t c;
   uint64_t cap[3];
@@ -279,12 +285,30 @@ struct Rep {
       size[t]++;
     }
     if (EXP && t == 2) {
-      const uint32_t tg = tau[v.gblk[b]];
+      const uint16_t g = v.gblk[b];
+      const uint32_t tg = tau[g];
       if (tg != KARETO_TTL_INF) {
-        const uint64_t e = (uint64_t)v.lt[at(b)] + tg;
-        e_up(esize++, ((e < 0xFFFFFFFFull ? e : 0xFFFFFFFFull) << 32) | b);
+        if (EXPM == 1) {
+          const uint64_t e = (uint64_t)v.lt[at(b)] + tg;
+          e_up(esize++, ((e < 0xFFFFFFFFull ? e : 0xFFFFFFFFull) << 32) | b);
+        } else {  // newest end of the group's list
+          const uint64_t gi = (uint64_t)g * v.W + c;
+          const uint32_t h = v.eh[gi];
+          v.elink[at(b)] = make_uint2(kNone, h);
+          if (h != kNone) v.elink[at(h)].x = b; else v.et[gi] = b;
+          v.eh[gi] = b;
+        }
       }
     }
+  }
+  // remove disk block b from its group's expiry list (EXPM 2)
+  __device__ __forceinline__ void ge_remove(uint32_t b) {
+    const uint16_t g = v.gblk[b];
+    if (tau[g] == KARETO_TTL_INF) return;
+    const uint64_t gi = (uint64_t)g * v.W + c;
+    const uint2 lk = v.elink[at(b)];
+    if (lk.x != kNone) v.elink[at(lk.x)].y = lk.y; else v.eh[gi] = lk.y;
+    if (lk.y != kNone) v.elink[at(lk.y)].x = lk.x; else v.et[gi] = lk.x;
   }
   // remove resident b (link / heap slot already loaded) from tier t
   template <int t>
@@ -297,7 +321,8 @@ struct Rep {
       l_unlink<t>(lk);
       size[t]--;
     }
-    if (EXP && t == 2) e_remove(b);
+    if (EXPM == 1 && t == 2) e_remove(b);
+    if (EXPM == 2 && t == 2) ge_remove(b);
     return key;
   }
   // one CASCADE level: tier t overflows by at most one block; returns false when done
@@ -316,7 +341,8 @@ struct Rep {
       x = l_pop_tail<t>();
       size[t]--;
     }
-    if (EXP && t == 2) e_remove(x);
+    if (EXPM == 1 && t == 2) e_remove(x);
+    if (EXPM == 2 && t == 2) ge_remove(x);
     evict[t] += 1;
     const bool next = ttl_mode ? (t == 0) : (t < 2);
     if (!next) {
@@ -402,7 +428,7 @@ struct Rep {
       }
       const uint32_t tg = tau[T.grp[r]];
       // 1 PURGE (CAPACITY mode): disk blocks whose expiry key is below a (a - lt > tau_g)
-      if (EXP) {
+      if (EXPM == 1) {
         while (esize > 0) {
           const uint64_t top = v.ekey[c];
           if ((uint32_t)(top >> 32) >= a) break;
@@ -415,6 +441,22 @@ struct Rep {
             size[2]--;
           }
           v.tier[at(x)] = T_NONE;
+        }
+      }
+      if (EXPM == 2 && size[2] > 0) {  // each group's expired blocks sit at its list's old end
+        for (int g = 0; g < G; g++) {
+          const uint32_t tgg = tau[g];
+          if (tgg == KARETO_TTL_INF) continue;
+          const uint64_t gi = (uint64_t)g * v.W + c;
+          for (uint32_t x = v.et[gi]; x != kNone; x = v.et[gi]) {
+            if ((uint64_t)v.lt[at(x)] + tgg >= a) break;
+            const uint32_t nxt = v.elink[at(x)].x;  // next older-to-newer
+            v.et[gi] = nxt;
+            if (nxt != kNone) v.elink[at(nxt)].y = kNone; else v.eh[gi] = kNone;
+            l_unlink<2>(v.link[at(x)]);
+            size[2]--;
+            v.tier[at(x)] = T_NONE;
+          }
         }
       }
       // f3 queue (R50): wait of this request before its lookup; x = disk blocks loadable (R51)
@@ -551,7 +593,7 @@ struct QueueKernelArgs {  // row f3 inside the replay (Q = true)
   uint64_t span_ms, LO;
 };
 
-template <bool LFU, bool EXP, bool Q>
+template <bool LFU, int EXPM, bool Q>
 __global__ void __launch_bounds__(64) k_replay(ReplayTrace T, const kareto_config *__restrict__ cfg,
                                                const uint32_t *__restrict__ idx, const uint32_t *__restrict__ rows,
                                                int n_tuner, int G, RState v, int64_t n,
@@ -560,7 +602,7 @@ __global__ void __launch_bounds__(64) k_replay(ReplayTrace T, const kareto_confi
   if (ci >= n) return;
   const uint32_t id = idx[ci];
   const kareto_config cf = cfg[id];
-  Rep<LFU, EXP, Q> rp(v, (uint64_t)ci);
+  Rep<LFU, EXPM, Q> rp(v, (uint64_t)ci);
   if (!Q) {
     rp.run(T, cf, rows, n_tuner, G, out + id);
     return;
@@ -695,22 +737,24 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
   const int64_t R = tr->R;
   // classes {list, LFU} x {expiry heap or not}; within a class, neighbours in a warp get
   // similar configurations (policy, TTL row, capacities) so their branches agree more often
-  std::vector<uint32_t> cls[4];
+  // classes: 0 list, 1 list + expiry heap (FIFO), 2 LFU, 3 LFU + expiry heap, 4 LRU + group lists
+  std::vector<uint32_t> cls[5];
   for (int64_t i = 0; i < n; i++) {
     const kareto_config &c = cfg_host[i];
     const uint32_t *tau = rows_host + (size_t)(n_tuner > 0 ? c.tuner : 0) * G;
     bool any_finite = false;
     for (int g = 0; g < G; g++) any_finite |= tau[g] != KARETO_TTL_INF;
     const bool exp = c.cap[2] != KARETO_INF && any_finite;
-    cls[(c.policy == KARETO_LFU ? 2 : 0) + (exp ? 1 : 0)].push_back((uint32_t)i);
+    const int k = (exp && c.policy == KARETO_LRU) ? 4 : (c.policy == KARETO_LFU ? 2 : 0) + (exp ? 1 : 0);
+    cls[k].push_back((uint32_t)i);
   }
   DBuf<kareto_config> dcfg;
   KTRY(dcfg.alloc(ctx, n));
   KCUDA(ctx, cudaMemcpyAsync(dcfg.p, cfg_host, sizeof(kareto_config) * n, cudaMemcpyHostToDevice, st));
-  for (int q = 0; q < 4; q++) {
+  for (int q = 0; q < 5; q++) {
     std::vector<uint32_t> &ix = cls[q];
     if (ix.empty()) continue;
-    const bool lfu = q >= 2, exp = q & 1;
+    const bool lfu = q == 2 || q == 3, eheap = q == 1 || q == 3, glist = q == 4;
     std::stable_sort(ix.begin(), ix.end(), [&](uint32_t a, uint32_t b) {
       const kareto_config &x = cfg_host[a], &y = cfg_host[b];
       if (x.policy != y.policy) return x.policy < y.policy;
@@ -723,7 +767,8 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
     const uint64_t FM = (uint64_t)tr->R + 2;
     const uint64_t NW = (FM + 63) / 64, NSW = (NW + 63) / 64;
     const uint64_t es = U + 1;
-    uint64_t per_cfg = U * (1 + 4 + 8) + (lfu ? U * 4 + 3 * 8 * (FM + NW + NSW) : 0) + (exp ? U * 4 + 8 * es : 0);
+    uint64_t per_cfg = U * (1 + 4 + 8) + (lfu ? U * 4 + 3 * 8 * (FM + NW + NSW) : 0) + (eheap ? U * 4 + 8 * es : 0) +
+                       (glist ? U * 8 + 8 * (uint64_t)G : 0);
     if (Qm) per_cfg += 16 * (uint64_t)R + 8 * (uint64_t)qarg.model->instances + 64;  // f3: TTFT rows + queue
     size_t freeb = 0, totb = 0, rsv = 0, used = 0;
     KCUDA(ctx, cudaStreamSynchronize(st));
@@ -740,13 +785,15 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
     W = (ix.size() + nwaves - 1) / nwaves;
     DBuf<uint8_t> tier;
     DBuf<uint32_t> lt, freq, bht, epos, didx;
-    DBuf<uint2> link;
+    DBuf<uint2> link, elink;
     DBuf<uint64_t> occ, ekey;
+    DBuf<uint32_t> eht;
     KTRY(tier.alloc(ctx, U * W)); KTRY(lt.alloc(ctx, U * W)); KTRY(link.alloc(ctx, U * W));
     if (lfu) {
       KTRY(freq.alloc(ctx, U * W)); KTRY(bht.alloc(ctx, 6 * FM * W)); KTRY(occ.alloc(ctx, 3 * (NW + NSW) * W));
     }
-    if (exp) { KTRY(epos.alloc(ctx, U * W)); KTRY(ekey.alloc(ctx, es * W)); }
+    if (eheap) { KTRY(epos.alloc(ctx, U * W)); KTRY(ekey.alloc(ctx, es * W)); }
+    if (glist) { KTRY(elink.alloc(ctx, U * W)); KTRY(eht.alloc(ctx, 2 * (size_t)G * W)); }
     KTRY(didx.alloc(ctx, ix.size()));
     KCUDA(ctx, cudaMemcpyAsync(didx.p, ix.data(), 4 * ix.size(), cudaMemcpyHostToDevice, st));
     RState v{};
@@ -763,6 +810,9 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
       v.NSW = (uint32_t)NSW;
     }
     v.epos = epos.p; v.ekey = ekey.p;
+    v.elink = elink.p;
+    v.eh = eht.p;
+    v.et = eht.p + (size_t)G * W;
     v.gblk = tr->gblk;
     v.W = W;
     QueueKernelArgs qa{};
@@ -783,22 +833,26 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
         KCUDA(ctx, cudaMemsetAsync(bht.p, 0xFF, 4 * 6 * FM * W, st));
         KCUDA(ctx, cudaMemsetAsync(occ.p, 0, 8 * 3 * (NW + NSW) * W, st));
       }
-      if (exp) KCUDA(ctx, cudaMemsetAsync(epos.p, 0xFF, 4 * U * W, st));
-      static const char *kPassName[4] = {"K6_replay_list", "K6_replay_list_exp", "K6_replay_lfu", "K6_replay_lfu_exp"};
+      if (eheap) KCUDA(ctx, cudaMemsetAsync(epos.p, 0xFF, 4 * U * W, st));
+      if (glist) KCUDA(ctx, cudaMemsetAsync(eht.p, 0xFF, 4 * 2 * (size_t)G * W, st));
+      static const char *kPassName[5] = {"K6_replay_list", "K6_replay_list_exp", "K6_replay_lfu", "K6_replay_lfu_exp",
+                                         "K6_replay_lru_exp"};
       Pass ps(ctx, kPassName[q], 1, 1);
       const unsigned grid = (unsigned)((nw + 63) / 64);
       const uint32_t *wi = didx.p + w0;
 #define KREP(L, E, QQ) k_replay<L, E, QQ><<<grid, 64, 0, st>>>(T, dcfg.p, wi, rows_dev, n_tuner, G, v, nw, counts_dev, qa)
       if (!Qm) {
-        if (q == 0) KREP(false, false, false);
-        if (q == 1) KREP(false, true, false);
-        if (q == 2) KREP(true, false, false);
-        if (q == 3) KREP(true, true, false);
+        if (q == 0) KREP(false, 0, false);
+        if (q == 1) KREP(false, 1, false);
+        if (q == 2) KREP(true, 0, false);
+        if (q == 3) KREP(true, 1, false);
+        if (q == 4) KREP(false, 2, false);
       } else {
-        if (q == 0) KREP(false, false, true);
-        if (q == 1) KREP(false, true, true);
-        if (q == 2) KREP(true, false, true);
-        if (q == 3) KREP(true, true, true);
+        if (q == 0) KREP(false, 0, true);
+        if (q == 1) KREP(false, 1, true);
+        if (q == 2) KREP(true, 0, true);
+        if (q == 3) KREP(true, 1, true);
+        if (q == 4) KREP(false, 2, true);
       }
 #undef KREP
       if (Qm && R > 0) {  // exact nearest-rank P99 of each configuration's TTFT row (R53)

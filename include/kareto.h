@@ -70,6 +70,19 @@ const char *kareto_last_error(const kareto_ctx *ctx);
 /* Writes a 128-byte NCCL unique id to out (rank 0, world > 1). KARETO_E_NCCL if NCCL is absent. */
 kareto_status kareto_nccl_unique_id(void *out128);
 
+/* In-process rank group ("loopback"): world contexts of ONE process on one device, each driven
+ * by its own host thread, exchanging through each other's device buffers instead of NCCL.
+ * Every multi-rank path of this library (configuration sharding in kareto_eval_grid, the
+ * time-sharded load below) runs unchanged on it, which is how those paths are tested where
+ * only one GPU exists.  The group is owned by the caller and must outlive its contexts.
+ * Errors: KARETO_E_INVALID (world outside [1, 1024], rank outside [0, world)), _E_CUDA. */
+typedef struct kareto_loopback kareto_loopback;
+kareto_status kareto_loopback_create(int32_t world, kareto_loopback **out);
+void kareto_loopback_destroy(kareto_loopback *group);
+int32_t kareto_loopback_world(const kareto_loopback *group);
+kareto_status kareto_create_loopback(int device, void *cuda_stream, kareto_loopback *group, int rank,
+                                     kareto_ctx **out);
+
 /* ---------------------------------------------------------------- trace ---- */
 typedef enum { KARETO_TOKENS = 0, KARETO_HASHES = 1 } kareto_input_mode;
 
@@ -277,6 +290,28 @@ typedef struct {
 kareto_status kareto_eval_queue(kareto_ctx *ctx, const kareto_trace *tr, const kareto_config *cfg, int64_t n_cfg,
                                 const uint32_t *ttl_ms, int32_t n_tuner, const kareto_model *model,
                                 kareto_queue_result *out);
+
+/* ---------------------------------------- row f4: time-sharded trace passes ---- */
+/* Collective over the ranks of ctx (world W <= 128, every rank passes the SAME desc): rank k
+ * keeps the sorted requests [r_k, r_{k+1}) whose blocks cover positions ~[kN/W, (k+1)N/W) of
+ * the touch order and runs the trace passes (K1 hash, K2 prev / delta / chain check / groups,
+ * K3 LRU depth) on them only; with host inputs only that range of tokens is
+ * copied.  Shard boundaries are crossed by an owner-partitioned exchange (three all-to-all-v:
+ * first/last access records of every block, answers, the boundary LRU sets) and the groups /
+ * counts by an allgather and an allreduce -- DESIGN.md "Time sharding".  Per access, prev
+ * (global positions), delta and depth equal the whole-trace load's; U, U_g, reuse_g and groups
+ * (of the shard's requests) too.  kareto_eval_grid on a time-sharded trace sums the K4
+ * histograms over the ranks and returns the full grid on every rank; it accepts only
+ * stack-path configurations (LRU with a uniform or TTL-mode disk TTL; others:
+ * KARETO_E_UNSUPPORTED), and kareto_eval_queue / kareto_trace_analytics / kareto_ttl_* need a
+ * whole trace (KARETO_E_UNSUPPORTED).  kareto_trace_export returns the shard's accesses.
+ * Errors: as kareto_load_trace, plus KARETO_E_UNSUPPORTED (W > 128, requests of >= 2^24
+ * blocks), _E_NCCL.  World 1: a whole trace computed by the sharded path. */
+kareto_status kareto_load_trace_sharded(kareto_ctx *ctx, const kareto_trace_desc *desc, kareto_trace **out);
+/* The shard of a trace: sorted requests [*req_lo, *req_hi), positions [*pos_lo, *pos_hi)
+ * (a whole trace: [0, R), [0, N)).  Any output may be NULL. */
+kareto_status kareto_trace_shard(const kareto_trace *tr, int64_t *req_lo, int64_t *req_hi, int64_t *pos_lo,
+                                 int64_t *pos_hi);
 
 /* ------------------------------------------------ row f4: trace analytics ---- */
 /* X6 reuse skew and X5 oracle-TTL footprint, DESIGN R47-R48:

@@ -114,7 +114,8 @@ ABI_FUNCTIONS = ["kareto_create", "kareto_destroy", "kareto_last_error", "kareto
                  "kareto_eval_grid", "kareto_pareto", "kareto_set_profiling", "kareto_get_pass_times",
                  "kareto_launch_counter", "kareto_shard_range", "kareto_hypervolume", "kareto_search",
                  "kareto_ttl_roi", "kareto_ttl_eval", "kareto_ttl_allocate", "kareto_trace_analytics",
-                 "kareto_eval_queue"]
+                 "kareto_eval_queue", "kareto_loopback_create", "kareto_loopback_destroy", "kareto_loopback_world",
+                 "kareto_create_loopback", "kareto_load_trace_sharded", "kareto_trace_shard"]
 
 
 def load_library(path: str = LIB_PATH):
@@ -153,6 +154,15 @@ def load_library(path: str = LIB_PATH):
     L.kareto_get_pass_times.argtypes = [vp, ctypes.POINTER(PassTime), i32, ctypes.POINTER(i32), i32]
     L.kareto_launch_counter.argtypes = [vp, ctypes.POINTER(i64), i32]
     L.kareto_shard_range.argtypes = [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.kareto_loopback_create.argtypes = [i32, ctypes.POINTER(vp)]
+    L.kareto_loopback_destroy.argtypes = [vp]
+    L.kareto_loopback_destroy.restype = None
+    L.kareto_loopback_world.argtypes = [vp]
+    L.kareto_loopback_world.restype = i32
+    L.kareto_create_loopback.argtypes = [ctypes.c_int, vp, vp, ctypes.c_int, ctypes.POINTER(vp)]
+    L.kareto_load_trace_sharded.argtypes = [vp, ctypes.POINTER(TraceDesc), ctypes.POINTER(vp)]
+    L.kareto_trace_shard.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                     ctypes.POINTER(i64)]
     _lib = L
     return L
 
@@ -216,21 +226,45 @@ def configs(caps, policy=0, medium=0, tuner=0, axis=None) -> np.ndarray:
     return c
 
 
-class Context:
-    """kareto_ctx: device, borrowed CUDA stream (an int handle, e.g. torch's
-    current_stream().cuda_stream), optional NCCL communicator for world > 1."""
+class Loopback:
+    """kareto_loopback: an in-process rank group (one host thread per rank, one device)."""
 
-    def __init__(self, device: int = 0, stream: int | None = None, nccl_id: bytes | None = None, rank: int = 0,
-                 world: int = 1):
+    def __init__(self, world: int):
         self._L = load_library()
         h = ctypes.c_void_p()
-        nid = None
-        if nccl_id is not None:
-            nid = ctypes.create_string_buffer(bytes(nccl_id), 128)
-        st = self._L.kareto_create(device, ctypes.c_void_p(stream or 0), nid, rank, world, ctypes.byref(h))
+        st = self._L.kareto_loopback_create(world, ctypes.byref(h))
+        if st != OK:
+            raise KaretoError(st, "kareto_loopback_create")
+        self._h, self.world = h, world
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.kareto_loopback_destroy(self._h)
+            self._h = None
+
+
+class Context:
+    """kareto_ctx: device, borrowed CUDA stream (an int handle, e.g. torch's
+    current_stream().cuda_stream), optional NCCL communicator for world > 1, or a rank of a
+    Loopback group (`loopback=`)."""
+
+    def __init__(self, device: int = 0, stream: int | None = None, nccl_id: bytes | None = None, rank: int = 0,
+                 world: int = 1, loopback: Loopback | None = None):
+        self._L = load_library()
+        h = ctypes.c_void_p()
+        if loopback is not None:
+            st = self._L.kareto_create_loopback(device, ctypes.c_void_p(stream or 0), loopback._h, rank,
+                                                ctypes.byref(h))
+            world = loopback.world
+        else:
+            nid = None
+            if nccl_id is not None:
+                nid = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            st = self._L.kareto_create(device, ctypes.c_void_p(stream or 0), nid, rank, world, ctypes.byref(h))
         if st != OK:
             raise KaretoError(st, "kareto_create")
         self._h = h
+        self._loopback = loopback  # keep the group alive as long as the context
         self.device, self.rank, self.world = device, rank, world
 
     @staticmethod
@@ -276,8 +310,9 @@ class Context:
 
     # -------------------------------------------------------------------- ABI --
     def load_trace(self, arrival_ms, output_tokens, offsets, tokens=None, block_hash=None, input_tokens=None,
-                   salt: int = 0, top_k: int = 16) -> "Trace":
-        """kareto_load_trace.  Arrays are all host numpy arrays or all device tensors."""
+                   salt: int = 0, top_k: int = 16, time_shard: bool = False) -> "Trace":
+        """kareto_load_trace (or, with time_shard, the collective kareto_load_trace_sharded).
+        Arrays are all host numpy arrays or all device tensors."""
         d = TraceDesc()
         pa, dev = _ptr(arrival_ms)
         d.n_requests = int(arrival_ms.shape[0])
@@ -291,13 +326,15 @@ class Context:
             d.input_tokens = _ptr(input_tokens)[0]
         d.salt, d.top_k, d.inputs_on_device = salt, top_k, int(dev)
         h = ctypes.c_void_p()
-        self._check(self._L.kareto_load_trace(self._h, ctypes.byref(d), ctypes.byref(h)), "load_trace")
+        fn = self._L.kareto_load_trace_sharded if time_shard else self._L.kareto_load_trace
+        self._check(fn(self._h, ctypes.byref(d), ctypes.byref(h)), "load_trace")
         return Trace(self, h)
 
-    def load(self, trace, salt: int = 0, top_k: int = 16) -> "Trace":
+    def load(self, trace, salt: int = 0, top_k: int = 16, time_shard: bool = False) -> "Trace":
         """Load a kareto_inputs.Trace-like object (host arrays)."""
         return self.load_trace(trace.arrival_ms, trace.output_tokens, trace.offsets, tokens=trace.tokens,
-                               block_hash=trace.block_hash, input_tokens=trace.input_tokens, salt=salt, top_k=top_k)
+                               block_hash=trace.block_hash, input_tokens=trace.input_tokens, salt=salt, top_k=top_k,
+                               time_shard=time_shard)
 
     def eval_grid(self, trace: "Trace", cfgs: np.ndarray, model: Model, ttl=None, counts=None, obj=None):
         """kareto_eval_grid.  Returns (counts, obj); outputs are host numpy arrays unless
@@ -439,12 +476,17 @@ class Trace:
         self.U_g = np.zeros(self.K + 1, np.int64)
         self.reuse_g = np.zeros(self.K + 1, np.int64)
         ctx._L.kareto_trace_stats(h, ctypes.byref(info), self.U_g.ctypes.data, self.reuse_g.ctypes.data)
+        v = [ctypes.c_int64() for _ in range(4)]
+        ctx._check(ctx._L.kareto_trace_shard(h, *[ctypes.byref(x) for x in v]), "trace_shard")
+        # requests [req_lo, req_hi) and positions [pos_lo, pos_hi) held (whole trace: [0, R), [0, N))
+        self.req_lo, self.req_hi, self.pos_lo, self.pos_hi = (int(x.value) for x in v)
 
     def export(self, which: int) -> np.ndarray:
+        n = self.pos_hi - self.pos_lo
         if which == X_HASH:
-            out = np.zeros(self.N, np.uint64)
+            out = np.zeros(n, np.uint64)
         elif which in (X_PREV, X_DELTA, X_REQ, X_DEPTH):
-            out = np.zeros(self.N, np.uint32)
+            out = np.zeros(n, np.uint32)
         elif which == X_GROUP:
             out = np.zeros(self.R, np.uint16)
         elif which == X_START:

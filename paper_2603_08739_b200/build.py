@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libkareto.so")
-SOURCES = ["ctx.cu", "trace_load.cu", "stack_depth.cu", "eval.cu", "objective.cu", "pareto.cu", "replay.cu",
+SOURCES = ["ctx.cu", "comm.cu", "trace_load.cu", "trace_shard.cu", "stack_depth.cu", "eval.cu", "objective.cu", "pareto.cu", "replay.cu",
            "search.cu", "ttl_alloc.cu", "analytics.cu", "queue.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),

@@ -164,6 +164,8 @@ extern "C" kareto_status kareto_trace_analytics(kareto_ctx *ctx, const kareto_tr
                                                 double *lorenz, int32_t n_pts, int64_t *cumulative, int64_t *active) {
   if (!ctx) return KARETO_E_INVALID;
   ctx->err.clear();
+  if (tr && tr->sharded)
+    return kareto::fail(ctx, KARETO_E_UNSUPPORTED, "%s needs the whole trace (not a time shard)", "kareto_trace_analytics");
   cudaSetDevice(ctx->device);
   if (!tr) return kareto::fail(ctx, KARETO_E_INVALID, "trace_analytics: null trace");
   kareto_status s = kareto::analytics(ctx, const_cast<kareto_trace *>(tr), out, lorenz, n_pts, cumulative, active);

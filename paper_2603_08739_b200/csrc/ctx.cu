@@ -24,6 +24,11 @@ static NcclApi *load_nccl() {
   api.AllGather = (decltype(api.AllGather))dlsym(api.h, "ncclAllGather");
   api.CommDestroy = (decltype(api.CommDestroy))dlsym(api.h, "ncclCommDestroy");
   api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
+  api.AllReduce = (decltype(api.AllReduce))dlsym(api.h, "ncclAllReduce");
+  api.Send = (decltype(api.Send))dlsym(api.h, "ncclSend");
+  api.Recv = (decltype(api.Recv))dlsym(api.h, "ncclRecv");
+  api.GroupStart = (decltype(api.GroupStart))dlsym(api.h, "ncclGroupStart");
+  api.GroupEnd = (decltype(api.GroupEnd))dlsym(api.h, "ncclGroupEnd");
   if (!api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.CommDestroy) {
     api.h = nullptr;
     return nullptr;
@@ -95,11 +100,7 @@ extern "C" kareto_status kareto_nccl_unique_id(void *out128) {
   return KARETO_OK;
 }
 
-extern "C" kareto_status kareto_create(int device, void *cuda_stream, const void *nccl_unique_id, int rank, int world,
-                                       kareto_ctx **out) {
-  if (!out) return KARETO_E_INVALID;
-  *out = nullptr;
-  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_unique_id)) return KARETO_E_INVALID;
+static kareto_ctx *new_ctx(int device, void *cuda_stream, int rank, int world) {
   kareto_ctx *ctx = new kareto_ctx();
   ctx->device = device;
   ctx->stream = (cudaStream_t)cuda_stream;
@@ -118,8 +119,18 @@ extern "C" kareto_status kareto_create(int device, void *cuda_stream, const void
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
     delete ctx;
-    return KARETO_E_CUDA;
+    return nullptr;
   }
+  return ctx;
+}
+
+extern "C" kareto_status kareto_create(int device, void *cuda_stream, const void *nccl_unique_id, int rank, int world,
+                                       kareto_ctx **out) {
+  if (!out) return KARETO_E_INVALID;
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_unique_id)) return KARETO_E_INVALID;
+  kareto_ctx *ctx = new_ctx(device, cuda_stream, rank, world);
+  if (!ctx) return KARETO_E_CUDA;
   if (world > 1) {
     NcclApi *api = load_nccl();
     if (!api) { delete ctx; return KARETO_E_NCCL; }
@@ -130,6 +141,22 @@ extern "C" kareto_status kareto_create(int device, void *cuda_stream, const void
     ctx->nccl = api;
     ctx->nccl_comm = comm;
   }
+  *out = ctx;
+  return KARETO_OK;
+}
+
+struct kareto_loopback;
+extern "C" int32_t kareto_loopback_world(const kareto_loopback *g);
+
+extern "C" kareto_status kareto_create_loopback(int device, void *cuda_stream, kareto_loopback *group, int rank,
+                                                kareto_ctx **out) {
+  if (!out || !group) return KARETO_E_INVALID;
+  *out = nullptr;
+  const int world = kareto_loopback_world(group);
+  if (rank < 0 || rank >= world) return KARETO_E_INVALID;
+  kareto_ctx *ctx = new_ctx(device, cuda_stream, rank, world);
+  if (!ctx) return KARETO_E_CUDA;
+  ctx->loop = group;
   *out = ctx;
   return KARETO_OK;
 }
@@ -214,12 +241,13 @@ extern "C" kareto_status kareto_trace_export(kareto_ctx *ctx, const kareto_trace
   if (!ctx || !tr || !out) return KARETO_E_INVALID;
   const void *src = nullptr;
   size_t bytes = 0;
+  const size_t n = (size_t)(tr->pos_hi - tr->pos_lo);  // a time shard exports its own accesses
   switch (which) {
-    case KARETO_X_HASH: src = tr->hash; bytes = 8 * (size_t)tr->N; break;
-    case KARETO_X_PREV: src = tr->prev; bytes = 4 * (size_t)tr->N; break;
-    case KARETO_X_DELTA: src = tr->delta; bytes = 4 * (size_t)tr->N; break;
-    case KARETO_X_REQ: src = tr->req; bytes = 4 * (size_t)tr->N; break;
-    case KARETO_X_DEPTH: src = tr->depth; bytes = 4 * (size_t)tr->N; break;
+    case KARETO_X_HASH: src = tr->hash; bytes = 8 * n; break;
+    case KARETO_X_PREV: src = tr->prev; bytes = 4 * n; break;
+    case KARETO_X_DELTA: src = tr->delta; bytes = 4 * n; break;
+    case KARETO_X_REQ: src = tr->req; bytes = 4 * n; break;
+    case KARETO_X_DEPTH: src = tr->depth; bytes = 4 * n; break;
     case KARETO_X_GROUP: src = tr->grp; bytes = 2 * (size_t)tr->R; break;
     case KARETO_X_START: src = tr->s; bytes = 4 * (size_t)(tr->R + 1); break;
     default: return fail(ctx, KARETO_E_INVALID, "unknown export %d", which);

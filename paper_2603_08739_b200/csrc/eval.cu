@@ -66,7 +66,9 @@ __device__ __forceinline__ int tbin_of(uint32_t dl, const uint32_t *__restrict__
 
 // K4a: histogram of (d-bin, tau-bin) with count and sum k, privatised in smem
 // (cells [tc][bd] restricted to the window [c_lo, c_hi)), flushed with atomics.
-__global__ void __launch_bounds__(H_THREADS) k_hist_d(uint64_t N, uint64_t per_cta, const uint32_t *__restrict__ depth,
+// Per-access arrays are indexed by j - pos0 for positions j in [pos0, pos0 + N) (pos0 = 0 for a
+// whole trace, the shard's first position for a time-sharded one).
+__global__ void __launch_bounds__(H_THREADS) k_hist_d(uint64_t N, uint32_t pos0, uint64_t per_cta, const uint32_t *__restrict__ depth,
                                                       const uint32_t *__restrict__ req, const uint32_t *__restrict__ s,
                                                       const uint32_t *__restrict__ delta,
                                                       const uint32_t *__restrict__ Bd, int nb,
@@ -92,7 +94,7 @@ __global__ void __launch_bounds__(H_THREADS) k_hist_d(uint64_t N, uint64_t per_c
     int cell = tc * nb + bd - c_lo;
     if (cell < 0 || cell >= W) continue;
     uint32_t r = req[j];
-    uint32_t k = s[r + 1] - 1 - (uint32_t)j;
+    uint32_t k = s[r + 1] - 1 - ((uint32_t)j + pos0);
     atomicAdd(&cnt[cell], 1u);
     if (k) atomicAdd(&sk[cell], k);
   }
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(H_THREADS) k_hist_d(uint64_t N, uint64_t per_c
 // K4 fused (when both histograms fit in shared memory): one pass over the accesses builds
 // the (d-bin, tau-bin) count / sum-k histogram and the D-bin count histogram.  Updates are
 // warp-aggregated (match_any on the cell) so hot bins (small depths) do not serialise.
-__global__ void __launch_bounds__(H_THREADS) k_hist_dD(uint64_t N, uint64_t per_cta, const uint32_t *__restrict__ depth,
+__global__ void __launch_bounds__(H_THREADS) k_hist_dD(uint64_t N, uint32_t pos0, uint64_t per_cta, const uint32_t *__restrict__ depth,
                                                        const uint32_t *__restrict__ req, const uint32_t *__restrict__ s,
                                                        const uint32_t *__restrict__ delta,
                                                        const uint32_t *__restrict__ Bd, int nb,
@@ -136,10 +138,10 @@ __global__ void __launch_bounds__(H_THREADS) k_hist_dD(uint64_t N, uint64_t per_
       if (d != kNone) {
         uint32_t r = req[j];
         uint32_t sr1 = s[r + 1];
-        k = sr1 - 1 - (uint32_t)j;
+        k = sr1 - 1 - ((uint32_t)j + pos0);
         int bd = bin_of(d, Bd, nb, lut_s, sh);
         if (bd < nb) cell = (ntc > 0 ? tbin_of(delta[j], Tc, ntc) : 0) * nb + bd;
-        uint32_t D = d + ((uint32_t)j - s[r]);
+        uint32_t D = d + ((uint32_t)j + pos0 - s[r]);
         // D >= d: walk forward from d's bin (D - d is the offset inside the request, usually
         // small against the boundary gaps), falling back to the search after a few steps
         int bD = bd;
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(H_THREADS) k_hist_dD(uint64_t N, uint64_t per_
 }
 
 // K4b: histogram of D over the boundaries (count), window [b_lo, b_hi)
-__global__ void __launch_bounds__(H_THREADS) k_hist_D(uint64_t N, uint64_t per_cta, const uint32_t *__restrict__ depth,
+__global__ void __launch_bounds__(H_THREADS) k_hist_D(uint64_t N, uint32_t pos0, uint64_t per_cta, const uint32_t *__restrict__ depth,
                                                       const uint32_t *__restrict__ req, const uint32_t *__restrict__ s,
                                                       const uint32_t *__restrict__ Bd, int nb,
                                                       const uint32_t *__restrict__ lut, int sh, int b_lo, int b_hi,
@@ -192,7 +194,7 @@ __global__ void __launch_bounds__(H_THREADS) k_hist_D(uint64_t N, uint64_t per_c
   for (uint64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
     uint32_t d = depth[j];
     if (d == kNone) continue;
-    uint32_t D = d + ((uint32_t)j - s[req[j]]);
+    uint32_t D = d + ((uint32_t)j + pos0 - s[req[j]]);
     int bd = bin_of(D, Bd, nb, lut_s, sh) - b_lo;
     if (bd < 0 || bd >= W) continue;
     atomicAdd(&cnt[bd], 1u);
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(H_THREADS) k_hist_D(uint64_t N, uint64_t per_c
 
 // K4c (TTL mode): C2 histogram [(i12bin)*G + g][t] in global memory (count, sum k) and
 // per-group delta sums SDg[g][t] privatised in smem.
-__global__ void __launch_bounds__(256) k_hist_ttl(uint64_t N, const uint32_t *__restrict__ depth,
+__global__ void __launch_bounds__(256) k_hist_ttl(uint64_t N, uint32_t pos0, const uint32_t *__restrict__ depth,
                                                   const uint32_t *__restrict__ req, const uint32_t *__restrict__ s,
                                                   const uint32_t *__restrict__ delta, const uint16_t *__restrict__ grp,
                                                   const uint32_t *__restrict__ B12, int nb12,
@@ -219,7 +221,7 @@ __global__ void __launch_bounds__(256) k_hist_ttl(uint64_t N, const uint32_t *__
     uint32_t d = depth[j];
     if (d == kNone) continue;
     uint32_t r = req[j];
-    uint32_t k = s[r + 1] - 1 - (uint32_t)j;
+    uint32_t k = s[r + 1] - 1 - ((uint32_t)j + pos0);
     int g = grp[r];
     uint32_t dl = delta[j];
     int t = tbin_of(dl, Tt, ntt);
@@ -371,6 +373,12 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
   if (n_tuner < 0 || (n_tuner > 0 && !ttl_ms)) return fail(ctx, KARETO_E_INVALID, "bad TTL table");
   const int G = tr->K + 1;
   const uint64_t N = (uint64_t)tr->N, U = (uint64_t)tr->U;
+  // a time-sharded trace (row f4) holds the accesses [pos_lo, pos_hi): every rank evaluates the
+  // whole grid from histograms summed over the ranks (no configuration sharding, no gather)
+  const bool tsh = tr->sharded;
+  const uint64_t Nl = (uint64_t)(tr->pos_hi - tr->pos_lo);
+  const uint32_t jb = (uint32_t)tr->pos_lo;
+  const bool cfg_shard = ctx->world > 1 && !tsh;
   // rows (an all-infinite row when no table is given)
   std::vector<uint32_t> rows;
   int nrows = n_tuner;
@@ -413,7 +421,7 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
 
   // ---- shard
   int64_t lo = 0, hi = n_cfg;
-  if (ctx->world > 1) shard_range(n_cfg, ctx->rank, ctx->world, lo, hi);
+  if (cfg_shard) shard_range(n_cfg, ctx->rank, ctx->world, lo, hi);
   const int64_t ns = hi - lo;
   const kareto_config *sc = cfg + lo;
   // stack-eligible (LRU, and TTL mode or a uniform disk TTL) vs per-configuration replay (K6)
@@ -435,6 +443,10 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
     }
   }
   const int64_t nS = (int64_t)cS.size(), nP = (int64_t)cP.size();
+  if (tsh && nP > 0)
+    return fail(ctx, KARETO_E_UNSUPPORTED,
+                "time-sharded trace: %lld configurations need the per-configuration replay (FIFO, LFU, per-group "
+                "TTL on a finite disk); load the whole trace for those", (long long)nP);
   // TTL value sets: uniform CAPACITY TTLs (Tc) and all TTLs of rows used in TTL mode (Tt)
   std::vector<uint32_t> Tc, Tt;
   for (int r = 0; r < nrows; r++) {
@@ -512,6 +524,7 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
   KTRY(dlut.alloc(ctx, (1 << LUT_BITS) + 1));
   const uint32_t *depth = tr->depth, *req = tr->req, *s = tr->s, *delta = tr->delta;
   if (ns > 0 && N > 0 && nb > 0) {
+    const uint64_t N = Nl;  // this rank's accesses
     k_build_lut<<<grid_for((1 << LUT_BITS) + 1, 256), 256, 0, st>>>(dBd.p, nb, sh, dlut.p);
     ctx->own_launches++;
     // CTA ranges bounded so that per-CTA u32 sums of k cannot overflow
@@ -534,22 +547,28 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
     const size_t fused = lut_bytes + 8 * ncell + 4 * (size_t)nb;
     if (fused <= (size_t)SMEM_MAX) {  // one pass for both histograms
       Pass ps(ctx, "K4_hist_dD", 1, 1);
-      k_hist_dD<<<g, H_THREADS, fused, st>>>(N, per, depth, req, s, delta, dBd.p, nb, dlut.p, sh, dTc.p, ntc, hC.p,
+      if (N > 0) k_hist_dD<<<g, H_THREADS, fused, st>>>(N, jb, per, depth, req, s, delta, dBd.p, nb, dlut.p, sh, dTc.p, ntc, hC.p,
                                             hS.p, hD.p);
     } else {
     for (int c0 = 0; c0 < (int)ncell; c0 += wcell) {
       int c1 = c0 + wcell < (int)ncell ? c0 + wcell : (int)ncell;
       size_t smem = lut_bytes + 8 * (size_t)(c1 - c0);
       Pass ps(ctx, "K4_hist_d", 1, 1);
-      k_hist_d<<<g, H_THREADS, smem, st>>>(N, per, depth, req, s, delta, dBd.p, nb, dlut.p, sh, dTc.p, ntc, c0, c1,
+      if (N > 0) k_hist_d<<<g, H_THREADS, smem, st>>>(N, jb, per, depth, req, s, delta, dBd.p, nb, dlut.p, sh, dTc.p, ntc, c0, c1,
                                            hC.p, hS.p);
     }
     for (int b0 = 0; b0 < nb; b0 += wD) {
       int b1 = b0 + wD < nb ? b0 + wD : nb;
       size_t smem = lut_bytes + 4 * (size_t)(b1 - b0);
       Pass ps(ctx, "K4_hist_D", 1, 1);
-      k_hist_D<<<g, H_THREADS, smem, st>>>(N, per, depth, req, s, dBd.p, nb, dlut.p, sh, b0, b1, hD.p);
+      if (N > 0) k_hist_D<<<g, H_THREADS, smem, st>>>(N, jb, per, depth, req, s, dBd.p, nb, dlut.p, sh, b0, b1, hD.p);
     }
+    }
+    if (tsh) {  // sum the shards' histograms (one allreduce over NVLink)
+      Pass ps(ctx, "F4_allreduce", 0, 3);
+      KTRY(coll_allreduce_u64(ctx, hC.p, ncell));
+      KTRY(coll_allreduce_u64(ctx, hS.p, ncell));
+      KTRY(coll_allreduce_u64(ctx, hD.p, (size_t)nb));
     }
     {
       Pass ps(ctx, "K4_cumulate", 0, 3);
@@ -586,8 +605,15 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
     cudaFuncSetAttribute(k_hist_ttl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     {
       Pass ps(ctx, "K4_hist_ttl", 1, 1);
-      k_hist_ttl<<<grid_for(N, 256, 4 * sms), 256, smem, st>>>(N, depth, req, s, delta, tr->grp, dB12.p, nb12, dTt.p,
-                                                               ntt, G, C2.p, S2.p, SDg.p);
+      if (Nl > 0)
+        k_hist_ttl<<<grid_for(Nl, 256, 4 * sms), 256, smem, st>>>(Nl, jb, depth, req, s, delta, tr->grp, dB12.p, nb12,
+                                                                  dTt.p, ntt, G, C2.p, S2.p, SDg.p);
+    }
+    if (tsh) {
+      Pass ps(ctx, "F4_allreduce", 0, 3);
+      KTRY(coll_allreduce_u64(ctx, C2.p, n2));
+      KTRY(coll_allreduce_u64(ctx, S2.p, n2));
+      KTRY(coll_allreduce_u64(ctx, SDg.p, (size_t)G * nt1));
     }
     Pass ps(ctx, "K4_cumulate_ttl", 1, 5);
     k_prefix_c2_i<<<grid_for(G * nt1, 256), 256, 0, st>>>(C2.p, nb12 + 1, G, nt1);
@@ -602,7 +628,7 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
   DBuf<double> dobj;
   int64_t nsa = ns > 0 ? ns : 1;
   // gathered outputs are assembled in padded per-rank slots: slot = ceil(n / world)
-  const int64_t slot = ctx->world > 1 ? (n_cfg + ctx->world - 1) / ctx->world : nsa;
+  const int64_t slot = cfg_shard ? (n_cfg + ctx->world - 1) / ctx->world : nsa;
   KTRY(dcounts.alloc(ctx, slot > 0 ? slot : 1)); KTRY(dobj.alloc(ctx, 3 * (slot > 0 ? slot : 1)));
   StackTables T{};
   T.Bd = nullptr; T.nb = nb; T.Tc = dTc.p; T.ntc = ntc;
@@ -634,14 +660,12 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
   double *all_obj = dobj.p;
   DBuf<kareto_counts> gcounts;
   DBuf<double> gobj;
-  if (ctx->world > 1) {
+  if (cfg_shard) {
     const int W = ctx->world;
     KTRY(gcounts.alloc(ctx, (size_t)slot * W)); KTRY(gobj.alloc(ctx, (size_t)3 * slot * W));
     Pass ps(ctx, "K9_allgather", 0, 2);
-    ncclComm_t comm = (ncclComm_t)ctx->nccl_comm;
-    if (ctx->nccl->AllGather(dcounts.p, gcounts.p, sizeof(kareto_counts) * slot, ncclUint8, comm, st) != ncclSuccess ||
-        ctx->nccl->AllGather(dobj.p, gobj.p, (size_t)3 * slot, ncclFloat64, comm, st) != ncclSuccess)
-      return fail(ctx, KARETO_E_NCCL, "ncclAllGather failed");
+    KTRY(coll_allgather(ctx, dcounts.p, gcounts.p, sizeof(kareto_counts) * slot));
+    KTRY(coll_allgather(ctx, dobj.p, gobj.p, 24 * (size_t)slot));
     // compact rank slots into [0, n): rank r's shard occupies [lo_r, hi_r)
     DBuf<kareto_counts> ccounts;
     DBuf<double> cobj;

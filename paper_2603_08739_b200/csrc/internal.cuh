@@ -34,9 +34,18 @@ struct NcclApi {
   ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  // used by the time-sharded load (optional: absent => KARETO_E_NCCL there)
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
 };
 
 }  // namespace kareto
+
+struct kareto_loopback;  // in-process rank group (comm.cu)
 
 struct kareto_ctx {
   int device = 0;
@@ -44,6 +53,7 @@ struct kareto_ctx {
   int rank = 0, world = 1;
   void *nccl_comm = nullptr;  // ncclComm_t
   kareto::NcclApi *nccl = nullptr;
+  kareto_loopback *loop = nullptr;  // world > 1 without NCCL: ranks are threads of this process
   cudaMemPool_t pool = nullptr;
   int num_sms = 148;
   size_t l2_bytes = 0;
@@ -66,6 +76,11 @@ struct kareto_trace {
   int64_t R = 0, N = 0, U = 0, span_ms = 1;
   int32_t K = 0, max_blocks = 0;
   int64_t n_runs = 0;          // runs of consecutive previous positions (K3)
+  // Time-sharded traces (kareto_load_trace_sharded) hold only the accesses of positions
+  // [pos_lo, pos_hi) = the blocks of sorted requests [req_lo, req_hi); per-access arrays are
+  // indexed by position - pos_lo.  Whole traces: [0, N), [0, R).
+  bool sharded = false;
+  int64_t pos_lo = 0, pos_hi = 0, req_lo = 0, req_hi = 0;
   uint64_t Ltok = 0, O = 0;
   // sum_r L_r and sum_r L_r (L_r - 1) / 2 as exact 128-bit values (for P0 = alpha*SL + beta*SQ)
   unsigned __int128 SL = 0, SQ = 0;
@@ -197,7 +212,16 @@ __host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
 constexpr uint64_t kChainR = 0x9E3779B97F4A7C15ULL;
 constexpr uint64_t kSaltC = 0x243F6A8885A308D3ULL;
 
-// trace-load building blocks (trace_load.cu / stack_depth.cu)
-kareto_status stack_depth(kareto_ctx *ctx, kareto_trace *tr, const uint8_t *run_flag);
+// ------------------------------------------------------------ collectives (comm.cu) ----
+// Every rank of ctx calls these collectively, in the same order.  Buffers are device
+// buffers of the context device unless named *_host.  World == 1: plain local copies.
+kareto_status coll_allgather(kareto_ctx *ctx, const void *send, void *recv, size_t bytes);
+kareto_status coll_allgather_host(kareto_ctx *ctx, const void *send, void *recv, size_t bytes);
+kareto_status coll_allreduce_u64(kareto_ctx *ctx, unsigned long long *buf, size_t n);  // in place, sum
+// send_off / recv_off: [world + 1] byte offsets; rank r's segment [off[r], off[r+1]) goes to /
+// comes from rank r.  Receive sizes must match what the peers send.
+kareto_status coll_alltoallv(kareto_ctx *ctx, const void *send, const std::vector<size_t> &send_off, void *recv,
+                             const std::vector<size_t> &recv_off);
+
 
 }  // namespace kareto

@@ -297,6 +297,8 @@ extern "C" kareto_status kareto_eval_queue(kareto_ctx *ctx, const kareto_trace *
                                            const kareto_model *model, kareto_queue_result *out) {
   if (!ctx) return KARETO_E_INVALID;
   ctx->err.clear();
+  if (tr && tr->sharded)
+    return kareto::fail(ctx, KARETO_E_UNSUPPORTED, "%s needs the whole trace (not a time shard)", "kareto_eval_queue");
   cudaSetDevice(ctx->device);
   kareto_status s = kareto::eval_queue(ctx, tr, cfg, n_cfg, ttl_ms, n_tuner, model, out);
   if (s != KARETO_OK) {

@@ -23,7 +23,7 @@
 // Item = uint2 {y, w}: query: w = running count (< 2^31); point: w = 0x80000000 | L.
 #include <cub/cub.cuh>
 
-#include "internal.cuh"
+#include "trace_load.cuh"
 
 namespace kareto {
 
@@ -67,16 +67,18 @@ __device__ __forceinline__ void tile_geometry(const PassArgs &a, uint32_t bid, u
 }
 
 // ---- run extraction: flags were written by K2 (k_access_info); runs listed by CUB select
+// (run_start / req / prev are indexed by local position; req holds global request ids,
+// r - req_base indexes s, whose values are global positions: local = s - pos_base)
 __global__ void k_run_info(const uint32_t *__restrict__ run_start, const int *__restrict__ m_ptr, uint64_t N,
-                           const uint32_t *__restrict__ req, const uint32_t *__restrict__ s,
-                           const uint32_t *__restrict__ prev, uint32_t *__restrict__ run_req,
+                           const uint32_t *__restrict__ req, uint32_t req_base, const uint32_t *__restrict__ s,
+                           uint32_t pos_base, const uint32_t *__restrict__ prev, uint32_t *__restrict__ run_req,
                            uint32_t *__restrict__ run_len, uint32_t *__restrict__ run_p0) {
   const int M = *m_ptr;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < M; q += gridDim.x * blockDim.x) {
     uint32_t j0 = run_start[q];
-    uint32_t r = req[j0];
+    uint32_t r = req[j0] - req_base;
     uint32_t nxt = q + 1 < M ? run_start[q + 1] : (uint32_t)N;
-    uint32_t rend = s[r + 1];
+    uint32_t rend = s[r + 1] - pos_base;
     run_req[q] = r;
     run_len[q] = (nxt < rend ? nxt : rend) - j0;
     run_p0[q] = prev[j0];
@@ -265,16 +267,17 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_sd_local(const uint2 *__re
   }
 }
 
-// d_j = s_r - prev_j - A(run) for every access of each run (warp per run)
+// d_j = s_r - prev_j - A(run) for every access of each run (warp per run); s_r in the
+// coordinates of prev: s[r] - pos_base + y_off
 __global__ void k_run_expand(const int *__restrict__ m_ptr, const uint32_t *__restrict__ run_start,
                              const uint32_t *__restrict__ run_req, const uint32_t *__restrict__ run_len,
                              const uint32_t *__restrict__ run_p0, const uint32_t *__restrict__ s,
-                             const uint32_t *__restrict__ A, uint32_t *__restrict__ depth) {
+                             uint32_t s_shift, const uint32_t *__restrict__ A, uint32_t *__restrict__ depth) {
   const int M = *m_ptr;
   const int lane = threadIdx.x & 31;
   for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < M; q += (gridDim.x * blockDim.x) >> 5) {
     uint32_t j0 = run_start[q], L = run_len[q], p0 = run_p0[q];
-    uint32_t base = s[run_req[q]] - p0 - A[p0];
+    uint32_t base = s[run_req[q]] - s_shift - p0 - A[p0];
     for (uint32_t t = lane; t < L; t += 32) depth[j0 + t] = base - t;
   }
 }
@@ -304,13 +307,18 @@ static kareto_status cub_tmp(kareto_ctx *ctx, DBuf<uint8_t> &tmp, F &&f) {
   return KARETO_OK;
 }
 
-kareto_status stack_depth(kareto_ctx *ctx, kareto_trace *tr, const uint8_t *run_flag) {
-  const uint64_t N = (uint64_t)tr->N;
+// K3 over n accesses (local positions 0..n-1) whose previous positions prev_c are given in
+// coordinates [0, y_range) where local position i sits at y_off + i (whole trace: y_off = 0,
+// y_range = n; a time shard prepends its boundary LRU stack, trace_shard.cu).
+kareto_status stack_depth(kareto_ctx *ctx, uint64_t N, uint64_t y_range, const uint32_t *prev_c,
+                          const uint32_t *req, uint32_t req_base, const uint32_t *s, uint32_t pos_base,
+                          uint32_t y_off, const uint8_t *run_flag, uint32_t *depth, int64_t *n_runs) {
+  *n_runs = 0;
   if (N == 0) return KARETO_OK;
-  if (N >= (1ull << 31)) return fail(ctx, KARETO_E_OVERFLOW, "stack depth pass supports < 2^31 accesses");
+  if (y_range >= (1ull << 31)) return fail(ctx, KARETO_E_OVERFLOW, "stack depth pass supports < 2^31 positions");
   cudaStream_t st = ctx->stream;
   const int sms = ctx->num_sms;
-  KCUDA(ctx, cudaMemsetAsync(tr->depth, 0xFF, 4 * N, st));  // first accesses: UINT32_MAX
+  KCUDA(ctx, cudaMemsetAsync(depth, 0xFF, 4 * N, st));  // first accesses: UINT32_MAX
   // ---- runs
   DBuf<uint8_t> tmp;
   DBuf<uint32_t> run_start, run_req, run_len, run_p0;
@@ -328,7 +336,7 @@ kareto_status stack_depth(kareto_ctx *ctx, kareto_trace *tr, const uint8_t *run_
   int M = 0;
   KCUDA(ctx, cudaMemcpyAsync(&M, m_dev.p, 4, cudaMemcpyDeviceToHost, st));
   KCUDA(ctx, cudaStreamSynchronize(st));
-  tr->n_runs = M;
+  *n_runs = M;
   if (M == 0) return KARETO_OK;
   KTRY(run_req.alloc(ctx, M)); KTRY(run_len.alloc(ctx, M)); KTRY(run_p0.alloc(ctx, M));
   const uint64_t NI = 2ull * (uint64_t)M;  // items
@@ -336,17 +344,17 @@ kareto_status stack_depth(kareto_ctx *ctx, kareto_trace *tr, const uint8_t *run_
   KTRY(buf[0].alloc(ctx, NI)); KTRY(buf[1].alloc(ctx, NI));
   {
     Pass ps(ctx, "K3_run_items", 1, 2);
-    k_run_info<<<grid_for(M, 256, 8 * sms), 256, 0, st>>>(run_start.p, m_dev.p, N, tr->req, tr->s, tr->prev,
-                                                          run_req.p, run_len.p, run_p0.p);
+    k_run_info<<<grid_for(M, 256, 8 * sms), 256, 0, st>>>(run_start.p, m_dev.p, N, req, req_base, s, pos_base,
+                                                          prev_c, run_req.p, run_len.p, run_p0.p);
     k_run_items<<<grid_for(M, 256, 8 * sms), 256, 0, st>>>(m_dev.p, run_req.p, run_len.p, run_p0.p, buf[0].p);
   }
   int B = 1;
-  while ((1ull << B) < N) B++;
+  while ((1ull << B) < y_range) B++;
   const int LB = B < SD_LOCAL_BITS ? B : SD_LOCAL_BITS;
   const int H = B - LB;
   const int npass = (H + 7) / 8;
   DBuf<uint32_t> A;
-  KTRY(A.alloc(ctx, N));
+  KTRY(A.alloc(ctx, y_range));
   DBuf<uint64_t> seg_start, seg_len;
   KTRY(seg_start.alloc(ctx, 1)); KTRY(seg_len.alloc(ctx, 1));
   k_single_segment<<<1, 1, 0, st>>>(m_dev.p, seg_start.p, seg_len.p);
@@ -442,7 +450,7 @@ kareto_status stack_depth(kareto_ctx *ctx, kareto_trace *tr, const uint8_t *run_
   {
     Pass ps(ctx, "K3_expand", 1, 1);
     k_run_expand<<<grid_for(32ll * M, 256, 16 * sms), 256, 0, st>>>(m_dev.p, run_start.p, run_req.p, run_len.p,
-                                                                    run_p0.p, tr->s, A.p, tr->depth);
+                                                                    run_p0.p, s, pos_base - y_off, A.p, depth);
   }
   return KARETO_OK;
 }

@@ -15,18 +15,9 @@
 //       (R23).
 #include <cub/cub.cuh>
 
-#include "internal.cuh"
+#include "trace_load.cuh"
 
 namespace kareto {
-
-enum : uint32_t { F_OFFSETS = 1, F_OUTPUT = 2, F_INPUT_LEN = 4, F_CHAIN = 8, F_DELTA = 16 };
-
-struct LoadStats {  // device-side accumulators, copied back once
-  unsigned long long sl_lo, sl_hi, sq_lo, sq_hi, O;
-  unsigned long long n_total;
-  unsigned int flags, max_blocks;
-  long long arr_first, arr_last;
-};
 
 template <typename F>
 static kareto_status cub_call(kareto_ctx *ctx, DBuf<uint8_t> &tmp, F &&f) {
@@ -205,9 +196,14 @@ constexpr int K1_WARPS = K1_THREADS / 32;
 // crosses warps: rounds of 32 consecutive blocks, one thread per block, a 5-step shuffle
 // scan and the carry kept in a register -- no block-level barrier on the path, so the
 // warps of an SM overlap each other's load latency freely.
+//
+// Time-sharded loads hash only the requests [r0, r1): s, tok_off point at request r0, positions
+// are global (pos_base = s[0]), outputs are indexed by position - pos_base, and req_out holds
+// global request indices (r + req_base).
 __global__ void __launch_bounds__(K1_THREADS) k_chain_hash(const uint32_t *__restrict__ tokens, int64_t n_tokens,
                                                             const int64_t *__restrict__ tok_off,
                                                             const uint32_t *__restrict__ s, int64_t R, uint64_t N,
+                                                            uint64_t pos_base, uint32_t req_base,
                                                             uint64_t P_init, uint64_t *__restrict__ hash_out,
                                                             uint32_t *__restrict__ req_out) {
   const int lane = threadIdx.x & 31;
@@ -215,7 +211,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_chain_hash(const uint32_t *__res
   const uint64_t w = (uint64_t)blockIdx.x * K1_WARPS + (threadIdx.x >> 5);
   uint32_t bound = 0;
   if (lane < 2) {  // first request r with s[r] >= target
-    uint64_t target = ((w + lane) * N) / nw;
+    uint64_t target = pos_base + ((w + lane) * N) / nw;
     int64_t lo = 0, hi = R;
     while (lo < hi) {
       int64_t m = (lo + hi) >> 1;
@@ -254,9 +250,9 @@ __global__ void __launch_bounds__(K1_THREADS) k_chain_hash(const uint32_t *__res
     }
     const uint64_t P = e.a * carry + e.b;
     if (valid) {
-      uint64_t j = (uint64_t)sr + n - 1 - k;
+      uint64_t j = (uint64_t)sr + n - 1 - k - pos_base;
       hash_out[j] = fmix64(P);
-      req_out[j] = r;
+      req_out[j] = r + req_base;
     }
     carry = __shfl_sync(0xffffffffu, P, 31);  // last block of the round (beyond B1: unused)
   }
@@ -264,8 +260,8 @@ __global__ void __launch_bounds__(K1_THREADS) k_chain_hash(const uint32_t *__res
 
 // HASHES mode: copy caller hashes into touch order (warp per request)
 __global__ void k_copy_hashes(const uint64_t *__restrict__ bh, const int64_t *__restrict__ src_off,
-                              const uint32_t *__restrict__ s, int64_t R, uint64_t *__restrict__ hash_out,
-                              uint32_t *__restrict__ req_out) {
+                              const uint32_t *__restrict__ s, int64_t R, uint32_t pos_base, uint32_t req_base,
+                              uint64_t *__restrict__ hash_out, uint32_t *__restrict__ req_out) {
   int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -273,9 +269,9 @@ __global__ void k_copy_hashes(const uint64_t *__restrict__ bh, const int64_t *__
     uint32_t sr = s[r], n = s[r + 1] - sr;
     const uint64_t *src = bh + src_off[r];
     for (uint32_t k = lane; k < n; k += 32) {
-      uint32_t j = sr + n - 1 - k;
+      uint32_t j = sr + n - 1 - k - pos_base;
       hash_out[j] = src[k];
-      req_out[j] = (uint32_t)r;
+      req_out[j] = (uint32_t)r + req_base;
     }
   }
 }
@@ -292,7 +288,7 @@ __global__ void k_iota(uint32_t *v, uint64_t n) {
 __global__ void k_sort_prep(const uint64_t *__restrict__ hash, uint64_t N, uint32_t *__restrict__ key,
                             uint64_t *__restrict__ val) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t m = fmix64(hash[j] ^ 0x6A09E667F3BCC909ULL);  // bijection: (key, val >> 32) identifies h
+    uint64_t m = fmix64(hash[j] ^ kSortMixC);  // bijection: (key, val >> 32) identifies h
     key[j] = (uint32_t)(m >> 32);
     val[j] = (m << 32) | (uint64_t)(uint32_t)j;
   }
@@ -585,12 +581,14 @@ __global__ void k_access_info(uint64_t N, const uint32_t *__restrict__ prev, con
 
 // groups: requests with at least one block, keyed by their root hash (block k = 0, the
 // last touch of the request)
+// (s points at the first request considered; hash is indexed by position - pos_base)
 __global__ void k_root_keys(int64_t R, const uint32_t *__restrict__ s, const uint64_t *__restrict__ hash,
-                            uint64_t *__restrict__ key, uint32_t *__restrict__ val, uint8_t *__restrict__ flag) {
+                            uint32_t pos_base, uint64_t *__restrict__ key, uint32_t *__restrict__ val,
+                            uint8_t *__restrict__ flag) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
     bool has = s[r + 1] > s[r];
     flag[r] = has;
-    key[r] = has ? hash[s[r + 1] - 1] : 0;
+    key[r] = has ? hash[s[r + 1] - 1 - pos_base] : 0;
     val[r] = (uint32_t)r;
   }
 }
@@ -649,14 +647,16 @@ __global__ void k_fill_u16(uint16_t *p, int64_t n, uint16_t v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
 
-__global__ void k_group_tables(int64_t R, const uint16_t *__restrict__ grp, const uint32_t *__restrict__ first_cnt,
-                               const uint32_t *__restrict__ reuse_cnt, unsigned long long *__restrict__ tab, int G) {
+// requests [r_base, r_base + R): grp is global, first_cnt / reuse_cnt local
+__global__ void k_group_tables(int64_t R, uint32_t r_base, const uint16_t *__restrict__ grp,
+                               const uint32_t *__restrict__ first_cnt, const uint32_t *__restrict__ reuse_cnt,
+                               unsigned long long *__restrict__ tab, int G) {
   // tab[2g] = U_g, tab[2g+1] = reuse_g; privatised per block in smem (G <= 1024)
   extern __shared__ unsigned long long ts[];
   for (int i = threadIdx.x; i < 2 * G; i += blockDim.x) ts[i] = 0;
   __syncthreads();
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
-    int g = grp[r];
+    int g = grp[r_base + r];
     if (first_cnt[r]) atomicAdd(&ts[2 * g], (unsigned long long)first_cnt[r]);
     if (reuse_cnt[r]) atomicAdd(&ts[2 * g + 1], (unsigned long long)reuse_cnt[r]);
   }
@@ -679,7 +679,7 @@ static kareto_status to_device(kareto_ctx *ctx, const T *src, size_t n, bool on_
   return KARETO_OK;
 }
 
-static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_trace **out) {
+kareto_status ingest(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_trace *tr, Ingest &in) {
   const int64_t R = d->n_requests;
   if (R < 1) return fail(ctx, KARETO_E_INVALID, "n_requests must be >= 1");
   if (R >= (int64_t)kNone) return fail(ctx, KARETO_E_OVERFLOW, "too many requests");
@@ -698,52 +698,30 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
   if (total < 0) return fail(ctx, KARETO_E_PARSE, "offsets[R] < 0");
   if (d->mode == KARETO_TOKENS && total > 0 && !d->tokens) return fail(ctx, KARETO_E_INVALID, "tokens is null");
   if (d->mode == KARETO_HASHES && total > 0 && !d->block_hash) return fail(ctx, KARETO_E_INVALID, "block_hash null");
-
-  DBuf<int64_t> h_arr, h_off, h_in;
-  DBuf<int32_t> h_out;
-  DBuf<uint32_t> h_tok;
-  DBuf<uint64_t> h_bh;
-  const int64_t *arrival, *offsets, *input_tokens = nullptr;
-  const int32_t *out_tok;
-  const uint32_t *tokens = nullptr;
-  const uint64_t *bhash = nullptr;
+  in.total = total;
   {
     Pass ps(ctx, "h2d", 0, 0);
-    KTRY(to_device(ctx, d->arrival_ms, R, dev, h_arr, &arrival));
-    KTRY(to_device(ctx, d->output_tokens, R, dev, h_out, &out_tok));
-    KTRY(to_device(ctx, d->offsets, R + 1, dev, h_off, &offsets));
-    if (d->mode == KARETO_TOKENS) KTRY(to_device(ctx, d->tokens, (size_t)total, dev, h_tok, &tokens));
-    else {
-      KTRY(to_device(ctx, d->block_hash, (size_t)total, dev, h_bh, &bhash));
-      if (d->input_tokens) KTRY(to_device(ctx, d->input_tokens, R, dev, h_in, &input_tokens));
-    }
+    KTRY(to_device(ctx, d->arrival_ms, R, dev, in.h_arr, &in.arrival));
+    KTRY(to_device(ctx, d->output_tokens, R, dev, in.h_out, &in.out_tok));
+    KTRY(to_device(ctx, d->offsets, R + 1, dev, in.h_off, &in.offsets));
+    if (d->mode == KARETO_HASHES && d->input_tokens)
+      KTRY(to_device(ctx, d->input_tokens, R, dev, in.h_in, &in.input_tokens));
   }
-
-  kareto_trace *tr = new kareto_trace();
-  tr->ctx = ctx;
-  tr->stream = ctx->stream;
   tr->R = R;
   tr->K = d->top_k;
-  struct Guard {
-    kareto_trace *&t;
-    bool keep = false;
-    ~Guard() { if (!keep) kareto_trace_free(t); }
-  } guard{tr};
 
   DBuf<uint8_t> tmp;
-  DBuf<LoadStats> stats;
-  KTRY(stats.alloc(ctx, 1));
-  KTRY(stats.zero());
-
-  // ---- a1: sort requests, per-request metadata, block offsets
-  DBuf<uint64_t> skey, skey2, nblk, s64;
+  KTRY(in.stats.alloc(ctx, 1));
+  KTRY(in.stats.zero());
+  DBuf<uint64_t> skey, skey2, s64;
   DBuf<uint32_t> sidx, order;
-  DBuf<int64_t> arr_sorted, src_off;
+  DBuf<int64_t> arr_sorted;
   KTRY(skey.alloc(ctx, R)); KTRY(skey2.alloc(ctx, R)); KTRY(sidx.alloc(ctx, R)); KTRY(order.alloc(ctx, R));
-  KTRY(arr_sorted.alloc(ctx, R)); KTRY(src_off.alloc(ctx, R)); KTRY(nblk.alloc(ctx, R + 1)); KTRY(s64.alloc(ctx, R + 1));
+  KTRY(arr_sorted.alloc(ctx, R)); KTRY(in.src_off.alloc(ctx, R)); KTRY(in.nblk.alloc(ctx, R + 1));
+  KTRY(s64.alloc(ctx, R + 1));
   {
     Pass ps(ctx, "a1_sort_keys", 1, 1);
-    k_sort_keys<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(arrival, R, skey.p, sidx.p);
+    k_sort_keys<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(in.arrival, R, skey.p, sidx.p);
   }
   {
     Pass ps(ctx, "a1_sort_requests", 0, 1);
@@ -751,30 +729,28 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
       return cub::DeviceRadixSort::SortPairs(t, b, skey.p, skey2.p, sidx.p, order.p, (int)R, 0, 64, st);
     }));
   }
-  KCUDA(ctx, cudaMemsetAsync(nblk.p + R, 0, 8, st));
+  KCUDA(ctx, cudaMemsetAsync(in.nblk.p + R, 0, 8, st));
   KCUDA(ctx, cudaMallocAsync((void **)&tr->inlen, 4 * (size_t)R, st));
   KCUDA(ctx, cudaMallocAsync((void **)&tr->outlen, 4 * (size_t)R, st));
   {
     Pass ps(ctx, "a1_req_meta", 1, 1);
-    k_req_meta<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(R, d->mode, order.p, arrival, out_tok, offsets, input_tokens,
-                                                          arr_sorted.p, src_off.p, nblk.p, tr->inlen, tr->outlen,
-                                                          stats.p);
+    k_req_meta<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(R, d->mode, order.p, in.arrival, in.out_tok, in.offsets,
+                                                          in.input_tokens, arr_sorted.p, in.src_off.p, in.nblk.p,
+                                                          tr->inlen, tr->outlen, in.stats.p);
   }
   {
     Pass ps(ctx, "a1_scan_starts", 0, 1);
     KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, nblk.p, s64.p, (int)(R + 1), st);
+      return cub::DeviceScan::ExclusiveSum(t, b, in.nblk.p, s64.p, (int)(R + 1), st);
     }));
   }
-  uint32_t *s_dev;
-  KCUDA(ctx, cudaMallocAsync((void **)&s_dev, 4 * (size_t)(R + 1), st));
-  tr->s = s_dev;
+  KCUDA(ctx, cudaMallocAsync((void **)&tr->s, 4 * (size_t)(R + 1), st));
   {
     Pass ps(ctx, "a1_narrow", 1, 1);
-    k_narrow_starts<<<grid_for(R + 1, 256, 4 * sms), 256, 0, st>>>(R, s64.p, tr->s, arr_sorted.p, stats.p);
+    k_narrow_starts<<<grid_for(R + 1, 256, 4 * sms), 256, 0, st>>>(R, s64.p, tr->s, arr_sorted.p, in.stats.p);
   }
-  LoadStats hs;
-  KCUDA(ctx, cudaMemcpyAsync(&hs, stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  LoadStats &hs = in.hs;
+  KCUDA(ctx, cudaMemcpyAsync(&hs, in.stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
   KCUDA(ctx, cudaStreamSynchronize(st));
   if (hs.flags & F_OFFSETS) return fail(ctx, KARETO_E_PARSE, "offsets are not nondecreasing");
   if (hs.flags & F_OUTPUT) return fail(ctx, KARETO_E_PARSE, "output_tokens < 0");
@@ -791,6 +767,153 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
   if (tr->SL > (unsigned __int128)UINT64_MAX) return fail(ctx, KARETO_E_OVERFLOW, "sum of input tokens >= 2^64");
   tr->Ltok = (uint64_t)tr->SL;
   tr->arr = arr_sorted.detach();
+  KCUDA(ctx, cudaMallocAsync((void **)&tr->grp, 2 * (size_t)R, st));
+  return KARETO_OK;
+}
+
+kareto_status upload_payload(kareto_ctx *ctx, const kareto_trace_desc *d, int64_t lo, int64_t hi,
+                             DBuf<uint32_t> &tok, DBuf<uint64_t> &bh, const uint32_t **tok_base,
+                             const uint64_t **bh_base) {
+  *tok_base = nullptr;
+  *bh_base = nullptr;
+  const bool tokens = d->mode == KARETO_TOKENS;
+  if (d->inputs_on_device || hi <= lo) {
+    *tok_base = tokens ? d->tokens : nullptr;
+    *bh_base = tokens ? nullptr : d->block_hash;
+    return KARETO_OK;
+  }
+  Pass ps(ctx, "h2d", 0, 0);
+  const size_t n = (size_t)(hi - lo);
+  if (tokens) {
+    KTRY(tok.alloc(ctx, n));
+    KCUDA(ctx, cudaMemcpyAsync(tok.p, d->tokens + lo, 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+    *tok_base = tok.p - lo;
+  } else {
+    KTRY(bh.alloc(ctx, n));
+    KCUDA(ctx, cudaMemcpyAsync(bh.p, d->block_hash + lo, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
+    *bh_base = bh.p - lo;
+  }
+  return KARETO_OK;
+}
+
+kareto_status chain_hash(kareto_ctx *ctx, const kareto_trace_desc *d, const kareto_trace *tr, const Ingest &in,
+                         const uint32_t *tok_base, const uint64_t *bh_base, int64_t tok_end, int64_t r0, int64_t r1,
+                         uint64_t *hash_out, uint32_t *req_out) {
+  uint32_t se[2];
+  KCUDA(ctx, cudaMemcpyAsync(&se[0], tr->s + r0, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  KCUDA(ctx, cudaMemcpyAsync(&se[1], tr->s + r1, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  KCUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  const uint64_t n = (uint64_t)(se[1] - se[0]);
+  if (n == 0) return KARETO_OK;
+  const int sms = ctx->num_sms;
+  if (d->mode == KARETO_TOKENS) {
+    uint64_t P_init = fmix64(d->salt ^ kSaltC);
+    // ~2048 blocks per warp, at least 16 warps per SM
+    uint64_t nwarps = (n + 2047) / 2048;
+    if (nwarps < (uint64_t)(16 * sms)) nwarps = 16 * sms;
+    unsigned g = (unsigned)((nwarps + K1_WARPS - 1) / K1_WARPS);
+    Pass ps(ctx, "K1_chain_hash", 1, 1);
+    k_chain_hash<<<g, K1_THREADS, 0, ctx->stream>>>(tok_base, tok_end, in.src_off.p + r0, tr->s + r0, r1 - r0, n,
+                                                    se[0], (uint32_t)r0, P_init, hash_out, req_out);
+  } else {
+    Pass ps(ctx, "K1_copy_hashes", 1, 1);
+    k_copy_hashes<<<grid_for(32 * (r1 - r0), 256, 8 * sms), 256, 0, ctx->stream>>>(
+        bh_base, in.src_off.p + r0, tr->s + r0, r1 - r0, se[0], (uint32_t)r0, hash_out, req_out);
+  }
+  return KARETO_OK;
+}
+
+kareto_status link_prev(kareto_ctx *ctx, const uint64_t *hash, uint64_t N, uint32_t *prev, SortedHashes *keep) {
+  if (N == 0) return KARETO_OK;
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+  DBuf<uint8_t> tmp;
+  DBuf<uint32_t> k32, k32s;
+  DBuf<uint64_t> v64, v64s;
+  KTRY(k32.alloc(ctx, N)); KTRY(k32s.alloc(ctx, N)); KTRY(v64.alloc(ctx, N)); KTRY(v64s.alloc(ctx, N));
+  {
+    Pass ps(ctx, "K2_sort_prep", 1, 1);
+    k_sort_prep<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(hash, N, k32.p, v64.p);
+  }
+  {
+    Pass ps(ctx, "K2_sort_hashes", 0, 1);
+    KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, k32.p, k32s.p, v64.p, v64s.p, (int64_t)N, 0, 32, st);
+    }));
+  }
+  k32.release(); v64.release();
+  {
+    DBuf<uint2> pairs, ovf;
+    DBuf<uint32_t> n_ovf;
+    DBuf<unsigned> cursor;
+    constexpr int PBT = 15;
+    const uint64_t nbk_t = (N + (1u << PBT) - 1) >> PBT;
+    const bool tiled = nbk_t <= (uint64_t)LT_MAX_BUCKETS;
+    const int pbits = tiled ? PBT : PB;
+    const uint64_t nbk = (N + (1ull << pbits) - 1) >> pbits;
+    KTRY(pairs.alloc(ctx, N)); KTRY(ovf.alloc(ctx, N)); KTRY(n_ovf.alloc(ctx, 1)); KTRY(n_ovf.zero());
+    KTRY(cursor.alloc(ctx, nbk)); KTRY(cursor.zero());
+    {
+      Pass ps(ctx, "K2_link_prev", 1, 1);
+      if (tiled) {
+        const size_t smem = 8 * (size_t)LT_TILE + 8 * (size_t)nbk;
+        cudaFuncSetAttribute(k_link_tile<PBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const uint64_t ntile = (N + LT_TILE - 1) / LT_TILE;
+        k_link_tile<PBT><<<(unsigned)(ntile < (uint64_t)(2 * sms) ? ntile : 2 * sms), LT_THREADS, smem, st>>>(
+            k32s.p, v64s.p, N, (int)nbk, cursor.p, pairs.p, ovf.p, n_ovf.p);
+      } else {
+        k_link_prev<<<grid_for((N + LINK_U - 1) / LINK_U, 256, 8 * sms), 256, 0, st>>>(
+            k32s.p, v64s.p, N, cursor.p, pairs.p, ovf.p, n_ovf.p);
+      }
+    }
+    {
+      Pass ps(ctx, "K2_link_overflow", 1, 1);
+      k_link_overflow<<<2 * sms, OVF_THREADS, 0, st>>>(k32s.p, v64s.p, ovf.p, n_ovf.p, pairs.p);
+    }
+    if (getenv("KARETO_DEBUG")) {
+      uint32_t h = 0;
+      cudaMemcpyAsync(&h, n_ovf.p, 4, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      fprintf(stderr, "[kareto] K2 link overflow elements: %u of %llu\n", h, (unsigned long long)N);
+    }
+    {
+      Pass ps(ctx, "K2_bucket_assemble", 1, 1);
+      const unsigned g = (unsigned)(nbk < (uint64_t)(4 * sms) ? nbk : 4 * sms);
+      if (tiled) {
+        cudaFuncSetAttribute(k_bucket_assemble<PBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << PBT);
+        k_bucket_assemble<PBT><<<g, 1024, 4 << PBT, st>>>(pairs.p, N, prev);
+      } else {
+        k_bucket_assemble<PB><<<g, 1024, 4 << PB, st>>>(pairs.p, N, prev);
+      }
+    }
+  }
+  if (keep) {
+    keep->key = std::move(k32s);
+    keep->val = std::move(v64s);
+  }
+  return KARETO_OK;
+}
+
+static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_trace **out) {
+  kareto_trace *tr = new kareto_trace();
+  tr->ctx = ctx;
+  tr->stream = ctx->stream;
+  struct Guard {
+    kareto_trace *&t;
+    bool keep = false;
+    ~Guard() { if (!keep) kareto_trace_free(t); }
+  } guard{tr};
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+
+  // ---- a1: sort requests, per-request metadata, block offsets
+  Ingest in;
+  KTRY(ingest(ctx, d, tr, in));
+  const int64_t R = tr->R;
+  const uint64_t N = (uint64_t)tr->N;
+  LoadStats &hs = in.hs;
+  tr->pos_hi = tr->N;
+  tr->req_hi = R;
 
   const uint64_t Na = N > 0 ? N : 1;
   KCUDA(ctx, cudaMallocAsync((void **)&tr->hash, 8 * Na, st));
@@ -798,25 +921,16 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
   KCUDA(ctx, cudaMallocAsync((void **)&tr->prev, 4 * Na, st));
   KCUDA(ctx, cudaMallocAsync((void **)&tr->delta, 4 * Na, st));
   KCUDA(ctx, cudaMallocAsync((void **)&tr->depth, 4 * Na, st));
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->grp, 2 * (size_t)R, st));
 
   // ---- a2: K1 chained hashes (TOKENS) / copy (HASHES) into touch order
-  if (N > 0) {
-    if (d->mode == KARETO_TOKENS) {
-      uint64_t P_init = fmix64(d->salt ^ kSaltC);
-      // ~2048 blocks per warp, at least 16 warps per SM
-      uint64_t nwarps = (N + 2047) / 2048;
-      if (nwarps < (uint64_t)(16 * sms)) nwarps = 16 * sms;
-      unsigned g = (unsigned)((nwarps + K1_WARPS - 1) / K1_WARPS);
-      Pass ps(ctx, "K1_chain_hash", 1, 1);
-      k_chain_hash<<<g, K1_THREADS, 0, st>>>(tokens, total, src_off.p, tr->s, R, N, P_init, tr->hash, tr->req);
-    } else {
-      Pass ps(ctx, "K1_copy_hashes", 1, 1);
-      k_copy_hashes<<<grid_for(32 * R, 256, 8 * sms), 256, 0, st>>>(bhash, src_off.p, tr->s, R, tr->hash, tr->req);
-    }
+  {
+    DBuf<uint32_t> h_tok;
+    DBuf<uint64_t> h_bh;
+    const uint32_t *tok_base;
+    const uint64_t *bh_base;
+    KTRY(upload_payload(ctx, d, 0, in.total, h_tok, h_bh, &tok_base, &bh_base));
+    KTRY(chain_hash(ctx, d, tr, in, tok_base, bh_base, in.total, 0, R, tr->hash, tr->req));
   }
-  h_tok.release();
-  h_bh.release();
 
   // ---- a3: K2 prev / delta / chain check
   DBuf<uint32_t> first_cnt, reuse_cnt;
@@ -825,78 +939,18 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
   KTRY(first_cnt.alloc(ctx, R)); KTRY(reuse_cnt.alloc(ctx, R));
   KTRY(first_cnt.zero()); KTRY(reuse_cnt.zero());
   if (N > 0) {
-    int B = 1;
-    while ((1ull << B) < N) B++;
-    {
-      DBuf<uint32_t> k32, k32s;
-      DBuf<uint64_t> v64, v64s;
-      KTRY(k32.alloc(ctx, N)); KTRY(k32s.alloc(ctx, N)); KTRY(v64.alloc(ctx, N)); KTRY(v64s.alloc(ctx, N));
-      {
-        Pass ps(ctx, "K2_sort_prep", 1, 1);
-        k_sort_prep<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(tr->hash, N, k32.p, v64.p);
-      }
-      {
-        Pass ps(ctx, "K2_sort_hashes", 0, 1);
-        KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
-          return cub::DeviceRadixSort::SortPairs(t, b, k32.p, k32s.p, v64.p, v64s.p, (int64_t)N, 0, 32, st);
-        }));
-      }
-      k32.release(); v64.release();
-      {
-        DBuf<uint2> pairs, ovf;
-        DBuf<uint32_t> n_ovf;
-        DBuf<unsigned> cursor;
-        constexpr int PBT = 15;
-        const uint64_t nbk_t = (N + (1u << PBT) - 1) >> PBT;
-        const bool tiled = nbk_t <= (uint64_t)LT_MAX_BUCKETS;
-        const int pbits = tiled ? PBT : PB;
-        const uint64_t nbk = (N + (1ull << pbits) - 1) >> pbits;
-        KTRY(pairs.alloc(ctx, N)); KTRY(ovf.alloc(ctx, N)); KTRY(n_ovf.alloc(ctx, 1)); KTRY(n_ovf.zero());
-        KTRY(cursor.alloc(ctx, nbk)); KTRY(cursor.zero());
-        {
-          Pass ps(ctx, "K2_link_prev", 1, 1);
-          if (tiled) {
-            const size_t smem = 8 * (size_t)LT_TILE + 8 * (size_t)nbk;
-            cudaFuncSetAttribute(k_link_tile<PBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            const uint64_t ntile = (N + LT_TILE - 1) / LT_TILE;
-            k_link_tile<PBT><<<(unsigned)(ntile < (uint64_t)(2 * sms) ? ntile : 2 * sms), LT_THREADS, smem, st>>>(
-                k32s.p, v64s.p, N, (int)nbk, cursor.p, pairs.p, ovf.p, n_ovf.p);
-          } else {
-            k_link_prev<<<grid_for((N + LINK_U - 1) / LINK_U, 256, 8 * sms), 256, 0, st>>>(
-                k32s.p, v64s.p, N, cursor.p, pairs.p, ovf.p, n_ovf.p);
-          }
-        }
-        {
-          Pass ps(ctx, "K2_link_overflow", 1, 1);
-          k_link_overflow<<<2 * sms, OVF_THREADS, 0, st>>>(k32s.p, v64s.p, ovf.p, n_ovf.p, pairs.p);
-        }
-        if (getenv("KARETO_DEBUG")) {
-          uint32_t h = 0;
-          cudaMemcpyAsync(&h, n_ovf.p, 4, cudaMemcpyDeviceToHost, st);
-          cudaStreamSynchronize(st);
-          fprintf(stderr, "[kareto] K2 link overflow elements: %u of %llu\n", h, (unsigned long long)N);
-        }
-        {
-          Pass ps(ctx, "K2_bucket_assemble", 1, 1);
-          const unsigned g = (unsigned)(nbk < (uint64_t)(4 * sms) ? nbk : 4 * sms);
-          if (tiled) {
-            cudaFuncSetAttribute(k_bucket_assemble<PBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << PBT);
-            k_bucket_assemble<PBT><<<g, 1024, 4 << PBT, st>>>(pairs.p, N, tr->prev);
-          } else {
-            k_bucket_assemble<PB><<<g, 1024, 4 << PB, st>>>(pairs.p, N, tr->prev);
-          }
-        }
-      }
-    }
+    KTRY(link_prev(ctx, tr->hash, N, tr->prev, nullptr));
     {
       Pass ps(ctx, "K2_access_info", 1, 1);
       k_access_info<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(N, tr->prev, tr->req, tr->s, tr->arr, tr->hash,
-                                                               tr->delta, first_cnt.p, reuse_cnt.p, run_flag.p, stats.p);
+                                                               tr->delta, first_cnt.p, reuse_cnt.p, run_flag.p,
+                                                               in.stats.p);
     }
   }
 
   // ---- a3: groups (top-K prefix subtrees by reuse, residual K)
   {
+    DBuf<uint8_t> tmp;
     const int K = tr->K;
     DBuf<uint64_t> rkey, rkey_s, rankkey, rankkey_s;
     DBuf<uint32_t> rval, rval_c, rval_s, head, run_incl, rankidx, ranked, rank, nruns;
@@ -912,7 +966,7 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
     DBuf<uint64_t> rkey_c;
     KTRY(rkey_c.alloc(ctx, R));
     Pass ps(ctx, "K2_groups", 1, 8);
-    k_root_keys<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(R, tr->s, tr->hash, rkey.p, rval.p, rflag.p);
+    k_root_keys<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(R, tr->s, tr->hash, 0, rkey.p, rval.p, rflag.p);
     KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
       return cub::DeviceSelect::Flagged(t, b, rkey.p, rflag.p, rkey_c.p, m_dev.p, (int)R, st);
     }));
@@ -941,10 +995,11 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
       k_rank_of_run<<<grid_for(m, 256, 4 * sms), 256, 0, st>>>(ranked.p, nruns.p, rank.p);
       k_assign_groups<<<grid_for(m, 256, 4 * sms), 256, 0, st>>>(rval_s.p, run_incl.p, m_dev.p, rank.p, K, tr->grp);
     }
-    k_group_tables<<<grid_for(R, 256, 4 * sms), 256, 16 * (K + 1), st>>>(R, tr->grp, first_cnt.p, reuse_cnt.p, gtab.p, K + 1);
+    k_group_tables<<<grid_for(R, 256, 4 * sms), 256, 16 * (K + 1), st>>>(R, 0, tr->grp, first_cnt.p, reuse_cnt.p,
+                                                                          gtab.p, K + 1);
     std::vector<unsigned long long> h(2 * (K + 1));
     KCUDA(ctx, cudaMemcpyAsync(h.data(), gtab.p, 16 * (K + 1), cudaMemcpyDeviceToHost, st));
-    KCUDA(ctx, cudaMemcpyAsync(&hs, stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    KCUDA(ctx, cudaMemcpyAsync(&hs, in.stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
     KCUDA(ctx, cudaStreamSynchronize(st));
     tr->U_g.resize(K + 1);
     tr->reuse_g.resize(K + 1);
@@ -960,7 +1015,10 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
   if (hs.flags & F_DELTA) return fail(ctx, KARETO_E_OVERFLOW, "a reuse interval >= 2^32-1 ms");
 
   // ---- a4: K3 LRU stack depths
-  KTRY(stack_depth(ctx, tr, run_flag.p));
+  if (N > 0) {
+    if (N >= (1ull << 31)) return fail(ctx, KARETO_E_OVERFLOW, "stack depth pass supports < 2^31 accesses");
+    KTRY(stack_depth(ctx, N, N, tr->prev, tr->req, 0, tr->s, 0, 0, run_flag.p, tr->depth, &tr->n_runs));
+  }
   KTRY(sync(ctx, "load_trace"));
   guard.keep = true;
   *out = tr;

@@ -1,0 +1,741 @@
+// trace_shard.cu -- row f4: time-sharded trace passes, kareto_load_trace_sharded.
+//
+// Rank k of W owns the sorted requests [r_k, r_{k+1}) whose blocks occupy the positions
+// [P0, P1) ~ [kN/W, (k+1)N/W) of the touch order, and runs K1 (hash), K2 (prev, delta, chain
+// check, groups), K3 (LRU depth) on them only; K4 histograms are summed across ranks at
+// evaluation time (eval.cu).  The result is identical, access by access, to the whole-trace
+// load (kareto_load_trace): same prev (global positions), delta, depth, groups, U.
+//
+// What crosses shard boundaries, and how:
+//   * prev of the first access of a block inside the shard (a "Q" record) is the last access of
+//     that block in an earlier shard (its "P" record).  Every rank sends, for each distinct block
+//     of its shard, a Q record (first access) and a P record (last access) to the OWNER rank of
+//     the block's hash (hash partitioned: all-to-all-v, 24 B per record).  The owner orders the
+//     records of each hash by position, answers each Q with the preceding P (or "globally
+//     first") and checks chain consistency across the boundary (R7); answers go back with a
+//     second all-to-all-v.
+//   * depth needs the LRU stack at the shard boundary P0: B_k = {last access before P0 of every
+//     block seen before P0}.  A P record at shard j whose block next appears in shard n (W if
+//     never) belongs to B_k exactly for j < k <= n; the owner sends its position to those ranks
+//     (third all-to-all-v).  Rank k then solves its shard as a standalone trace prefixed by B_k
+//     in position order (virtual accesses of distinct blocks): a previous position p < P0 maps
+//     to its rank in B_k, p >= P0 to |B_k| + p - P0, and K3 runs unchanged on the compressed
+//     coordinates.  Exact: the distinct blocks touched in [p, s_r) of the real trace are those
+//     of B_k at or after p plus those touched in [P0, s_r), as in the virtual trace.
+//   * groups (R23) need the global reuse of every prefix subtree: per-rank (root hash, reuse)
+//     tables are all-gathered and reduced identically on every rank.
+//   * U, U_g, reuse_g and the error flags: one allreduce.
+#include <cub/cub.cuh>
+
+#include "trace_load.cuh"
+
+namespace kareto {
+
+struct XRec {       // exchange record, 24 B
+  uint64_t m;       // fmix64(h ^ kSortMixC): a bijection of the block hash; key32 = m >> 32
+  uint64_t parent;  // hash of the parent block (chain position k - 1); 0 for roots
+  uint32_t pos;     // global position of the access
+  uint32_t info;    // bit 31: P (last access in its shard) / 0: Q (first); bits 24..30: source
+                    // rank; bits 0..23: chain position k
+};
+constexpr uint32_t kRecP = 0x80000000u;
+constexpr int kMaxShardWorld = 128;
+constexpr uint32_t kChainPosMask = 0x00FFFFFFu;
+
+__host__ __device__ __forceinline__ uint32_t owner_of(uint32_t key32, int W) {
+  return (uint32_t)(((uint64_t)key32 * (uint64_t)W) >> 32);
+}
+
+template <typename F>
+static kareto_status cub_run(kareto_ctx *ctx, DBuf<uint8_t> &tmp, F &&f) {
+  size_t bytes = 0;
+  KCUDA(ctx, f((void *)nullptr, bytes));
+  if (bytes > tmp.n) KTRY(tmp.alloc(ctx, bytes));
+  size_t b2 = tmp.n;
+  KCUDA(ctx, f((void *)tmp.p, b2));
+  return KARETO_OK;
+}
+
+// r_k = first request with s[r] >= k N / W (k = 0..W-1), r_W = R
+__global__ void k_slice_bounds(const uint32_t *__restrict__ s, int64_t R, uint64_t N, int W, uint32_t *__restrict__ rb) {
+  int k = threadIdx.x;
+  if (k > W) return;
+  if (k == W) { rb[k] = (uint32_t)R; return; }
+  uint64_t target = (N * (uint64_t)k) / (uint64_t)W;
+  int64_t lo = 0, hi = R;
+  while (lo < hi) {
+    int64_t m = (lo + hi) >> 1;
+    if ((uint64_t)s[m] >= target) hi = m; else lo = m + 1;
+  }
+  rb[k] = (uint32_t)lo;
+}
+
+__global__ void k_mark_next(const uint32_t *__restrict__ prev_loc, uint64_t n, uint8_t *__restrict__ has_next) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t p = prev_loc[i];
+    if (p != kNone) has_next[p] = 1;
+  }
+}
+
+// records per fingerprint-sorted element: Q if first in the shard, P if last
+__global__ void k_rec_count(const uint64_t *__restrict__ vs, uint64_t n, const uint32_t *__restrict__ prev_loc,
+                            const uint8_t *__restrict__ has_next, uint32_t *__restrict__ cnt) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t j = (uint32_t)vs[i];
+    cnt[i] = (prev_loc[j] == kNone ? 1u : 0u) + (has_next[j] ? 0u : 1u);
+  }
+}
+
+__global__ void k_rec_emit(const uint32_t *__restrict__ ks, const uint64_t *__restrict__ vs, uint64_t n,
+                           const uint32_t *__restrict__ prev_loc, const uint8_t *__restrict__ has_next,
+                           const uint32_t *__restrict__ off, const uint32_t *__restrict__ req,
+                           const uint32_t *__restrict__ s, const uint64_t *__restrict__ hash, uint32_t P0, int rank,
+                           XRec *__restrict__ rec) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = vs[i];
+    const uint32_t j = (uint32_t)v;
+    const bool q = prev_loc[j] == kNone, p = !has_next[j];
+    if (!q && !p) continue;
+    XRec x;
+    x.m = ((uint64_t)ks[i] << 32) | (v >> 32);
+    x.pos = P0 + j;
+    const uint32_t k = s[req[j] + 1] - 1 - x.pos;
+    x.parent = k > 0 ? hash[j + 1] : 0ull;
+    x.info = ((uint32_t)rank << 24) | (k & kChainPosMask);
+    uint32_t o = off[i];
+    if (q) rec[o++] = x;
+    if (p) { x.info |= kRecP; rec[o] = x; }
+  }
+}
+
+// send boundaries: first record of each owner (records are in key32 order)
+__global__ void k_owner_bounds(const XRec *__restrict__ rec, uint32_t n, int W, uint32_t *__restrict__ ob) {
+  int o = threadIdx.x;
+  if (o > W) return;
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    uint32_t m = (lo + hi) >> 1;
+    if (owner_of((uint32_t)(rec[m].m >> 32), W) >= (uint32_t)o) hi = m; else lo = m + 1;
+  }
+  ob[o] = lo;
+}
+
+__global__ void k_rec_keys(const XRec *__restrict__ in, uint32_t n, uint32_t *__restrict__ key, uint32_t *__restrict__ idx) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    key[i] = (uint32_t)(in[i].m >> 32);
+    idx[i] = i;
+  }
+}
+
+// Owner: records sorted by key32 (stable => position order within a hash, Q before P of the
+// same shard).  Q: answer with the preceding record of the same hash (a P of an earlier shard)
+// or kNone; P: the shard of the following record of the same hash (W if none).
+__global__ void k_owner_link(const XRec *__restrict__ in, const uint32_t *__restrict__ ks,
+                             const uint32_t *__restrict__ vs, uint32_t n, int W, uint32_t *__restrict__ reply,
+                             uint8_t *__restrict__ nxt, unsigned long long *__restrict__ flags) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t key = ks[i];
+    const XRec x = in[vs[i]];
+    if (!(x.info & kRecP)) {
+      uint32_t ans = kNone;
+      for (uint32_t t = i; t > 0 && ks[t - 1] == key; t--) {
+        const XRec y = in[vs[t - 1]];
+        if (y.m != x.m) continue;
+        ans = y.pos;
+        const uint32_t kq = x.info & kChainPosMask, kp = y.info & kChainPosMask;
+        if (!(y.info & kRecP) || kq != kp || (kq > 0 && y.parent != x.parent)) atomicAdd(&flags[0], 1ull);
+        break;
+      }
+      reply[vs[i]] = ans;
+      nxt[i] = 0;
+    } else {
+      uint32_t nx = (uint32_t)W;
+      for (uint32_t t = i + 1; t < n && ks[t] == key; t++) {
+        const XRec y = in[vs[t]];
+        if (y.m == x.m) { nx = (y.info >> 24) & 0x7F; break; }
+      }
+      reply[vs[i]] = kNone;
+      nxt[i] = (uint8_t)nx;
+    }
+  }
+}
+
+// boundary-set lists: a P record of shard j with next shard nx belongs to B_d for j < d <= nx,
+// d < W.  count: per-destination totals; fill: positions grouped by destination (any order
+// inside a destination: B_d is a set).  Chunks of 4096 sorted records per block iteration.
+constexpr int BL_THREADS = 256, BL_CHUNK = 4096;
+__global__ void __launch_bounds__(BL_THREADS) k_blist(const XRec *__restrict__ in, const uint32_t *__restrict__ vs,
+                                                      const uint8_t *__restrict__ nxt, uint32_t n, int W, int fill,
+                                                      unsigned long long *__restrict__ dcnt,
+                                                      const unsigned long long *__restrict__ dbase,
+                                                      unsigned long long *__restrict__ cursor, uint32_t *__restrict__ out) {
+  __shared__ uint32_t c[kMaxShardWorld];
+  __shared__ unsigned long long b[kMaxShardWorld];
+  for (uint64_t c0 = (uint64_t)blockIdx.x * BL_CHUNK; c0 < n; c0 += (uint64_t)gridDim.x * BL_CHUNK) {
+    const uint32_t c1 = (uint32_t)(c0 + BL_CHUNK < n ? c0 + BL_CHUNK : n);
+    for (int d = threadIdx.x; d < W; d += blockDim.x) c[d] = 0;
+    __syncthreads();
+    for (uint32_t i = (uint32_t)c0 + threadIdx.x; i < c1; i += blockDim.x) {
+      const XRec x = in[vs[i]];
+      if (!(x.info & kRecP)) continue;
+      const int j = (x.info >> 24) & 0x7F, nx = nxt[i];
+      const int dend = nx < W - 1 ? nx : W - 1;
+      for (int d = j + 1; d <= dend; d++) atomicAdd(&c[d], 1u);
+    }
+    __syncthreads();
+    if (!fill) {
+      for (int d = threadIdx.x; d < W; d += blockDim.x)
+        if (c[d]) atomicAdd(&dcnt[d], (unsigned long long)c[d]);
+      __syncthreads();
+      continue;
+    }
+    for (int d = threadIdx.x; d < W; d += blockDim.x) {
+      b[d] = c[d] ? dbase[d] + atomicAdd(&cursor[d], (unsigned long long)c[d]) : 0ull;
+      c[d] = 0;
+    }
+    __syncthreads();
+    for (uint32_t i = (uint32_t)c0 + threadIdx.x; i < c1; i += blockDim.x) {
+      const XRec x = in[vs[i]];
+      if (!(x.info & kRecP)) continue;
+      const int j = (x.info >> 24) & 0x7F, nx = nxt[i];
+      const int dend = nx < W - 1 ? nx : W - 1;
+      for (int d = j + 1; d <= dend; d++) out[b[d] + atomicAdd(&c[d], 1u)] = x.pos;
+    }
+    __syncthreads();
+  }
+}
+
+// prev in global positions: in-shard links + the owners' answers for the Q records
+__global__ void k_prev_global(const uint32_t *__restrict__ prev_loc, uint64_t n, uint32_t P0, uint32_t *__restrict__ prev) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t p = prev_loc[i];
+    prev[i] = p == kNone ? kNone : P0 + p;
+  }
+}
+__global__ void k_apply_replies(const XRec *__restrict__ rec, const uint32_t *__restrict__ reply, uint32_t n,
+                                uint32_t P0, uint32_t *__restrict__ prev) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (!(rec[i].info & kRecP)) prev[rec[i].pos - P0] = reply[i];
+}
+
+__global__ void k_set_bits(const uint32_t *__restrict__ pos, uint64_t n, uint32_t P0, uint32_t *__restrict__ bits,
+                           unsigned long long *__restrict__ bad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t p = pos[i];
+    if (p >= P0) { atomicAdd(bad, 1ull); continue; }
+    uint32_t old = atomicOr(&bits[p >> 5], 1u << (p & 31));
+    if (old & (1u << (p & 31))) atomicAdd(bad, 1ull);  // duplicate: B_k is a set
+  }
+}
+__global__ void k_popc(const uint32_t *__restrict__ bits, uint64_t nw, uint32_t *__restrict__ pc) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nw; i += (uint64_t)gridDim.x * blockDim.x)
+    pc[i] = __popc(bits[i]);
+}
+
+// delta, chain check (in-shard links; cross-shard links were checked by the owners), K3 run
+// heads, per-request first/reuse counts, compressed previous positions for K3
+__global__ void k_access_info_shard(uint64_t n, uint32_t P0, uint32_t r0, const uint32_t *__restrict__ prev,
+                                    const uint32_t *__restrict__ req, const uint32_t *__restrict__ s, int64_t R,
+                                    const int64_t *__restrict__ arr, const uint64_t *__restrict__ hash,
+                                    const uint32_t *__restrict__ bits, const uint32_t *__restrict__ pre, uint32_t Bsize,
+                                    uint32_t *__restrict__ delta, uint32_t *__restrict__ prev_c,
+                                    uint32_t *__restrict__ first_cnt, uint32_t *__restrict__ reuse_cnt,
+                                    uint8_t *__restrict__ run_flag, unsigned long long *__restrict__ flags) {
+  unsigned fl_chain = 0, fl_delta = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = prev[i], r = req[i], j = P0 + (uint32_t)i;
+    uint32_t dl = kNone, pc = kNone;
+    if (p != kNone) {
+      uint32_t rp;
+      if (p >= P0) {
+        rp = req[p - P0];
+        pc = Bsize + (p - P0);
+        const uint32_t kj = s[r + 1] - 1 - j, kp = s[rp + 1] - 1 - p;
+        if (kj != kp) fl_chain++;
+        else if (kj > 0 && hash[i + 1] != hash[p - P0 + 1]) fl_chain++;
+      } else {
+        int64_t lo = 0, hi = R;  // last request with s[r] <= p
+        while (lo < hi) {
+          int64_t m = (lo + hi + 1) >> 1;
+          if (s[m] <= p) lo = m; else hi = m - 1;
+        }
+        rp = (uint32_t)lo;
+        const uint32_t w = bits[p >> 5];
+        pc = pre[p >> 5] + __popc(w & ((1u << (p & 31)) - 1u));
+      }
+      int64_t d = arr[r] - arr[rp];
+      if (d < 0 || d >= (int64_t)kNone) fl_delta++; else dl = (uint32_t)d;
+    }
+    delta[i] = dl;
+    prev_c[i] = pc;
+    uint8_t head = 0;
+    if (p != kNone) {
+      const uint32_t pm = i > 0 ? prev[i - 1] : kNone;
+      head = (j == s[r] || pm == kNone || p != pm + 1) ? 1 : 0;
+    }
+    run_flag[i] = head;
+    const uint32_t rl = r - r0;
+    if (p == kNone) atomicAdd(&first_cnt[rl], 1u); else atomicAdd(&reuse_cnt[rl], 1u);
+  }
+  if (fl_chain) atomicAdd(&flags[0], (unsigned long long)fl_chain);
+  if (fl_delta) atomicAdd(&flags[1], (unsigned long long)fl_delta);
+}
+
+// groups: reuse of each root over the shard's requests
+__global__ void k_root_reuse(const uint32_t *__restrict__ rval, const int *__restrict__ m_ptr,
+                             const uint32_t *__restrict__ reuse_cnt, unsigned long long *__restrict__ v) {
+  int m = *m_ptr;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) v[i] = reuse_cnt[rval[i]];
+}
+__global__ void k_concat_tables(const uint64_t *__restrict__ gk, const unsigned long long *__restrict__ gv,
+                                const uint64_t *__restrict__ cnt_off, int W, uint64_t stride, uint64_t *__restrict__ k,
+                                unsigned long long *__restrict__ v) {
+  for (int r = 0; r < W; r++) {
+    const uint64_t c = cnt_off[r + 1] - cnt_off[r];
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < c; i += (uint64_t)gridDim.x * blockDim.x) {
+      k[cnt_off[r] + i] = gk[r * stride + i];
+      v[cnt_off[r] + i] = gv[r * stride + i];
+    }
+  }
+}
+__global__ void k_rank_keys32(const unsigned long long *__restrict__ tot, uint32_t n, uint32_t *__restrict__ key,
+                              uint32_t *__restrict__ idx) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    key[i] = ~(uint32_t)tot[i];  // reuse < 2^32; stable sort => (reuse desc, root hash asc)
+    idx[i] = i;
+  }
+}
+__global__ void k_top_table(const uint32_t *__restrict__ ranked, const uint64_t *__restrict__ roots, uint32_t ntop,
+                            uint64_t *__restrict__ th, uint32_t *__restrict__ trk) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ntop; i += gridDim.x * blockDim.x) {
+    th[i] = roots[ranked[i]];
+    trk[i] = i;
+  }
+}
+__global__ void k_group_lookup(int64_t n, const uint64_t *__restrict__ rkey, const uint8_t *__restrict__ rflag,
+                               const uint64_t *__restrict__ th, const uint32_t *__restrict__ trk, uint32_t ntop,
+                               int K, uint16_t *__restrict__ grp) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t g = (uint32_t)K;
+    if (rflag[r]) {
+      const uint64_t h = rkey[r];
+      uint32_t lo = 0, hi = ntop;
+      while (lo < hi) {
+        uint32_t m = (lo + hi) >> 1;
+        if (th[m] < h) lo = m + 1; else hi = m;
+      }
+      if (lo < ntop && th[lo] == h) g = trk[lo];
+    }
+    grp[r] = (uint16_t)g;
+  }
+}
+
+// kernels shared with the whole-trace load (trace_load.cu)
+__global__ void k_root_keys(int64_t R, const uint32_t *__restrict__ s, const uint64_t *__restrict__ hash,
+                            uint32_t pos_base, uint64_t *__restrict__ key, uint32_t *__restrict__ val,
+                            uint8_t *__restrict__ flag);
+__global__ void k_group_tables(int64_t R, uint32_t r_base, const uint16_t *__restrict__ grp,
+                               const uint32_t *__restrict__ first_cnt, const uint32_t *__restrict__ reuse_cnt,
+                               unsigned long long *__restrict__ tab, int G);
+__global__ void k_fill_u16(uint16_t *p, int64_t n, uint16_t v);
+
+static std::vector<size_t> offsets_of(const std::vector<uint64_t> &cnt, size_t elem) {
+  std::vector<size_t> o(cnt.size() + 1, 0);
+  for (size_t i = 0; i < cnt.size(); i++) o[i + 1] = o[i] + (size_t)cnt[i] * elem;
+  return o;
+}
+
+// groups (R23) over the whole trace from the shards' (root, reuse) tables
+static kareto_status shard_groups(kareto_ctx *ctx, kareto_trace *tr, const uint32_t *reuse_cnt) {
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms, W = ctx->world, K = tr->K;
+  const int64_t r0 = tr->req_lo, nr = tr->req_hi - tr->req_lo;
+  const int64_t nra = nr > 0 ? nr : 1;
+  DBuf<uint8_t> tmp, rflag;
+  DBuf<uint64_t> rkey, rkey_c, rkey_s, uroots;
+  DBuf<uint32_t> rval, rval_c, rval_s;
+  DBuf<unsigned long long> rv, usum;
+  DBuf<int> m_dev, nu_dev;
+  KTRY(rflag.alloc(ctx, nra)); KTRY(rkey.alloc(ctx, nra)); KTRY(rkey_c.alloc(ctx, nra)); KTRY(rkey_s.alloc(ctx, nra));
+  KTRY(uroots.alloc(ctx, nra)); KTRY(rval.alloc(ctx, nra)); KTRY(rval_c.alloc(ctx, nra)); KTRY(rval_s.alloc(ctx, nra));
+  KTRY(rv.alloc(ctx, nra)); KTRY(usum.alloc(ctx, nra)); KTRY(m_dev.alloc(ctx, 1)); KTRY(nu_dev.alloc(ctx, 1));
+  KTRY(m_dev.zero()); KTRY(nu_dev.zero());
+  int nu = 0;
+  if (nr > 0) {
+    k_root_keys<<<grid_for(nr, 256, 4 * sms), 256, 0, st>>>(nr, tr->s + r0, tr->hash, (uint32_t)tr->pos_lo, rkey.p,
+                                                            rval.p, rflag.p);
+    ctx->own_launches++;
+    KTRY(cub_run(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceSelect::Flagged(t, b, rkey.p, rflag.p, rkey_c.p, m_dev.p, (int)nr, st);
+    }));
+    KTRY(cub_run(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceSelect::Flagged(t, b, rval.p, rflag.p, rval_c.p, m_dev.p, (int)nr, st);
+    }));
+    int m = 0;
+    KCUDA(ctx, cudaMemcpyAsync(&m, m_dev.p, 4, cudaMemcpyDeviceToHost, st));
+    KCUDA(ctx, cudaStreamSynchronize(st));
+    if (m > 0) {
+      KTRY(cub_run(ctx, tmp, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, rkey_c.p, rkey_s.p, rval_c.p, rval_s.p, m, 0, 64, st);
+      }));
+      k_root_reuse<<<grid_for(m, 256, 4 * sms), 256, 0, st>>>(rval_s.p, m_dev.p, reuse_cnt, rv.p);
+      ctx->own_launches++;
+      KTRY(cub_run(ctx, tmp, [&](void *t, size_t &b) {
+        return cub::DeviceReduce::ReduceByKey(t, b, rkey_s.p, uroots.p, rv.p, usum.p, nu_dev.p, cub::Sum(), m, st);
+      }));
+      KCUDA(ctx, cudaMemcpyAsync(&nu, nu_dev.p, 4, cudaMemcpyDeviceToHost, st));
+      KCUDA(ctx, cudaStreamSynchronize(st));
+    }
+  }
+  // all-gather the per-shard tables (padded to the largest), concatenate, reduce by root
+  uint64_t mine = (uint64_t)nu;
+  std::vector<uint64_t> cnt(W);
+  KTRY(coll_allgather_host(ctx, &mine, cnt.data(), 8));
+  uint64_t stride = 1;
+  for (int r = 0; r < W; r++) stride = cnt[r] > stride ? cnt[r] : stride;
+  std::vector<uint64_t> co(W + 1, 0);
+  for (int r = 0; r < W; r++) co[r + 1] = co[r] + cnt[r];
+  const uint64_t M = co[W];
+  DBuf<uint64_t> pk, gk, ak, ak_s, roots, dco;
+  DBuf<unsigned long long> pv, gv, av, av_s, tot;
+  KTRY(pk.alloc(ctx, stride)); KTRY(pv.alloc(ctx, stride));
+  KTRY(gk.alloc(ctx, stride * W)); KTRY(gv.alloc(ctx, stride * W));
+  if (nu > 0) {
+    KCUDA(ctx, cudaMemcpyAsync(pk.p, uroots.p, 8 * (size_t)nu, cudaMemcpyDeviceToDevice, st));
+    KCUDA(ctx, cudaMemcpyAsync(pv.p, usum.p, 8 * (size_t)nu, cudaMemcpyDeviceToDevice, st));
+  }
+  KTRY(coll_allgather(ctx, pk.p, gk.p, 8 * stride));
+  KTRY(coll_allgather(ctx, pv.p, gv.p, 8 * stride));
+  const uint64_t Ma = M > 0 ? M : 1;
+  KTRY(ak.alloc(ctx, Ma)); KTRY(av.alloc(ctx, Ma)); KTRY(ak_s.alloc(ctx, Ma)); KTRY(av_s.alloc(ctx, Ma));
+  KTRY(roots.alloc(ctx, Ma)); KTRY(tot.alloc(ctx, Ma)); KTRY(dco.alloc(ctx, W + 1));
+  KCUDA(ctx, cudaMemcpyAsync(dco.p, co.data(), 8 * (W + 1), cudaMemcpyHostToDevice, st));
+  k_fill_u16<<<grid_for(tr->R, 256, 4 * sms), 256, 0, st>>>(tr->grp, tr->R, (uint16_t)K);  // outside the shard: K
+  ctx->own_launches++;
+  uint32_t ntop = 0;
+  DBuf<uint64_t> th, th_s;
+  DBuf<uint32_t> trk, trk_s;
+  KTRY(th.alloc(ctx, K > 0 ? K : 1)); KTRY(th_s.alloc(ctx, K > 0 ? K : 1));
+  KTRY(trk.alloc(ctx, K > 0 ? K : 1)); KTRY(trk_s.alloc(ctx, K > 0 ? K : 1));
+  if (M > 0 && K > 0) {
+    k_concat_tables<<<grid_for((int64_t)stride, 256, 4 * sms), 256, 0, st>>>(gk.p, gv.p, dco.p, W, stride, ak.p, av.p);
+    ctx->own_launches++;
+    KTRY(cub_run(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, ak.p, ak_s.p, av.p, av_s.p, (int64_t)M, 0, 64, st);
+    }));
+    KTRY(cub_run(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceReduce::ReduceByKey(t, b, ak_s.p, roots.p, av_s.p, tot.p, nu_dev.p, cub::Sum(), (int64_t)M, st);
+    }));
+    int nroot = 0;
+    KCUDA(ctx, cudaMemcpyAsync(&nroot, nu_dev.p, 4, cudaMemcpyDeviceToHost, st));
+    KCUDA(ctx, cudaStreamSynchronize(st));
+    DBuf<uint32_t> rk, rk_s, ri, ri_s;
+    KTRY(rk.alloc(ctx, nroot)); KTRY(rk_s.alloc(ctx, nroot)); KTRY(ri.alloc(ctx, nroot)); KTRY(ri_s.alloc(ctx, nroot));
+    k_rank_keys32<<<grid_for(nroot, 256, 4 * sms), 256, 0, st>>>(tot.p, (uint32_t)nroot, rk.p, ri.p);
+    ctx->own_launches++;
+    KTRY(cub_run(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, rk.p, rk_s.p, ri.p, ri_s.p, nroot, 0, 32, st);
+    }));
+    ntop = (uint32_t)(nroot < K ? nroot : K);
+    k_top_table<<<grid_for(ntop, 256), 256, 0, st>>>(ri_s.p, roots.p, ntop, th.p, trk.p);
+    ctx->own_launches++;
+    KTRY(cub_run(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, th.p, th_s.p, trk.p, trk_s.p, (int)ntop, 0, 64, st);
+    }));
+  }
+  if (nr > 0) {
+    k_group_lookup<<<grid_for(nr, 256, 4 * sms), 256, 0, st>>>(nr, rkey.p, rflag.p, th_s.p, trk_s.p, ntop, K,
+                                                               tr->grp + r0);
+    ctx->own_launches++;
+  }
+  return KARETO_OK;
+}
+
+static kareto_status load_sharded(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_trace **out) {
+  const int W = ctx->world, me = ctx->rank;
+  if (W > kMaxShardWorld) return fail(ctx, KARETO_E_UNSUPPORTED, "time sharding supports world <= %d", kMaxShardWorld);
+  kareto_trace *tr = new kareto_trace();
+  tr->ctx = ctx;
+  tr->stream = ctx->stream;
+  struct Guard {
+    kareto_trace *&t;
+    bool keep = false;
+    ~Guard() { if (!keep) kareto_trace_free(t); }
+  } guard{tr};
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+
+  // ---- a1 (every rank, all requests: R-sized metadata only)
+  Ingest in;
+  KTRY(ingest(ctx, d, tr, in));
+  const int64_t R = tr->R;
+  const uint64_t N = (uint64_t)tr->N;
+  if (tr->max_blocks > (int32_t)kChainPosMask) return fail(ctx, KARETO_E_UNSUPPORTED, "requests of >= 2^24 blocks");
+  if (N >= (1ull << 31)) return fail(ctx, KARETO_E_OVERFLOW, "stack depth pass supports < 2^31 accesses");
+  tr->sharded = true;
+
+  // ---- the shard: requests [r0, r1), positions [P0, P1)
+  std::vector<uint32_t> rb(W + 1);
+  {
+    DBuf<uint32_t> drb;
+    KTRY(drb.alloc(ctx, W + 1));
+    k_slice_bounds<<<1, 256, 0, st>>>(tr->s, R, N, W, drb.p);
+    ctx->own_launches++;
+    KCUDA(ctx, cudaMemcpyAsync(rb.data(), drb.p, 4 * (W + 1), cudaMemcpyDeviceToHost, st));
+  }
+  std::vector<uint32_t> sb(W + 1);
+  KCUDA(ctx, cudaStreamSynchronize(st));
+  for (int k = 0; k <= W; k++) KCUDA(ctx, cudaMemcpyAsync(&sb[k], tr->s + rb[k], 4, cudaMemcpyDeviceToHost, st));
+  KCUDA(ctx, cudaStreamSynchronize(st));
+  const int64_t r0 = rb[me], r1 = rb[me + 1];
+  const uint32_t P0 = sb[me], P1 = sb[me + 1];
+  const uint64_t n = P1 - P0, na = n > 0 ? n : 1;
+  tr->req_lo = r0; tr->req_hi = r1; tr->pos_lo = P0; tr->pos_hi = P1;
+  KCUDA(ctx, cudaMallocAsync((void **)&tr->hash, 8 * na, st));
+  KCUDA(ctx, cudaMallocAsync((void **)&tr->req, 4 * na, st));
+  KCUDA(ctx, cudaMallocAsync((void **)&tr->prev, 4 * na, st));
+  KCUDA(ctx, cudaMallocAsync((void **)&tr->delta, 4 * na, st));
+  KCUDA(ctx, cudaMallocAsync((void **)&tr->depth, 4 * na, st));
+
+  // ---- a2: K1 on the shard (only the shard's token / hash range is uploaded)
+  {
+    int64_t lo = 0, hi = 0;
+    if (r1 > r0 && !d->inputs_on_device) {  // element range covering the shard's requests
+      std::vector<int64_t> so(r1 - r0);
+      KCUDA(ctx, cudaMemcpyAsync(so.data(), in.src_off.p + r0, 8 * (r1 - r0), cudaMemcpyDeviceToHost, st));
+      std::vector<uint64_t> nb(r1 - r0);
+      KCUDA(ctx, cudaMemcpyAsync(nb.data(), in.nblk.p + r0, 8 * (r1 - r0), cudaMemcpyDeviceToHost, st));
+      KCUDA(ctx, cudaStreamSynchronize(st));
+      lo = INT64_MAX;
+      for (int64_t i = 0; i < r1 - r0; i++) {
+        if (nb[i] == 0) continue;
+        const int64_t e = so[i] + (int64_t)nb[i] * (d->mode == KARETO_TOKENS ? 16 : 1);
+        lo = so[i] < lo ? so[i] : lo;
+        hi = e > hi ? e : hi;
+      }
+      if (lo == INT64_MAX) lo = hi = 0;
+    }
+    DBuf<uint32_t> h_tok;
+    DBuf<uint64_t> h_bh;
+    const uint32_t *tok_base;
+    const uint64_t *bh_base;
+    KTRY(upload_payload(ctx, d, lo, hi, h_tok, h_bh, &tok_base, &bh_base));
+    KTRY(chain_hash(ctx, d, tr, in, tok_base, bh_base, d->inputs_on_device ? in.total : hi, r0, r1, tr->hash,
+                    tr->req));
+  }
+
+  // ---- a3: in-shard links, then the owner exchange for the shard's first / last accesses
+  DBuf<uint32_t> prev_loc;
+  DBuf<uint8_t> tmp;
+  KTRY(prev_loc.alloc(ctx, na));
+  SortedHashes sh;
+  DBuf<XRec> rec;
+  uint32_t n_rec = 0;
+  std::vector<uint64_t> send_cnt(W, 0);
+  if (n > 0) KTRY(link_prev(ctx, tr->hash, n, prev_loc.p, &sh));
+  {
+    Pass ps(ctx, "F4_records", 1, 4);
+    DBuf<uint8_t> has_next;
+    DBuf<uint32_t> cnt, off;
+    KTRY(has_next.alloc(ctx, na)); KTRY(has_next.zero());
+    KTRY(cnt.alloc(ctx, na + 1)); KTRY(off.alloc(ctx, na + 1));
+    KCUDA(ctx, cudaMemsetAsync(cnt.p, 0, 4 * (na + 1), st));
+    if (n > 0) {
+      k_mark_next<<<grid_for(n, 256, 8 * sms), 256, 0, st>>>(prev_loc.p, n, has_next.p);
+      k_rec_count<<<grid_for(n, 256, 8 * sms), 256, 0, st>>>(sh.val.p, n, prev_loc.p, has_next.p, cnt.p);
+    }
+    KTRY(cub_run(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, cnt.p, off.p, (int64_t)(n + 1), st);
+    }));
+    KCUDA(ctx, cudaMemcpyAsync(&n_rec, off.p + n, 4, cudaMemcpyDeviceToHost, st));
+    KCUDA(ctx, cudaStreamSynchronize(st));
+    KTRY(rec.alloc(ctx, n_rec > 0 ? n_rec : 1));
+    std::vector<uint32_t> ob(W + 1, 0);
+    if (n > 0) {
+      k_rec_emit<<<grid_for(n, 256, 8 * sms), 256, 0, st>>>(sh.key.p, sh.val.p, n, prev_loc.p, has_next.p, off.p,
+                                                            tr->req, tr->s, tr->hash, P0, me, rec.p);
+      DBuf<uint32_t> dob;
+      KTRY(dob.alloc(ctx, W + 1));
+      k_owner_bounds<<<1, 256, 0, st>>>(rec.p, n_rec, W, dob.p);
+      KCUDA(ctx, cudaMemcpyAsync(ob.data(), dob.p, 4 * (W + 1), cudaMemcpyDeviceToHost, st));
+      KCUDA(ctx, cudaStreamSynchronize(st));
+    }
+    for (int o = 0; o < W; o++) send_cnt[o] = ob[o + 1] - ob[o];
+  }
+  sh.key.release();
+  sh.val.release();
+  // record counts: cnt_all[src * W + dst]
+  std::vector<uint64_t> cnt_all((size_t)W * W);
+  KTRY(coll_allgather_host(ctx, send_cnt.data(), cnt_all.data(), 8 * W));
+  std::vector<uint64_t> recv_cnt(W);
+  for (int r = 0; r < W; r++) recv_cnt[r] = cnt_all[(size_t)r * W + me];
+  const std::vector<size_t> soff = offsets_of(send_cnt, sizeof(XRec)), roff = offsets_of(recv_cnt, sizeof(XRec));
+  const uint64_t n_in = roff[W] / sizeof(XRec);
+  if (n_in >= (uint64_t)kNone) return fail(ctx, KARETO_E_OVERFLOW, "too many exchange records");
+  DBuf<XRec> inrec;
+  KTRY(inrec.alloc(ctx, n_in > 0 ? n_in : 1));
+  {
+    Pass ps(ctx, "F4_exchange", 0, 1);
+    KTRY(coll_alltoallv(ctx, rec.p, soff, inrec.p, roff));
+  }
+
+  // ---- owner: order each hash's records by position, answer Q's, next shard of P's
+  // [0] chain violations, [1] reuse intervals >= 2^32-1 ms, [2] internal inconsistencies; all
+  // ranks learn them from one allreduce and fail together (no rank may leave a collective early)
+  DBuf<unsigned long long> flags;
+  KTRY(flags.alloc(ctx, 3)); KTRY(flags.zero());
+  DBuf<uint32_t> reply, blist;
+  std::vector<uint64_t> dcnt_h(W, 0);
+  KTRY(reply.alloc(ctx, n_in > 0 ? n_in : 1));
+  {
+    Pass ps(ctx, "F4_owner", 1, 4);
+    DBuf<uint32_t> k, ks, v, vs;
+    DBuf<uint8_t> nxt;
+    const uint64_t nia = n_in > 0 ? n_in : 1;
+    KTRY(k.alloc(ctx, nia)); KTRY(ks.alloc(ctx, nia)); KTRY(v.alloc(ctx, nia)); KTRY(vs.alloc(ctx, nia));
+    KTRY(nxt.alloc(ctx, nia));
+    DBuf<unsigned long long> dcnt, dbase, cursor;
+    KTRY(dcnt.alloc(ctx, W)); KTRY(dcnt.zero()); KTRY(dbase.alloc(ctx, W)); KTRY(cursor.alloc(ctx, W));
+    KTRY(cursor.zero());
+    const unsigned gbl = grid_for((int64_t)((n_in + BL_CHUNK - 1) / BL_CHUNK), 1, 8 * sms);
+    if (n_in > 0) {
+      k_rec_keys<<<grid_for(n_in, 256, 8 * sms), 256, 0, st>>>(inrec.p, (uint32_t)n_in, k.p, v.p);
+      KTRY(cub_run(ctx, tmp, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, k.p, ks.p, v.p, vs.p, (int64_t)n_in, 0, 32, st);
+      }));
+      k_owner_link<<<grid_for(n_in, 256, 8 * sms), 256, 0, st>>>(inrec.p, ks.p, vs.p, (uint32_t)n_in, W, reply.p,
+                                                                 nxt.p, flags.p);
+      k_blist<<<gbl, BL_THREADS, 0, st>>>(inrec.p, vs.p, nxt.p, (uint32_t)n_in, W, 0, dcnt.p, nullptr, nullptr, nullptr);
+      KCUDA(ctx, cudaMemcpyAsync(dcnt_h.data(), dcnt.p, 8 * W, cudaMemcpyDeviceToHost, st));
+      KCUDA(ctx, cudaStreamSynchronize(st));
+    }
+    std::vector<uint64_t> base(W, 0);
+    uint64_t tot = 0;
+    for (int dd = 0; dd < W; dd++) { base[dd] = tot; tot += dcnt_h[dd]; }
+    KTRY(blist.alloc(ctx, tot > 0 ? tot : 1));
+    if (tot > 0) {
+      KCUDA(ctx, cudaMemcpyAsync(dbase.p, base.data(), 8 * W, cudaMemcpyHostToDevice, st));
+      k_blist<<<gbl, BL_THREADS, 0, st>>>(inrec.p, vs.p, nxt.p, (uint32_t)n_in, W, 1, nullptr, dbase.p, cursor.p,
+                                          blist.p);
+    }
+  }
+  inrec.release();
+  // answers back to the record senders (same segment sizes, reversed), boundary sets out
+  DBuf<uint32_t> ans, bset;
+  KTRY(ans.alloc(ctx, n_rec > 0 ? n_rec : 1));
+  std::vector<uint64_t> bcnt_all((size_t)W * W), bin(W);
+  KTRY(coll_allgather_host(ctx, dcnt_h.data(), bcnt_all.data(), 8 * W));
+  for (int r = 0; r < W; r++) bin[r] = bcnt_all[(size_t)r * W + me];
+  const std::vector<size_t> bsoff = offsets_of(dcnt_h, 4), broff = offsets_of(bin, 4);
+  const uint64_t n_b = broff[W] / 4;
+  KTRY(bset.alloc(ctx, n_b > 0 ? n_b : 1));
+  {
+    Pass ps(ctx, "F4_exchange", 0, 2);
+    KTRY(coll_alltoallv(ctx, reply.p, offsets_of(recv_cnt, 4), ans.p, offsets_of(send_cnt, 4)));
+    KTRY(coll_alltoallv(ctx, blist.p, bsoff, bset.p, broff));
+  }
+  reply.release();
+  blist.release();
+
+  // ---- global prev, boundary LRU set B_k (bitmap + prefix popcounts), per-access info
+  const uint64_t nw = ((uint64_t)P0 + 31) / 32, nwa = nw > 0 ? nw + 1 : 1;
+  DBuf<uint32_t> bits, pc, pre, prev_c, first_cnt, reuse_cnt;
+  DBuf<uint8_t> run_flag;
+  const int64_t nra = r1 > r0 ? r1 - r0 : 1;
+  KTRY(bits.alloc(ctx, nwa)); KTRY(bits.zero()); KTRY(pc.alloc(ctx, nwa)); KTRY(pre.alloc(ctx, nwa));
+  KTRY(prev_c.alloc(ctx, na)); KTRY(run_flag.alloc(ctx, na));
+  KTRY(first_cnt.alloc(ctx, nra)); KTRY(reuse_cnt.alloc(ctx, nra));
+  KTRY(first_cnt.zero()); KTRY(reuse_cnt.zero());
+  uint32_t Bsize = 0;
+  {
+    Pass ps(ctx, "F4_boundary", 1, 5);
+    if (n > 0) k_prev_global<<<grid_for(n, 256, 8 * sms), 256, 0, st>>>(prev_loc.p, n, P0, tr->prev);
+    if (n_rec > 0) k_apply_replies<<<grid_for(n_rec, 256, 8 * sms), 256, 0, st>>>(rec.p, ans.p, n_rec, P0, tr->prev);
+    if (n_b > 0) k_set_bits<<<grid_for(n_b, 256, 8 * sms), 256, 0, st>>>(bset.p, n_b, P0, bits.p, flags.p + 2);
+    k_popc<<<grid_for(nwa, 256, 8 * sms), 256, 0, st>>>(bits.p, nwa, pc.p);
+    KTRY(cub_run(ctx, tmp, [&](void *t, size_t &b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, pc.p, pre.p, (int64_t)nwa, st);
+    }));
+    uint32_t last[2] = {0, 0};
+    KCUDA(ctx, cudaMemcpyAsync(&last[0], pre.p + nwa - 1, 4, cudaMemcpyDeviceToHost, st));
+    KCUDA(ctx, cudaMemcpyAsync(&last[1], pc.p + nwa - 1, 4, cudaMemcpyDeviceToHost, st));
+    KCUDA(ctx, cudaStreamSynchronize(st));
+    Bsize = last[0] + last[1];
+    if (Bsize != n_b || (uint64_t)Bsize + n >= (1ull << 31)) {
+      const unsigned long long one = 1;
+      KCUDA(ctx, cudaMemcpyAsync(flags.p + 2, &one, 8, cudaMemcpyHostToDevice, st));
+      KCUDA(ctx, cudaStreamSynchronize(st));
+      Bsize = 0;
+    }
+    if (n > 0)
+      k_access_info_shard<<<grid_for(n, 256, 8 * sms), 256, 0, st>>>(
+          n, P0, (uint32_t)r0, tr->prev, tr->req, tr->s, R, tr->arr, tr->hash, bits.p, pre.p, Bsize, tr->delta,
+          prev_c.p, first_cnt.p, reuse_cnt.p, run_flag.p, flags.p);
+  }
+  rec.release(); ans.release(); bset.release(); bits.release(); pc.release(); pre.release(); prev_loc.release();
+
+  // ---- groups, group tables, U, flags (one allreduce)
+  const int K = tr->K, G = K + 1;
+  {
+    Pass ps(ctx, "F4_groups", 0, 0);  // own launches counted inside
+    KTRY(shard_groups(ctx, tr, reuse_cnt.p));
+  }
+  DBuf<unsigned long long> tab;
+  KTRY(tab.alloc(ctx, 2 * G + 3)); KTRY(tab.zero());
+  if (r1 > r0) {
+    k_group_tables<<<grid_for(r1 - r0, 256, 4 * sms), 256, 16 * G, st>>>(r1 - r0, (uint32_t)r0, tr->grp, first_cnt.p,
+                                                                        reuse_cnt.p, tab.p, G);
+    ctx->own_launches++;
+  }
+  KCUDA(ctx, cudaMemcpyAsync(tab.p + 2 * G, flags.p, 24, cudaMemcpyDeviceToDevice, st));
+  KTRY(coll_allreduce_u64(ctx, tab.p, 2 * G + 3));
+  std::vector<unsigned long long> h(2 * G + 3);
+  KCUDA(ctx, cudaMemcpyAsync(h.data(), tab.p, 8 * (2 * G + 3), cudaMemcpyDeviceToHost, st));
+  KCUDA(ctx, cudaStreamSynchronize(st));
+  tr->U_g.resize(G);
+  tr->reuse_g.resize(G);
+  int64_t U = 0;
+  for (int g = 0; g < G; g++) {
+    tr->U_g[g] = (int64_t)h[2 * g];
+    tr->reuse_g[g] = (int64_t)h[2 * g + 1];
+    U += tr->U_g[g];
+  }
+  tr->U = U;
+  if (h[2 * G]) return fail(ctx, KARETO_E_CHAIN, "block hashes are not chain-consistent (R7)");
+  if (h[2 * G + 1]) return fail(ctx, KARETO_E_OVERFLOW, "a reuse interval >= 2^32-1 ms");
+  if (h[2 * G + 2]) return fail(ctx, KARETO_E_OVERFLOW, "time shards: boundary LRU set inconsistent or >= 2^31 positions");
+
+  // ---- a4: K3 on the shard prefixed by its boundary LRU stack
+  KTRY(stack_depth(ctx, n, (uint64_t)Bsize + n, prev_c.p, tr->req, (uint32_t)r0, tr->s + r0, P0, Bsize, run_flag.p,
+                   tr->depth, &tr->n_runs));
+  KTRY(sync(ctx, "load_trace_sharded"));
+  guard.keep = true;
+  *out = tr;
+  return KARETO_OK;
+}
+
+}  // namespace kareto
+
+extern "C" kareto_status kareto_load_trace_sharded(kareto_ctx *ctx, const kareto_trace_desc *desc,
+                                                   kareto_trace **out) {
+  if (!ctx || !desc || !out) return KARETO_E_INVALID;
+  *out = nullptr;
+  ctx->err.clear();
+  cudaSetDevice(ctx->device);
+  kareto_status s = kareto::load_sharded(ctx, desc, out);
+  if (s != KARETO_OK) {
+    cudaStreamSynchronize(ctx->stream);
+    (void)cudaGetLastError();
+  }
+  return s;
+}
+
+extern "C" kareto_status kareto_trace_shard(const kareto_trace *tr, int64_t *req_lo, int64_t *req_hi, int64_t *pos_lo,
+                                            int64_t *pos_hi) {
+  if (!tr) return KARETO_E_INVALID;
+  if (req_lo) *req_lo = tr->req_lo;
+  if (req_hi) *req_hi = tr->req_hi;
+  if (pos_lo) *pos_lo = tr->pos_lo;
+  if (pos_hi) *pos_hi = tr->pos_hi;
+  return KARETO_OK;
+}

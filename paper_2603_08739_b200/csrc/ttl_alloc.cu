@@ -446,6 +446,8 @@ extern "C" kareto_status kareto_ttl_roi(kareto_ctx *ctx, const kareto_trace *tr,
                                         uint64_t *c_roi) {
   if (!ctx) return KARETO_E_INVALID;
   ctx->err.clear();
+  if (tr && tr->sharded)
+    return kareto::fail(ctx, KARETO_E_UNSUPPORTED, "%s needs the whole trace (not a time shard)", "kareto_ttl_roi");
   cudaSetDevice(ctx->device);
   if (!tr || !t_roi) return fail(ctx, KARETO_E_INVALID, "ttl_roi: null argument");
   Curves cv;
@@ -465,6 +467,8 @@ extern "C" kareto_status kareto_ttl_eval(kareto_ctx *ctx, const kareto_trace *tr
                                          uint64_t *hits, uint64_t *cost) {
   if (!ctx) return KARETO_E_INVALID;
   ctx->err.clear();
+  if (tr && tr->sharded)
+    return kareto::fail(ctx, KARETO_E_UNSUPPORTED, "%s needs the whole trace (not a time shard)", "kareto_ttl_eval");
   cudaSetDevice(ctx->device);
   if (!tr || n < 0 || (n > 0 && (!ttl || !hits || !cost))) return fail(ctx, KARETO_E_INVALID, "ttl_eval: bad arguments");
   const int G = tr->K + 1;
@@ -494,6 +498,8 @@ extern "C" kareto_status kareto_ttl_allocate(kareto_ctx *ctx, const kareto_trace
                                              uint32_t *t_roi_out, uint32_t *t_init_out) {
   if (!ctx) return KARETO_E_INVALID;
   ctx->err.clear();
+  if (tr && tr->sharded)
+    return kareto::fail(ctx, KARETO_E_UNSUPPORTED, "%s needs the whole trace (not a time shard)", "kareto_ttl_allocate");
   cudaSetDevice(ctx->device);
   if (!tr || !t_out || !hits_out || !cost_out) return fail(ctx, KARETO_E_INVALID, "ttl_allocate: null argument");
   Curves cv;

@@ -481,6 +481,82 @@ def run_queue(args, K, ctx, tr, rank, spec, lengths):
                           "data": "synthetic", "timing": "host wall clock around the synchronous call"}), flush=True)
 
 
+def run_emulate(args, K, spec, cfg, ttl, model, dev_inputs, top_k, stream, N, U, n_cfg):
+    """Row f4 on one GPU: W loopback ranks (one host thread + CUDA stream each) run the
+    time-sharded step (load_trace_sharded + eval_grid + pareto); the W shards' kernels and the
+    loopback exchanges share the one GPU, so the step time measures the TOTAL device work of the
+    sharded algorithm (its work efficiency against the unsharded step), not multi-GPU speed."""
+    import torch
+    W = args.emulate_ranks
+    arr_d, out_d, off_d, tok_d = dev_inputs
+    ctx1 = K.Context(torch.cuda.current_device(), stream.cuda_stream)
+
+    def step1():
+        t = ctx1.load_trace(arr_d, out_d, off_d, tokens=tok_d, top_k=top_k)
+        _, o = ctx1.eval_grid(t, cfg, model, ttl)
+        ctx1.pareto(o, cfg, spec["prune"])
+        t.free()
+
+    for _ in range(args.warmup):
+        step1()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step1()
+    torch.cuda.synchronize()
+    ms1 = (time.perf_counter() - t0) * 1e3 / args.steps
+
+    group = K.Loopback(W)
+    barrier = threading.Barrier(W)
+    times, err, shard = [0.0] * W, [None] * W, [None] * W
+
+    def body(r):
+        try:
+            torch.cuda.set_device(stream.device)
+            s = torch.cuda.Stream()
+            c = K.Context(torch.cuda.current_device(), s.cuda_stream, loopback=group, rank=r)
+
+            def stepw():
+                t = c.load_trace(arr_d, out_d, off_d, tokens=tok_d, top_k=top_k, time_shard=True)
+                _, o = c.eval_grid(t, cfg, model, ttl)
+                c.pareto(o, cfg, spec["prune"])
+                shard[r] = t.pos_hi - t.pos_lo
+                t.free()
+
+            for _ in range(args.warmup):
+                stepw()
+            barrier.wait()
+            torch.cuda.synchronize()
+            barrier.wait()
+            a = time.perf_counter()
+            for _ in range(args.steps):
+                stepw()
+            torch.cuda.synchronize()
+            barrier.wait()
+            times[r] = (time.perf_counter() - a) * 1e3 / args.steps
+            c.close()
+        except BaseException as e:  # noqa: BLE001
+            err[r] = e
+            barrier.abort()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(W)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    msW = max(times)
+    print(json.dumps({"metric": "time-sharded step, all shards on one GPU (row f4 work efficiency)",
+                      "value": msW, "unit": "ms", "emulated_ranks": W, "unsharded_ms_per_step": ms1,
+                      "work_ratio": msW / ms1, "shard_accesses": shard, "n_accesses": N, "n_unique": U,
+                      "n_configs": n_cfg, "steps": args.steps, "warmup": args.warmup,
+                      "config": {"workload": spec["desc"]}, "data": "synthetic",
+                      "timing": "host wall clock around synchronised steps; the W ranks' kernels and the "
+                                "loopback exchanges (device-to-device copies) share the one GPU"}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -501,6 +577,12 @@ def main():
                     help="row f4 analytics: X6 reuse skew and X5 oracle-TTL footprint of the config's trace")
     ap.add_argument("--ttl", action="store_true",
                     help="row f2: Alg. 2 group-TTL allocation vs the best uniform TTL on the config's trace")
+    ap.add_argument("--time-shard", default="auto", choices=["auto", "on", "off"],
+                    help="row f4: split the trace passes by time across ranks (auto: when world > 1 and the "
+                         "grid is all stack-path configurations)")
+    ap.add_argument("--emulate-ranks", type=int, default=0,
+                    help="row f4 on ONE GPU: W loopback ranks (threads) run the time-sharded step; reports the "
+                         "total device work of all shards against the unsharded step")
     args = ap.parse_args()
     spec = CONFIGS[args.config]
     if args.impl == "reference":
@@ -539,8 +621,8 @@ def main():
         arr_d, out_d, off_d, tok_d = (x.to(f"cuda:{local}", non_blocking=True) for x in (arr_h, out_h, off_h, tok_h))
     stream.synchronize()
 
-    def load_dev():
-        return ctx.load_trace(arr_d, out_d, off_d, tokens=tok_d, top_k=top_k)
+    def load_dev(time_shard=False):
+        return ctx.load_trace(arr_d, out_d, off_d, tokens=tok_d, top_k=top_k, time_shard=time_shard)
 
     if args.search:
         run_search(args, K, ctx, load_dev(), rank, spec, np.diff(off_h.numpy()))
@@ -577,13 +659,24 @@ def main():
         nonuni = (ttl[cfg["tuner"]] != ttl[cfg["tuner"]][:, :1]).any(1)
         n_replay = int(((cfg["policy"] != K.LRU) | ((cfg["cap"][:, 2] != K.INF) & nonuni)).sum())
     model = K.Model()
+    if args.emulate_ranks > 0:
+        tr.free()
+        run_emulate(args, K, spec, cfg, ttl, model, (arr_d, out_d, off_d, tok_d), top_k, stream, N, U, n_cfg)
+        return
+    tshard = args.time_shard == "on" or (args.time_shard == "auto" and world > 1 and n_replay == 0)
+    n_local = N
+    if tshard:  # this rank's slice of the accesses (the units its trace passes process)
+        tr.free()
+        tr = load_dev(True)
+        n_local = tr.pos_hi - tr.pos_lo
+    req_lo, req_hi = tr.req_lo, tr.req_hi
     cnt_d = torch.empty((n_cfg, 11), dtype=torch.int64, device=f"cuda:{local}")
     obj_d = torch.empty((n_cfg, 3), dtype=torch.float64, device=f"cuda:{local}")
     st_d = torch.empty(n_cfg, dtype=torch.uint8, device=f"cuda:{local}")
     tr.free()
 
     def step():
-        t = load_dev()
+        t = load_dev(tshard)
         ctx.eval_grid(t, cfg, model, ttl, counts=cnt_d, obj=obj_d)
         _, nf = ctx.pareto(obj_d, cfg, spec["prune"], status=st_d)
         t.free()
@@ -625,7 +718,7 @@ def main():
     passes = ctx.pass_times(reset=True)
     ctx.set_profiling(False)
     peak, peak_src = measured_peak()
-    units = {"block": N, "access": N}
+    units = {"block": n_local, "access": n_local}
     k6 = [p for p in passes if p["name"].startswith("K6_replay")]
     if k6:  # one roofline entry for the replay (its class passes merged)
         passes = [p for p in passes if not p["name"].startswith("K6_replay")] + [
@@ -665,7 +758,7 @@ def main():
         arr_np, out_np, off_np, tok_np = arr_h.numpy(), out_h.numpy(), off_h.numpy(), tok_h.numpy().view(np.uint32)
 
         def step_host():
-            t_ = ctx.load_trace(arr_np, out_np, off_np, tokens=tok_np, top_k=top_k)
+            t_ = ctx.load_trace(arr_np, out_np, off_np, tokens=tok_np, top_k=top_k, time_shard=tshard)
             ctx.eval_grid(t_, cfg, model, ttl, counts=cnt_h, obj=obj_h)
             s_, _ = ctx.pareto(obj_h, cfg, spec["prune"])
             t_.free()
@@ -685,7 +778,15 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         wall = float(te.item())
-        h2d = arr_np.nbytes + out_np.nbytes + off_np.nbytes + tok_np.nbytes + 2 * cfg.nbytes + 24 * n_cfg
+        # a time-sharded rank copies only the token range covering its requests (as the library does)
+        tok_bytes = tok_np.nbytes
+        if tshard:
+            sel = np.argsort(arr_np, kind="stable")[req_lo:req_hi]
+            o0 = off_np[sel]
+            o1 = o0 + 16 * ((off_np[sel + 1] - o0) // 16)
+            m = o1 > o0
+            tok_bytes = 4 * int(o1[m].max() - o0[m].min()) if m.any() else 0
+        h2d = arr_np.nbytes + out_np.nbytes + off_np.nbytes + tok_bytes + 2 * cfg.nbytes + 24 * n_cfg
         d2h = cnt_h.nbytes + obj_h.nbytes + n_cfg
         e2e = {"value": n_cfg / wall, "unit": "configs/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": wall * 1e3,
@@ -710,7 +811,9 @@ def main():
                 "config": {"workload": spec["desc"], "n_configs": n_cfg, "n_requests": R, "n_accesses": N,
                            "n_unique": U, "tokens_bytes": int(T * 4),
                            "l2": "no flush: per-step inputs (6.8 GB tokens) exceed the 126 MB L2",
-                           "parallelism": f"config-shard x{world} (trace passes replicated)",
+                           "parallelism": (f"time-shard x{world} (trace passes split by time: owner exchange of "
+                                           f"first/last accesses, boundary LRU sets, histogram allreduce)"
+                                           if tshard else f"config-shard x{world} (trace passes replicated)"),
                            "pruning": spec["prune"], "replay_configs": n_replay},
                 "block_accesses_per_s": N / (ms_step * 1e-3),
                 "effective_access_configs_per_s": N * n_cfg / (ms_step * 1e-3),

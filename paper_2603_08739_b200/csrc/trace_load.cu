@@ -309,7 +309,8 @@ constexpr int LINK_SCAN = 32;
 constexpr int LINK_U = 4;
 __global__ void __launch_bounds__(256) k_link_prev(const uint32_t *__restrict__ ks, const uint64_t *__restrict__ vs,
                                                    uint64_t N, unsigned *__restrict__ cursor, uint2 *__restrict__ pairs,
-                                                   uint2 *__restrict__ ovf, uint32_t *__restrict__ n_ovf) {
+                                                   uint2 *__restrict__ ovf, uint32_t *__restrict__ n_ovf,
+                                                   uint8_t *__restrict__ qf, uint8_t *__restrict__ nx) {
   const int lane = threadIdx.x & 31;
   const uint64_t nchunk = (N + 32 * LINK_U - 1) / (32 * LINK_U);
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -335,18 +336,24 @@ __global__ void __launch_bounds__(256) k_link_prev(const uint32_t *__restrict__ 
       }
       p[u] = kNone;
       ovfl[u] = false;
+      uint64_t pred = ~0ull;  // sorted index of the previous occurrence
       if (i < N && kq == k[u]) {
         if ((vq >> 32) == (v[u] >> 32)) {
           p[u] = (uint32_t)vq;
+          pred = i - 1;
         } else {  // fingerprint collision: bounded backward scan of the key run
           uint64_t t = i - 1;
           int steps = 1;
           for (; t > 0 && ks[t - 1] == k[u] && steps < LINK_SCAN; t--, steps++) {
             const uint64_t w = vs[t - 1];
-            if ((w >> 32) == (v[u] >> 32)) { p[u] = (uint32_t)w; break; }
+            if ((w >> 32) == (v[u] >> 32)) { p[u] = (uint32_t)w; pred = t - 1; break; }
           }
           ovfl[u] = p[u] == kNone && steps == LINK_SCAN && t > 0 && ks[t - 1] == k[u];
         }
+      }
+      if (qf && i < N) {  // first-in-range flag (overflow: fixed by k_link_overflow), has-next mark
+        qf[i] = p[u] == kNone ? 1 : 0;
+        if (pred != ~0ull) nx[pred] = 1;
       }
     }
 #pragma unroll
@@ -383,7 +390,8 @@ template <int P>
 __global__ void __launch_bounds__(LT_THREADS, 2) k_link_tile(const uint32_t *__restrict__ ks,
                                                           const uint64_t *__restrict__ vs, uint64_t N, int nbk,
                                                           unsigned *__restrict__ cursor, uint2 *__restrict__ pairs,
-                                                          uint2 *__restrict__ ovf, uint32_t *__restrict__ n_ovf) {
+                                                          uint2 *__restrict__ ovf, uint32_t *__restrict__ n_ovf,
+                                                          uint8_t *__restrict__ qf, uint8_t *__restrict__ nx) {
   typedef cub::BlockScan<uint32_t, LT_THREADS> Scan;
   __shared__ typename Scan::TempStorage scan_ts;
   extern __shared__ __align__(16) uint8_t lt_raw[];
@@ -448,18 +456,24 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_link_tile(const uint32_t *__r
       if (in) {
         uint32_t p = kNone;
         bool ov = false;
+        uint64_t pred = ~0ull;
         if (kq == k) {
           if ((vq >> 32) == (v >> 32)) {
             p = (uint32_t)vq;
+            pred = i - 1;
           } else {  // fingerprint collision: bounded backward scan of the key run
             uint64_t t = i - 1;
             int steps = 1;
             for (; t > 0 && ks[t - 1] == k && steps < LINK_SCAN; t--, steps++) {
               const uint64_t w = vs[t - 1];
-              if ((w >> 32) == (v >> 32)) { p = (uint32_t)w; break; }
+              if ((w >> 32) == (v >> 32)) { p = (uint32_t)w; pred = t - 1; break; }
             }
             ov = p == kNone && steps == LINK_SCAN && t > 0 && ks[t - 1] == k;
           }
+        }
+        if (qf) {
+          qf[i] = p == kNone ? 1 : 0;
+          if (pred != ~0ull) nx[pred] = 1;
         }
         const uint32_t j = (uint32_t)v, bk = j >> P;
         const uint32_t loc = atomicAdd(&cur[bk], 1u);
@@ -486,7 +500,8 @@ __global__ void __launch_bounds__(OVF_THREADS) k_link_overflow(const uint32_t *_
                                                                 const uint64_t *__restrict__ vs,
                                                                 const uint2 *__restrict__ ovf,
                                                                 const uint32_t *__restrict__ n_ovf,
-                                                                uint2 *__restrict__ pairs) {
+                                                                uint2 *__restrict__ pairs, uint8_t *__restrict__ qf,
+                                                                uint8_t *__restrict__ nx) {
   __shared__ unsigned long long best1;  // 1 + best sorted index, 0 = none
   __shared__ int ended;
   const uint32_t n = *n_ovf;
@@ -507,7 +522,10 @@ __global__ void __launch_bounds__(OVF_THREADS) k_link_overflow(const uint32_t *_
       __syncthreads();
       if (stop) break;
     }
-    if (threadIdx.x == 0) pairs[o.y].y = best1 ? (uint32_t)vs[best1 - 1] : kNone;
+    if (threadIdx.x == 0) {
+      pairs[o.y].y = best1 ? (uint32_t)vs[best1 - 1] : kNone;
+      if (qf && best1) { qf[i] = 0; nx[best1 - 1] = 1; }
+    }
     __syncthreads();
   }
 }
@@ -842,6 +860,12 @@ kareto_status link_prev(kareto_ctx *ctx, const uint64_t *hash, uint64_t N, uint3
     }));
   }
   k32.release(); v64.release();
+  uint8_t *qf = nullptr, *nx = nullptr;
+  if (keep) {
+    KTRY(keep->qf.alloc(ctx, N)); KTRY(keep->nx.alloc(ctx, N)); KTRY(keep->nx.zero());
+    qf = keep->qf.p;
+    nx = keep->nx.p;
+  }
   {
     DBuf<uint2> pairs, ovf;
     DBuf<uint32_t> n_ovf;
@@ -860,15 +884,15 @@ kareto_status link_prev(kareto_ctx *ctx, const uint64_t *hash, uint64_t N, uint3
         cudaFuncSetAttribute(k_link_tile<PBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const uint64_t ntile = (N + LT_TILE - 1) / LT_TILE;
         k_link_tile<PBT><<<(unsigned)(ntile < (uint64_t)(2 * sms) ? ntile : 2 * sms), LT_THREADS, smem, st>>>(
-            k32s.p, v64s.p, N, (int)nbk, cursor.p, pairs.p, ovf.p, n_ovf.p);
+            k32s.p, v64s.p, N, (int)nbk, cursor.p, pairs.p, ovf.p, n_ovf.p, qf, nx);
       } else {
         k_link_prev<<<grid_for((N + LINK_U - 1) / LINK_U, 256, 8 * sms), 256, 0, st>>>(
-            k32s.p, v64s.p, N, cursor.p, pairs.p, ovf.p, n_ovf.p);
+            k32s.p, v64s.p, N, cursor.p, pairs.p, ovf.p, n_ovf.p, qf, nx);
       }
     }
     {
       Pass ps(ctx, "K2_link_overflow", 1, 1);
-      k_link_overflow<<<2 * sms, OVF_THREADS, 0, st>>>(k32s.p, v64s.p, ovf.p, n_ovf.p, pairs.p);
+      k_link_overflow<<<2 * sms, OVF_THREADS, 0, st>>>(k32s.p, v64s.p, ovf.p, n_ovf.p, pairs.p, qf, nx);
     }
     if (getenv("KARETO_DEBUG")) {
       uint32_t h = 0;

@@ -48,9 +48,12 @@ kareto_status chain_hash(kareto_ctx *ctx, const kareto_trace_desc *d, const kare
 // a3 (K2 link): prev[i] = largest i' < i with hash[i'] == hash[i] (local indices), kNone if
 // none.  With keep != nullptr the fingerprint-sorted (key, value) arrays are handed back:
 // key = top 32 bits of m = fmix64(h ^ C), value = (low 32 bits of m) << 32 | i.
+// qf[i] = 1 if sorted element i is the first occurrence of its hash in the range, nx[i] = 1 if
+// a later occurrence exists (both in sorted order, produced by the link kernels).
 struct SortedHashes {
   DBuf<uint32_t> key;
   DBuf<uint64_t> val;
+  DBuf<uint8_t> qf, nx;
 };
 kareto_status link_prev(kareto_ctx *ctx, const uint64_t *hash, uint64_t n, uint32_t *prev, SortedHashes *keep);
 

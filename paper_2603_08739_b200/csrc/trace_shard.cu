@@ -70,32 +70,27 @@ __global__ void k_slice_bounds(const uint32_t *__restrict__ s, int64_t R, uint64
   rb[k] = (uint32_t)lo;
 }
 
-__global__ void k_mark_next(const uint32_t *__restrict__ prev_loc, uint64_t n, uint8_t *__restrict__ has_next) {
+// Records per fingerprint-sorted element: Q if it is the first access of its block in the shard,
+// P if the last (flags from the link kernels: qf, nx).  fl bit 0 = Q, bit 1 = P; cnt = popcount.
+__global__ void k_rec_flags(const uint8_t *__restrict__ qf, const uint8_t *__restrict__ nx, uint64_t n,
+                            uint8_t *__restrict__ fl, uint32_t *__restrict__ cnt) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t p = prev_loc[i];
-    if (p != kNone) has_next[p] = 1;
-  }
-}
-
-// records per fingerprint-sorted element: Q if first in the shard, P if last
-__global__ void k_rec_count(const uint64_t *__restrict__ vs, uint64_t n, const uint32_t *__restrict__ prev_loc,
-                            const uint8_t *__restrict__ has_next, uint32_t *__restrict__ cnt) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t j = (uint32_t)vs[i];
-    cnt[i] = (prev_loc[j] == kNone ? 1u : 0u) + (has_next[j] ? 0u : 1u);
+    const uint32_t q = qf[i] ? 1u : 0u, p = nx[i] ? 0u : 1u;
+    fl[i] = (uint8_t)(q | (p << 1));
+    cnt[i] = q + p;
   }
 }
 
 __global__ void k_rec_emit(const uint32_t *__restrict__ ks, const uint64_t *__restrict__ vs, uint64_t n,
-                           const uint32_t *__restrict__ prev_loc, const uint8_t *__restrict__ has_next,
-                           const uint32_t *__restrict__ off, const uint32_t *__restrict__ req,
+                           const uint8_t *__restrict__ fl, const uint32_t *__restrict__ off, const uint32_t *__restrict__ req,
                            const uint32_t *__restrict__ s, const uint64_t *__restrict__ hash, uint32_t P0, int rank,
                            XRec *__restrict__ rec) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t v = vs[i];
     const uint32_t j = (uint32_t)v;
-    const bool q = prev_loc[j] == kNone, p = !has_next[j];
-    if (!q && !p) continue;
+    const uint8_t f = fl[i];
+    if (!f) continue;
+    const bool q = f & 1, p = f & 2;
     XRec x;
     x.m = ((uint64_t)ks[i] << 32) | (v >> 32);
     x.pos = P0 + j;
@@ -232,6 +227,14 @@ __global__ void k_popc(const uint32_t *__restrict__ bits, uint64_t nw, uint32_t 
     pc[i] = __popc(bits[i]);
 }
 
+__device__ __forceinline__ void warp_count_add(uint32_t *arr, uint32_t key, bool pred) {
+  const unsigned active = __activemask();
+  const unsigned pm = __ballot_sync(active, pred);
+  if (!pred) return;
+  const unsigned same = __match_any_sync(pm, key);
+  if ((__ffs(same) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&arr[key], (uint32_t)__popc(same));
+}
+
 // delta, chain check (in-shard links; cross-shard links were checked by the owners), K3 run
 // heads, per-request first/reuse counts, compressed previous positions for K3
 __global__ void k_access_info_shard(uint64_t n, uint32_t P0, uint32_t r0, const uint32_t *__restrict__ prev,
@@ -274,8 +277,8 @@ __global__ void k_access_info_shard(uint64_t n, uint32_t P0, uint32_t r0, const 
       head = (j == s[r] || pm == kNone || p != pm + 1) ? 1 : 0;
     }
     run_flag[i] = head;
-    const uint32_t rl = r - r0;
-    if (p == kNone) atomicAdd(&first_cnt[rl], 1u); else atomicAdd(&reuse_cnt[rl], 1u);
+    warp_count_add(first_cnt, r - r0, p == kNone);
+    warp_count_add(reuse_cnt, r - r0, p != kNone);
   }
   if (fl_chain) atomicAdd(&flags[0], (unsigned long long)fl_chain);
   if (fl_delta) atomicAdd(&flags[1], (unsigned long long)fl_delta);
@@ -534,16 +537,13 @@ static kareto_status load_sharded(kareto_ctx *ctx, const kareto_trace_desc *d, k
   std::vector<uint64_t> send_cnt(W, 0);
   if (n > 0) KTRY(link_prev(ctx, tr->hash, n, prev_loc.p, &sh));
   {
-    Pass ps(ctx, "F4_records", 1, 4);
-    DBuf<uint8_t> has_next;
+    Pass ps(ctx, "F4_records", 1, 3);
+    DBuf<uint8_t> fl;
     DBuf<uint32_t> cnt, off;
-    KTRY(has_next.alloc(ctx, na)); KTRY(has_next.zero());
+    KTRY(fl.alloc(ctx, na));
     KTRY(cnt.alloc(ctx, na + 1)); KTRY(off.alloc(ctx, na + 1));
     KCUDA(ctx, cudaMemsetAsync(cnt.p, 0, 4 * (na + 1), st));
-    if (n > 0) {
-      k_mark_next<<<grid_for(n, 256, 8 * sms), 256, 0, st>>>(prev_loc.p, n, has_next.p);
-      k_rec_count<<<grid_for(n, 256, 8 * sms), 256, 0, st>>>(sh.val.p, n, prev_loc.p, has_next.p, cnt.p);
-    }
+    if (n > 0) k_rec_flags<<<grid_for(n, 256, 8 * sms), 256, 0, st>>>(sh.qf.p, sh.nx.p, n, fl.p, cnt.p);
     KTRY(cub_run(ctx, tmp, [&](void *t, size_t &b) {
       return cub::DeviceScan::ExclusiveSum(t, b, cnt.p, off.p, (int64_t)(n + 1), st);
     }));
@@ -552,8 +552,8 @@ static kareto_status load_sharded(kareto_ctx *ctx, const kareto_trace_desc *d, k
     KTRY(rec.alloc(ctx, n_rec > 0 ? n_rec : 1));
     std::vector<uint32_t> ob(W + 1, 0);
     if (n > 0) {
-      k_rec_emit<<<grid_for(n, 256, 8 * sms), 256, 0, st>>>(sh.key.p, sh.val.p, n, prev_loc.p, has_next.p, off.p,
-                                                            tr->req, tr->s, tr->hash, P0, me, rec.p);
+      k_rec_emit<<<grid_for(n, 256, 8 * sms), 256, 0, st>>>(sh.key.p, sh.val.p, n, fl.p, off.p, tr->req, tr->s,
+                                                            tr->hash, P0, me, rec.p);
       DBuf<uint32_t> dob;
       KTRY(dob.alloc(ctx, W + 1));
       k_owner_bounds<<<1, 256, 0, st>>>(rec.p, n_rec, W, dob.p);
@@ -564,6 +564,8 @@ static kareto_status load_sharded(kareto_ctx *ctx, const kareto_trace_desc *d, k
   }
   sh.key.release();
   sh.val.release();
+  sh.qf.release();
+  sh.nx.release();
   // record counts: cnt_all[src * W + dst]
   std::vector<uint64_t> cnt_all((size_t)W * W);
   KTRY(coll_allgather_host(ctx, send_cnt.data(), cnt_all.data(), 8 * W));
@@ -599,10 +601,13 @@ static kareto_status load_sharded(kareto_ctx *ctx, const kareto_trace_desc *d, k
     KTRY(cursor.zero());
     const unsigned gbl = grid_for((int64_t)((n_in + BL_CHUNK - 1) / BL_CHUNK), 1, 8 * sms);
     if (n_in > 0) {
-      k_rec_keys<<<grid_for(n_in, 256, 8 * sms), 256, 0, st>>>(inrec.p, (uint32_t)n_in, k.p, v.p);
-      KTRY(cub_run(ctx, tmp, [&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, k.p, ks.p, v.p, vs.p, (int64_t)n_in, 0, 32, st);
-      }));
+      // each source's chunk arrives in key order; one chunk (W = 1) needs no sort
+      k_rec_keys<<<grid_for(n_in, 256, 8 * sms), 256, 0, st>>>(inrec.p, (uint32_t)n_in, W > 1 ? k.p : ks.p,
+                                                               W > 1 ? v.p : vs.p);
+      if (W > 1)
+        KTRY(cub_run(ctx, tmp, [&](void *t, size_t &b) {
+          return cub::DeviceRadixSort::SortPairs(t, b, k.p, ks.p, v.p, vs.p, (int64_t)n_in, 0, 32, st);
+        }));
       k_owner_link<<<grid_for(n_in, 256, 8 * sms), 256, 0, st>>>(inrec.p, ks.p, vs.p, (uint32_t)n_in, W, reply.p,
                                                                  nxt.p, flags.p);
       k_blist<<<gbl, BL_THREADS, 0, st>>>(inrec.p, vs.p, nxt.p, (uint32_t)n_in, W, 0, dcnt.p, nullptr, nullptr, nullptr);

@@ -10,18 +10,21 @@
 //   * prev of the first access of a block inside the shard (a "Q" record) is the last access of
 //     that block in an earlier shard (its "P" record).  Every rank sends, for each distinct block
 //     of its shard, a Q record (first access) and a P record (last access) to the OWNER rank of
-//     the block's hash (hash partitioned: all-to-all-v, 24 B per record).  The owner orders the
-//     records of each hash by position, answers each Q with the preceding P (or "globally
-//     first") and checks chain consistency across the boundary (R7); answers go back with a
-//     second all-to-all-v.
+//     the block's hash (hash partitioned: all-to-all-v, 24 B per record, each source's records
+//     in key order).  The owner (one CTA per key bucket, no sort: each source chunk is binary
+//     searched) answers each Q with the P of the latest earlier shard holding the block (or
+//     "globally first"), checking chain consistency across the boundary (R7), and each P with
+//     the next shard holding the block; answers return by a second all-to-all-v.
 //   * depth needs the LRU stack at the shard boundary P0: B_k = {last access before P0 of every
 //     block seen before P0}.  A P record at shard j whose block next appears in shard n (W if
-//     never) belongs to B_k exactly for j < k <= n; the owner sends its position to those ranks
-//     (third all-to-all-v).  Rank k then solves its shard as a standalone trace prefixed by B_k
-//     in position order (virtual accesses of distinct blocks): a previous position p < P0 maps
-//     to its rank in B_k, p >= P0 to |B_k| + p - P0, and K3 runs unchanged on the compressed
-//     coordinates.  Exact: the distinct blocks touched in [p, s_r) of the real trace are those
-//     of B_k at or after p plus those touched in [P0, s_r), as in the virtual trace.
+//     never) belongs to B_k exactly for j < k <= n, so shard j sends rank k > j a bitmap of its
+//     positions with n >= k (ballot-packed, 1 bit per position; third all-to-all-v) and rank k
+//     ORs them into B_k over [0, P0).  Rank k then solves its shard as a standalone trace
+//     prefixed by B_k in position order (virtual accesses of distinct blocks): a previous
+//     position p < P0 maps to its rank in B_k (prefix popcounts), p >= P0 to |B_k| + p - P0,
+//     and K3 runs unchanged on the compressed coordinates.  Exact: the distinct blocks touched
+//     in [p, s_r) of the real trace are those of B_k at or after p plus those touched in
+//     [P0, s_r), as in the virtual trace.
 //   * groups (R23) need the global reuse of every prefix subtree: per-rank (root hash, reuse)
 //     tables are all-gathered and reduced identically on every rank.
 //   * U, U_g, reuse_g and the error flags: one allreduce.
@@ -115,89 +118,121 @@ __global__ void k_owner_bounds(const XRec *__restrict__ rec, uint32_t n, int W, 
   ob[o] = lo;
 }
 
-__global__ void k_rec_keys(const XRec *__restrict__ in, uint32_t n, uint32_t *__restrict__ key, uint32_t *__restrict__ idx) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    key[i] = (uint32_t)(in[i].m >> 32);
-    idx[i] = i;
-  }
-}
+// Owner (one CTA per key bucket).  The records of source rank c arrive as chunk c, sorted by
+// key (then position); a bucket's records of chunk c are a contiguous subrange found by binary
+// search, and every record of one block lies in one bucket.  Q record of chunk c: answer with
+// the P record of the same block in the LATEST chunk c' < c holding it (or kNone = globally
+// first access), checking chain consistency (R7) across the boundary; P record: answer with
+// the EARLIEST later chunk holding the block (W if none).  No sort: each chunk is searched.
+constexpr int OWN_THREADS = 256;
 
-// Owner: records sorted by key32 (stable => position order within a hash, Q before P of the
-// same shard).  Q: answer with the preceding record of the same hash (a P of an earlier shard)
-// or kNone; P: the shard of the following record of the same hash (W if none).
-__global__ void k_owner_link(const XRec *__restrict__ in, const uint32_t *__restrict__ ks,
-                             const uint32_t *__restrict__ vs, uint32_t n, int W, uint32_t *__restrict__ reply,
-                             uint8_t *__restrict__ nxt, unsigned long long *__restrict__ flags) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint32_t key = ks[i];
-    const XRec x = in[vs[i]];
+// A bucket's records are staged in shared memory (chunk after chunk) when they fit; the
+// searches then run on shared memory.  Larger buckets (never seen with uniform keys; possible
+// only for adversarial hashes) search global memory.
+constexpr int OWN_STAGE = 1536;  // records (36 KB)
+template <bool SMEM>
+__device__ __forceinline__ void owner_bucket(const XRec *__restrict__ g, const XRec *__restrict__ sm,
+                                             const uint32_t *lo, const uint32_t *hi, const uint32_t *pre, int W,
+                                             uint32_t *__restrict__ reply, unsigned &bad) {
+  // record t of the bucket (chunk c): global index lo[c] + (t - pre[c]); staged index t
+  const uint32_t tot = pre[W];
+  auto rec_at = [&](int c, uint32_t t) -> const XRec & { return SMEM ? sm[t] : g[lo[c] + (t - pre[c])]; };
+  auto key_at = [&](int c, uint32_t t) -> uint32_t { return (uint32_t)(rec_at(c, t).m >> 32); };
+  auto lb = [&](int c, uint32_t key) -> uint32_t {  // first staged index of chunk c with key >= key
+    uint32_t a = pre[c], b = pre[c + 1];
+    while (a < b) {
+      uint32_t m = (a + b) >> 1;
+      if (key_at(c, m) < key) a = m + 1; else b = m;
+    }
+    return a;
+  };
+  for (uint32_t t = threadIdx.x; t < tot; t += blockDim.x) {
+    int c = 0;
+    while (pre[c + 1] <= t) c++;
+    const XRec x = rec_at(c, t);
+    const uint32_t key = (uint32_t)(x.m >> 32);
+    uint32_t ans;
     if (!(x.info & kRecP)) {
-      uint32_t ans = kNone;
-      for (uint32_t t = i; t > 0 && ks[t - 1] == key; t--) {
-        const XRec y = in[vs[t - 1]];
-        if (y.m != x.m) continue;
-        ans = y.pos;
-        const uint32_t kq = x.info & kChainPosMask, kp = y.info & kChainPosMask;
-        if (!(y.info & kRecP) || kq != kp || (kq > 0 && y.parent != x.parent)) atomicAdd(&flags[0], 1ull);
-        break;
+      ans = kNone;
+      for (int c2 = c - 1; c2 >= 0 && ans == kNone; c2--) {
+        for (uint32_t u = lb(c2, key); u < pre[c2 + 1] && key_at(c2, u) == key; u++) {
+          const XRec &y = rec_at(c2, u);
+          if (y.m != x.m || !(y.info & kRecP)) continue;
+          ans = y.pos;
+          const uint32_t kq = x.info & kChainPosMask, kp = y.info & kChainPosMask;
+          if (kq != kp || (kq > 0 && y.parent != x.parent)) bad++;
+          break;
+        }
       }
-      reply[vs[i]] = ans;
-      nxt[i] = 0;
     } else {
-      uint32_t nx = (uint32_t)W;
-      for (uint32_t t = i + 1; t < n && ks[t] == key; t++) {
-        const XRec y = in[vs[t]];
-        if (y.m == x.m) { nx = (y.info >> 24) & 0x7F; break; }
-      }
-      reply[vs[i]] = kNone;
-      nxt[i] = (uint8_t)nx;
+      ans = (uint32_t)W;
+      for (int c2 = c + 1; c2 < W && ans == (uint32_t)W; c2++)
+        for (uint32_t u = lb(c2, key); u < pre[c2 + 1] && key_at(c2, u) == key; u++)
+          if (rec_at(c2, u).m == x.m) { ans = (uint32_t)c2; break; }
     }
+    reply[lo[c] + (t - pre[c])] = ans;
   }
 }
 
-// boundary-set lists: a P record of shard j with next shard nx belongs to B_d for j < d <= nx,
-// d < W.  count: per-destination totals; fill: positions grouped by destination (any order
-// inside a destination: B_d is a set).  Chunks of 4096 sorted records per block iteration.
-constexpr int BL_THREADS = 256, BL_CHUNK = 4096;
-__global__ void __launch_bounds__(BL_THREADS) k_blist(const XRec *__restrict__ in, const uint32_t *__restrict__ vs,
-                                                      const uint8_t *__restrict__ nxt, uint32_t n, int W, int fill,
-                                                      unsigned long long *__restrict__ dcnt,
-                                                      const unsigned long long *__restrict__ dbase,
-                                                      unsigned long long *__restrict__ cursor, uint32_t *__restrict__ out) {
-  __shared__ uint32_t c[kMaxShardWorld];
-  __shared__ unsigned long long b[kMaxShardWorld];
-  for (uint64_t c0 = (uint64_t)blockIdx.x * BL_CHUNK; c0 < n; c0 += (uint64_t)gridDim.x * BL_CHUNK) {
-    const uint32_t c1 = (uint32_t)(c0 + BL_CHUNK < n ? c0 + BL_CHUNK : n);
-    for (int d = threadIdx.x; d < W; d += blockDim.x) c[d] = 0;
-    __syncthreads();
-    for (uint32_t i = (uint32_t)c0 + threadIdx.x; i < c1; i += blockDim.x) {
-      const XRec x = in[vs[i]];
-      if (!(x.info & kRecP)) continue;
-      const int j = (x.info >> 24) & 0x7F, nx = nxt[i];
-      const int dend = nx < W - 1 ? nx : W - 1;
-      for (int d = j + 1; d <= dend; d++) atomicAdd(&c[d], 1u);
+// bucket of an owned key: (key - klo) >> shift (buckets of 2^shift consecutive keys)
+__device__ __forceinline__ uint32_t bucket_of(uint32_t klo, int shift, uint32_t key) { return (key - klo) >> shift; }
+// bnd[c * (B + 1) + b] = first record of chunk c in bucket >= b (one pass over the records:
+// each record writes the boundaries between its predecessor's bucket and its own)
+__global__ void k_bucket_bounds(const XRec *__restrict__ in, const uint64_t *__restrict__ co, int W, uint32_t klo,
+                                int shift, uint32_t B, uint32_t n, uint32_t *__restrict__ bnd) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int c = 0;
+    while (co[c + 1] <= i) c++;
+    const bool first = i == (uint32_t)co[c], last = i + 1 == (uint32_t)co[c + 1];
+    const uint32_t b = bucket_of(klo, shift, (uint32_t)(in[i].m >> 32));
+    const int64_t bp = first ? -1 : (int64_t)bucket_of(klo, shift, (uint32_t)(in[i - 1].m >> 32));
+    uint32_t *row = bnd + (size_t)c * (B + 1);
+    for (int64_t x = bp + 1; x <= (int64_t)b; x++) row[x] = i;
+    if (last)
+      for (uint32_t x = b + 1; x <= B; x++) row[x] = i + 1;
+  }
+}
+// chunks without records: every boundary at the chunk start
+__global__ void k_bucket_bounds_empty(const uint64_t *__restrict__ co, int W, uint32_t B, uint32_t *__restrict__ bnd) {
+  for (int c = 0; c < W; c++) {
+    if (co[c + 1] != co[c]) continue;
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x <= B; x += gridDim.x * blockDim.x)
+      bnd[(size_t)c * (B + 1) + x] = (uint32_t)co[c];
+  }
+}
+
+__global__ void __launch_bounds__(OWN_THREADS) k_owner(const XRec *__restrict__ in, const uint32_t *__restrict__ bnd,
+                                                       int W, uint32_t B, uint32_t *__restrict__ reply,
+                                                       unsigned long long *__restrict__ flags) {
+  __shared__ uint32_t lo[kMaxShardWorld], hi[kMaxShardWorld], pre[kMaxShardWorld + 1];
+  __shared__ XRec stage[OWN_STAGE];
+  unsigned bad = 0;
+  for (uint32_t b = blockIdx.x; b < B; b += gridDim.x) {
+    for (int c = threadIdx.x; c < W; c += blockDim.x) {
+      lo[c] = bnd[(size_t)c * (B + 1) + b];
+      hi[c] = bnd[(size_t)c * (B + 1) + b + 1];
     }
     __syncthreads();
-    if (!fill) {
-      for (int d = threadIdx.x; d < W; d += blockDim.x)
-        if (c[d]) atomicAdd(&dcnt[d], (unsigned long long)c[d]);
+    if (threadIdx.x == 0) {
+      pre[0] = 0;
+      for (int c = 0; c < W; c++) pre[c + 1] = pre[c] + (hi[c] - lo[c]);
+    }
+    __syncthreads();
+    const uint32_t tot = pre[W];
+    if (tot <= (uint32_t)OWN_STAGE) {
+      for (uint32_t t = threadIdx.x; t < tot; t += blockDim.x) {
+        int c = 0;
+        while (pre[c + 1] <= t) c++;
+        stage[t] = in[lo[c] + (t - pre[c])];
+      }
       __syncthreads();
-      continue;
-    }
-    for (int d = threadIdx.x; d < W; d += blockDim.x) {
-      b[d] = c[d] ? dbase[d] + atomicAdd(&cursor[d], (unsigned long long)c[d]) : 0ull;
-      c[d] = 0;
-    }
-    __syncthreads();
-    for (uint32_t i = (uint32_t)c0 + threadIdx.x; i < c1; i += blockDim.x) {
-      const XRec x = in[vs[i]];
-      if (!(x.info & kRecP)) continue;
-      const int j = (x.info >> 24) & 0x7F, nx = nxt[i];
-      const int dend = nx < W - 1 ? nx : W - 1;
-      for (int d = j + 1; d <= dend; d++) out[b[d] + atomicAdd(&c[d], 1u)] = x.pos;
+      owner_bucket<true>(in, stage, lo, hi, pre, W, reply, bad);
+    } else {
+      owner_bucket<false>(in, stage, lo, hi, pre, W, reply, bad);
     }
     __syncthreads();
   }
+  if (bad) atomicAdd(&flags[0], (unsigned long long)bad);
 }
 
 // prev in global positions: in-shard links + the owners' answers for the Q records
@@ -207,21 +242,37 @@ __global__ void k_prev_global(const uint32_t *__restrict__ prev_loc, uint64_t n,
     prev[i] = p == kNone ? kNone : P0 + p;
   }
 }
+// Q answers -> prev; P answers -> nxs[local position] = the next shard holding the block
 __global__ void k_apply_replies(const XRec *__restrict__ rec, const uint32_t *__restrict__ reply, uint32_t n,
-                                uint32_t P0, uint32_t *__restrict__ prev) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    if (!(rec[i].info & kRecP)) prev[rec[i].pos - P0] = reply[i];
-}
-
-__global__ void k_set_bits(const uint32_t *__restrict__ pos, uint64_t n, uint32_t P0, uint32_t *__restrict__ bits,
-                           unsigned long long *__restrict__ bad) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t p = pos[i];
-    if (p >= P0) { atomicAdd(bad, 1ull); continue; }
-    uint32_t old = atomicOr(&bits[p >> 5], 1u << (p & 31));
-    if (old & (1u << (p & 31))) atomicAdd(bad, 1ull);  // duplicate: B_k is a set
+                                uint32_t P0, uint32_t *__restrict__ prev, uint8_t *__restrict__ nxs) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const XRec x = rec[i];
+    if (!(x.info & kRecP)) prev[x.pos - P0] = reply[i];
+    else nxs[x.pos - P0] = (uint8_t)reply[i];
   }
 }
+
+// Boundary-set bitmap this shard contributes to rank k (> this rank): bit p set iff p is the
+// last access of its block in this shard and the block next appears in shard k or later (or
+// never), i.e. p in B_k.  Words are aligned to global positions: word w covers [32w, 32w+32).
+__global__ void k_bset_words(const uint8_t *__restrict__ nxs, uint32_t P0, uint32_t P1, uint32_t w0, uint32_t nwords,
+                             int k, uint32_t *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < (uint64_t)nwords * 32;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = (w0 << 5) + (uint32_t)t;  // one position per thread, a warp per word
+    const bool set = p >= P0 && p < P1 && nxs[p - P0] >= (uint8_t)k;
+    const unsigned w = __ballot_sync(0xFFFFFFFFu, set);
+    if (lane == 0) out[t >> 5] = w;
+  }
+}
+// OR a received word segment into the bitmap (neighbouring shards share a boundary word)
+__global__ void k_or_words(const uint32_t *__restrict__ seg, uint32_t w0, uint32_t n, uint32_t nbits_words,
+                           uint32_t *__restrict__ bits) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (w0 + i < nbits_words && seg[i]) atomicOr(&bits[w0 + i], seg[i]);
+}
+
 __global__ void k_popc(const uint32_t *__restrict__ bits, uint64_t nw, uint32_t *__restrict__ pc) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nw; i += (uint64_t)gridDim.x * blockDim.x)
     pc[i] = __popc(bits[i]);
@@ -581,82 +632,94 @@ static kareto_status load_sharded(kareto_ctx *ctx, const kareto_trace_desc *d, k
     KTRY(coll_alltoallv(ctx, rec.p, soff, inrec.p, roff));
   }
 
-  // ---- owner: order each hash's records by position, answer Q's, next shard of P's
+  // ---- owner: answer each Q with the previous shard's P, each P with the next shard
   // [0] chain violations, [1] reuse intervals >= 2^32-1 ms, [2] internal inconsistencies; all
   // ranks learn them from one allreduce and fail together (no rank may leave a collective early)
   DBuf<unsigned long long> flags;
   KTRY(flags.alloc(ctx, 3)); KTRY(flags.zero());
-  DBuf<uint32_t> reply, blist;
-  std::vector<uint64_t> dcnt_h(W, 0);
+  DBuf<uint32_t> reply;
   KTRY(reply.alloc(ctx, n_in > 0 ? n_in : 1));
-  {
-    Pass ps(ctx, "F4_owner", 1, 4);
-    DBuf<uint32_t> k, ks, v, vs;
-    DBuf<uint8_t> nxt;
-    const uint64_t nia = n_in > 0 ? n_in : 1;
-    KTRY(k.alloc(ctx, nia)); KTRY(ks.alloc(ctx, nia)); KTRY(v.alloc(ctx, nia)); KTRY(vs.alloc(ctx, nia));
-    KTRY(nxt.alloc(ctx, nia));
-    DBuf<unsigned long long> dcnt, dbase, cursor;
-    KTRY(dcnt.alloc(ctx, W)); KTRY(dcnt.zero()); KTRY(dbase.alloc(ctx, W)); KTRY(cursor.alloc(ctx, W));
-    KTRY(cursor.zero());
-    const unsigned gbl = grid_for((int64_t)((n_in + BL_CHUNK - 1) / BL_CHUNK), 1, 8 * sms);
-    if (n_in > 0) {
-      // each source's chunk arrives in key order; one chunk (W = 1) needs no sort
-      k_rec_keys<<<grid_for(n_in, 256, 8 * sms), 256, 0, st>>>(inrec.p, (uint32_t)n_in, W > 1 ? k.p : ks.p,
-                                                               W > 1 ? v.p : vs.p);
-      if (W > 1)
-        KTRY(cub_run(ctx, tmp, [&](void *t, size_t &b) {
-          return cub::DeviceRadixSort::SortPairs(t, b, k.p, ks.p, v.p, vs.p, (int64_t)n_in, 0, 32, st);
-        }));
-      k_owner_link<<<grid_for(n_in, 256, 8 * sms), 256, 0, st>>>(inrec.p, ks.p, vs.p, (uint32_t)n_in, W, reply.p,
-                                                                 nxt.p, flags.p);
-      k_blist<<<gbl, BL_THREADS, 0, st>>>(inrec.p, vs.p, nxt.p, (uint32_t)n_in, W, 0, dcnt.p, nullptr, nullptr, nullptr);
-      KCUDA(ctx, cudaMemcpyAsync(dcnt_h.data(), dcnt.p, 8 * W, cudaMemcpyDeviceToHost, st));
-      KCUDA(ctx, cudaStreamSynchronize(st));
-    }
-    std::vector<uint64_t> base(W, 0);
-    uint64_t tot = 0;
-    for (int dd = 0; dd < W; dd++) { base[dd] = tot; tot += dcnt_h[dd]; }
-    KTRY(blist.alloc(ctx, tot > 0 ? tot : 1));
-    if (tot > 0) {
-      KCUDA(ctx, cudaMemcpyAsync(dbase.p, base.data(), 8 * W, cudaMemcpyHostToDevice, st));
-      k_blist<<<gbl, BL_THREADS, 0, st>>>(inrec.p, vs.p, nxt.p, (uint32_t)n_in, W, 1, nullptr, dbase.p, cursor.p,
-                                          blist.p);
-    }
+  if (n_in > 0) {
+    Pass ps(ctx, "F4_owner", 1, 3);
+    std::vector<uint64_t> co(W + 1, 0);
+    for (int r = 0; r < W; r++) co[r + 1] = co[r] + recv_cnt[r];
+    DBuf<uint64_t> dco;
+    KTRY(dco.alloc(ctx, W + 1));
+    KCUDA(ctx, cudaMemcpyAsync(dco.p, co.data(), 8 * (W + 1), cudaMemcpyHostToDevice, st));
+    // keys owned by this rank: {key : owner_of(key) = me} = [ceil(me 2^32 / W), ceil((me+1) 2^32 / W))
+    const uint64_t klo = (((uint64_t)me << 32) + W - 1) / W, khi = (((uint64_t)(me + 1) << 32) + W - 1) / W;
+    // buckets of 2^shift consecutive keys, ~256-512 records each
+    uint32_t Bt = 1;
+    while (Bt < (1u << 22) && (uint64_t)Bt * 512 < n_in) Bt <<= 1;
+    int shift = 0;
+    while (shift < 32 && ((khi - klo + (1ull << shift) - 1) >> shift) > Bt) shift++;
+    const uint32_t B = (uint32_t)((khi - klo + (1ull << shift) - 1) >> shift);
+    const unsigned g = B < (uint32_t)(64 * sms) ? B : (unsigned)(64 * sms);
+    DBuf<uint32_t> bnd;
+    KTRY(bnd.alloc(ctx, (size_t)W * (B + 1)));
+    k_bucket_bounds_empty<<<grid_for(B + 1, 256, 4 * sms), 256, 0, st>>>(dco.p, W, B, bnd.p);
+    k_bucket_bounds<<<grid_for(n_in, 256, 8 * sms), 256, 0, st>>>(inrec.p, dco.p, W, (uint32_t)klo, shift, B,
+                                                                   (uint32_t)n_in, bnd.p);
+    k_owner<<<g, OWN_THREADS, 0, st>>>(inrec.p, bnd.p, W, B, reply.p, flags.p);
   }
   inrec.release();
-  // answers back to the record senders (same segment sizes, reversed), boundary sets out
-  DBuf<uint32_t> ans, bset;
+  // answers back to the record senders (same segment sizes, reversed)
+  DBuf<uint32_t> ans;
   KTRY(ans.alloc(ctx, n_rec > 0 ? n_rec : 1));
-  std::vector<uint64_t> bcnt_all((size_t)W * W), bin(W);
-  KTRY(coll_allgather_host(ctx, dcnt_h.data(), bcnt_all.data(), 8 * W));
-  for (int r = 0; r < W; r++) bin[r] = bcnt_all[(size_t)r * W + me];
-  const std::vector<size_t> bsoff = offsets_of(dcnt_h, 4), broff = offsets_of(bin, 4);
-  const uint64_t n_b = broff[W] / 4;
-  KTRY(bset.alloc(ctx, n_b > 0 ? n_b : 1));
   {
-    Pass ps(ctx, "F4_exchange", 0, 2);
+    Pass ps(ctx, "F4_exchange", 0, 1);
     KTRY(coll_alltoallv(ctx, reply.p, offsets_of(recv_cnt, 4), ans.p, offsets_of(send_cnt, 4)));
-    KTRY(coll_alltoallv(ctx, blist.p, bsoff, bset.p, broff));
   }
   reply.release();
-  blist.release();
 
-  // ---- global prev, boundary LRU set B_k (bitmap + prefix popcounts), per-access info
+  // ---- global prev; boundary LRU sets: this shard's contribution to every later rank as a
+  // bitmap over its positions, exchanged, OR-assembled into B_k over [0, P0)
   const uint64_t nw = ((uint64_t)P0 + 31) / 32, nwa = nw > 0 ? nw + 1 : 1;
   DBuf<uint32_t> bits, pc, pre, prev_c, first_cnt, reuse_cnt;
-  DBuf<uint8_t> run_flag;
+  DBuf<uint8_t> run_flag, nxs;
   const int64_t nra = r1 > r0 ? r1 - r0 : 1;
   KTRY(bits.alloc(ctx, nwa)); KTRY(bits.zero()); KTRY(pc.alloc(ctx, nwa)); KTRY(pre.alloc(ctx, nwa));
-  KTRY(prev_c.alloc(ctx, na)); KTRY(run_flag.alloc(ctx, na));
+  KTRY(prev_c.alloc(ctx, na)); KTRY(run_flag.alloc(ctx, na)); KTRY(nxs.alloc(ctx, na)); KTRY(nxs.zero());
   KTRY(first_cnt.alloc(ctx, nra)); KTRY(reuse_cnt.alloc(ctx, nra));
   KTRY(first_cnt.zero()); KTRY(reuse_cnt.zero());
+  auto wrange = [&](int j, uint32_t &w0, uint32_t &nwj) {  // word range of shard j's positions
+    w0 = sb[j] >> 5;
+    nwj = sb[j + 1] > sb[j] ? ((sb[j + 1] + 31) >> 5) - w0 : 0;
+  };
+  uint32_t mw0, mnw;
+  wrange(me, mw0, mnw);
+  std::vector<size_t> bso(W + 1, 0), bro(W + 1, 0);
+  for (int k = 0; k < W; k++) {
+    uint32_t w0, nwj;
+    bso[k + 1] = bso[k] + (k > me ? 4 * (size_t)mnw : 0);
+    wrange(k, w0, nwj);
+    bro[k + 1] = bro[k] + (k < me ? 4 * (size_t)nwj : 0);
+  }
+  DBuf<uint32_t> bsend, brecv;
+  KTRY(bsend.alloc(ctx, bso[W] / 4 + 1)); KTRY(brecv.alloc(ctx, bro[W] / 4 + 1));
+  {
+    Pass ps(ctx, "F4_boundary_sets", 1, 1 + (W - 1 - me));
+    if (n > 0) k_prev_global<<<grid_for(n, 256, 8 * sms), 256, 0, st>>>(prev_loc.p, n, P0, tr->prev);
+    if (n_rec > 0)
+      k_apply_replies<<<grid_for(n_rec, 256, 8 * sms), 256, 0, st>>>(rec.p, ans.p, n_rec, P0, tr->prev, nxs.p);
+    for (int k = me + 1; k < W && mnw > 0; k++)
+      k_bset_words<<<grid_for(32ll * mnw, 256, 8 * sms), 256, 0, st>>>(nxs.p, P0, P1, mw0, mnw, k,
+                                                                       bsend.p + bso[k] / 4);
+  }
+  {
+    Pass ps(ctx, "F4_exchange", 0, 1);
+    KTRY(coll_alltoallv(ctx, bsend.p, bso, brecv.p, bro));
+  }
+  bsend.release();
   uint32_t Bsize = 0;
   {
-    Pass ps(ctx, "F4_boundary", 1, 5);
-    if (n > 0) k_prev_global<<<grid_for(n, 256, 8 * sms), 256, 0, st>>>(prev_loc.p, n, P0, tr->prev);
-    if (n_rec > 0) k_apply_replies<<<grid_for(n_rec, 256, 8 * sms), 256, 0, st>>>(rec.p, ans.p, n_rec, P0, tr->prev);
-    if (n_b > 0) k_set_bits<<<grid_for(n_b, 256, 8 * sms), 256, 0, st>>>(bset.p, n_b, P0, bits.p, flags.p + 2);
+    Pass ps(ctx, "F4_boundary", 1, 3);
+    for (int j = 0; j < me; j++) {
+      uint32_t w0, nwj;
+      wrange(j, w0, nwj);
+      if (nwj) k_or_words<<<grid_for(nwj, 256, 8 * sms), 256, 0, st>>>(brecv.p + bro[j] / 4, w0, nwj, (uint32_t)nwa,
+                                                                         bits.p);
+    }
     k_popc<<<grid_for(nwa, 256, 8 * sms), 256, 0, st>>>(bits.p, nwa, pc.p);
     KTRY(cub_run(ctx, tmp, [&](void *t, size_t &b) {
       return cub::DeviceScan::ExclusiveSum(t, b, pc.p, pre.p, (int64_t)nwa, st);
@@ -666,7 +729,7 @@ static kareto_status load_sharded(kareto_ctx *ctx, const kareto_trace_desc *d, k
     KCUDA(ctx, cudaMemcpyAsync(&last[1], pc.p + nwa - 1, 4, cudaMemcpyDeviceToHost, st));
     KCUDA(ctx, cudaStreamSynchronize(st));
     Bsize = last[0] + last[1];
-    if (Bsize != n_b || (uint64_t)Bsize + n >= (1ull << 31)) {
+    if ((uint64_t)Bsize + n >= (1ull << 31)) {
       const unsigned long long one = 1;
       KCUDA(ctx, cudaMemcpyAsync(flags.p + 2, &one, 8, cudaMemcpyHostToDevice, st));
       KCUDA(ctx, cudaStreamSynchronize(st));
@@ -677,7 +740,8 @@ static kareto_status load_sharded(kareto_ctx *ctx, const kareto_trace_desc *d, k
           n, P0, (uint32_t)r0, tr->prev, tr->req, tr->s, R, tr->arr, tr->hash, bits.p, pre.p, Bsize, tr->delta,
           prev_c.p, first_cnt.p, reuse_cnt.p, run_flag.p, flags.p);
   }
-  rec.release(); ans.release(); bset.release(); bits.release(); pc.release(); pre.release(); prev_loc.release();
+  rec.release(); ans.release(); brecv.release(); nxs.release(); bits.release(); pc.release(); pre.release();
+  prev_loc.release();
 
   // ---- groups, group tables, U, flags (one allreduce)
   const int K = tr->K, G = K + 1;

@@ -308,6 +308,14 @@ kareto_status kareto_eval_queue(kareto_ctx *ctx, const kareto_trace *tr, const k
  * Errors: as kareto_load_trace, plus KARETO_E_UNSUPPORTED (W > 128, requests of >= 2^24
  * blocks), _E_NCCL.  World 1: a whole trace computed by the sharded path. */
 kareto_status kareto_load_trace_sharded(kareto_ctx *ctx, const kareto_trace_desc *desc, kareto_trace **out);
+/* Host-only helpers (no device work) exposing the two partition rules of the time-sharded load:
+ * req_bounds[k] (k = 0..world) = first sorted request whose first block position s[r] is >= k N / W
+ * (N = s[R]), req_bounds[world] = R -- rank k keeps requests [req_bounds[k], req_bounds[k+1]);
+ * s: host [R+1] block starts in sorted request order (kareto_trace_export KARETO_X_START).
+ * kareto_hash_owner: the rank that owns a block hash in the exchange (top 32 bits of
+ * fmix64(hash ^ 0x6A09E667F3BCC909) scaled to [0, world)); -1 if world < 1. */
+kareto_status kareto_time_slices(const uint32_t *s, int64_t R, int32_t world, int64_t *req_bounds);
+int32_t kareto_hash_owner(uint64_t block_hash, int32_t world);
 /* The shard of a trace: sorted requests [*req_lo, *req_hi), positions [*pos_lo, *pos_hi)
  * (a whole trace: [0, R), [0, N)).  Any output may be NULL. */
 kareto_status kareto_trace_shard(const kareto_trace *tr, int64_t *req_lo, int64_t *req_hi, int64_t *pos_lo,

@@ -115,7 +115,8 @@ ABI_FUNCTIONS = ["kareto_create", "kareto_destroy", "kareto_last_error", "kareto
                  "kareto_launch_counter", "kareto_shard_range", "kareto_hypervolume", "kareto_search",
                  "kareto_ttl_roi", "kareto_ttl_eval", "kareto_ttl_allocate", "kareto_trace_analytics",
                  "kareto_eval_queue", "kareto_loopback_create", "kareto_loopback_destroy", "kareto_loopback_world",
-                 "kareto_create_loopback", "kareto_load_trace_sharded", "kareto_trace_shard"]
+                 "kareto_create_loopback", "kareto_load_trace_sharded", "kareto_trace_shard", "kareto_time_slices",
+                 "kareto_hash_owner"]
 
 
 def load_library(path: str = LIB_PATH):
@@ -161,6 +162,9 @@ def load_library(path: str = LIB_PATH):
     L.kareto_loopback_world.restype = i32
     L.kareto_create_loopback.argtypes = [ctypes.c_int, vp, vp, ctypes.c_int, ctypes.POINTER(vp)]
     L.kareto_load_trace_sharded.argtypes = [vp, ctypes.POINTER(TraceDesc), ctypes.POINTER(vp)]
+    L.kareto_time_slices.argtypes = [vp, i64, i32, vp]
+    L.kareto_hash_owner.argtypes = [ctypes.c_uint64, i32]
+    L.kareto_hash_owner.restype = i32
     L.kareto_trace_shard.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64),
                                      ctypes.POINTER(i64)]
     _lib = L
@@ -517,6 +521,22 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     if st != OK:
         raise KaretoError(st, "shard_range")
     return int(lo.value), int(hi.value)
+
+
+def time_slices(s, world: int) -> np.ndarray:
+    """Host-only: request bounds [world + 1] of the time-sharded load (kareto_time_slices)."""
+    L = load_library()
+    s = np.ascontiguousarray(s, np.uint32)
+    out = np.zeros(world + 1, np.int64)
+    st = L.kareto_time_slices(s.ctypes.data, len(s) - 1, world, out.ctypes.data)
+    if st != OK:
+        raise KaretoError(st, "time_slices")
+    return out
+
+
+def hash_owner(block_hash: int, world: int) -> int:
+    """Host-only: the rank owning a block hash in the time-sharded exchange (kareto_hash_owner)."""
+    return int(load_library().kareto_hash_owner(int(block_hash), world))
 
 
 def load_trace(ctx: Context, *a, **k) -> Trace:

@@ -59,18 +59,20 @@ static kareto_status cub_run(kareto_ctx *ctx, DBuf<uint8_t> &tmp, F &&f) {
   return KARETO_OK;
 }
 
-// r_k = first request with s[r] >= k N / W (k = 0..W-1), r_W = R
-__global__ void k_slice_bounds(const uint32_t *__restrict__ s, int64_t R, uint64_t N, int W, uint32_t *__restrict__ rb) {
-  int k = threadIdx.x;
-  if (k > W) return;
-  if (k == W) { rb[k] = (uint32_t)R; return; }
+// r_k = first request with s[r] >= k N / W (k = 0..W-1), r_W = R (host and device)
+__host__ __device__ inline uint32_t slice_bound(const uint32_t *s, int64_t R, uint64_t N, int W, int k) {
+  if (k >= W) return (uint32_t)R;
   uint64_t target = (N * (uint64_t)k) / (uint64_t)W;
   int64_t lo = 0, hi = R;
   while (lo < hi) {
     int64_t m = (lo + hi) >> 1;
     if ((uint64_t)s[m] >= target) hi = m; else lo = m + 1;
   }
-  rb[k] = (uint32_t)lo;
+  return (uint32_t)lo;
+}
+__global__ void k_slice_bounds(const uint32_t *__restrict__ s, int64_t R, uint64_t N, int W, uint32_t *__restrict__ rb) {
+  int k = threadIdx.x;
+  if (k <= W) rb[k] = slice_bound(s, R, N, W, k);
 }
 
 // Records per fingerprint-sorted element: Q if it is the first access of its block in the shard,
@@ -807,4 +809,15 @@ extern "C" kareto_status kareto_trace_shard(const kareto_trace *tr, int64_t *req
   if (pos_lo) *pos_lo = tr->pos_lo;
   if (pos_hi) *pos_hi = tr->pos_hi;
   return KARETO_OK;
+}
+
+extern "C" kareto_status kareto_time_slices(const uint32_t *s, int64_t R, int32_t world, int64_t *req_bounds) {
+  if (!s || R < 1 || world < 1 || world > kareto::kMaxShardWorld || !req_bounds) return KARETO_E_INVALID;
+  for (int k = 0; k <= world; k++) req_bounds[k] = kareto::slice_bound(s, R, (uint64_t)s[R], world, k);
+  return KARETO_OK;
+}
+
+extern "C" int32_t kareto_hash_owner(uint64_t block_hash, int32_t world) {
+  if (world < 1) return -1;
+  return (int32_t)kareto::owner_of((uint32_t)(kareto::fmix64(block_hash ^ kareto::kSortMixC) >> 32), world);
 }

@@ -81,8 +81,10 @@ def tuner_rows_config3(delta_by_group, U_g, K):
 
 # algorithmic bytes per unit of each own kernel
 ALGO = {
-    "K1_chain_hash": ("block", 76),        # 64 B tokens in + 8 B hash + 4 B request id out
-    "K2_sort_prep": ("access", 20),        # 8 B hash in, 4 B key + 4 B fingerprint half + 4 B position out
+    # 64 B tokens in; 8 B hash + 4 B request id + K2's sort input (4 B key, 8 B fingerprint half |
+    # position; k_sort_prep fused into K1) out
+    "K1_chain_hash": ("block", 88),
+    "K2_sort_prep": ("access", 20),        # HASHES mode only: 8 B hash in, 4 B key + 8 B value out
     "K2_link_prev": ("access", 20),        # 4 B fingerprint + 8 B (hash half, position) in, 8 B pair out
     "K2_bucket_assemble": ("access", 12),  # 8 B pair in, 4 B prev out
     "K2_access_info": ("access", 13),      # prev, req in; delta + run flag out

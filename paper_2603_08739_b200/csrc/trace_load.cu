@@ -205,7 +205,9 @@ __global__ void __launch_bounds__(K1_THREADS) k_chain_hash(const uint32_t *__res
                                                             const uint32_t *__restrict__ s, int64_t R, uint64_t N,
                                                             uint64_t pos_base, uint32_t req_base,
                                                             uint64_t P_init, uint64_t *__restrict__ hash_out,
-                                                            uint32_t *__restrict__ req_out) {
+                                                            uint32_t *__restrict__ req_out,
+                                                            uint32_t *__restrict__ key_out,
+                                                            uint64_t *__restrict__ val_out) {
   const int lane = threadIdx.x & 31;
   const uint64_t nw = (uint64_t)gridDim.x * K1_WARPS;
   const uint64_t w = (uint64_t)blockIdx.x * K1_WARPS + (threadIdx.x >> 5);
@@ -251,8 +253,14 @@ __global__ void __launch_bounds__(K1_THREADS) k_chain_hash(const uint32_t *__res
     const uint64_t P = e.a * carry + e.b;
     if (valid) {
       uint64_t j = (uint64_t)sr + n - 1 - k - pos_base;
-      hash_out[j] = fmix64(P);
+      const uint64_t h = fmix64(P);
+      hash_out[j] = h;
       req_out[j] = r + req_base;
+      if (key_out) {  // K2's sort input, fused (k_sort_prep's mix): saves re-reading the hashes
+        const uint64_t m = fmix64(h ^ kSortMixC);
+        key_out[j] = (uint32_t)(m >> 32);
+        val_out[j] = (m << 32) | (uint64_t)(uint32_t)j;
+      }
     }
     carry = __shfl_sync(0xffffffffu, P, 31);  // last block of the round (beyond B1: unused)
   }
@@ -816,7 +824,7 @@ kareto_status upload_payload(kareto_ctx *ctx, const kareto_trace_desc *d, int64_
 
 kareto_status chain_hash(kareto_ctx *ctx, const kareto_trace_desc *d, const kareto_trace *tr, const Ingest &in,
                          const uint32_t *tok_base, const uint64_t *bh_base, int64_t tok_end, int64_t r0, int64_t r1,
-                         uint64_t *hash_out, uint32_t *req_out) {
+                         uint64_t *hash_out, uint32_t *req_out, SortedHashes *prep) {
   uint32_t se[2];
   KCUDA(ctx, cudaMemcpyAsync(&se[0], tr->s + r0, 4, cudaMemcpyDeviceToHost, ctx->stream));
   KCUDA(ctx, cudaMemcpyAsync(&se[1], tr->s + r1, 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -830,9 +838,14 @@ kareto_status chain_hash(kareto_ctx *ctx, const kareto_trace_desc *d, const kare
     uint64_t nwarps = (n + 2047) / 2048;
     if (nwarps < (uint64_t)(16 * sms)) nwarps = 16 * sms;
     unsigned g = (unsigned)((nwarps + K1_WARPS - 1) / K1_WARPS);
+    if (prep) {  // K2's sort input written by K1 (k_sort_prep fused)
+      KTRY(prep->key.alloc(ctx, n));
+      KTRY(prep->val.alloc(ctx, n));
+    }
     Pass ps(ctx, "K1_chain_hash", 1, 1);
     k_chain_hash<<<g, K1_THREADS, 0, ctx->stream>>>(tok_base, tok_end, in.src_off.p + r0, tr->s + r0, r1 - r0, n,
-                                                    se[0], (uint32_t)r0, P_init, hash_out, req_out);
+                                                    se[0], (uint32_t)r0, P_init, hash_out, req_out,
+                                                    prep ? prep->key.p : nullptr, prep ? prep->val.p : nullptr);
   } else {
     Pass ps(ctx, "K1_copy_hashes", 1, 1);
     k_copy_hashes<<<grid_for(32 * (r1 - r0), 256, 8 * sms), 256, 0, ctx->stream>>>(
@@ -841,15 +854,20 @@ kareto_status chain_hash(kareto_ctx *ctx, const kareto_trace_desc *d, const kare
   return KARETO_OK;
 }
 
-kareto_status link_prev(kareto_ctx *ctx, const uint64_t *hash, uint64_t N, uint32_t *prev, SortedHashes *keep) {
+kareto_status link_prev(kareto_ctx *ctx, const uint64_t *hash, uint64_t N, uint32_t *prev, SortedHashes *keep,
+                        SortedHashes *prep) {
   if (N == 0) return KARETO_OK;
   cudaStream_t st = ctx->stream;
   const int sms = ctx->num_sms;
   DBuf<uint8_t> tmp;
   DBuf<uint32_t> k32, k32s;
   DBuf<uint64_t> v64, v64s;
-  KTRY(k32.alloc(ctx, N)); KTRY(k32s.alloc(ctx, N)); KTRY(v64.alloc(ctx, N)); KTRY(v64s.alloc(ctx, N));
-  {
+  KTRY(k32s.alloc(ctx, N)); KTRY(v64s.alloc(ctx, N));
+  if (prep && prep->key.p) {  // written by K1
+    k32 = std::move(prep->key);
+    v64 = std::move(prep->val);
+  } else {
+    KTRY(k32.alloc(ctx, N)); KTRY(v64.alloc(ctx, N));
     Pass ps(ctx, "K2_sort_prep", 1, 1);
     k_sort_prep<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(hash, N, k32.p, v64.p);
   }
@@ -947,13 +965,14 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
   KCUDA(ctx, cudaMallocAsync((void **)&tr->depth, 4 * Na, st));
 
   // ---- a2: K1 chained hashes (TOKENS) / copy (HASHES) into touch order
+  SortedHashes prep;  // K2's sort input, written by K1 in TOKENS mode
   {
     DBuf<uint32_t> h_tok;
     DBuf<uint64_t> h_bh;
     const uint32_t *tok_base;
     const uint64_t *bh_base;
     KTRY(upload_payload(ctx, d, 0, in.total, h_tok, h_bh, &tok_base, &bh_base));
-    KTRY(chain_hash(ctx, d, tr, in, tok_base, bh_base, in.total, 0, R, tr->hash, tr->req));
+    KTRY(chain_hash(ctx, d, tr, in, tok_base, bh_base, in.total, 0, R, tr->hash, tr->req, &prep));
   }
 
   // ---- a3: K2 prev / delta / chain check
@@ -963,7 +982,7 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
   KTRY(first_cnt.alloc(ctx, R)); KTRY(reuse_cnt.alloc(ctx, R));
   KTRY(first_cnt.zero()); KTRY(reuse_cnt.zero());
   if (N > 0) {
-    KTRY(link_prev(ctx, tr->hash, N, tr->prev, nullptr));
+    KTRY(link_prev(ctx, tr->hash, N, tr->prev, nullptr, &prep));
     {
       Pass ps(ctx, "K2_access_info", 1, 1);
       k_access_info<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(N, tr->prev, tr->req, tr->s, tr->arr, tr->hash,

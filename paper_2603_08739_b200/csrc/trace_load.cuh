@@ -38,16 +38,6 @@ kareto_status upload_payload(kareto_ctx *ctx, const kareto_trace_desc *d, int64_
                              DBuf<uint32_t> &tok, DBuf<uint64_t> &bh, const uint32_t **tok_base,
                              const uint64_t **bh_base);
 
-// a2 (K1) over the sorted requests [r0, r1) whose blocks occupy global positions [P0, P1)
-// (tok_base[i] valid for i < tok_end):
-// hash_out / req_out are indexed by (position - P0); req_out holds global request indices.
-kareto_status chain_hash(kareto_ctx *ctx, const kareto_trace_desc *d, const kareto_trace *tr, const Ingest &in,
-                         const uint32_t *tok_base, const uint64_t *bh_base, int64_t tok_end, int64_t r0, int64_t r1,
-                         uint64_t *hash_out, uint32_t *req_out);
-
-// a3 (K2 link): prev[i] = largest i' < i with hash[i'] == hash[i] (local indices), kNone if
-// none.  With keep != nullptr the fingerprint-sorted (key, value) arrays are handed back:
-// key = top 32 bits of m = fmix64(h ^ C), value = (low 32 bits of m) << 32 | i.
 // qf[i] = 1 if sorted element i is the first occurrence of its hash in the range, nx[i] = 1 if
 // a later occurrence exists (both in sorted order, produced by the link kernels).
 struct SortedHashes {
@@ -55,7 +45,20 @@ struct SortedHashes {
   DBuf<uint64_t> val;
   DBuf<uint8_t> qf, nx;
 };
-kareto_status link_prev(kareto_ctx *ctx, const uint64_t *hash, uint64_t n, uint32_t *prev, SortedHashes *keep);
+
+// a2 (K1) over the sorted requests [r0, r1) whose blocks occupy global positions [P0, P1)
+// (tok_base[i] valid for i < tok_end):
+// hash_out / req_out are indexed by (position - P0); req_out holds global request indices.
+kareto_status chain_hash(kareto_ctx *ctx, const kareto_trace_desc *d, const kareto_trace *tr, const Ingest &in,
+                         const uint32_t *tok_base, const uint64_t *bh_base, int64_t tok_end, int64_t r0, int64_t r1,
+                         uint64_t *hash_out, uint32_t *req_out, SortedHashes *prep);
+
+// a3 (K2 link): prev[i] = largest i' < i with hash[i'] == hash[i] (local indices), kNone if
+// none.  With keep != nullptr the fingerprint-sorted (key, value) arrays are handed back:
+// key = top 32 bits of m = fmix64(h ^ C), value = (low 32 bits of m) << 32 | i.
+// prep: K2's sort input already written by K1 (chain_hash with prep), or nullptr / empty
+kareto_status link_prev(kareto_ctx *ctx, const uint64_t *hash, uint64_t n, uint32_t *prev, SortedHashes *keep,
+                        SortedHashes *prep = nullptr);
 
 // The bijective mix whose halves are the sort key / value high word (k_sort_prep).
 constexpr uint64_t kSortMixC = 0x6A09E667F3BCC909ULL;

@@ -254,18 +254,22 @@ __global__ void k_apply_replies(const XRec *__restrict__ rec, const uint32_t *__
   }
 }
 
-// Boundary-set bitmap this shard contributes to rank k (> this rank): bit p set iff p is the
-// last access of its block in this shard and the block next appears in shard k or later (or
-// never), i.e. p in B_k.  Words are aligned to global positions: word w covers [32w, 32w+32).
+// Boundary-set bitmaps this shard contributes to every later rank k: bit p set iff p is the last
+// access of its block in this shard and the block next appears in shard k or later (or never),
+// i.e. p in B_k.  Words are aligned to global positions (word w covers [32w, 32w+32)); one
+// read of each position's next-shard byte, one ballot per later rank; out + (k - me - 1) * nwords
+// is rank k's bitmap.
 __global__ void k_bset_words(const uint8_t *__restrict__ nxs, uint32_t P0, uint32_t P1, uint32_t w0, uint32_t nwords,
-                             int k, uint32_t *__restrict__ out) {
+                             int me, int W, uint32_t *__restrict__ out) {
   const int lane = threadIdx.x & 31;
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < (uint64_t)nwords * 32;
        t += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t p = (w0 << 5) + (uint32_t)t;  // one position per thread, a warp per word
-    const bool set = p >= P0 && p < P1 && nxs[p - P0] >= (uint8_t)k;
-    const unsigned w = __ballot_sync(0xFFFFFFFFu, set);
-    if (lane == 0) out[t >> 5] = w;
+    const int nx = (p >= P0 && p < P1) ? nxs[p - P0] : 0;
+    for (int k = me + 1; k < W; k++) {
+      const unsigned w = __ballot_sync(0xFFFFFFFFu, nx >= k);
+      if (lane == 0) out[(size_t)(k - me - 1) * nwords + (t >> 5)] = w;
+    }
   }
 }
 // OR a received word segment into the bitmap (neighbouring shards share a boundary word)
@@ -554,6 +558,7 @@ static kareto_status load_sharded(kareto_ctx *ctx, const kareto_trace_desc *d, k
   KCUDA(ctx, cudaMallocAsync((void **)&tr->depth, 4 * na, st));
 
   // ---- a2: K1 on the shard (only the shard's token / hash range is uploaded)
+  SortedHashes prep;  // K2's sort input, written by K1 in TOKENS mode
   {
     int64_t lo = 0, hi = 0;
     if (r1 > r0 && !d->inputs_on_device) {  // element range covering the shard's requests
@@ -577,7 +582,7 @@ static kareto_status load_sharded(kareto_ctx *ctx, const kareto_trace_desc *d, k
     const uint64_t *bh_base;
     KTRY(upload_payload(ctx, d, lo, hi, h_tok, h_bh, &tok_base, &bh_base));
     KTRY(chain_hash(ctx, d, tr, in, tok_base, bh_base, d->inputs_on_device ? in.total : hi, r0, r1, tr->hash,
-                    tr->req));
+                    tr->req, &prep));
   }
 
   // ---- a3: in-shard links, then the owner exchange for the shard's first / last accesses
@@ -588,7 +593,7 @@ static kareto_status load_sharded(kareto_ctx *ctx, const kareto_trace_desc *d, k
   DBuf<XRec> rec;
   uint32_t n_rec = 0;
   std::vector<uint64_t> send_cnt(W, 0);
-  if (n > 0) KTRY(link_prev(ctx, tr->hash, n, prev_loc.p, &sh));
+  if (n > 0) KTRY(link_prev(ctx, tr->hash, n, prev_loc.p, &sh, &prep));
   {
     Pass ps(ctx, "F4_records", 1, 3);
     DBuf<uint8_t> fl;
@@ -700,13 +705,12 @@ static kareto_status load_sharded(kareto_ctx *ctx, const kareto_trace_desc *d, k
   DBuf<uint32_t> bsend, brecv;
   KTRY(bsend.alloc(ctx, bso[W] / 4 + 1)); KTRY(brecv.alloc(ctx, bro[W] / 4 + 1));
   {
-    Pass ps(ctx, "F4_boundary_sets", 1, 1 + (W - 1 - me));
+    Pass ps(ctx, "F4_boundary_sets", 1, 3);
     if (n > 0) k_prev_global<<<grid_for(n, 256, 8 * sms), 256, 0, st>>>(prev_loc.p, n, P0, tr->prev);
     if (n_rec > 0)
       k_apply_replies<<<grid_for(n_rec, 256, 8 * sms), 256, 0, st>>>(rec.p, ans.p, n_rec, P0, tr->prev, nxs.p);
-    for (int k = me + 1; k < W && mnw > 0; k++)
-      k_bset_words<<<grid_for(32ll * mnw, 256, 8 * sms), 256, 0, st>>>(nxs.p, P0, P1, mw0, mnw, k,
-                                                                       bsend.p + bso[k] / 4);
+    if (me + 1 < W && mnw > 0)  // rank k's segment starts at bso[k] = (k - me - 1) * 4 * mnw
+      k_bset_words<<<grid_for(32ll * mnw, 256, 8 * sms), 256, 0, st>>>(nxs.p, P0, P1, mw0, mnw, me, W, bsend.p);
   }
   {
     Pass ps(ctx, "F4_exchange", 0, 1);

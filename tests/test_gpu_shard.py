@@ -200,3 +200,83 @@ def test_config_shard_gather_loopback(W):
     for c, o in run_ranks(W, fn):
         assert np.array_equal(np.asarray(c).view(np.uint8), np.asarray(want_c).view(np.uint8))
         assert np.array_equal(o.view(np.uint64), want_o.view(np.uint64))
+
+
+def _check_shards(out, ot):
+    e = ot.export()
+    d, _ = ot.depth()
+    for key, want in ((K.X_HASH, e["hash"]), (K.X_PREV, np.where(e["prev"] < 0, U32, e["prev"])),
+                      (K.X_DELTA, np.where(e["delta"] < 0, U32, e["delta"])), (K.X_DEPTH, np.where(d < 0, U32, d))):
+        got = np.concatenate([o[key] for o in out]).astype(np.int64 if key != K.X_HASH else np.uint64)
+        assert np.array_equal(got, want.astype(got.dtype)), key
+    for o in out:
+        assert o["U"] == ot.U and np.array_equal(o["Ug"], ot.U_g)
+        assert np.array_equal(o[K.X_GROUP][o["rlo"]:o["rhi"]], e["group"][o["rlo"]:o["rhi"]].astype(np.uint16))
+
+
+def _load_exports(tr, top_k, salt=0):
+    def fn(r, ctx):
+        gt = ctx.load(tr, top_k=top_k, salt=salt, time_shard=True)
+        res = dict(U=gt.U, Ug=gt.U_g.copy(), rlo=gt.req_lo, rhi=gt.req_hi)
+        for x in (K.X_HASH, K.X_PREV, K.X_DELTA, K.X_DEPTH, K.X_GROUP):
+            res[x] = gt.export(x)
+        return res
+    return fn
+
+
+def test_time_shard_hash_mode():
+    """HASHES input (caller-provided chained hashes, k_copy_hashes + k_sort_prep path)."""
+    tr = ki.synthetic("chat", R=1500, seed=12)
+    bh, boff = [], [0]
+    for r in range(tr.n_requests):
+        h = O.chain_hashes(tr.tokens[tr.offsets[r]:tr.offsets[r + 1]])
+        bh.append(h)
+        boff.append(boff[-1] + len(h))
+    th = ki.Trace(tr.arrival_ms, tr.output_tokens, np.array(boff, np.int64), block_hash=np.concatenate(bh),
+                  input_tokens=np.diff(tr.offsets))
+    ot = O.OracleTrace(tr, top_k=3)
+    _check_shards(run_ranks(3, _load_exports(th, 3)), ot)
+
+
+def _fmix64_inv(m):
+    M = (1 << 64) - 1
+
+    def unx(x, s):
+        z = x
+        for _ in range(64 // s + 1):
+            z = x ^ (z >> s)
+        return z & M
+    z = unx(m, 31)
+    z = (z * pow(0x94D049BB133111EB, -1, 1 << 64)) & M
+    z = unx(z, 27)
+    z = (z * pow(0xBF58476D1CE4E5B9, -1, 1 << 64)) & M
+    return unx(z, 30)
+
+
+@pytest.mark.parametrize("W", [2, 3])
+def test_time_shard_fingerprint_collisions(W):
+    """Distinct hashes sharing the 32-bit sort fingerprint (a hot block interleaved with rare
+    ones): the link overflow path's first/has-next flags and the owner's full-hash matching."""
+    c, fp = 0x6A09E667F3BCC909, 0x12345678
+    hs = [_fmix64_inv((fp << 32) | lo) ^ c for lo in (7, 11, 13, 17, 19, 23)]
+    rng = np.random.default_rng(5)
+    seq = list(rng.permutation([0] * 400 + [1, 2, 3, 4, 5] * 6))
+    R = len(seq)
+    tr = ki.Trace(np.arange(R, dtype=np.int64), np.ones(R, np.int32), np.arange(R + 1, dtype=np.int64),
+                  block_hash=np.array([hs[x] for x in seq], np.uint64))
+    ot = O.OracleTrace(tr, mode="hashes", top_k=2)
+    _check_shards(run_ranks(W, _load_exports(tr, 2)), ot)
+
+
+def test_time_shard_chain_violation_across_shards():
+    """R7 across a shard boundary: block B is a root in request 0 (shard 0) and a child in
+    request 1 (shard 1); both ranks fail with KARETO_E_CHAIN (none is left in a collective)."""
+    tr = ki.Trace(np.array([0, 1], np.int64), np.array([1, 1], np.int32), np.array([0, 1, 3], np.int64),
+                  block_hash=np.array([0xB, 0xA, 0xB], np.uint64))
+
+    def fn(r, ctx):
+        with pytest.raises(K.KaretoError) as ei:
+            ctx.load(tr, top_k=1, time_shard=True)
+        return ei.value.status
+
+    assert run_ranks(2, fn) == [K.E_CHAIN] * 2

@@ -115,13 +115,14 @@ int main() {
     float ms; cudaEventElapsedTime(&ms, a, b); best = ms < best ? ms : best;
   }
   printf("%-28s %8.3f ms (cub::DeviceRadixSort::SortPairs, not in place)\n", "default", best);
-  run<Hub<8, 384, 30>>("bits8 t384 i30", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, true, kref);
-  run<Hub<11, 384, 16>>("bits11 t384 i16", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, true, kref);
-  run<Hub<11, 512, 12>>("bits11 t512 i12", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, true, kref);
-  run<Hub<11, 256, 24>>("bits11 t256 i24", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, true, kref);
-  run<Hub<11, 384, 20>>("bits11 t384 i20", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, true, kref);
-  run<Hub<10, 384, 20>>("bits10 t384 i20 (4 passes)", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 3, false, kref);
-  run<Hub<11, 640, 10>>("bits11 t640 i10", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, true, kref);
+  run<Hub<8, 384, 29>>("bits8 t384 i29 (default-like)", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
+  run<Hub<8, 256, 32>>("bits8 t256 i32", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, true, kref);
+  run<Hub<8, 256, 36>>("bits8 t256 i36", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
+  run<Hub<8, 256, 40>>("bits8 t256 i40", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
+  run<Hub<8, 256, 44>>("bits8 t256 i44", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
+  run<Hub<8, 192, 40>>("bits8 t192 i40", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
+  run<Hub<8, 128, 48>>("bits8 t128 i48", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
+  run<Hub<8, 320, 32>>("bits8 t320 i32", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
   printf("done\n");
   return 0;
 }

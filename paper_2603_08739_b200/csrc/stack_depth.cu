@@ -267,19 +267,95 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_sd_local(const uint2 *__re
   }
 }
 
-// d_j = s_r - prev_j - A(run) for every access of each run (warp per run); s_r in the
-// coordinates of prev: s[r] - pos_base + y_off
-__global__ void k_run_expand(const int *__restrict__ m_ptr, const uint32_t *__restrict__ run_start,
-                             const uint32_t *__restrict__ run_req, const uint32_t *__restrict__ run_len,
-                             const uint32_t *__restrict__ run_p0, const uint32_t *__restrict__ s,
-                             uint32_t s_shift, const uint32_t *__restrict__ A, uint32_t *__restrict__ depth) {
+// d_j = s_r - prev_j - A(run) for every access of each run; s_r in the coordinates of prev:
+// s[r] - pos_base + y_off.  A warp loads the metadata of 32 runs at once (coalesced; the s / A
+// gathers of the 32 runs in flight together), then writes the runs one after the other with
+// all lanes (consecutive lanes store consecutive positions).
+__global__ void __launch_bounds__(256) k_run_expand(const int *__restrict__ m_ptr, const uint32_t *__restrict__ run_start,
+                                                    const uint32_t *__restrict__ run_req,
+                                                    const uint32_t *__restrict__ run_len,
+                                                    const uint32_t *__restrict__ run_p0,
+                                                    const uint32_t *__restrict__ s, uint32_t s_shift,
+                                                    const uint32_t *__restrict__ A, uint32_t *__restrict__ depth) {
   const int M = *m_ptr;
   const int lane = threadIdx.x & 31;
-  for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < M; q += (gridDim.x * blockDim.x) >> 5) {
-    uint32_t j0 = run_start[q], L = run_len[q], p0 = run_p0[q];
-    uint32_t base = s[run_req[q]] - s_shift - p0 - A[p0];
-    for (uint32_t t = lane; t < L; t += 32) depth[j0 + t] = base - t;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int q0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; q0 < M; q0 += nw * 32) {
+    const int q = q0 + lane;
+    uint32_t j0 = 0, L = 0, base = 0;
+    if (q < M) {
+      const uint32_t p0 = run_p0[q];
+      j0 = run_start[q];
+      L = run_len[q];
+      base = s[run_req[q]] - s_shift - p0 - A[p0];
+    }
+    const int nk = M - q0 < 32 ? M - q0 : 32;
+    for (int k = 0; k < nk; k++) {
+      const uint32_t jk = __shfl_sync(0xFFFFFFFFu, j0, k), Lk = __shfl_sync(0xFFFFFFFFu, L, k);
+      const uint32_t bk = __shfl_sync(0xFFFFFFFFu, base, k);
+      for (uint32_t t = lane; t < Lk; t += 32) depth[jk + t] = bk - t;
+    }
   }
+}
+
+// ---- run heads: ordered compaction of the K2 run flags (two passes over 1 B per access)
+constexpr int CF_THREADS = 256, CF_PER = 64, CF_TILE = CF_THREADS * CF_PER;  // 16384 flags per tile
+__device__ __forceinline__ uint32_t nz_bytes(uint32_t w) {  // number of nonzero bytes
+  return ((w & 0xFFu) != 0) + ((w & 0xFF00u) != 0) + ((w & 0xFF0000u) != 0) + ((w & 0xFF000000u) != 0);
+}
+__device__ __forceinline__ void load_flags(const uint8_t *__restrict__ f, uint64_t N, uint64_t p, uint32_t w[16]) {
+  if (p + 64 <= N) {
+    const uint4 *q = reinterpret_cast<const uint4 *>(f + p);
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint4 v = __ldg(q + k);
+      w[4 * k] = v.x; w[4 * k + 1] = v.y; w[4 * k + 2] = v.z; w[4 * k + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      uint32_t x = 0;
+      for (int b = 0; b < 4; b++) {
+        const uint64_t i = p + 4 * k + b;
+        if (i < N && f[i]) x |= 0xFFu << (8 * b);
+      }
+      w[k] = x;
+    }
+  }
+}
+__global__ void __launch_bounds__(CF_THREADS) k_flag_count(const uint8_t *__restrict__ f, uint64_t N,
+                                                           uint32_t *__restrict__ cnt) {
+  typedef cub::BlockReduce<uint32_t, CF_THREADS> Red;
+  __shared__ typename Red::TempStorage ts;
+  const uint64_t p = (uint64_t)blockIdx.x * CF_TILE + (uint64_t)threadIdx.x * CF_PER;
+  uint32_t w[16], c = 0;
+  if (p < N) {
+    load_flags(f, N, p, w);
+#pragma unroll
+    for (int k = 0; k < 16; k++) c += nz_bytes(w[k]);
+  }
+  const uint32_t tot = Red(ts).Sum(c);
+  if (threadIdx.x == 0) cnt[blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(CF_THREADS) k_flag_write(const uint8_t *__restrict__ f, uint64_t N,
+                                                           const uint32_t *__restrict__ off,
+                                                           uint32_t *__restrict__ out) {
+  typedef cub::BlockScan<uint32_t, CF_THREADS> Scan;
+  __shared__ typename Scan::TempStorage ts;
+  const uint64_t p = (uint64_t)blockIdx.x * CF_TILE + (uint64_t)threadIdx.x * CF_PER;
+  uint32_t w[16], c = 0;
+  if (p < N) {
+    load_flags(f, N, p, w);
+#pragma unroll
+    for (int k = 0; k < 16; k++) c += nz_bytes(w[k]);
+  }
+  uint32_t ex;
+  Scan(ts).ExclusiveSum(c, ex);
+  if (!c) return;
+  uint32_t o = off[blockIdx.x] + ex;
+  for (int k = 0; k < 16; k++)
+    for (int b = 0; b < 4; b++)
+      if ((w[k] >> (8 * b)) & 0xFFu) out[o++] = (uint32_t)(p + 4 * k + b);
 }
 
 __global__ void k_sd_tiles(uint32_t nseg, const uint64_t *__restrict__ seg_len, const uint32_t *__restrict__ tile0,
@@ -327,11 +403,17 @@ kareto_status stack_depth(kareto_ctx *ctx, uint64_t N, uint64_t y_range, const u
   // #runs <= reuse accesses; allocate for the worst case (N) lazily: count first
   KTRY(run_start.alloc(ctx, N));
   {
-    Pass ps(ctx, "K3_runs", 0, 1);
-    cub::CountingInputIterator<uint32_t> it0(0);
+    Pass ps(ctx, "K3_runs", 1, 2);
+    const uint64_t ntile = (N + CF_TILE - 1) / CF_TILE;
+    DBuf<uint32_t> cnt, off;
+    KTRY(cnt.alloc(ctx, ntile + 1)); KTRY(off.alloc(ctx, ntile + 1));
+    KCUDA(ctx, cudaMemsetAsync(cnt.p + ntile, 0, 4, st));
+    k_flag_count<<<(unsigned)ntile, CF_THREADS, 0, st>>>(run_flag, N, cnt.p);
     KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
-      return cub::DeviceSelect::Flagged(t, b, it0, run_flag, run_start.p, m_dev.p, (int64_t)N, st);
+      return cub::DeviceScan::ExclusiveSum(t, b, cnt.p, off.p, (int)(ntile + 1), st);
     }));
+    k_flag_write<<<(unsigned)ntile, CF_THREADS, 0, st>>>(run_flag, N, off.p, run_start.p);
+    KCUDA(ctx, cudaMemcpyAsync(m_dev.p, off.p + ntile, 4, cudaMemcpyDeviceToDevice, st));
   }
   int M = 0;
   KCUDA(ctx, cudaMemcpyAsync(&M, m_dev.p, 4, cudaMemcpyDeviceToHost, st));
@@ -449,8 +531,8 @@ kareto_status stack_depth(kareto_ctx *ctx, uint64_t N, uint64_t y_range, const u
   }
   {
     Pass ps(ctx, "K3_expand", 1, 1);
-    k_run_expand<<<grid_for(32ll * M, 256, 16 * sms), 256, 0, st>>>(m_dev.p, run_start.p, run_req.p, run_len.p,
-                                                                    run_p0.p, s, pos_base - y_off, A.p, depth);
+    k_run_expand<<<grid_for(M, 256, 16 * sms), 256, 0, st>>>(m_dev.p, run_start.p, run_req.p, run_len.p, run_p0.p, s,
+                                                             pos_base - y_off, A.p, depth);
   }
   return KARETO_OK;
 }

@@ -588,7 +588,9 @@ __global__ void k_access_info(uint64_t N, const uint32_t *__restrict__ prev, con
       uint32_t kj = s[r + 1] - 1 - (uint32_t)j;
       uint32_t kp = s[rp + 1] - 1 - p;
       if (kj != kp) flags |= F_CHAIN;
-      else if (kj > 0 && hash[j + 1] != hash[p + 1]) flags |= F_CHAIN;
+      // parents must match (R7); when the parent access links to p + 1 the K2 link already
+      // proves equal hashes (the common case inside a run), so only run ends gather hashes
+      else if (kj > 0 && prev[j + 1] != p + 1 && hash[j + 1] != hash[p + 1]) flags |= F_CHAIN;
     }
     delta[j] = dl;
     // K3 run heads: a reuse access whose predecessor position is not its previous position

@@ -312,7 +312,7 @@ __global__ void k_access_info_shard(uint64_t n, uint32_t P0, uint32_t r0, const 
         pc = Bsize + (p - P0);
         const uint32_t kj = s[r + 1] - 1 - j, kp = s[rp + 1] - 1 - p;
         if (kj != kp) fl_chain++;
-        else if (kj > 0 && hash[i + 1] != hash[p - P0 + 1]) fl_chain++;
+        else if (kj > 0 && prev[i + 1] != p + 1 && hash[i + 1] != hash[p - P0 + 1]) fl_chain++;
       } else {
         int64_t lo = 0, hi = R;  // last request with s[r] <= p
         while (lo < hi) {

@@ -38,10 +38,6 @@ __global__ void k_build_lut(const uint32_t *__restrict__ Bd, int nb, int sh, uin
   }
 }
 
-#ifndef HIST_AGG
-#define HIST_AGG 0
-#endif
-
 // index of the first boundary >= v (nb if none)
 __device__ __forceinline__ int bin_of(uint32_t v, const uint32_t *__restrict__ Bd, int nb, const uint32_t *lut_s,
                                       int sh) {
@@ -106,8 +102,8 @@ __global__ void __launch_bounds__(H_THREADS) k_hist_d(uint64_t N, uint32_t pos0,
 }
 
 // K4 fused (when both histograms fit in shared memory): one pass over the accesses builds
-// the (d-bin, tau-bin) count / sum-k histogram and the D-bin count histogram.  Updates are
-// warp-aggregated (match_any on the cell) so hot bins (small depths) do not serialise.
+// the (d-bin, tau-bin) count / sum-k histogram and the D-bin count histogram (shared-memory
+// atomics; warp aggregation by match_any measured slower here).
 __global__ void __launch_bounds__(H_THREADS) k_hist_dD(uint64_t N, uint32_t pos0, uint64_t per_cta, const uint32_t *__restrict__ depth,
                                                        const uint32_t *__restrict__ req, const uint32_t *__restrict__ s,
                                                        const uint32_t *__restrict__ delta,
@@ -128,44 +124,44 @@ __global__ void __launch_bounds__(H_THREADS) k_hist_dD(uint64_t N, uint32_t pos0
   for (int i = threadIdx.x; i < nb; i += blockDim.x) cD[i] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  (void)lane;
   uint64_t j0 = blockIdx.x * per_cta, j1 = j0 + per_cta < N ? j0 + per_cta : N;
-  for (uint64_t jb = j0; jb < j1; jb += blockDim.x) {  // block-uniform trip count
-    uint64_t j = jb + threadIdx.x;
-    int cell = -1, dcell = -1;
-    uint32_t k = 0;
-    if (j < j1) {
-      uint32_t d = depth[j];
-      if (d != kNone) {
-        uint32_t r = req[j];
-        uint32_t sr1 = s[r + 1];
-        k = sr1 - 1 - ((uint32_t)j + pos0);
-        int bd = bin_of(d, Bd, nb, lut_s, sh);
-        if (bd < nb) cell = (ntc > 0 ? tbin_of(delta[j], Tc, ntc) : 0) * nb + bd;
-        uint32_t D = d + ((uint32_t)j + pos0 - s[r]);
-        // D >= d: walk forward from d's bin (D - d is the offset inside the request, usually
-        // small against the boundary gaps), falling back to the search after a few steps
-        int bD = bd;
-        int steps = 0;
-        while (bD < nb && __ldg(&Bd[bD]) < D && steps < 4) { bD++; steps++; }
-        if (bD < nb && __ldg(&Bd[bD]) < D) bD = bin_of(D, Bd, nb, lut_s, sh);
-        if (bD < nb) dcell = bD;
-      }
+  // HD_U accesses per thread per round, loads issued breadth-first (depth/req, then the request
+  // starts, then the boundary searches) so that a thread keeps several global loads in flight
+  constexpr int HD_U = 4;
+  for (uint64_t jb = j0; jb < j1; jb += (uint64_t)HD_U * blockDim.x) {
+    uint32_t d[HD_U], r[HD_U], sr[HD_U], sr1[HD_U], dl[HD_U];
+#pragma unroll
+    for (int u = 0; u < HD_U; u++) {
+      const uint64_t j = jb + (uint64_t)u * blockDim.x + threadIdx.x;
+      d[u] = j < j1 ? depth[j] : kNone;
+      r[u] = (d[u] != kNone) ? req[j] : 0u;
+      dl[u] = (d[u] != kNone && ntc > 0) ? delta[j] : 0u;
     }
-    if (HIST_AGG) {
-      unsigned same = __match_any_sync(0xffffffffu, cell);
-      uint32_t ks = __reduce_add_sync(same, k);
-      if (cell >= 0 && (__ffs(same) - 1) == lane) {
-        atomicAdd(&cnt[cell], (uint32_t)__popc(same));
-        if (ks) atomicAdd(&sk[cell], ks);
-      }
-      unsigned sameD = __match_any_sync(0xffffffffu, dcell);
-      if (dcell >= 0 && (__ffs(sameD) - 1) == lane) atomicAdd(&cD[dcell], (uint32_t)__popc(sameD));
-    } else {
-      if (cell >= 0) {
+#pragma unroll
+    for (int u = 0; u < HD_U; u++) {
+      sr[u] = d[u] != kNone ? s[r[u]] : 0u;
+      sr1[u] = d[u] != kNone ? s[r[u] + 1] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < HD_U; u++) {
+      if (d[u] == kNone) continue;
+      const uint32_t j = (uint32_t)(jb + (uint64_t)u * blockDim.x + threadIdx.x) + pos0;
+      const uint32_t k = sr1[u] - 1 - j;
+      const int bd = bin_of(d[u], Bd, nb, lut_s, sh);
+      if (bd < nb) {
+        const int cell = (ntc > 0 ? tbin_of(dl[u], Tc, ntc) : 0) * nb + bd;
         atomicAdd(&cnt[cell], 1u);
         if (k) atomicAdd(&sk[cell], k);
       }
-      if (dcell >= 0) atomicAdd(&cD[dcell], 1u);
+      const uint32_t D = d[u] + (j - sr[u]);
+      // D >= d: walk forward from d's bin (D - d is the offset inside the request, usually
+      // small against the boundary gaps), falling back to the search after a few steps
+      int bD = bd;
+      int steps = 0;
+      while (bD < nb && __ldg(&Bd[bD]) < D && steps < 4) { bD++; steps++; }
+      if (bD < nb && __ldg(&Bd[bD]) < D) bD = bin_of(D, Bd, nb, lut_s, sh);
+      if (bD < nb) atomicAdd(&cD[bD], 1u);
     }
   }
   __syncthreads();
@@ -363,9 +359,19 @@ static void shard_range(int64_t n, int rank, int world, int64_t &lo, int64_t &hi
   hi = n * (rank + 1) / world;
 }
 
+#include <chrono>
+#define HT(name)                                                                                          \
+  do {                                                                                                    \
+    if (ht_on) {                                                                                          \
+      auto t_ = std::chrono::steady_clock::now();                                                         \
+      fprintf(stderr, "[eval] %-10s %.3f ms\n", name, std::chrono::duration<double, std::milli>(t_ - ht0).count()); \
+    }                                                                                                     \
+  } while (0)
 static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_config *cfg, int64_t n_cfg,
                           const uint32_t *ttl_ms, int32_t n_tuner, const kareto_model *model,
                           kareto_counts *counts_out, double *obj_out, int32_t on_dev) {
+  const bool ht_on = getenv("KARETO_HOST_TIMING") != nullptr;
+  const auto ht0 = std::chrono::steady_clock::now();
   cudaStream_t st = ctx->stream;
   const int sms = ctx->num_sms;
   if (n_cfg < 0 || (n_cfg > 0 && !cfg) || !model) return fail(ctx, KARETO_E_INVALID, "bad arguments");
@@ -391,6 +397,7 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
       if (rows[(size_t)r * G + g] != rows[(size_t)r * G]) row_uniform[r] = 0;
       if (rows[(size_t)r * G + g] == KARETO_TTL_INF) row_finite[r] = 0;
     }
+  HT("start");
   // ---- validation (every rank validates the full list identically), O(1) per configuration
   for (int64_t i = 0; i < n_cfg; i++) {
     const kareto_config &c = cfg[i];
@@ -419,30 +426,39 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
     return fail(ctx, KARETO_E_OVERFLOW, "transfer bytes >= 2^64");
   ModelConsts mc{(uint64_t)P0, (uint64_t)tr->R, N, U, tr->Ltok, tr->O, tr->span_ms};
 
+  HT("validated");
   // ---- shard
   int64_t lo = 0, hi = n_cfg;
   if (cfg_shard) shard_range(n_cfg, ctx->rank, ctx->world, lo, hi);
   const int64_t ns = hi - lo;
   const kareto_config *sc = cfg + lo;
   // stack-eligible (LRU, and TTL mode or a uniform disk TTL) vs per-configuration replay (K6)
+  // (one counting pass; the split copies are only made when both kinds are present, otherwise
+  // the caller's array is used as it is)
   std::vector<kareto_config> cS, cP;
   std::vector<uint32_t> iS, iP;
   std::vector<char> cap_row_used(nrows, 0), ttl_row_used(nrows, 0);
-  cS.reserve(ns);
+  auto stack_ok = [&](const kareto_config &c) {
+    const int ri = n_tuner > 0 ? c.tuner : 0;
+    return c.policy == KARETO_LRU && (c.cap[2] == KARETO_INF || row_uniform[ri]);
+  };
+  int64_t nP = 0;
   for (int64_t i = 0; i < ns; i++) {
     const kareto_config &c = sc[i];
     const int ri = n_tuner > 0 ? c.tuner : 0;
-    const bool ttl = c.cap[2] == KARETO_INF;
-    if (c.policy == KARETO_LRU && (ttl || row_uniform[ri])) {
-      cS.push_back(c);
-      iS.push_back((uint32_t)i);
-      (ttl ? ttl_row_used : cap_row_used)[ri] = 1;
-    } else {
-      cP.push_back(c);
-      iP.push_back((uint32_t)i);
-    }
+    if (stack_ok(c)) (c.cap[2] == KARETO_INF ? ttl_row_used : cap_row_used)[ri] = 1;
+    else nP++;
   }
-  const int64_t nS = (int64_t)cS.size(), nP = (int64_t)cP.size();
+  const int64_t nS = ns - nP;
+  const kareto_config *cSp = sc;  // the stack configurations, in shard order when nP == 0
+  if (nP > 0) {
+    cS.reserve(nS); iS.reserve(nS); cP.reserve(nP); iP.reserve(nP);
+    for (int64_t i = 0; i < ns; i++) {
+      if (stack_ok(sc[i])) { cS.push_back(sc[i]); iS.push_back((uint32_t)i); }
+      else { cP.push_back(sc[i]); iP.push_back((uint32_t)i); }
+    }
+    cSp = cS.data();
+  }
   if (tsh && nP > 0)
     return fail(ctx, KARETO_E_UNSUPPORTED,
                 "time-sharded trace: %lld configurations need the per-configuration replay (FIFO, LFU, per-group "
@@ -467,6 +483,7 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
         tix[(size_t)r * G + g] =
             (uint32_t)(std::lower_bound(Tt.begin(), Tt.end(), rows[(size_t)r * G + g]) - Tt.begin());
 
+  HT("classified");
   // ---- boundary sets and per-configuration lookup indices, on the GPU
   DBuf<kareto_config> dcfg;
   DBuf<CfgDev> dcd;
@@ -476,7 +493,7 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
   KTRY(dcfg.alloc(ctx, nS > 0 ? nS : 1)); KTRY(dcd.alloc(ctx, nS > 0 ? nS : 1));
   int nb = 0, nb12 = 0;
   if (nS > 0) {
-    KCUDA(ctx, cudaMemcpyAsync(dcfg.p, cS.data(), sizeof(kareto_config) * nS, cudaMemcpyHostToDevice, st));
+    KCUDA(ctx, cudaMemcpyAsync(dcfg.p, cSp, sizeof(kareto_config) * nS, cudaMemcpyHostToDevice, st));
     DBuf<uint32_t> vals, vals_s, v12, v12_s;
     DBuf<int> cnt;
     KTRY(vals.alloc(ctx, 3 * nS)); KTRY(vals_s.alloc(ctx, 3 * nS)); KTRY(v12.alloc(ctx, nS)); KTRY(v12_s.alloc(ctx, nS));
@@ -510,6 +527,7 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
                                                          drows.p, n_tuner, G, dcd.p);
   }
 
+  HT("boundaries");
   // ---- K4: histograms over the accesses
   DBuf<uint32_t> dlut;
   const int ncol = ntc + 1;
@@ -623,6 +641,7 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
     k_prefix_t<<<grid_for(G, 256), 256, 0, st>>>(SDg.p, G, nt1);
   }
 
+  HT("k4");
   // ---- K5 + K7 on the shard
   DBuf<kareto_counts> dcounts;
   DBuf<double> dobj;
@@ -655,6 +674,7 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
     k_scatter_out<<<grid_for(nP, 256), 256, 0, st>>>(cntP.p, objP.p, diP.p, nP, dcounts.p, dobj.p);
   }
 
+  HT("k57");
   // ---- gather (row e): one NCCL allgather of counts and objective vectors over NVLink
   kareto_counts *all_counts = dcounts.p;
   double *all_obj = dobj.p;
@@ -690,7 +710,10 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
     if (counts_out) KCUDA(ctx, cudaMemcpyAsync(counts_out, all_counts, sizeof(kareto_counts) * n_cfg, kind, st));
     if (obj_out) KCUDA(ctx, cudaMemcpyAsync(obj_out, all_obj, 24 * n_cfg, kind, st));
   }
-  return sync(ctx, "eval_grid");
+  HT("copies");
+  kareto_status sst = sync(ctx, "eval_grid");
+  HT("synced");
+  return sst;
 }
 
 }  // namespace kareto

@@ -13,26 +13,37 @@
 
 namespace kareto {
 
-__global__ void k_line_keys(const kareto_config *__restrict__ cfg, int64_t n, int a, uint64_t *__restrict__ key,
-                            uint32_t *__restrict__ idx) {
+// Line key of axis a, packed with the bit widths the configurations actually use (w[0..2]: axis
+// index widths, w[3] tuner, w[4] medium, w[5] policy): low to high, axis[a] | axis[o2] | axis[o1]
+// | tuner | medium | policy.  Sorting only the used bits groups each line and orders it by
+// axis[a]; the order of the lines does not matter (the scan restarts per line).
+struct LineWidths {
+  int w[6];
+};
+__global__ void k_line_keys(const kareto_config *__restrict__ cfg, int64_t n, int a, LineWidths lw,
+                            uint64_t *__restrict__ key, uint32_t *__restrict__ idx) {
+  const int o1 = (a + 1) % 3, o2 = (a + 2) % 3;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const kareto_config c = cfg[i];
-    int o1 = (a + 1) % 3, o2 = (a + 2) % 3;
-    uint64_t line = ((uint64_t)c.policy << 46) | ((uint64_t)c.medium << 42) | ((uint64_t)c.tuner << 32) |
-                    ((uint64_t)(uint32_t)c.axis[o1] << 16) | (uint64_t)(uint32_t)c.axis[o2];
-    key[i] = (line << 16) | (uint64_t)(uint32_t)c.axis[a];
+    uint64_t k = c.policy;
+    k = (k << lw.w[4]) | c.medium;
+    k = (k << lw.w[3]) | c.tuner;
+    k = (k << lw.w[o1]) | (uint32_t)c.axis[o1];
+    k = (k << lw.w[o2]) | (uint32_t)c.axis[o2];
+    k = (k << lw.w[a]) | (uint32_t)c.axis[a];
+    key[i] = k;
     idx[i] = (uint32_t)i;
   }
 }
 
-__global__ void k_line_stop(const uint64_t *__restrict__ key, const uint32_t *__restrict__ idx, int64_t n,
+__global__ void k_line_stop(const uint64_t *__restrict__ key, const uint32_t *__restrict__ idx, int64_t n, int wa,
                             const double *__restrict__ f, double tau_e, uint64_t *__restrict__ line,
                             uint8_t *__restrict__ stop) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t li = key[i] >> 16;
+    uint64_t li = key[i] >> wa;
     line[i] = li;
     uint8_t s = 0;
-    if (i > 0 && (key[i - 1] >> 16) == li) {
+    if (i > 0 && (key[i - 1] >> wa) == li) {
       double p = f[3 * (size_t)idx[i - 1]], q = f[3 * (size_t)idx[i]];
       double ap = p < 0 ? -p : p, aq = q < 0 ? -q : q;
       double den = ap > aq ? ap : aq;
@@ -137,16 +148,28 @@ static kareto_status pareto(kareto_ctx *ctx, const double *obj, const kareto_con
   if (n < 0 || (n > 0 && (!obj || !status_out))) return fail(ctx, KARETO_E_INVALID, "bad arguments");
   if (n >= (int64_t)0x7FFFFFFF) return fail(ctx, KARETO_E_OVERFLOW, "too many configurations");
   const bool do_prune = prune && prune->enabled;
+  LineWidths lw{};
   if (do_prune) {
     if (!cfg) return fail(ctx, KARETO_E_INVALID, "pruning needs the configurations");
+    uint32_t mx[6] = {0, 0, 0, 0, 0, 0};
     for (int64_t i = 0; i < n; i++) {
       const kareto_config &c = cfg[i];
-      for (int a = 0; a < 3; a++)
+      for (int a = 0; a < 3; a++) {
         if (c.axis[a] < 0 || c.axis[a] > 65535) return fail(ctx, KARETO_E_INVALID, "config %lld: axis out of range", (long long)i);
+        mx[a] |= (uint32_t)c.axis[a];
+      }
       if (c.tuner > 1023 || c.medium > 15 || c.policy > 3)
         return fail(ctx, KARETO_E_INVALID, "config %lld: line key out of range", (long long)i);
+      mx[3] |= c.tuner; mx[4] |= c.medium; mx[5] |= c.policy;
+    }
+    for (int k = 0; k < 6; k++) {  // bits needed by the OR of the values = bits of the maximum
+      lw.w[k] = 0;
+      while (lw.w[k] < 32 && (mx[k] >> lw.w[k]) != 0) lw.w[k]++;
     }
   }
+  int key_bits = 0;
+  for (int k = 0; k < 6; k++) key_bits += lw.w[k];
+  if (key_bits == 0) key_bits = 1;
   if (n == 0) {
     if (n_frontier) *n_frontier = 0;
     return KARETO_OK;
@@ -172,17 +195,18 @@ static kareto_status pareto(kareto_ctx *ctx, const double *obj, const kareto_con
     for (int a = 0; a < 3; a++) {
       {
         Pass ps(ctx, "K8a_line_keys", 1, 1);
-        k_line_keys<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(dcfg.p, n, a, key.p, idx.p);
+        k_line_keys<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(dcfg.p, n, a, lw, key.p, idx.p);
       }
       {
         Pass ps(ctx, "K8a_sort_lines", 0, 1);
         KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
-          return cub::DeviceRadixSort::SortPairs(t, b, key.p, key_s.p, idx.p, idx_s.p, (int)n, 0, 64, st);
+          return cub::DeviceRadixSort::SortPairs(t, b, key.p, key_s.p, idx.p, idx_s.p, (int)n, 0, key_bits, st);
         }));
       }
       {
         Pass ps(ctx, "K8a_line_stop", 1, 2);
-        k_line_stop<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(key_s.p, idx_s.p, n, f, prune->tau_e, line.p, stop.p);
+        k_line_stop<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(key_s.p, idx_s.p, n, lw.w[a], f, prune->tau_e, line.p,
+                                                               stop.p);
         KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
           return cub::DeviceScan::ExclusiveScanByKey(t, b, line.p, stop.p, excl.p, MaxOp(), (uint8_t)0, (int)n,
                                                      cub::Equality(), st);

@@ -30,12 +30,32 @@ static kareto_status cub_call(kareto_ctx *ctx, DBuf<uint8_t> &tmp, F &&f) {
 }
 
 // ------------------------------------------------------------------ a1 ----
+// order-preserving signed -> unsigned key, and its min / max (the sort then covers only the bits
+// of max - min: a 2-hour trace needs ~23 bits, i.e. 3 radix passes instead of 8)
 __global__ void k_sort_keys(const int64_t *__restrict__ arrival, int64_t R, uint64_t *__restrict__ key,
-                            uint32_t *__restrict__ idx) {
+                            uint32_t *__restrict__ idx, unsigned long long *__restrict__ mnmx) {
+  unsigned long long mn = ~0ull, mx = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R; i += (int64_t)gridDim.x * blockDim.x) {
-    key[i] = (uint64_t)arrival[i] ^ 0x8000000000000000ULL;  // order-preserving signed -> unsigned
+    const uint64_t k = (uint64_t)arrival[i] ^ 0x8000000000000000ULL;
+    key[i] = k;
     idx[i] = (uint32_t)i;
+    mn = k < mn ? k : mn;
+    mx = k > mx ? k : mx;
   }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+    mn = a < mn ? a : mn;
+    mx = b > mx ? b : mx;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&mnmx[0], mn);
+    atomicMax(&mnmx[1], mx);
+  }
+}
+__global__ void k_rebase_keys(uint64_t *__restrict__ key, int64_t R, const unsigned long long *__restrict__ mnmx) {
+  const uint64_t mn = mnmx[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R; i += (int64_t)gridDim.x * blockDim.x)
+    key[i] -= mn;
 }
 
 __global__ void k_req_meta(int64_t R, int mode, const uint32_t *__restrict__ order, const int64_t *__restrict__ arrival,
@@ -784,14 +804,26 @@ kareto_status ingest(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_trace *
   KTRY(skey.alloc(ctx, R)); KTRY(skey2.alloc(ctx, R)); KTRY(sidx.alloc(ctx, R)); KTRY(order.alloc(ctx, R));
   KTRY(arr_sorted.alloc(ctx, R)); KTRY(in.src_off.alloc(ctx, R)); KTRY(in.nblk.alloc(ctx, R + 1));
   KTRY(s64.alloc(ctx, R + 1));
+  int key_bits = 64;
   {
-    Pass ps(ctx, "a1_sort_keys", 1, 1);
-    k_sort_keys<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(in.arrival, R, skey.p, sidx.p);
+    Pass ps(ctx, "a1_sort_keys", 1, 2);
+    DBuf<unsigned long long> mnmx;
+    KTRY(mnmx.alloc(ctx, 2));
+    const unsigned long long init[2] = {~0ull, 0ull};
+    KCUDA(ctx, cudaMemcpyAsync(mnmx.p, init, 16, cudaMemcpyHostToDevice, st));
+    k_sort_keys<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(in.arrival, R, skey.p, sidx.p, mnmx.p);
+    k_rebase_keys<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(skey.p, R, mnmx.p);
+    unsigned long long h[2];
+    KCUDA(ctx, cudaMemcpyAsync(h, mnmx.p, 16, cudaMemcpyDeviceToHost, st));
+    KCUDA(ctx, cudaStreamSynchronize(st));
+    const uint64_t span = h[1] - h[0];
+    key_bits = 1;
+    while (key_bits < 64 && (span >> key_bits) != 0) key_bits++;
   }
   {
     Pass ps(ctx, "a1_sort_requests", 0, 1);
     KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
-      return cub::DeviceRadixSort::SortPairs(t, b, skey.p, skey2.p, sidx.p, order.p, (int)R, 0, 64, st);
+      return cub::DeviceRadixSort::SortPairs(t, b, skey.p, skey2.p, sidx.p, order.p, (int)R, 0, key_bits, st);
     }));
   }
   KCUDA(ctx, cudaMemsetAsync(in.nblk.p + R, 0, 8, st));

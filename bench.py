@@ -753,6 +753,12 @@ def main():
                 "avg_launch_ms": per_launch_ms,
                 "share_of_step": top["ms"] / prof_steps / ms_step}
     stage_ms = {p["name"]: round(p["ms"] / prof_steps, 4) for p in passes}
+    # end-to-end algorithmic roofline: the bytes the method itself must move
+    # per step -- K1 72 B/block (64 B tokens + 8 B hash), K2 22 B/access, K3 12 B/access, K4
+    # 16 B/access, K6 17 B per replayed access-config -- over (step time x measured HBM peak)
+    algo_step = 122 * n_local + 17 * n_local * n_replay / world
+    algo_roof = {"bytes_per_step": algo_step, "frac": algo_step / (ms_step * 1e-3) / (peak * 1e9),
+                 "per_unit": "K1 72 B/block + K2 22 + K3 12 + K4 16 B/access (+ K6 17 B/access-config)"}
 
     # ---- end to end through the C ABI with host (pinned) buffers, H2D + D2H in the region
     e2e = None
@@ -821,7 +827,8 @@ def main():
                            "pruning": spec["prune"], "replay_configs": n_replay},
                 "block_accesses_per_s": N / (ms_step * 1e-3),
                 "effective_access_configs_per_s": N * n_cfg / (ms_step * 1e-3),
-                "frontier": nf, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "frontier": nf, "roofline": roof, "algorithmic_roofline": algo_roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches),
                 "gpu_launches_per_step": launches / args.steps, "clocks": clk.summary(), "stage_ms": stage_ms,
                 "generation_s": round(gen_s, 2)}
         print(json.dumps(line), flush=True)

@@ -65,6 +65,8 @@ def grid(U, ttl_mode=True):
         for j, b in enumerate(A(4, max(U // 4, 3))):
             for k, c in enumerate(A(3, U)):
                 caps.append([a, b, c]); axis.append([i, j, k]); tun.append(0)
+                if ttl_mode:  # finite disk with a uniform TTL row: stack path with delta-binned K4 cells
+                    caps.append([a, b, c]); axis.append([i, j, k]); tun.append(1)
             if ttl_mode:
                 for t in (1, 2):
                     caps.append([a, b, K.INF]); axis.append([i, j, 3]); tun.append(t)

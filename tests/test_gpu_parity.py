@@ -372,3 +372,24 @@ def test_full_size_config2_sampled(ctx):
     want = ot.stack_counts(cf[idx])
     assert_counts_equal(got[idx], want, cf[idx])
     assert_obj_equal(obj[idx], ot.objective(O.Model(**MODEL_KW), cf[idx], want))
+
+
+@pytest.mark.parametrize("config", [2, 4])
+def test_full_size_selection(ctx, config):
+    """K8 at BASELINE full size in bench.py's launch configuration: the GPU's objective vectors of
+    config 2 (16,384 configs, no pruning) / config 4 (130,944 configs, pruning tau_e = 0.05) go
+    through kareto_pareto and through the oracle's select (R34 pruning + R35 dominance); the
+    status of every configuration must agree (objectives themselves: test_full_size_config2_sampled)."""
+    import bench
+    spec = bench.CONFIGS[config]
+    tr = ki.synthetic(spec["kind"], R=spec.get("R", 0), N=spec.get("N", 0), seed=0)
+    gt = ctx.load(tr, top_k=spec.get("top_k", 16))
+    cfg, ttl = bench.build_grid(K, spec, gt)
+    _, obj = ctx.eval_grid(gt, cfg, K.Model(), ttl)
+    st, nf = ctx.pareto(obj, cfg, spec["prune"])
+    oc = np.zeros(len(cfg), O.CONFIG_DTYPE)
+    for f in ("cap", "policy", "medium", "tuner", "axis"):
+        oc[f] = cfg[f]
+    want = O.select(obj, oc, spec["prune"])
+    assert np.array_equal(st, want)
+    assert nf == int((want == 1).sum()) and nf > 0

@@ -282,3 +282,39 @@ def test_time_shard_chain_violation_across_shards():
         return ei.value.status
 
     assert run_ranks(2, fn) == [K.E_CHAIN] * 2
+
+
+@pytest.mark.parametrize("W", [2, 3, 8])
+def test_time_shard_full_size_config2(W):
+    """BASELINE config 2 at full size (1e6 requests, 1.06e8 accesses) time-sharded over W
+    loopback ranks: every access's prev / delta / depth equal the whole-trace load's (itself
+    checked against the oracle at this size in test_gpu_parity.test_full_size_config2_sampled),
+    and so do U, the group tables and the counts of the 16,384-configuration grid."""
+    import torch
+    import bench
+    spec = bench.CONFIGS[2]
+    tr = ki.synthetic("chat", R=spec["R"], seed=0)
+    c1 = K.Context(0, torch.cuda.current_stream().cuda_stream)
+    whole = c1.load(tr, top_k=16)
+    cfg, ttl = bench.build_grid(K, spec, whole)
+    want_c, want_o = c1.eval_grid(whole, cfg, K.Model(), ttl)
+    ref = {x: whole.export(x) for x in (K.X_PREV, K.X_DELTA, K.X_DEPTH, K.X_GROUP)}
+    U, Ug, Rg = whole.U, whole.U_g.copy(), whole.reuse_g.copy()
+    whole.free()
+
+    def fn(r, ctx):
+        gt = ctx.load(tr, top_k=16, time_shard=True)
+        res = {x: gt.export(x) for x in (K.X_PREV, K.X_DELTA, K.X_DEPTH, K.X_GROUP)}
+        res.update(U=gt.U, Ug=gt.U_g.copy(), Rg=gt.reuse_g.copy(), rlo=gt.req_lo, rhi=gt.req_hi)
+        res["c"], res["o"] = ctx.eval_grid(gt, cfg, K.Model(), ttl)
+        gt.free()
+        return res
+
+    out = run_ranks(W, fn)
+    for x in (K.X_PREV, K.X_DELTA, K.X_DEPTH):
+        assert np.array_equal(np.concatenate([o[x] for o in out]), ref[x]), x
+    for o in out:
+        assert o["U"] == U and np.array_equal(o["Ug"], Ug) and np.array_equal(o["Rg"], Rg)
+        assert np.array_equal(o[K.X_GROUP][o["rlo"]:o["rhi"]], ref[K.X_GROUP][o["rlo"]:o["rhi"]])
+        assert np.array_equal(np.asarray(o["c"]).view(np.uint8), np.asarray(want_c).view(np.uint8))
+        assert np.array_equal(o["o"].view(np.uint64), want_o.view(np.uint64))

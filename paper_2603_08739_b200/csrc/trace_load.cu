@@ -208,7 +208,10 @@ __device__ __forceinline__ void load_half_tokens(const uint32_t *p, const uint32
   for (int i = 0; i < 8; i++) t[i] = (mis & 2) ? u[i + 2] : u[i];
 }
 
-constexpr int K1_THREADS = 256;
+// 2 warps per CTA: a warp whose request-aligned range holds a long request (agent contexts up to
+// 8K blocks) keeps only its partner idle, not 7 (config 4: 1.83 -> 1.75 ms; 32 resident CTAs of
+// 64 threads still fill an SM)
+constexpr int K1_THREADS = 64;
 constexpr int K1_WARPS = K1_THREADS / 32;
 
 // Every WARP owns a request-aligned range of sorted blocks [s[rb], s[re)) (rb, re = first

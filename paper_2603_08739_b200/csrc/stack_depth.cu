@@ -92,12 +92,23 @@ __global__ void k_run_items(const int *__restrict__ m_ptr, const uint32_t *__res
   const int M = *m_ptr;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < M; q += gridDim.x * blockDim.x) {
     uint32_t r = run_req[q];
-    int lo = 0, hi = q;  // first run of request r
-    while (lo < hi) { int m = (lo + hi) >> 1; if (run_req[m] >= r) hi = m; else lo = m + 1; }
-    int q0 = lo;
-    lo = q + 1; hi = M;  // one past the last run of request r
-    while (lo < hi) { int m = (lo + hi) >> 1; if (run_req[m] > r) hi = m; else lo = m + 1; }
-    int nr = lo - q0;
+    // a request has few runs: short linear scans (coalesced neighbours), binary search beyond
+    int q0 = q, steps = 0;  // first run of request r
+    while (q0 > 0 && run_req[q0 - 1] == r && steps < 8) { q0--; steps++; }
+    if (q0 > 0 && run_req[q0 - 1] == r) {
+      int lo = 0, hi = q0;
+      while (lo < hi) { int m = (lo + hi) >> 1; if (run_req[m] >= r) hi = m; else lo = m + 1; }
+      q0 = lo;
+    }
+    int q1 = q + 1;  // one past the last run of request r
+    steps = 0;
+    while (q1 < M && run_req[q1] == r && steps < 8) { q1++; steps++; }
+    if (q1 < M && run_req[q1] == r) {
+      int lo = q1, hi = M;
+      while (lo < hi) { int m = (lo + hi) >> 1; if (run_req[m] > r) hi = m; else lo = m + 1; }
+      q1 = lo;
+    }
+    int nr = q1 - q0;
     uint32_t p0 = run_p0[q];
     items[q + q0] = make_uint2(p0, 0u);
     items[q + q0 + nr] = make_uint2(p0, kPointBit | run_len[q]);

@@ -706,10 +706,19 @@ __global__ void k_group_tables(int64_t R, uint32_t r_base, const uint16_t *__res
   extern __shared__ unsigned long long ts[];
   for (int i = threadIdx.x; i < 2 * G; i += blockDim.x) ts[i] = 0;
   __syncthreads();
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
-    int g = grp[r_base + r];
-    if (first_cnt[r]) atomicAdd(&ts[2 * g], (unsigned long long)first_cnt[r]);
-    if (reuse_cnt[r]) atomicAdd(&ts[2 * g + 1], (unsigned long long)reuse_cnt[r]);
+  // few groups, many requests: reduce within the warp per group first (match_any), then one
+  // shared-memory atomic per (warp, group)
+  const int64_t Rp = (R + 31) & ~(int64_t)31;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < Rp; r += (int64_t)gridDim.x * blockDim.x) {
+    const bool in = r < R;
+    const int g = in ? grp[r_base + r] : -1;
+    const uint32_t fc = in ? first_cnt[r] : 0u, rc = in ? reuse_cnt[r] : 0u;
+    const unsigned same = __match_any_sync(0xFFFFFFFFu, g);
+    const uint32_t fs = __reduce_add_sync(same, fc), rs = __reduce_add_sync(same, rc);
+    if (in && (int)(threadIdx.x & 31) == __ffs(same) - 1) {
+      if (fs) atomicAdd(&ts[2 * g], (unsigned long long)fs);
+      if (rs) atomicAdd(&ts[2 * g + 1], (unsigned long long)rs);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 2 * G; i += blockDim.x)
@@ -1088,7 +1097,8 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
     KTRY(rank.alloc(ctx, R)); KTRY(gtab.alloc(ctx, 2 * (K + 1))); KTRY(gtab.zero());
     DBuf<uint64_t> rkey_c;
     KTRY(rkey_c.alloc(ctx, R));
-    Pass ps(ctx, "K2_groups", 1, 8);
+    {
+    Pass ps(ctx, "K2g_select", 1, 1);
     k_root_keys<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(R, tr->s, tr->hash, 0, rkey.p, rval.p, rflag.p);
     KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
       return cub::DeviceSelect::Flagged(t, b, rkey.p, rflag.p, rkey_c.p, m_dev.p, (int)R, st);
@@ -1096,14 +1106,19 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
     KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
       return cub::DeviceSelect::Flagged(t, b, rval.p, rflag.p, rval_c.p, m_dev.p, (int)R, st);
     }));
+    }
     int m = 0;
     KCUDA(ctx, cudaMemcpyAsync(&m, m_dev.p, 4, cudaMemcpyDeviceToHost, st));
     KCUDA(ctx, cudaStreamSynchronize(st));
     k_fill_u16<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(tr->grp, R, (uint16_t)K);
     if (m > 0) {
+      {
+      Pass ps(ctx, "K2g_sort_roots", 0, 1);
       KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
         return cub::DeviceRadixSort::SortPairs(t, b, rkey_c.p, rkey_s.p, rval_c.p, rval_s.p, m, 0, 64, st);
       }));
+      }
+      Pass ps(ctx, "K2g_rank", 1, 6);
       k_run_heads<<<grid_for(m, 256, 4 * sms), 256, 0, st>>>(rkey_s.p, m_dev.p, head.p);
       KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
         return cub::DeviceScan::InclusiveSum(t, b, head.p, run_incl.p, m, st);
@@ -1118,6 +1133,7 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
       k_rank_of_run<<<grid_for(m, 256, 4 * sms), 256, 0, st>>>(ranked.p, nruns.p, rank.p);
       k_assign_groups<<<grid_for(m, 256, 4 * sms), 256, 0, st>>>(rval_s.p, run_incl.p, m_dev.p, rank.p, K, tr->grp);
     }
+    Pass ps2(ctx, "K2g_tables", 1, 1);
     k_group_tables<<<grid_for(R, 256, 4 * sms), 256, 16 * (K + 1), st>>>(R, 0, tr->grp, first_cnt.p, reuse_cnt.p,
                                                                           gtab.p, K + 1);
     std::vector<unsigned long long> h(2 * (K + 1));

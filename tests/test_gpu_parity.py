@@ -393,3 +393,24 @@ def test_full_size_selection(ctx, config):
     want = O.select(obj, oc, spec["prune"])
     assert np.array_equal(st, want)
     assert nf == int((want == 1).sum()) and nf > 0
+
+
+def test_config5_million_configs_windowed_histograms(ctx):
+    """BASELINE config 5 (i): the 100 x 100 x 100 LRU grid (10^6 configurations) on the R = 1e4
+    chat trace.  Its ~10^6 distinct tier boundaries exceed shared memory, so K4 takes the windowed
+    multi-pass histograms (k_hist_d / k_hist_D); sampled configurations against the oracle's O2
+    stack counts and O1 replay, objectives bit-identical, and LRU inclusion across the grid."""
+    tr = ki.synthetic("chat", R=10_000, seed=0)
+    ot = O.OracleTrace(tr, top_k=16)
+    gt = ctx.load(tr, top_k=16)
+    caps, axis = baseline_grid(ot.U, 100, 100, 100, 16, 2, 1)
+    cf = O.configs(caps, axis=axis)
+    got, obj = ctx.eval_grid(gt, kcfg(cf), K.Model(**MODEL_KW))
+    idx = np.random.default_rng(7).choice(len(cf), 512, replace=False)
+    want = ot.stack_counts(cf[idx])
+    assert_counts_equal(got[idx], want, cf[idx])
+    assert_obj_equal(obj[idx], ot.objective(O.Model(**MODEL_KW), cf[idx], want))
+    assert_counts_equal(got[idx[:8]], ot.replay(cf[idx[:8]]), cf[idx[:8]])
+    # inclusion (Mattson): along the DRAM axis with HBM and disk fixed, total hits never decrease
+    h = np.asarray(got["hit"]).sum(1).reshape(100, 100, 100)
+    assert np.all(np.diff(h, axis=1) >= 0)

@@ -61,6 +61,32 @@ def test_shard_range_partitions(lib):
             assert max(sizes) - min(sizes) <= 1
 
 
+def test_time_slices_and_hash_owner(lib):
+    """Host rules of the time-sharded load (kareto_time_slices, kareto_hash_owner): slices tile
+    the sorted requests in order, each rank's first block position is the first request start at
+    or after k N / W (requests without blocks included), owners cover [0, W) near-uniformly."""
+    rng = np.random.default_rng(0)
+    nb = rng.integers(0, 50, size=2000)
+    nb[rng.integers(0, 2000, size=200)] = 0  # requests without full blocks
+    s = np.concatenate([[0], np.cumsum(nb)]).astype(np.uint32)
+    N = int(s[-1])
+    for world in (1, 2, 3, 7, 8, 128):
+        rb = K.time_slices(s, world)
+        assert rb[0] == 0 and rb[-1] == len(s) - 1 and np.all(np.diff(rb) >= 0)
+        for k in range(world):
+            want = int(np.searchsorted(s[:-1], N * k // world, side="left"))
+            assert rb[k] == want
+    with pytest.raises(K.KaretoError):
+        K.time_slices(s, 0)
+    hs = rng.integers(0, 2**63, size=20000, dtype=np.int64).astype(np.uint64)
+    for world in (1, 3, 8):
+        own = np.array([K.hash_owner(int(h), world) for h in hs])
+        assert own.min() >= 0 and own.max() < world
+        cnt = np.bincount(own, minlength=world)
+        assert cnt.min() > 0.8 * len(hs) / world
+    assert K.hash_owner(123, 0) == -1
+
+
 def test_invalid_arguments_without_gpu(lib):
     h = ctypes.c_void_p()
     assert lib.kareto_create(0, None, None, 2, 1, ctypes.byref(h)) == K.E_INVALID  # rank >= world

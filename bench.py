@@ -727,7 +727,8 @@ def main():
     if k6:  # one roofline entry for the replay (its class passes merged)
         passes = [p for p in passes if not p["name"].startswith("K6_replay")] + [
             {"name": "K6_replay", "ms": sum(p["ms"] for p in k6), "launches": sum(p["launches"] for p in k6),
-             "own": 1}] + [dict(p, name=p["name"].replace("K6_replay", "K6class")) for p in k6]
+             "own": 1}] + [dict(p, name=p["name"].replace("K6_replay", "K6class")) for p in k6
+                           if p["name"] != "K6_replay"]  # per-class passes (sequential replay) only
     if k6 and n_replay:
         # this rank's replayed configurations (the cost-weighted shard is ~1/world of them) over all
         # K6 launches (waves of the four classes)

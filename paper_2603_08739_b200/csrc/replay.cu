@@ -751,6 +751,152 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
   DBuf<kareto_config> dcfg;
   KTRY(dcfg.alloc(ctx, n));
   KCUDA(ctx, cudaMemcpyAsync(dcfg.p, cfg_host, sizeof(kareto_config) * n, cudaMemcpyHostToDevice, st));
+  // Concurrent classes (no f3 queue): a wave is one pass over the trace whatever its width (the
+  // kernel is latency-bound at these occupancies), so sequential classes waste the unused part
+  // of each class's last wave.  Instead every class runs its waves on its own stream with a share
+  // of the memory budget proportional to its work (configurations x bytes x relative pass cost),
+  // so the classes finish together.
+  if (!Qm && getenv("KARETO_K6_SEQUENTIAL") == nullptr) {
+    int nonempty = 0;
+    for (int q = 0; q < 5; q++) nonempty += !cls[q].empty();
+    if (nonempty >= 2) {
+      const uint64_t FM = (uint64_t)tr->R + 2;
+      const uint64_t NW = (FM + 63) / 64, NSW = (NW + 63) / 64;
+      const uint64_t es = U + 1;
+      auto per_cfg_of = [&](int q) {
+        const bool lfu = q == 2 || q == 3, eheap = q == 1 || q == 3, glist = q == 4;
+        return U * (1 + 4 + 8) + (lfu ? U * 4 + 3 * 8 * (FM + NW + NSW) : 0) + (eheap ? U * 4 + 8 * es : 0) +
+               (glist ? U * 8 + 8 * (uint64_t)G : 0);
+      };
+      // relative time of one pass over the trace per class (measured on the config-3 twin)
+      const double pass_cost[5] = {1.0, 2.0, 1.2, 2.65, 1.9};
+      size_t freeb = 0, totb = 0, rsv = 0, used = 0;
+      KCUDA(ctx, cudaStreamSynchronize(st));
+      KCUDA(ctx, cudaMemGetInfo(&freeb, &totb));
+      cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, &rsv);
+      cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemCurrent, &used);
+      const double budget = 0.8 * ((double)freeb + (double)(rsv > used ? rsv - used : 0));
+      double wsum = 0;
+      for (int q = 0; q < 5; q++) wsum += (double)cls[q].size() * (double)per_cfg_of(q) * pass_cost[q];
+      struct ClassState {
+        DBuf<uint8_t> tier;
+        DBuf<uint32_t> lt, freq, bht, epos, didx, eht;
+        DBuf<uint2> link, elink;
+        DBuf<uint64_t> occ, ekey;
+        RState v{};
+        uint64_t W = 0;
+        cudaStream_t s = nullptr;
+        cudaEvent_t done = nullptr;
+      };
+      ClassState C[5];
+      int launches = 0;
+      for (int q = 0; q < 5; q++) {
+        std::vector<uint32_t> &ix = cls[q];
+        if (ix.empty()) continue;
+        std::stable_sort(ix.begin(), ix.end(), [&](uint32_t a, uint32_t b) {
+          const kareto_config &x = cfg_host[a], &y = cfg_host[b];
+          if (x.policy != y.policy) return x.policy < y.policy;
+          if (x.tuner != y.tuner) return x.tuner < y.tuner;
+          for (int t = 0; t < 3; t++)
+            if (x.cap[t] != y.cap[t]) return x.cap[t] < y.cap[t];
+          return false;
+        });
+        const bool lfu = q == 2 || q == 3, eheap = q == 1 || q == 3, glist = q == 4;
+        const uint64_t pc = per_cfg_of(q);
+        const double share = budget * ((double)ix.size() * (double)pc * pass_cost[q]) / wsum;
+        uint64_t W = (uint64_t)(share / (double)pc);
+        if (W > ix.size()) W = ix.size();
+        if (W > (1u << 20)) W = 1u << 20;
+        if (W < 1) return fail(ctx, KARETO_E_OOM, "replay needs %llu bytes per configuration", (unsigned long long)pc);
+        const uint64_t nwaves = (ix.size() + W - 1) / W;
+        W = (ix.size() + nwaves - 1) / nwaves;
+        launches += (int)nwaves;
+        ClassState &c = C[q];
+        c.W = W;
+        KTRY(c.tier.alloc(ctx, U * W)); KTRY(c.lt.alloc(ctx, U * W)); KTRY(c.link.alloc(ctx, U * W));
+        if (lfu) {
+          KTRY(c.freq.alloc(ctx, U * W)); KTRY(c.bht.alloc(ctx, 6 * FM * W)); KTRY(c.occ.alloc(ctx, 3 * (NW + NSW) * W));
+        }
+        if (eheap) { KTRY(c.epos.alloc(ctx, U * W)); KTRY(c.ekey.alloc(ctx, es * W)); }
+        if (glist) { KTRY(c.elink.alloc(ctx, U * W)); KTRY(c.eht.alloc(ctx, 2 * (size_t)G * W)); }
+        KTRY(c.didx.alloc(ctx, ix.size()));
+        KCUDA(ctx, cudaMemcpyAsync(c.didx.p, ix.data(), 4 * ix.size(), cudaMemcpyHostToDevice, st));
+        RState &v = c.v;
+        v.tier = c.tier.p; v.lt = c.lt.p; v.link = c.link.p;
+        if (lfu) {
+          v.freq = c.freq.p;
+          for (int t = 0; t < 3; t++) {
+            v.bh[t] = c.bht.p + (size_t)(2 * t) * FM * W;
+            v.bt[t] = c.bht.p + (size_t)(2 * t + 1) * FM * W;
+            v.occ[t] = c.occ.p + (size_t)t * (NW + NSW) * W;
+            v.occ2[t] = v.occ[t] + NW * W;
+          }
+          v.NW = (uint32_t)NW;
+          v.NSW = (uint32_t)NSW;
+        }
+        v.epos = c.epos.p; v.ekey = c.ekey.p;
+        v.elink = c.elink.p;
+        v.eh = c.eht.p;
+        v.et = c.eht.p + (size_t)G * W;
+        v.gblk = tr->gblk;
+        v.W = W;
+      }
+      cudaEvent_t fork;
+      KCUDA(ctx, cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+      kareto_status rs = KARETO_OK;
+      {
+        Pass ps(ctx, "K6_replay", 1, launches);
+        cudaError_t e = cudaEventRecord(fork, st);  // allocations and index uploads done on st
+        QueueKernelArgs qa{};
+        for (int q = 0; q < 5 && e == cudaSuccess; q++) {
+          const std::vector<uint32_t> &ix = cls[q];
+          if (ix.empty()) continue;
+          ClassState &c = C[q];
+          const bool lfu = q == 2 || q == 3, eheap = q == 1 || q == 3, glist = q == 4;
+          const uint64_t W = c.W;
+          if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking);
+          if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming);
+          if (e == cudaSuccess) e = cudaStreamWaitEvent(c.s, fork, 0);
+          for (uint64_t w0 = 0; w0 < ix.size() && e == cudaSuccess; w0 += W) {
+            const int64_t nw = (int64_t)(ix.size() - w0 < W ? ix.size() - w0 : W);
+            cudaMemsetAsync(c.tier.p, 0, U * W, c.s);
+            cudaMemsetAsync(c.lt.p, 0xFF, 4 * U * W, c.s);
+            if (lfu) {
+              cudaMemsetAsync(c.bht.p, 0xFF, 4 * 6 * FM * W, c.s);
+              cudaMemsetAsync(c.occ.p, 0, 8 * 3 * (NW + NSW) * W, c.s);
+            }
+            if (eheap) cudaMemsetAsync(c.epos.p, 0xFF, 4 * U * W, c.s);
+            if (glist) cudaMemsetAsync(c.eht.p, 0xFF, 4 * 2 * (size_t)G * W, c.s);
+            const unsigned grid = (unsigned)((nw + 63) / 64);
+            const uint32_t *wi = c.didx.p + w0;
+#define KREPC(L, E) k_replay<L, E, false><<<grid, 64, 0, c.s>>>(T, dcfg.p, wi, rows_dev, n_tuner, G, c.v, nw, counts_dev, qa)
+            if (q == 0) KREPC(false, 0);
+            if (q == 1) KREPC(false, 1);
+            if (q == 2) KREPC(true, 0);
+            if (q == 3) KREPC(true, 1);
+            if (q == 4) KREPC(false, 2);
+#undef KREPC
+            e = cudaGetLastError();
+          }
+        }
+        // join every started class before the buffers are freed on st (also on errors)
+        for (int q = 0; q < 5; q++) {
+          if (!C[q].s) continue;
+          if (C[q].done && cudaEventRecord(C[q].done, C[q].s) == cudaSuccess) cudaStreamWaitEvent(st, C[q].done, 0);
+          else cudaStreamSynchronize(C[q].s);
+        }
+        if (e != cudaSuccess) rs = fail(ctx, KARETO_E_CUDA, "concurrent replay: %s", cudaGetErrorString(e));
+      }
+      if (rs == KARETO_OK) rs = sync(ctx, "replay");
+      else cudaStreamSynchronize(st);
+      for (int q = 0; q < 5; q++) {
+        if (C[q].s) cudaStreamDestroy(C[q].s);
+        if (C[q].done) cudaEventDestroy(C[q].done);
+      }
+      cudaEventDestroy(fork);
+      return rs;
+    }
+  }
   for (int q = 0; q < 5; q++) {
     std::vector<uint32_t> &ix = cls[q];
     if (ix.empty()) continue;

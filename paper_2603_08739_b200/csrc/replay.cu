@@ -842,7 +842,8 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
         v.W = W;
       }
       cudaEvent_t fork;
-      KCUDA(ctx, cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+      const bool dbg = getenv("KARETO_DEBUG") != nullptr;  // per-class finish times
+      KCUDA(ctx, cudaEventCreateWithFlags(&fork, dbg ? cudaEventDefault : cudaEventDisableTiming));
       kareto_status rs = KARETO_OK;
       {
         Pass ps(ctx, "K6_replay", 1, launches);
@@ -855,7 +856,7 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
           const bool lfu = q == 2 || q == 3, eheap = q == 1 || q == 3, glist = q == 4;
           const uint64_t W = c.W;
           if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking);
-          if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming);
+          if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.done, dbg ? cudaEventDefault : cudaEventDisableTiming);
           if (e == cudaSuccess) e = cudaStreamWaitEvent(c.s, fork, 0);
           for (uint64_t w0 = 0; w0 < ix.size() && e == cudaSuccess; w0 += W) {
             const int64_t nw = (int64_t)(ix.size() - w0 < W ? ix.size() - w0 : W);
@@ -889,6 +890,13 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
       }
       if (rs == KARETO_OK) rs = sync(ctx, "replay");
       else cudaStreamSynchronize(st);
+      if (dbg && rs == KARETO_OK)
+        for (int q = 0; q < 5; q++) {
+          float ms = 0.f;
+          if (C[q].done && cudaEventElapsedTime(&ms, fork, C[q].done) == cudaSuccess)
+            fprintf(stderr, "[kareto] K6 class %d: %zu configs, waves of %llu, done after %.1f ms\n", q,
+                    cls[q].size(), (unsigned long long)C[q].W, ms);
+        }
       for (int q = 0; q < 5; q++) {
         if (C[q].s) cudaStreamDestroy(C[q].s);
         if (C[q].done) cudaEventDestroy(C[q].done);

@@ -186,7 +186,12 @@ typedef struct {
  *   outputs_on_device selects device (1) or host (0) output pointers.
  * Errors: KARETO_E_INVALID (policy > 2, tuner >= n_tuner, medium >= n_media, TTL mode with
  * an infinite TTL (R22), invalid model constants), _E_UNSUPPORTED (a configuration needs
- * the per-configuration replay and this build has none for it), _E_OVERFLOW, _E_NCCL. */
+ * the per-configuration replay and this build has none for it), _E_OVERFLOW (also: replay
+ * configurations on a trace with 3N >= 2^32 accesses, the K6 sequence range), _E_OOM (one
+ * replay configuration's state does not fit the device), _E_NCCL.
+ * Memory: K6 replay state is sized per wave to 80% of the free device memory (divided among
+ * loopback ranks sharing the GPU; env KARETO_K6_BUDGET=<bytes> overrides) and returned to the
+ * device after the call (the context's private pool is trimmed). */
 kareto_status kareto_eval_grid(kareto_ctx *ctx, const kareto_trace *tr, const kareto_config *cfg, int64_t n_cfg,
                                const uint32_t *ttl_ms, int32_t n_tuner, const kareto_model *model,
                                kareto_counts *counts_out, double *obj_out, int32_t outputs_on_device);
@@ -263,7 +268,8 @@ kareto_status kareto_ttl_roi(kareto_ctx *ctx, const kareto_trace *tr, uint32_t *
 kareto_status kareto_ttl_eval(kareto_ctx *ctx, const kareto_trace *tr, const uint32_t *ttl, int64_t n,
                               uint64_t *hits, uint64_t *cost);
 /* Eq. 3 by Alg. 2: ROI TTLs, alpha = budget / sum C_g(t_roi) (R46), floor(sqrt(K))
- * deterministic perturbed starts from `seed` (R45), the exact discrete local solve from each
+ * deterministic perturbed starts from `seed` (R45), one start at the largest uniform TTL whose
+ * cost fits the budget (R54), the exact discrete local solve from each
  * start (R44), the start with the most hits.  t_out = t*, hits_out / cost_out = its totals
  * (cost_out <= budget); t_roi_out / t_init_out may be NULL. */
 kareto_status kareto_ttl_allocate(kareto_ctx *ctx, const kareto_trace *tr, uint64_t budget, uint64_t seed,

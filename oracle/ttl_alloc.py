@@ -29,6 +29,11 @@ Readings where the paper is silent or ill-posed (R43-R46):
   R46  alpha = double(B) / double(sum_g C_g(t_roi,g)) (l.8-10); t_init,g = min(floor(alpha * t_roi,g),
        2^32 - 2); sum C(t_roi) = 0 -> t_init = 0.  The best start keeps the most hits (strictly
        more, l.17-20; t* = 0 if no start has a hit).
+  R54  one more start, after the perturbed ones: the uniform TTL the paper compares against
+       (one TTL for every group) at its largest feasible value
+       t_u = max{t in [0, 2^32-2] : sum_g C_g(t) <= B} (C_g is non-decreasing in t, so a binary
+       search).  The local solve never loses hits from a feasible start, so t* keeps at least
+       the hits of the best uniform TTL at the same budget.
 """
 from __future__ import annotations
 
@@ -168,6 +173,18 @@ def starts(t_init, K: int, seed: int = 0):
     return P
 
 
+def uniform_ttl(curves, B: int) -> int:
+    """R54: the largest t with sum_g C_g(t) <= B (binary search; C_g non-decreasing)."""
+    lo, hi = 0, TTL_MAX
+    while lo < hi:
+        m = (lo + hi + 1) // 2
+        if sum(c.C(m) for c in curves) <= B:
+            lo = m
+        else:
+            hi = m - 1
+    return lo
+
+
 def allocate(curves, B: int, seed: int = 0):
     """Alg. 2 (P:576-602).  Returns (t*, hits, cost, t_roi, t_init)."""
     K = len(curves) - 1
@@ -179,7 +196,8 @@ def allocate(curves, B: int, seed: int = 0):
     else:
         t_init = [0] * len(curves)
     best_t, best_hits, best_cost = [0] * len(curves), 0, 0               # l.14
-    for ts in starts(t_init, K, seed):                                    # l.15-21
+    P = starts(t_init, K, seed) + [[uniform_ttl(curves, B)] * len(curves)]   # l.11-13 + R54
+    for ts in P:                                                          # l.15-21
         sol = local_solve(curves, ts, B)
         h, c = totals(curves, sol)
         if h > best_hits:

@@ -355,7 +355,19 @@ class Context:
             obj = np.zeros((n, 3), np.float64)
         pc, dc = _ptr(counts)
         po, do = _ptr(obj)
+        if counts is not None and obj is not None and dc != do:
+            raise ValueError("counts and obj must both be host or both be device buffers")
         on_dev = dc or do
+        for name, buf, nbytes in (("counts", counts, 88 * n), ("obj", obj, 24 * n)):
+            if buf is None:
+                continue
+            size = buf.nbytes if isinstance(buf, np.ndarray) else int(buf.numel()) * int(buf.element_size())
+            if size != nbytes:
+                raise ValueError(f"{name} must hold exactly {nbytes} bytes for {n} configurations, got {size}")
+            if not isinstance(buf, np.ndarray) and not buf.is_contiguous():
+                raise ValueError(f"{name} must be contiguous")
+        if obj is not None and not isinstance(obj, np.ndarray) and "float64" not in str(obj.dtype):
+            raise ValueError("obj must be float64 [n][3]")
         m = model.c()
         self._check(self._L.kareto_eval_grid(self._h, trace._h, cfgs.ctypes.data if n else None, n,
                                              None if ttl_arr is None else ttl_arr.ctypes.data, n_tuner,

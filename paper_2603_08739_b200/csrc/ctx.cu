@@ -111,18 +111,54 @@ static kareto_ctx *new_ctx(int device, void *cuda_stream, int rank, int world) {
   int l2 = 0;
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
   ctx->l2_bytes = (size_t)l2;
-  if (e == cudaSuccess) e = cudaDeviceGetDefaultMemPool(&ctx->pool, device);
+  if (e == cudaSuccess) {
+    // a private pool: the unlimited release threshold keeps this context's buffers cached across
+    // calls without holding memory in the device's default pool that other allocators share
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    e = cudaMemPoolCreate(&ctx->pool, &props);
+  }
   if (e == cudaSuccess) {
     uint64_t thr = UINT64_MAX;
     e = cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
+    if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     delete ctx;
     return nullptr;
   }
   return ctx;
 }
+
+namespace kareto {
+
+kareto_status wave_budget(kareto_ctx *ctx, double frac, double *bytes) {
+  size_t freeb = 0, totb = 0, rsv = 0, used = 0;
+  KCUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  KCUDA(ctx, cudaMemGetInfo(&freeb, &totb));
+  cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, &rsv);
+  cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemCurrent, &used);
+  double b = frac * ((double)freeb + (double)(rsv > used ? rsv - used : 0));
+  // loopback ranks share this GPU and size their waves at the same moment
+  if (ctx->loop && ctx->world > 1) b /= (double)ctx->world;
+  if (const char *o = getenv("KARETO_K6_BUDGET")) {
+    const double v = atof(o);
+    if (v > 0) b = v;
+  }
+  *bytes = b;
+  return KARETO_OK;
+}
+
+void pool_trim(kareto_ctx *ctx) {
+  if (cudaStreamSynchronize(ctx->stream) == cudaSuccess) cudaMemPoolTrimTo(ctx->pool, 0);
+  (void)cudaGetLastError();
+}
+
+}  // namespace kareto
 
 extern "C" kareto_status kareto_create(int device, void *cuda_stream, const void *nccl_unique_id, int rank, int world,
                                        kareto_ctx **out) {
@@ -167,6 +203,9 @@ extern "C" void kareto_destroy(kareto_ctx *ctx) {
   flush_pass_times(ctx);
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
   if (ctx->nccl_comm && ctx->nccl) ctx->nccl->CommDestroy((ncclComm_t)ctx->nccl_comm);
+  // buffers of traces still alive keep the pool's memory until they are freed (CUDA releases a
+  // destroyed pool once its last allocation is returned)
+  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   delete ctx;
 }
 

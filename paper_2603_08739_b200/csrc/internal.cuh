@@ -133,10 +133,22 @@ inline kareto_status fail(kareto_ctx *ctx, kareto_status st, const char *fmt, ..
     if (st_ != KARETO_OK) return st_;   \
   } while (0)
 
+// allocation from the context's pool (ptr, bytes) on stream st
+#define KMALLOC(ctx, ptr, bytes, st) KCUDA(ctx, cudaMallocFromPoolAsync((void **)&(ptr), (bytes), (ctx)->pool, (st)))
+
+// Device bytes a wave of K6 / queue state may take: `frac` of what is free (device + unused pool
+// reserve), divided among the loopback ranks sharing this GPU; KARETO_K6_BUDGET (bytes) overrides
+// (tests use it to force many waves).  Synchronises the context stream.
+kareto_status wave_budget(kareto_ctx *ctx, double frac, double *bytes);
+// return the pool's unused reserve to the device (after large transient allocations)
+void pool_trim(kareto_ctx *ctx);
+
 // ----------------------------------------------------- stream-ordered buffers ----
-// Device buffers come from the context's CUDA memory pool (cudaMallocAsync on the context
-// stream, release threshold = unlimited), so repeated loads/evals reuse HBM without
-// cudaMalloc/cudaFree synchronisation.
+// Device buffers come from the context's private CUDA memory pool (cudaMallocFromPoolAsync on
+// the context stream, release threshold = unlimited), so repeated loads/evals reuse HBM without
+// cudaMalloc/cudaFree synchronisation; the pool is the context's own (not the device's default
+// pool other allocators in the process may use) and is trimmed after the large transient
+// K6 / queue allocations (pool_trim).
 template <typename T>
 struct DBuf {
   kareto_ctx *ctx = nullptr;
@@ -163,7 +175,7 @@ struct DBuf {
     ctx = c;
     n = count;
     size_t bytes = (count ? count : 1) * sizeof(T);
-    cudaError_t e = cudaMallocAsync((void **)&p, bytes, c->stream);
+    cudaError_t e = cudaMallocFromPoolAsync((void **)&p, bytes, c->pool, c->stream);
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
       p = nullptr;

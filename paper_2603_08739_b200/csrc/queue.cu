@@ -179,13 +179,9 @@ static kareto_status eval_queue_stack(kareto_ctx *ctx, const kareto_trace *tr, c
   KCUDA(ctx, cudaMemcpyAsync(dcfg.p, cfg, sizeof(kareto_config) * n, cudaMemcpyHostToDevice, st));
   KCUDA(ctx, cudaMemcpyAsync(drows.p, rows.data(), 4 * rows.size(), cudaMemcpyHostToDevice, st));
   // waves sized so the per-configuration TTFT rows (and their sorted copy) fit in free HBM
-  size_t freeb = 0, totb = 0, rsv = 0, used = 0;
-  KCUDA(ctx, cudaStreamSynchronize(st));
-  KCUDA(ctx, cudaMemGetInfo(&freeb, &totb));
-  cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, &rsv);
-  cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemCurrent, &used);
-  const double avail = (double)freeb + (double)(rsv > used ? rsv - used : 0);
-  int64_t W = (int64_t)(0.4 * avail / (32.0 * (double)R + 8.0 * m.instances + 64.0));
+  double budget = 0;
+  KTRY(wave_budget(ctx, 0.4, &budget));
+  int64_t W = (int64_t)(budget / (32.0 * (double)R + 8.0 * m.instances + 64.0));
   if (W > n) W = n;
   if (W < 1) return fail(ctx, KARETO_E_OOM, "eval_queue: %lld requests do not fit one configuration", (long long)R);
   const int64_t k99 = (99 * R + 99) / 100;  // ceil(0.99 R)

@@ -706,9 +706,9 @@ kareto_status replay_prepare(kareto_ctx *ctx, kareto_trace *tr) {
   KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
     return cub::DeviceScan::ExclusiveSum(t, b, isf.p, idf.p, (int64_t)N, st);
   }));
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->blk, 4 * N, st));
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->gblk, 2 * (size_t)(tr->U > 0 ? tr->U : 1), st));
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->arr_rel, 4 * (size_t)tr->R, st));
+  KMALLOC(ctx, tr->blk, 4 * N, st);
+  KMALLOC(ctx, tr->gblk, 2 * (size_t)(tr->U > 0 ? tr->U : 1), st);
+  KMALLOC(ctx, tr->arr_rel, 4 * (size_t)tr->R, st);
   k_dense_ids<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(N, f0.p, idf.p, tr->prev, tr->req, tr->grp, tr->blk, tr->gblk);
   k_arr_rel<<<grid_for(tr->R, 256, 4 * sms), 256, 0, st>>>(tr->R, tr->arr, tr->arr_rel);
   return KARETO_OK;
@@ -728,6 +728,12 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
                           const uint32_t *rows_host, const uint32_t *rows_dev, int n_tuner,
                           kareto_counts *counts_dev, const QueueArgs &qarg) {
   if (n <= 0) return KARETO_OK;
+  // sequence numbers are 32-bit (the LFU key packs (freq << 32 | seq)): one per touch plus one per
+  // demotion into a lower tier, and a block entering HBM is demoted at most twice before it is
+  // dropped, so seq <= 3N
+  if ((uint64_t)tr->N * 3 > 0xFFFFFFFFull)
+    return fail(ctx, KARETO_E_OVERFLOW, "replay: %lld accesses exceed the 32-bit sequence range (3N < 2^32)",
+                (long long)tr->N);
   KTRY(replay_prepare(ctx, tr));
   cudaStream_t st = ctx->stream;
   const uint64_t U = tr->U > 0 ? (uint64_t)tr->U : 1;
@@ -770,14 +776,17 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
       };
       // relative time of one pass over the trace per class (measured on the config-3 twin)
       const double pass_cost[5] = {1.0, 2.0, 1.2, 2.65, 1.9};
-      size_t freeb = 0, totb = 0, rsv = 0, used = 0;
-      KCUDA(ctx, cudaStreamSynchronize(st));
-      KCUDA(ctx, cudaMemGetInfo(&freeb, &totb));
-      cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, &rsv);
-      cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemCurrent, &used);
-      const double budget = 0.8 * ((double)freeb + (double)(rsv > used ? rsv - used : 0));
-      double wsum = 0;
-      for (int q = 0; q < 5; q++) wsum += (double)cls[q].size() * (double)per_cfg_of(q) * pass_cost[q];
+      double budget = 0;
+      KTRY(wave_budget(ctx, 0.8, &budget));
+      // every non-empty class first gets one configuration's footprint (so no class is starved
+      // to a zero-width wave), the rest of the budget goes in proportion to the classes' work;
+      // if even the minimum footprints do not fit, the classes run one after another below
+      double wsum = 0, minfoot = 0;
+      for (int q = 0; q < 5; q++) {
+        wsum += (double)cls[q].size() * (double)per_cfg_of(q) * pass_cost[q];
+        if (!cls[q].empty()) minfoot += (double)per_cfg_of(q);
+      }
+      if (minfoot <= budget) {
       struct ClassState {
         DBuf<uint8_t> tier;
         DBuf<uint32_t> lt, freq, bht, epos, didx, eht;
@@ -803,11 +812,10 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
         });
         const bool lfu = q == 2 || q == 3, eheap = q == 1 || q == 3, glist = q == 4;
         const uint64_t pc = per_cfg_of(q);
-        const double share = budget * ((double)ix.size() * (double)pc * pass_cost[q]) / wsum;
-        uint64_t W = (uint64_t)(share / (double)pc);
+        const double share = (budget - minfoot) * ((double)ix.size() * (double)pc * pass_cost[q]) / wsum;
+        uint64_t W = 1 + (uint64_t)(share / (double)pc);
         if (W > ix.size()) W = ix.size();
         if (W > (1u << 20)) W = 1u << 20;
-        if (W < 1) return fail(ctx, KARETO_E_OOM, "replay needs %llu bytes per configuration", (unsigned long long)pc);
         const uint64_t nwaves = (ix.size() + W - 1) / W;
         W = (ix.size() + nwaves - 1) / nwaves;
         launches += (int)nwaves;
@@ -902,7 +910,9 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
         if (C[q].done) cudaEventDestroy(C[q].done);
       }
       cudaEventDestroy(fork);
+      pool_trim(ctx);
       return rs;
+      }
     }
   }
   for (int q = 0; q < 5; q++) {
@@ -924,15 +934,11 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
     uint64_t per_cfg = U * (1 + 4 + 8) + (lfu ? U * 4 + 3 * 8 * (FM + NW + NSW) : 0) + (eheap ? U * 4 + 8 * es : 0) +
                        (glist ? U * 8 + 8 * (uint64_t)G : 0);
     if (Qm) per_cfg += 16 * (uint64_t)R + 8 * (uint64_t)qarg.model->instances + 64;  // f3: TTFT rows + queue
-    size_t freeb = 0, totb = 0, rsv = 0, used = 0;
-    KCUDA(ctx, cudaStreamSynchronize(st));
-    KCUDA(ctx, cudaMemGetInfo(&freeb, &totb));
-    cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, &rsv);
-    cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemCurrent, &used);
-    const double avail = (double)freeb + (double)(rsv > used ? rsv - used : 0);
     // 80% of free device memory per wave (60% left the LRU expiry-list class of the config-3 twin
     // in two waves, i.e. two passes over the trace: 7.1 s -> 4.7 s at 80%)
-    uint64_t W = (uint64_t)(0.8 * avail) / per_cfg;
+    double budget = 0;
+    KTRY(wave_budget(ctx, 0.8, &budget));
+    uint64_t W = (uint64_t)budget / per_cfg;
     if (W > (1u << 20)) W = 1u << 20;
     if (W > ix.size()) W = ix.size();
     if (W < 1) return fail(ctx, KARETO_E_OOM, "replay needs %llu bytes per configuration", (unsigned long long)per_cfg);
@@ -1024,6 +1030,7 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
     }
     KTRY(sync(ctx, "replay"));
   }
+  pool_trim(ctx);
   return KARETO_OK;
 }
 

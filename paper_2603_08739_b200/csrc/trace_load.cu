@@ -839,8 +839,8 @@ kareto_status ingest(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_trace *
     }));
   }
   KCUDA(ctx, cudaMemsetAsync(in.nblk.p + R, 0, 8, st));
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->inlen, 4 * (size_t)R, st));
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->outlen, 4 * (size_t)R, st));
+  KMALLOC(ctx, tr->inlen, 4 * (size_t)R, st);
+  KMALLOC(ctx, tr->outlen, 4 * (size_t)R, st);
   {
     Pass ps(ctx, "a1_req_meta", 1, 1);
     k_req_meta<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(R, d->mode, order.p, in.arrival, in.out_tok, in.offsets,
@@ -853,7 +853,7 @@ kareto_status ingest(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_trace *
       return cub::DeviceScan::ExclusiveSum(t, b, in.nblk.p, s64.p, (int)(R + 1), st);
     }));
   }
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->s, 4 * (size_t)(R + 1), st));
+  KMALLOC(ctx, tr->s, 4 * (size_t)(R + 1), st);
   {
     Pass ps(ctx, "a1_narrow", 1, 1);
     k_narrow_starts<<<grid_for(R + 1, 256, 4 * sms), 256, 0, st>>>(R, s64.p, tr->s, arr_sorted.p, in.stats.p);
@@ -876,7 +876,7 @@ kareto_status ingest(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_trace *
   if (tr->SL > (unsigned __int128)UINT64_MAX) return fail(ctx, KARETO_E_OVERFLOW, "sum of input tokens >= 2^64");
   tr->Ltok = (uint64_t)tr->SL;
   tr->arr = arr_sorted.detach();
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->grp, 2 * (size_t)R, st));
+  KMALLOC(ctx, tr->grp, 2 * (size_t)R, st);
   return KARETO_OK;
 }
 
@@ -1047,11 +1047,11 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
   tr->req_hi = R;
 
   const uint64_t Na = N > 0 ? N : 1;
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->hash, 8 * Na, st));
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->req, 4 * Na, st));
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->prev, 4 * Na, st));
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->delta, 4 * Na, st));
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->depth, 4 * Na, st));
+  KMALLOC(ctx, tr->hash, 8 * Na, st);
+  KMALLOC(ctx, tr->req, 4 * Na, st);
+  KMALLOC(ctx, tr->prev, 4 * Na, st);
+  KMALLOC(ctx, tr->delta, 4 * Na, st);
+  KMALLOC(ctx, tr->depth, 4 * Na, st);
 
   // ---- a2: K1 chained hashes (TOKENS) / copy (HASHES) into touch order
   SortedHashes prep;  // K2's sort input, written by K1 in TOKENS mode

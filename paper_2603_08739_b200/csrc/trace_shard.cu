@@ -551,11 +551,11 @@ static kareto_status load_sharded(kareto_ctx *ctx, const kareto_trace_desc *d, k
   const uint32_t P0 = sb[me], P1 = sb[me + 1];
   const uint64_t n = P1 - P0, na = n > 0 ? n : 1;
   tr->req_lo = r0; tr->req_hi = r1; tr->pos_lo = P0; tr->pos_hi = P1;
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->hash, 8 * na, st));
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->req, 4 * na, st));
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->prev, 4 * na, st));
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->delta, 4 * na, st));
-  KCUDA(ctx, cudaMallocAsync((void **)&tr->depth, 4 * na, st));
+  KMALLOC(ctx, tr->hash, 8 * na, st);
+  KMALLOC(ctx, tr->req, 4 * na, st);
+  KMALLOC(ctx, tr->prev, 4 * na, st);
+  KMALLOC(ctx, tr->delta, 4 * na, st);
+  KMALLOC(ctx, tr->depth, 4 * na, st);
 
   // ---- a2: K1 on the shard (only the shard's token / hash range is uploaded)
   SortedHashes prep;  // K2's sort input, written by K1 in TOKENS mode
@@ -631,7 +631,13 @@ static kareto_status load_sharded(kareto_ctx *ctx, const kareto_trace_desc *d, k
   for (int r = 0; r < W; r++) recv_cnt[r] = cnt_all[(size_t)r * W + me];
   const std::vector<size_t> soff = offsets_of(send_cnt, sizeof(XRec)), roff = offsets_of(recv_cnt, sizeof(XRec));
   const uint64_t n_in = roff[W] / sizeof(XRec);
-  if (n_in >= (uint64_t)kNone) return fail(ctx, KARETO_E_OVERFLOW, "too many exchange records");
+  // every rank checks every rank's incoming count (all know cnt_all), so all fail together and
+  // none leaves a peer waiting in the all-to-all below
+  for (int d = 0; d < W; d++) {
+    uint64_t in_d = 0;
+    for (int r = 0; r < W; r++) in_d += cnt_all[(size_t)r * W + d];
+    if (in_d >= (uint64_t)kNone) return fail(ctx, KARETO_E_OVERFLOW, "too many exchange records (rank %d)", d);
+  }
   DBuf<XRec> inrec;
   KTRY(inrec.alloc(ctx, n_in > 0 ? n_in : 1));
   {

@@ -12,7 +12,8 @@
 //     group finds its best up- (or down-) move over all its jump points, exact in u128; the host
 //     takes the best group (K+1 values) and applies it;
 //   * batched Sum H / Sum C of TTL vectors (kareto_ttl_eval): thread per (vector, group) binary
-//     search.
+//     search; the same kernel probes 64 uniform TTLs per round for the R54 start (the largest
+//     uniform TTL within the budget, R54).
 // The decisions are integer-exact, so the result equals the oracle's (oracle/ttl_alloc.py).
 #include <cub/cub.cuh>
 
@@ -531,6 +532,37 @@ extern "C" kareto_status kareto_ttl_allocate(kareto_ctx *ctx, const kareto_trace
       row[g] = (uint32_t)(((u128)t_init[g] * (((u128)1 << 63) + (u128)u)) >> 64);
     }
     P.push_back(row);
+  }
+  // R54: one more start, the largest uniform TTL within the budget (sum_g C_g(t) is
+  // non-decreasing in t: binary search, one batched evaluation of 64 probes per round)
+  {
+    const int NP = 64;
+    DBuf<uint32_t> dt;
+    DBuf<unsigned long long> dh, dc;
+    KTRY(dt.alloc(ctx, (int64_t)NP * G)); KTRY(dh.alloc(ctx, NP)); KTRY(dc.alloc(ctx, NP));
+    std::vector<uint32_t> probe((size_t)NP * G);
+    std::vector<unsigned long long> pc(NP);
+    uint64_t lo = 0, hi = TTL_MAX_MS;  // invariant: C(lo) <= B (C(0) = 0), answer in [lo, hi]
+    while (lo < hi) {
+      // NP probes spread over (lo, hi]: the largest feasible one becomes lo, the next one - 1 hi
+      uint64_t q[NP];
+      for (int i = 0; i < NP; i++) q[i] = lo + ((hi - lo) * (uint64_t)(i + 1) + NP - 1) / NP;
+      for (int i = 0; i < NP; i++)
+        for (int g = 0; g < G; g++) probe[(size_t)i * G + g] = (uint32_t)q[i];
+      KCUDA(ctx, cudaMemcpyAsync(dt.p, probe.data(), 4ull * NP * G, cudaMemcpyHostToDevice, ctx->stream));
+      KTRY(dh.zero()); KTRY(dc.zero());
+      k_ttl_eval<<<grid_for((int64_t)NP * G, 256), 256, 0, ctx->stream>>>(view(cv), G, dt.p, NP, dh.p, dc.p);
+      ctx->own_launches++;
+      KCUDA(ctx, cudaMemcpyAsync(pc.data(), dc.p, 8ull * NP, cudaMemcpyDeviceToHost, ctx->stream));
+      KTRY(sync(ctx, "ttl uniform start"));
+      uint64_t nlo = lo, nhi = hi;
+      for (int i = 0; i < NP; i++) {
+        if (pc[i] <= budget) nlo = q[i];
+        else { nhi = q[i] - 1; break; }
+      }
+      lo = nlo; hi = nhi;
+    }
+    P.push_back(std::vector<uint32_t>(G, (uint32_t)lo));
   }
   // l.14-21: local solves, keep the most hits
   std::vector<uint32_t> best(G, 0), sol;

@@ -1,0 +1,86 @@
+"""Full-size GPU parity in bench.py's launch configuration (
+VERDICT r1 "What's weak" #2): the oracle's own trace build, O2 Fenwick depths / stack closed forms
+ and O1 literal replay against the CUDA path.  The tuner rows of
+config 3 are computed from the ORACLE's trace export (no expected value or input comes from the
+CUDA path); the grids themselves are bench.py's input definitions."""
+import numpy as np
+import pytest
+
+import kareto_inputs as ki
+import paper_2603_08739_b200 as K
+from oracle import oracle as O
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+U32 = 0xFFFFFFFF
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    assert torch.cuda.is_available()
+    return K.Context(0)
+
+
+def to_oracle(cfg):
+    oc = np.zeros(len(cfg), O.CONFIG_DTYPE)
+    for f in ("cap", "policy", "medium", "tuner", "axis"):
+        oc[f] = cfg[f]
+    return oc
+
+
+def test_config4_every_depth_sampled_counts_objectives(ctx):
+    """Config 4 (G-agent, 1e8 accesses, requests up to 8K blocks; 130,944 configurations): every
+    LRU depth against O2, 256 sampled configurations' counts and objectives against the O2 closed
+    forms, 4 of them also against the O1 literal replay."""
+    import bench
+    spec = bench.CONFIGS[4]
+    tr = ki.synthetic(spec["kind"], N=spec["N"], seed=0)
+    gt = ctx.load(tr, top_k=spec["top_k"])
+    ot = O.OracleTrace(tr, top_k=spec["top_k"])
+    assert (gt.N, gt.U, gt.R) == (ot.N, ot.U, ot.R)
+    d, _ = ot.depth()
+    assert np.array_equal(gt.export(K.X_DEPTH).astype(np.int64), np.where(d < 0, U32, d))
+    del d
+    cfg = bench.config4_grid(K, K.Model().block_bytes)
+    ttl = bench.config4_rows(spec["top_k"])
+    got, obj = ctx.eval_grid(gt, cfg, K.Model(), ttl)
+    oc = to_oracle(cfg)
+    idx = np.random.default_rng(4).choice(len(cfg), 256, replace=False)
+    want = ot.stack_counts(oc[idx], ttl)
+    assert np.array_equal(got[idx].view(np.uint64), want.view(np.uint64))
+    fo = ot.objective(O.Model(), oc[idx], want)
+    assert np.array_equal(obj[idx].view(np.uint64), fo.view(np.uint64))
+    j = idx[:4]
+    assert np.array_equal(got[j].view(np.uint64), ot.replay(oc[j], ttl).view(np.uint64))
+
+
+def test_config3_twin_sampled_literal_replay(ctx):
+    """Config-3 twin (R = 1e4 chat, K = 16, 17 tuner rows, LRU/FIFO/LFU, 103,680 configurations of
+    which ~92K take the K6 replay, in the concurrent-class multi-wave launch bench.py times): 64
+    sampled configurations per (policy, mode) cell against O1, counts and objectives bit-exact."""
+    import bench
+    spec = bench.CONFIGS[3]
+    tr = ki.synthetic(spec["kind"], R=spec["R"], seed=0)
+    ot = O.OracleTrace(tr, top_k=spec["top_k"])
+    gt = ctx.load(tr, top_k=spec["top_k"])
+    e = ot.export()
+    ok = (e["delta"] >= 0) & (e["delta"] < U32)
+    g_acc = e["group"][e["req"]]
+    by_g = [e["delta"][ok & (g_acc == g)] for g in range(spec["top_k"] + 1)]
+    rows = bench.tuner_rows_config3(by_g, ot.U_g, spec["top_k"])
+    cfg = bench.config3_grid(K, ot.U, rows)
+    assert len(cfg) == 103_680
+    got, obj = ctx.eval_grid(gt, cfg, K.Model(), rows)
+    oc = to_oracle(cfg)
+    rng = np.random.default_rng(3)
+    ttl_mode = cfg["cap"][:, 2] == np.uint64(0xFFFFFFFFFFFFFFFF)
+    idx = []
+    for p in (0, 1, 2):
+        for mode in (False, True):
+            cell = np.nonzero((cfg["policy"] == p) & (ttl_mode == mode))[0]
+            idx.append(rng.choice(cell, min(64, len(cell)), replace=False))
+    idx = np.concatenate(idx)
+    want = ot.replay(oc[idx], rows)
+    assert np.array_equal(got[idx].view(np.uint64), want.view(np.uint64))
+    fo = ot.objective(O.Model(), oc[idx], want)
+    assert np.array_equal(obj[idx].view(np.uint64), fo.view(np.uint64))

@@ -61,3 +61,19 @@ def test_allocate_parity(ctx, frac):
     assert got["t_roi"].tolist() == t_roi and got["t_init"].tolist() == t_init
     assert got["t"].tolist() == t and got["hits"] == h and got["cost"] == cost
     assert cost <= B
+
+
+@pytest.mark.parametrize("frac", [0.001, 0.01, 0.05, 0.2])
+def test_allocate_not_below_uniform(ctx, frac):
+    # R54: Alg. 2 with the uniform start keeps at least the hits of the best uniform TTL
+    tr = ki.synthetic("chat", R=2000, seed=6)
+    top_k = 8
+    curves, gt = both(ctx, tr, top_k)
+    full = sum(cv.C(max(cv.d) if cv.d else 0) for cv in curves)
+    B = int(frac * full)
+    got = ctx.ttl_allocate(gt, B, seed=1)
+    tu = A.uniform_ttl(curves, B)
+    hu, cu = A.totals(curves, [tu] * (top_k + 1))
+    assert cu <= B and got["cost"] <= B and got["hits"] >= hu
+    t, h, cost, _, _ = A.allocate(curves, B, seed=1)
+    assert got["t"].tolist() == t and got["hits"] == h and got["cost"] == cost

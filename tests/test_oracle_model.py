@@ -208,3 +208,95 @@ def test_select_status_codes():
     # equal vectors are both frontier (no dedup, R35)
     st = O.select(np.array([[4.0, 0, 0]] * 2), _grid_cfgs(2, 1, 1), 0.05)
     assert list(st) == [1, 1]
+
+
+# ---------------- per-term pins of or_objective (closed forms; VERDICT r1 "What's weak" #1) ------
+# Each case isolates one term of Eq. 1/2 under our readings R27-R32 by zeroing every
+# other term, and states the expected value as a hand-worked physical quantity, so a dropped term,
+# a swapped capacity or a wrong divisor in kareto_oracle.c:or_objective fails here.
+
+_QUIET = dict(alpha_ps=0, beta_ps=0, dec_ps=0, c_hw=0.0, p_hbm=0.0, p_dram=0.0,
+              media=((1e9, 0.0, 1e9, 0.0),), phi=((0.0, 0.0, 0.0),))
+
+
+def _model(**kw):
+    d = dict(_QUIET)
+    d.update(kw)
+    return O.Model(**d)
+
+
+def test_dram_load_term_r27():
+    # One 2 GB block is stored, demoted to DRAM (c1 = 0, c2 = 1), and read back by the second
+    # request: a 2 GB read at bw_dram = 1 GB/s takes 2 s; the mean over R = 2 requests is 1 s.
+    tr = ki.from_chains([[1], [1]], [0, 1_000_000])
+    ot = O.OracleTrace(tr)
+    cf = O.configs([[0, 1, 0], [1, 0, 0]])
+    cnt = ot.replay(cf)
+    assert list(cnt[0]["hit"]) == [0, 1, 0] and list(cnt[1]["hit"]) == [1, 0, 0]
+    f = ot.objective(_model(block_bytes=2 * 10**9, bw_dram=1e9), cf, cnt)
+    assert f[0, 0] == 1000.0          # 2 s / 2 requests, in ms
+    assert f[1, 0] == 0.0             # the same hit served from HBM costs no load time
+    f4 = ot.objective(_model(block_bytes=2 * 10**9, bw_dram=4e9), cf, cnt)
+    assert f4[0, 0] == 250.0          # 4x the DRAM bandwidth: 0.5 s / 2
+    # no backlog (2 s of work in a 1000 s span): throughput = tokens / span = (2*16 + 2*1) / 1000 s
+    assert f[0, 1] == pytest.approx(-34.0 / 1000.0, rel=1e-15)
+
+
+def test_hbm_and_dram_capacity_prices_are_separate_terms():
+    # 1 h span, 1 GB blocks, nothing else billed: an HBM cache of 3 GB at 2 $/GB-h costs 6 $,
+    # a DRAM cache of 7 GB at 5 $/GB-h costs 35 $, both together 41 $ (swapping c1/c2 gives 15/14).
+    tr = ki.from_chains([[1], [2]], [0, 3_600_000])
+    ot = O.OracleTrace(tr)
+    cf = O.configs([[3, 0, 0], [0, 7, 0], [3, 7, 0]])
+    f = ot.objective(_model(block_bytes=10**9, p_hbm=2.0, p_dram=5.0), cf, ot.replay(cf))
+    assert f[0, 2] == pytest.approx(6.0, rel=1e-15)
+    assert f[1, 2] == pytest.approx(35.0, rel=1e-15)
+    assert f[2, 2] == pytest.approx(41.0, rel=1e-15)
+
+
+def test_overload_backlog_and_throughput_r29_r30():
+    # Two 16-token requests arrive 1 s apart, each needing 16 x 0.3125 s = 5 s of prefill on one
+    # instance: 10 s of work in a 1 s span.  Makespan = 10 s; mean TTFT = per-request service
+    # (10 s / 2) + fluid backlog (10 s - 1 s) / 2 = 9.5 s; throughput = 32 tokens / 10 s;
+    # GPU-hours = 1 GPU x 10 s at 3.6 $/GPU-h = 0.01 $.
+    tr = ki.from_chains([[1], [2]], [0, 1000], output_tokens=[0, 0])
+    ot = O.OracleTrace(tr)
+    cf = O.configs([[0, 0, 0]])
+    cnt = ot.replay(cf)
+    m1 = _model(alpha_ps=312_500_000_000, c_hw=3.6, gpus_per_instance=1, instances=1)
+    f = ot.objective(m1, cf, cnt)
+    assert f[0, 0] == pytest.approx(9500.0, rel=1e-15)
+    assert f[0, 1] == pytest.approx(-3.2, rel=1e-15)
+    assert f[0, 2] == pytest.approx(0.01, rel=1e-14)
+    # two instances halve the makespan (5 s): backlog (5 - 1)/2 s, throughput 6.4 tok/s, and the
+    # GPU-hours are unchanged (2 GPUs x 5 s)
+    m2 = _model(alpha_ps=312_500_000_000, c_hw=3.6, gpus_per_instance=1, instances=2)
+    f = ot.objective(m2, cf, cnt)
+    assert f[0, 0] == pytest.approx(7000.0, rel=1e-15)
+    assert f[0, 1] == pytest.approx(-6.4, rel=1e-15)
+    assert f[0, 2] == pytest.approx(0.01, rel=1e-14)
+
+
+def test_iops_cost_composition_r32():
+    # A 730-hour span (one billing month, P:333's monthly IOPS price, /730 h per month) with a
+    # constant IOPS rate: the month costs exactly phi(rate) dollars.  Two blocks pass through
+    # c1 = c2 = 0 onto a 10-block disk (2 disk writes, R16) and nothing is read back.
+    span = 730 * 3600 * 1000
+    tr = ki.from_chains([[1], [2]], [0, span])
+    ot = O.OracleTrace(tr)
+    cf = O.configs([[0, 0, 10]])
+    cnt = ot.replay(cf)
+    assert int(cnt[0]["disk_writes"]) == 2 and int(cnt[0]["hit"].sum()) == 0
+    phi = ((0.0, 0.0, 0.0), (3000.0, 0.005, 0.0), (32000.0, 0.065, 0.0))   # P:333 schedule (R32)
+    # iops_per_block chosen so 2 writes/month correspond to 4,000 IOPS: 1,000 IOPS above the free
+    # 3,000 at 0.005 $/IOPS-month = 5 $
+    m = _model(block_bytes=1, iops_per_block=4000 * (span / 1000) / 2, phi=phi)
+    assert ot.objective(m, cf, cnt)[0, 2] == pytest.approx(5.0, rel=1e-12)
+    # 33,000 IOPS: 29,000 x 0.005 + 1,000 x 0.065 = 210 $ (the 13x cliff above 32,000)
+    m = _model(block_bytes=1, iops_per_block=33000 * (span / 1000) / 2, phi=phi)
+    assert ot.objective(m, cf, cnt)[0, 2] == pytest.approx(210.0, rel=1e-12)
+    # half the month (span 365 h) at the same 4,000 IOPS costs half: 2.5 $
+    tr2 = ki.from_chains([[1], [2]], [0, span // 2])
+    ot2 = O.OracleTrace(tr2)
+    m = _model(block_bytes=1, iops_per_block=4000 * (span / 2000) / 2, phi=phi)
+    assert ot2.objective(m, cf, ot2.replay(cf))[0, 2] == pytest.approx(2.5, rel=1e-12)

@@ -79,6 +79,18 @@ def test_spec_allocation_examples():
     assert cost == 0 and h == 0
 
 
+def test_uniform_ttl_is_the_largest_feasible():
+    rng = np.random.default_rng(5)
+    for _ in range(100):
+        G = int(rng.integers(1, 4))
+        curves = [A.Curve(rng.integers(0, 30, size=int(rng.integers(0, 9))).tolist(), int(rng.integers(1, 4)))
+                  for _ in range(G)]
+        B = int(rng.integers(0, 300))
+        t = A.uniform_ttl(curves, B)
+        assert A.totals(curves, [t] * G)[1] <= B
+        assert t == A.TTL_MAX or A.totals(curves, [t + 1] * G)[1] > B
+
+
 def test_allocation_near_optimal_and_feasible():
     rng = np.random.default_rng(2)
     ratios = []
@@ -91,5 +103,12 @@ def test_allocation_near_optimal_and_feasible():
         assert cost <= B and A.totals(curves, t) == (h, cost)
         opt = exhaustive(curves, B)
         assert h <= opt
+        # R54: never below the best uniform TTL at the same budget (uniform t checked by brute force
+        # over every integer TTL up to the largest interval, beyond which H is flat)
+        top = max([max(c.d) for c in curves if c.d] + [0])
+        uni = max(A.totals(curves, [t] * G)[0] for t in range(top + 1) if A.totals(curves, [t] * G)[1] <= B)
+        assert h >= uni
         ratios.append(1.0 if opt == 0 else h / opt)
-    assert np.mean(ratios) >= 0.95 and min(ratios) >= 0.5
+    # a greedy exchange on integer step curves can miss the optimum by one step on tiny instances
+    # (5 of 6 hits); on average it is within 2 %
+    assert np.mean(ratios) >= 0.98 and np.mean(np.array(ratios) >= 0.9) >= 0.95 and min(ratios) >= 0.5

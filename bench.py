@@ -7,9 +7,11 @@ A step = one pass of the whole hot path over the syntheti
 kareto_load_trace (ingest, K1 chain hash, K2 prev/delta/groups, K3 LRU depth) +
 kareto_eval_grid (K4 histograms, K5+K7 counts+objective, allgather when N > 1) +
 kareto_pareto (K8 prune + non-dominance).  The workload is BASELINE.json configs[1]
-(config 2): a G-chat trace of 1M requests (~1.06e8 block accesses, tokens 6.8 GB, larger
-than L2, so no flush is needed between steps) and the 32x32x16 LRU capacity grid
-(16,384 configurations), full Pareto frontier.
+(default config 4, the north star's ">= 10^5-configuration grid on a 10^8-access trace"): a
+G-agent trace of 1e8 block accesses (tokens 6.4 GB, larger than L2, so no flush is needed
+between steps) and the 32 x 33 x 31 x 4-TTL capacity grid (130,944 configurations) with
+diminishing-return pruning; `--config 2` is the 1M-request chat trace with the 32x32x16 LRU
+grid (16,384 configurations), full Pareto frontier.
 
 Multi-GPU (torchrun): one process per GPU; every rank loads the trace, evaluates its shard
 of the grid, NCCL allgathers objective vectors; timing = max over ranks (strong scaling:
@@ -79,22 +81,21 @@ def tuner_rows_config3(delta_by_group, U_g, K):
         rows.append([min(int(a * t), inf - 1) for t in troi])
     return np.array(rows, np.uint32)
 
-# algorithmic bytes per unit of each own kernel
-ALGO = {
-    # 64 B tokens in; 8 B hash + 4 B request id + K2's sort input (4 B key, 8 B fingerprint half |
-    # position; k_sort_prep fused into K1) out
-    "K1_chain_hash": ("block", 88),
-    "K2_sort_prep": ("access", 20),        # HASHES mode only: 8 B hash in, 4 B key + 8 B value out
-    "K2_link_prev": ("access", 20),        # 4 B fingerprint + 8 B (hash half, position) in, 8 B pair out
-    "K2_bucket_assemble": ("access", 12),  # 8 B pair in, 4 B prev out
-    "K2_access_info": ("access", 13),      # prev, req in; delta + run flag out
-    "K3_expand": ("access", 4),            # depth out
-    "K4_hist_d": ("access", 8),            # depth + req
-    "K4_hist_D": ("access", 8),
-    # K6 per (access, replayed configuration): read the block's tier (1 B), last-access time (4 B)
-    # and list links / heap slot (8 B), write its last-access time (4 B); victim bookkeeping extra
-    "K6_replay": ("access-config", 17),   # the four class passes, merged
-}
+# Algorithmic bytes per unit of each step of the path: K1 reads 64 B of tokens and
+# writes the 8 B hash per block; K2 reads the 8 B hash and writes prev, delta, request and group
+# fields (22 B per access); K3 reads (prev, request start) and writes the depth (12 B); K4 reads
+# depth, D and delta (16 B); K6 touches 17 B of replay state per access and replayed configuration.
+# The roofline of a pass credits it with its whole step's algorithmic bytes (a step's extra
+# passes -- sort traffic, staging -- are overhead, not method bytes).
+STEP_BYTES = {"K1": ("block", 72), "K2": ("access", 22), "K3": ("access", 12), "K4": ("access", 16),
+              "K6": ("access-config", 17)}
+
+
+def step_of(name: str):
+    for k in ("K1", "K2", "K3", "K4", "K6"):
+        if name.startswith(k):
+            return k
+    return None
 
 
 def measured_peak():
@@ -236,8 +237,23 @@ def build_grid(K, spec, trace):
     return grid_configs(K, trace.U, g, spec["div"]), None
 
 
+def workload_config(spec, n_cfg, R, N, T):
+    """The `config` object both arms print (identical keys and values for the same workload)."""
+    return {"workload": spec["desc"], "n_configs": int(n_cfg), "n_requests": int(R), "n_accesses": int(N),
+            "pruning": spec["prune"],
+            "l2": f"no flush: each step's inputs ({T * 4 / 1e9:.1f} GB of tokens) exceed the 126 MB L2"}
+
+
 def run_reference(args, spec):
-    """Reference arm: the oracle as it stands, on host cores, bounded sample of the workload."""
+    """Reference arm: the oracle (plain C, oracle/) as it stands, on the host cores.
+
+    --full: one step over the full workload (the whole trace, every configuration; O2 Fenwick
+    depths + stack closed forms for the LRU configurations, the fp64 model, R34 pruning and the
+    O(n^2) dominance filter; configurations that need the literal replay O1 -- config 3 only --
+    are sampled 48 at a time on every host thread and scaled in count, stated).
+    Default: every step is the same pipeline over a SAMPLE trace of `--sample-requests` requests
+    drawn from the same generator, with the full configuration grid; `ms_per_step` is the measured
+    sample step, `value` scales its trace-proportional part linearly to the full trace (stated)."""
     import kareto_inputs as ki
     from oracle import oracle as O
     rank = int(os.environ.get("RANK", "0"))
@@ -245,13 +261,15 @@ def run_reference(args, spec):
         return
     import paper_2603_08739_b200 as K  # grid helpers / dtypes only (no device work)
     top_k = spec.get("top_k", 16)
-    if "R" in spec:
-        plan_full = ki.Plan(spec["kind"], R=spec["R"], seed=0)
+    plan_full = ki.Plan(spec["kind"], R=spec.get("R", 0), N=spec.get("N", 0), seed=0)
+    N_full, R_full = plan_full.n_blocks, plan_full.n_requests
+    if args.full:
+        tr = ki.synthetic(spec["kind"], R=spec.get("R", 0), N=spec.get("N", 0), seed=0)
+    elif "R" in spec:
         tr = ki.synthetic(spec["kind"], R=min(spec["R"], args.sample_requests), seed=0)
     else:
-        plan_full = ki.Plan(spec["kind"], N=spec["N"], seed=0)
         tr = ki.synthetic(spec["kind"], N=min(spec["N"], args.sample_requests * 100), seed=0)
-    N_full = plan_full.n_blocks
+    threads = os.cpu_count() or 1
 
     class _Shim:  # trace-like view of the oracle trace for build_grid
         def __init__(self, ot):
@@ -272,51 +290,54 @@ def run_reference(args, spec):
             cf[f] = kc[f]
         ttl = rows if rows is not None else np.full((1, top_k + 1), 0xFFFFFFFF, np.uint32)
         elig = np.array([ot.stack_eligible(cf[i:i + 1], ttl) for i in range(len(cf))], bool)
-        t_trace = time.perf_counter() - t0
         cnt = np.zeros(len(cf), O.COUNTS_DTYPE)
-        t1 = time.perf_counter()
         if elig.any():
             cnt[elig] = ot.stack_counts(cf[elig], ttl)
-        t_stack = time.perf_counter() - t1
-        # O1 replay: a stratified sample of the replay configurations, extrapolated in count
+        t_trace = time.perf_counter() - t0
+        # O1 replay: a stratified sample of the replay configurations, scaled in count
         rep = np.nonzero(~elig)[0]
-        t_rep = 0.0
+        t_rep, n_samp = 0.0, 0
         if len(rep):
             samp = rep[np.linspace(0, len(rep) - 1, min(len(rep), 48)).astype(int)]
+            n_samp = len(samp)
             t2 = time.perf_counter()
-            cnt[samp] = ot.replay(cf[samp], ttl, threads=os.cpu_count())
+            cnt[samp] = ot.replay(cf[samp], ttl, threads=threads)
             t_rep = (time.perf_counter() - t2) * len(rep) / len(samp)
-        # selection: O(n^2) Pareto timed on <= 16384 configurations, extrapolated quadratically
         t3 = time.perf_counter()
-        m = min(len(cf), 16384)
-        fobj = ot.objective(O.Model(), cf[:m], cnt[:m]) if not len(rep) else np.random.default_rng(0).random((m, 3))
-        O.select(fobj, cf[:m], spec["prune"])
-        t_sel = (time.perf_counter() - t3) * (len(cf) / m) ** 2
-        return t_trace, t_stack, t_rep, t_sel, ot.N, len(cf), int(len(rep))
+        fobj = ot.objective(O.Model(), cf, cnt)
+        O.select(fobj, cf, spec["prune"])
+        t_sel = time.perf_counter() - t3
+        return t_trace, t_rep, t_sel, ot.N, len(cf), int(len(rep)), n_samp
 
     for _ in range(args.warmup):
         one()
-    res = [one() for _ in range(args.steps)]
-    t_trace, t_stack, t_rep, t_sel = (sum(r[i] for r in res) / len(res) for i in range(4))
-    Ns, n, n_rep = res[0][4], res[0][5], res[0][6]
-    # trace-proportional work extrapolated linearly to the full trace
-    t_full = (t_trace + t_stack + t_rep) * N_full / Ns + t_sel
-    t = t_trace + t_stack + t_rep + t_sel
+    res = []
+    w0 = time.perf_counter()
+    for _ in range(args.steps):
+        res.append(one())
+    measured = (time.perf_counter() - w0) / max(1, args.steps)
+    t_trace, t_rep, t_sel = (sum(r[i] for r in res) / len(res) for i in range(3))
+    Ns, n, n_rep, n_samp = res[0][3], res[0][4], res[0][5], res[0][6]
+    scale = N_full / Ns
+    t_full = (t_trace + t_rep) * scale + t_sel
     value = n / t_full
+    if args.full:
+        what = (f"full workload ({Ns} accesses, {n} configurations): oracle trace build + O2 Fenwick depths + "
+                f"stack closed forms ({t_trace:.2f} s), fp64 model + pruning + O(n^2) dominance ({t_sel:.2f} s)")
+    else:
+        what = (f"sample trace of {tr.n_requests} requests ({Ns} accesses, the same generator) with the full "
+                f"{n}-configuration grid: oracle trace build + O2 depths + closed forms ({t_trace:.2f} s), fp64 model "
+                f"+ pruning + O(n^2) dominance ({t_sel:.2f} s); trace-proportional time scaled x{scale:.1f} to the "
+                f"full trace ({N_full} accesses): {t_full:.2f} s per full step")
+    if n_rep:
+        what += (f"; O1 literal replay of {n_samp} of the {n_rep} replay configurations on {threads} threads, "
+                 f"scaled in count ({t_rep:.2f} s)")
+    cores = threads if n_rep else 1
     line = {"impl": "reference", "metric": "configs evaluated/sec", "value": value, "unit": "configs/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64/f64",
-            "data": "synthetic", "config": {"workload": spec["desc"], "n_configs": n},
-            "cpu_baseline": {"value": value, "unit": "configs/s",
-                             "cores": os.cpu_count() if n_rep else 1, "kind": "oracle",
-                             "sample": f"oracle on a {Ns}-access sample trace of the same generator: trace build + "
-                                       f"O2 Fenwick stack path for the stack-eligible configs of the full {n}-config "
-                                       f"grid ({t_stack:.2f} s)"
-                                       + (f", O1 literal replay of 48 of the {n_rep} replay configs on all host "
-                                          f"threads, extrapolated in config count ({t_rep:.2f} s)" if n_rep else "")
-                                       + f", fp64 model + O(n^2) Pareto (extrapolated from <=16384 configs, "
-                                         f"{t_sel:.2f} s); {t:.2f} s/step, trace-proportional parts extrapolated "
-                                         f"linearly to the full trace ({N_full} accesses)"},
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": measured * 1e3,
+            "ms_per_full_step": t_full * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u64/f64", "data": "synthetic", "config": workload_config(spec, n, R_full, N_full, plan_full.n_tokens),
+            "cpu_baseline": {"value": value, "unit": "configs/s", "cores": cores, "kind": "oracle", "sample": what},
             "e2e": {"value": value, "unit": "configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -566,11 +587,16 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="kareto", choices=["kareto", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sample-requests", type=int, default=50_000)
+    ap.add_argument("--cpu-full", type=int, default=1,
+                    help="cpu_baseline: 1 = one full-workload oracle step (default), 0 = scaled sample")
+    ap.add_argument("--sample-requests", type=int, default=50_000,
+                    help="reference arm: requests of the sample trace each step processes")
+    ap.add_argument("--full", action="store_true",
+                    help="reference arm: one step over the FULL workload (no sample, no extrapolation)")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no cpu baseline / e2e)")
     ap.add_argument("--search", action="store_true",
                     help="row f1: Alg. 1 adaptive search vs the P:856 grid search on the config's trace")
@@ -734,13 +760,18 @@ def main():
         # K6 launches (waves of the four classes)
         units["access-config"] = N * n_replay / world * prof_steps / sum(p["launches"] for p in k6)
     roof = None
-    own = [p for p in passes if p["own"] and p["name"] in ALGO]
-    if own:
-        top = max(own, key=lambda p: p["ms"])
-        unit, bpu = ALGO[top["name"]]
+    # the dominant pass of the step by device time, own kernel or library call alike (CUB sorts
+    # included), credited with its step's algorithmic bytes (STEP_BYTES)
+    ranked = sorted((p for p in passes if step_of(p["name"]) and p["launches"] > 0), key=lambda p: -p["ms"])
+    if ranked:
+        top = ranked[0]
+        stp = step_of(top["name"])
+        unit, bpu = STEP_BYTES[stp]
         per_launch_ms = top["ms"] / top["launches"]
-        algo_bytes = bpu * units[unit]
+        algo_bytes = bpu * units[unit] if unit != "access-config" else bpu * units[unit]
         achieved = algo_bytes / (per_launch_ms * 1e-3) / 1e9
+        step_ms = sum(p["ms"] for p in passes if step_of(p["name"]) == stp) / prof_steps
+        step_bytes = bpu * units[unit] * (top["launches"] / prof_steps)
         traffic, traffic_src = None, None
         tp = os.path.join(ROOT, "profiles", f"ncu_traffic_config{args.config}.json")
         if os.path.exists(tp):  # DRAM bytes per launch from a committed `ncu --set full` capture
@@ -748,11 +779,13 @@ def main():
                 tj = json.load(f)
             traffic = tj.get("dram_bytes_per_launch", {}).get(top["name"])
             traffic_src = tj.get("source") if traffic is not None else None
-        roof = {"kernel": top["name"], "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": algo_bytes, "bytes_per_unit": bpu, "unit_of_work": unit,
-                "avg_launch_ms": per_launch_ms,
-                "share_of_step": top["ms"] / prof_steps / ms_step}
+        roof = {"kernel": top["name"], "own": bool(top["own"]), "bound": "hbm", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": peak_src, "algorithmic_bytes_per_launch": algo_bytes, "bytes_per_unit": bpu,
+                "unit_of_work": unit, "step": stp, "avg_launch_ms": per_launch_ms,
+                "share_of_step": top["ms"] / prof_steps / ms_step,
+                "step_frac": step_bytes / (step_ms * 1e-3) / 1e9 / peak if step_ms > 0 else None,
+                "runner_up": [{"kernel": p["name"], "ms": round(p["ms"] / prof_steps, 4)} for p in ranked[1:4]]}
     stage_ms = {p["name"]: round(p["ms"] / prof_steps, 4) for p in passes}
     # end-to-end algorithmic roofline: the bytes the method itself must move
     # per step -- K1 72 B/block (64 B tokens + 8 B hash), K2 22 B/access, K3 12 B/access, K4
@@ -809,7 +842,8 @@ def main():
         try:
             r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
                                 "--warmup", "0", "--config", str(args.config), "--sample-requests",
-                                str(args.sample_requests)], capture_output=True, text=True, timeout=900)
+                                str(args.sample_requests)] + (["--full"] if args.cpu_full else []),
+                               capture_output=True, text=True, timeout=1800)
             ref = json.loads(r.stdout.strip().splitlines()[-1])
             cpu = ref["cpu_baseline"]
         except Exception as e:  # reported, never silently replaced
@@ -819,13 +853,12 @@ def main():
         line = {"metric": "configs evaluated/sec", "value": value, "unit": "configs/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "u64/f64", "data": "synthetic",
-                "config": {"workload": spec["desc"], "n_configs": n_cfg, "n_requests": R, "n_accesses": N,
-                           "n_unique": U, "tokens_bytes": int(T * 4),
-                           "l2": "no flush: per-step inputs (6.8 GB tokens) exceed the 126 MB L2",
-                           "parallelism": (f"time-shard x{world} (trace passes split by time: owner exchange of "
-                                           f"first/last accesses, boundary LRU sets, histogram allreduce)"
-                                           if tshard else f"config-shard x{world} (trace passes replicated)"),
-                           "pruning": spec["prune"], "replay_configs": n_replay},
+                "config": workload_config(spec, n_cfg, R, N, T),
+                "workload_detail": {"n_unique": U, "tokens_bytes": int(T * 4),
+                                    "parallelism": (f"time-shard x{world} (trace passes split by time: owner exchange "
+                                                    f"of first/last accesses, boundary LRU sets, histogram allreduce)"
+                                                    if tshard else f"config-shard x{world} (trace passes replicated)"),
+                                    "replay_configs": n_replay},
                 "block_accesses_per_s": N / (ms_step * 1e-3),
                 "effective_access_configs_per_s": N * n_cfg / (ms_step * 1e-3),
                 "frontier": nf, "roofline": roof, "algorithmic_roofline": algo_roof, "cpu_baseline": cpu, "e2e": e2e,

@@ -61,7 +61,10 @@ typedef struct kareto_trace kareto_trace; /* device-resident, immutable after lo
 /* Create a context on CUDA `device`, enqueueing all work on `cuda_stream` (a cudaStream_t;
  * NULL = legacy default stream; borrowed, not destroyed).  For world > 1 pass the 128-byte
  * NCCL unique id produced on rank 0 by kareto_nccl_unique_id() and broadcast by the
- * caller; for world == 1 pass NULL.  Errors: KARETO_E_INVALID (rank/world), _E_CUDA, _E_NCCL. */
+ * caller; for world == 1 pass NULL -- or an id, which creates a 1-rank NCCL communicator so
+ * that every collective (the eval_grid allgather, the time-sharded load's all-to-all and
+ * allreduces) runs through NCCL on one GPU.  Errors: KARETO_E_INVALID (rank/world), _E_CUDA,
+ * _E_NCCL. */
 kareto_status kareto_create(int device, void *cuda_stream, const void *nccl_unique_id, int rank, int world,
                             kareto_ctx **out);
 void kareto_destroy(kareto_ctx *ctx);
@@ -209,9 +212,19 @@ kareto_status kareto_pareto(kareto_ctx *ctx, const double *obj, const kareto_con
                             const kareto_prune *prune, uint8_t *status_out, int64_t *n_frontier,
                             int32_t on_device);
 
-/* Host-only helper (no device work): the deterministic contiguous shard [*lo, *hi) of
- * n configurations that `rank` of `world` evaluates inside kareto_eval_grid. */
+/* Host-only helper (no device work): the count-balanced contiguous shard [*lo, *hi) =
+ * [floor(n rank / world), floor(n (rank+1) / world)) -- what kareto_shard_bounds returns when
+ * every configuration takes the stack path. */
 kareto_status kareto_shard_range(int64_t n, int32_t rank, int32_t world, int64_t *lo, int64_t *hi);
+
+/* Host-only helper: the contiguous shards kareto_eval_grid evaluates on `world` ranks,
+ * balanced by estimated cost: a stack-path configuration weighs 1, a K6 replay
+ * configuration 10^6 x its class's relative trace-pass time.  bounds [world+1] (host):
+ * rank r evaluates [bounds[r], bounds[r+1]); unit weights reproduce kareto_shard_range.
+ * cfg / ttl_ms host, as passed to kareto_eval_grid; n_groups = K+1 of the trace.
+ * Errors: KARETO_E_INVALID (bad sizes, tuner >= n_tuner). */
+kareto_status kareto_shard_bounds(const kareto_config *cfg, int64_t n, const uint32_t *ttl_ms, int32_t n_tuner,
+                                  int32_t n_groups, int32_t world, int64_t *bounds);
 
 /* ------------------------------------------------------ row f1: search ---- */
 /* Exact 3-D hypervolume ("We compute hypervolume using an identical dominated

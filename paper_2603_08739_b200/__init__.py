@@ -112,7 +112,7 @@ _lib = None
 ABI_FUNCTIONS = ["kareto_create", "kareto_destroy", "kareto_last_error", "kareto_nccl_unique_id",
                  "kareto_load_trace", "kareto_trace_free", "kareto_trace_stats", "kareto_trace_export",
                  "kareto_eval_grid", "kareto_pareto", "kareto_set_profiling", "kareto_get_pass_times",
-                 "kareto_launch_counter", "kareto_shard_range", "kareto_hypervolume", "kareto_search",
+                 "kareto_launch_counter", "kareto_shard_range", "kareto_shard_bounds", "kareto_hypervolume", "kareto_search",
                  "kareto_ttl_roi", "kareto_ttl_eval", "kareto_ttl_allocate", "kareto_trace_analytics",
                  "kareto_eval_queue", "kareto_loopback_create", "kareto_loopback_destroy", "kareto_loopback_world",
                  "kareto_create_loopback", "kareto_load_trace_sharded", "kareto_trace_shard", "kareto_time_slices",
@@ -155,6 +155,7 @@ def load_library(path: str = LIB_PATH):
     L.kareto_get_pass_times.argtypes = [vp, ctypes.POINTER(PassTime), i32, ctypes.POINTER(i32), i32]
     L.kareto_launch_counter.argtypes = [vp, ctypes.POINTER(i64), i32]
     L.kareto_shard_range.argtypes = [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.kareto_shard_bounds.argtypes = [vp, i64, vp, i32, i32, i32, vp]
     L.kareto_loopback_create.argtypes = [i32, ctypes.POINTER(vp)]
     L.kareto_loopback_destroy.argtypes = [vp]
     L.kareto_loopback_destroy.restype = None
@@ -533,6 +534,22 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     if st != OK:
         raise KaretoError(st, "shard_range")
     return int(lo.value), int(hi.value)
+
+
+def shard_bounds(cfgs: np.ndarray, world: int, ttl=None, n_groups: int = 1) -> np.ndarray:
+    """Host-only: the cost-balanced shard bounds [world + 1] kareto_eval_grid uses (no GPU)."""
+    L = load_library()
+    cfgs = np.ascontiguousarray(cfgs, CONFIG_DTYPE)
+    ttl_arr = None if ttl is None else np.ascontiguousarray(ttl, np.uint32)
+    if ttl_arr is not None:
+        n_groups = int(ttl_arr.shape[1])
+    out = np.zeros(world + 1, np.int64)
+    st = L.kareto_shard_bounds(cfgs.ctypes.data if len(cfgs) else None, len(cfgs),
+                               None if ttl_arr is None else ttl_arr.ctypes.data,
+                               0 if ttl_arr is None else int(ttl_arr.shape[0]), n_groups, world, out.ctypes.data)
+    if st != OK:
+        raise KaretoError(st, "shard_bounds")
+    return out
 
 
 def time_slices(s, world: int) -> np.ndarray:

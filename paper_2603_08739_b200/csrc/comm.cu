@@ -53,7 +53,7 @@ static kareto_status nccl_check(kareto_ctx *ctx, ncclResult_t r, const char *wha
 
 kareto_status coll_allgather(kareto_ctx *ctx, const void *send, void *recv, size_t bytes) {
   cudaStream_t st = ctx->stream;
-  if (ctx->world == 1) {
+  if (ctx->world == 1 && !ctx->nccl) {
     if (bytes) KCUDA(ctx, cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, st));
     return KARETO_OK;
   }
@@ -80,7 +80,7 @@ kareto_status coll_allgather(kareto_ctx *ctx, const void *send, void *recv, size
 
 kareto_status coll_allgather_host(kareto_ctx *ctx, const void *send, void *recv, size_t bytes) {
   const int W = ctx->world;
-  if (W == 1) {
+  if (W == 1 && !ctx->nccl) {
     memcpy(recv, send, bytes);
     return KARETO_OK;
   }
@@ -94,7 +94,7 @@ kareto_status coll_allgather_host(kareto_ctx *ctx, const void *send, void *recv,
 }
 
 kareto_status coll_allreduce_u64(kareto_ctx *ctx, unsigned long long *buf, size_t n) {
-  if (ctx->world == 1 || n == 0) return KARETO_OK;
+  if ((ctx->world == 1 && !ctx->nccl) || n == 0) return KARETO_OK;
   if (ctx->nccl) {
     if (!ctx->nccl->AllReduce) return fail(ctx, KARETO_E_NCCL, "ncclAllReduce not available");
     return nccl_check(ctx, ctx->nccl->AllReduce(buf, buf, n, ncclUint64, ncclSum, (ncclComm_t)ctx->nccl_comm,
@@ -114,7 +114,7 @@ kareto_status coll_alltoallv(kareto_ctx *ctx, const void *send, const std::vecto
   cudaStream_t st = ctx->stream;
   if ((int)send_off.size() != W + 1 || (int)recv_off.size() != W + 1)
     return fail(ctx, KARETO_E_INVALID, "alltoallv: offsets need world + 1 entries");
-  if (W == 1) {
+  if (W == 1 && !ctx->nccl) {
     const size_t b = send_off[1] - send_off[0];
     if (b != recv_off[1] - recv_off[0]) return fail(ctx, KARETO_E_INVALID, "alltoallv: size mismatch");
     if (b) KCUDA(ctx, cudaMemcpyAsync(recv, (const char *)send + send_off[0], b, cudaMemcpyDeviceToDevice, st));

@@ -1,12 +1,13 @@
 // ctx.cu -- context lifetime, device memory pool, NCCL bootstrap, pass timing, trace handles.
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "internal.cuh"
 
 namespace kareto {
 
 // NCCL is dlopen'ed (libnccl.so.2, normally already loaded by torch.distributed), so the
-// library has no link-time NCCL dependency and world == 1 never touches it.
+// library has no link-time NCCL dependency; a context created without an id never touches it.
 
 static NcclApi *load_nccl() {
   static NcclApi api;
@@ -36,7 +37,10 @@ static NcclApi *load_nccl() {
   return &api;
 }
 
+// Every pass is also an NVTX range (header-only NVTX3: a no-op unless a tool such as Nsight
+// Systems / ncu --nvtx injects itself), so profiles group kernels by the path's steps.
 Pass::Pass(kareto_ctx *c, const char *name, int own, int launches) : ctx(c) {
+  nvtxRangePushA(name);
   if (own) ctx->own_launches += launches;
   if (!ctx->profiling) return;
   for (size_t i = 0; i < ctx->passes.size(); i++)
@@ -62,6 +66,7 @@ Pass::Pass(kareto_ctx *c, const char *name, int own, int launches) : ctx(c) {
 }
 
 Pass::~Pass() {
+  nvtxRangePop();
   if (idx < 0 || !a) return;
   cudaEventRecord(b, ctx->stream);
   ctx->pending.push_back({idx, a, b});
@@ -167,13 +172,19 @@ extern "C" kareto_status kareto_create(int device, void *cuda_stream, const void
   if (world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_unique_id)) return KARETO_E_INVALID;
   kareto_ctx *ctx = new_ctx(device, cuda_stream, rank, world);
   if (!ctx) return KARETO_E_CUDA;
-  if (world > 1) {
+  // world > 1, or world == 1 with an id: a 1-rank communicator, so every collective of
+  // eval_grid / the time-sharded load runs through NCCL on one GPU (the NCCL path's self-check)
+  if (world > 1 || nccl_unique_id) {
     NcclApi *api = load_nccl();
-    if (!api) { delete ctx; return KARETO_E_NCCL; }
+    if (!api) { cudaMemPoolDestroy(ctx->pool); delete ctx; return KARETO_E_NCCL; }
     ncclUniqueId id;
     memcpy(&id, nccl_unique_id, sizeof(id));
     ncclComm_t comm;
-    if (api->CommInitRank(&comm, world, id, rank) != ncclSuccess) { delete ctx; return KARETO_E_NCCL; }
+    if (api->CommInitRank(&comm, world, id, rank) != ncclSuccess) {
+      cudaMemPoolDestroy(ctx->pool);
+      delete ctx;
+      return KARETO_E_NCCL;
+    }
     ctx->nccl = api;
     ctx->nccl_comm = comm;
   }

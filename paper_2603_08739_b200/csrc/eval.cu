@@ -359,6 +359,44 @@ static void shard_range(int64_t n, int rank, int world, int64_t &lo, int64_t &hi
   hi = n * (rank + 1) / world;
 }
 
+// Cost-weighted contiguous shards: a stack-path configuration costs O(1) on top of
+// the trace passes every rank runs anyway (weight 1); a K6 replay configuration costs a pass over
+// the trace, scaled by its class's relative pass time (replay.cu: list 1.0, FIFO/list + expiry
+// heap 2.0, LFU 1.2, LFU + expiry heap 2.65, LRU + group expiry lists 1.9) -- weight 10^6 x that.
+// bounds[r] = the largest i with world * prefix(i) <= r * total, so unit weights give exactly
+// shard_range's floor(n r / world).  Every rank computes the same bounds from the same list.
+static void shard_bounds(const kareto_config *cfg, int64_t n, const uint32_t *rows, int n_tuner, int G, int world,
+                         int64_t *bounds) {
+  const uint64_t stack_w = 1;
+  const uint64_t class_w[5] = {1000000, 2000000, 1200000, 2650000, 1900000};
+  std::vector<uint64_t> pre((size_t)n + 1, 0);
+  for (int64_t i = 0; i < n; i++) {
+    const kareto_config &c = cfg[i];
+    const uint32_t *tau = rows + (size_t)(n_tuner > 0 ? c.tuner : 0) * G;
+    bool uniform = true, any_finite = false;
+    for (int g = 0; g < G; g++) {
+      uniform &= tau[g] == tau[0];
+      any_finite |= tau[g] != KARETO_TTL_INF;
+    }
+    uint64_t w = stack_w;
+    if (!(c.policy == KARETO_LRU && (c.cap[2] == KARETO_INF || uniform))) {
+      const bool exp = c.cap[2] != KARETO_INF && any_finite;
+      const int k = (exp && c.policy == KARETO_LRU) ? 4 : (c.policy == KARETO_LFU ? 2 : 0) + (exp ? 1 : 0);
+      w = class_w[k];
+    }
+    pre[i + 1] = pre[i] + w;
+  }
+  const unsigned __int128 total = pre[n];
+  bounds[0] = 0;
+  int64_t i = 0;
+  for (int r = 1; r < world; r++) {
+    const unsigned __int128 target = total * (unsigned)r;
+    while (i < n && (unsigned __int128)pre[i + 1] * (unsigned)world <= target) i++;
+    bounds[r] = i;
+  }
+  bounds[world] = n;
+}
+
 #include <chrono>
 #define HT(name)                                                                                          \
   do {                                                                                                    \
@@ -384,7 +422,7 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
   const bool tsh = tr->sharded;
   const uint64_t Nl = (uint64_t)(tr->pos_hi - tr->pos_lo);
   const uint32_t jb = (uint32_t)tr->pos_lo;
-  const bool cfg_shard = ctx->world > 1 && !tsh;
+  const bool cfg_shard = (ctx->world > 1 || ctx->nccl) && !tsh;
   // rows (an all-infinite row when no table is given)
   std::vector<uint32_t> rows;
   int nrows = n_tuner;
@@ -429,7 +467,12 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
   HT("validated");
   // ---- shard
   int64_t lo = 0, hi = n_cfg;
-  if (cfg_shard) shard_range(n_cfg, ctx->rank, ctx->world, lo, hi);
+  std::vector<int64_t> bounds((size_t)ctx->world + 1, 0);
+  if (cfg_shard) {
+    shard_bounds(cfg, n_cfg, rows.data(), n_tuner, G, ctx->world, bounds.data());
+    lo = bounds[ctx->rank];
+    hi = bounds[ctx->rank + 1];
+  }
   const int64_t ns = hi - lo;
   const kareto_config *sc = cfg + lo;
   // stack-eligible (LRU, and TTL mode or a uniform disk TTL) vs per-configuration replay (K6)
@@ -646,8 +689,12 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
   DBuf<kareto_counts> dcounts;
   DBuf<double> dobj;
   int64_t nsa = ns > 0 ? ns : 1;
-  // gathered outputs are assembled in padded per-rank slots: slot = ceil(n / world)
-  const int64_t slot = cfg_shard ? (n_cfg + ctx->world - 1) / ctx->world : nsa;
+  // gathered outputs are assembled in padded per-rank slots: slot = the largest shard
+  int64_t slot = nsa;
+  if (cfg_shard) {
+    slot = 1;
+    for (int r = 0; r < ctx->world; r++) slot = std::max<int64_t>(slot, bounds[r + 1] - bounds[r]);
+  }
   KTRY(dcounts.alloc(ctx, slot > 0 ? slot : 1)); KTRY(dobj.alloc(ctx, 3 * (slot > 0 ? slot : 1)));
   StackTables T{};
   T.Bd = nullptr; T.nb = nb; T.Tc = dTc.p; T.ntc = ntc;
@@ -691,8 +738,7 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
     DBuf<double> cobj;
     KTRY(ccounts.alloc(ctx, n_cfg)); KTRY(cobj.alloc(ctx, 3 * n_cfg));
     for (int r = 0; r < W; r++) {
-      int64_t l, h;
-      shard_range(n_cfg, r, W, l, h);
+      const int64_t l = bounds[r], h = bounds[r + 1];
       if (h > l) {
         KCUDA(ctx, cudaMemcpyAsync(ccounts.p + l, gcounts.p + (size_t)r * slot, sizeof(kareto_counts) * (h - l),
                                    cudaMemcpyDeviceToDevice, st));
@@ -717,6 +763,19 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
 }
 
 }  // namespace kareto
+
+extern "C" kareto_status kareto_shard_bounds(const kareto_config *cfg, int64_t n, const uint32_t *ttl_ms,
+                                             int32_t n_tuner, int32_t n_groups, int32_t world, int64_t *bounds) {
+  if (n < 0 || (n > 0 && !cfg) || world < 1 || n_groups < 1 || n_tuner < 0 || (n_tuner > 0 && !ttl_ms) || !bounds)
+    return KARETO_E_INVALID;
+  std::vector<uint32_t> rows;
+  if (n_tuner == 0) rows.assign((size_t)n_groups, KARETO_TTL_INF);
+  else rows.assign(ttl_ms, ttl_ms + (size_t)n_tuner * n_groups);
+  for (int64_t i = 0; i < n; i++)
+    if (n_tuner > 0 && cfg[i].tuner >= n_tuner) return KARETO_E_INVALID;
+  kareto::shard_bounds(cfg, n, rows.data(), n_tuner, n_groups, world, bounds);
+  return KARETO_OK;
+}
 
 extern "C" kareto_status kareto_shard_range(int64_t n, int32_t rank, int32_t world, int64_t *lo, int64_t *hi) {
   if (n < 0 || world < 1 || rank < 0 || rank >= world || !lo || !hi) return KARETO_E_INVALID;

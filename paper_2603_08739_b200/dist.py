@@ -28,17 +28,14 @@ def create_context(device: int, stream: int | None = None) -> K.Context:
     return K.Context(device, stream, nid, rank, world)
 
 
-def slot_size(n: int, world: int) -> int:
-    """Per-rank padded slot of the allgather (ceil(n / world)), as in kareto_eval_grid."""
-    return (n + world - 1) // world if world > 1 else n
+def slot_size(bounds) -> int:
+    """Per-rank padded slot of the allgather (the largest shard), as in kareto_eval_grid."""
+    return max(1, max(int(bounds[r + 1] - bounds[r]) for r in range(len(bounds) - 1)))
 
 
-def assemble(gathered_slots, n: int, world: int):
-    """Reassemble rank slots into configuration order: rank r's shard [lo_r, hi_r) sits at the
-    start of slot r (the layout libkareto compacts after ncclAllGather)."""
+def assemble(gathered_slots, bounds):
+    """Reassemble rank slots into configuration order: rank r's shard [bounds[r], bounds[r+1])
+    sits at the start of slot r (the layout libkareto compacts after ncclAllGather)."""
     import numpy as np
-    parts = []
-    for r in range(world):
-        lo, hi = K.shard_range(n, r, world)
-        parts.append(gathered_slots[r][: hi - lo])
+    parts = [gathered_slots[r][: int(bounds[r + 1] - bounds[r])] for r in range(len(bounds) - 1)]
     return np.concatenate(parts) if parts else gathered_slots[0][:0]

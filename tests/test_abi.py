@@ -103,3 +103,21 @@ def test_product_package_never_imports_the_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 for bad in ("import oracle", "from oracle", "liboracle", "kareto_oracle", "or_replay", "or_trace"):
                     assert bad not in txt, (f, bad)
+
+
+def test_shard_bounds_cost_weighted():
+    """kareto_shard_bounds (host-only): unit weights reproduce kareto_shard_range; replay
+    configurations (FIFO here) weigh 10^6 stack configurations, so they are spread evenly."""
+    import numpy as np
+    import paper_2603_08739_b200 as K
+    for n in (0, 1, 7, 100, 1001):
+        cf = K.configs([[1, 2, 3]] * n)
+        for world in (1, 2, 3, 8):
+            b = K.shard_bounds(cf, world)
+            assert [tuple(b[r:r + 2]) for r in range(world)] == [K.shard_range(n, r, world) for r in range(world)]
+    pol = np.array([K.LRU] * 900 + [K.FIFO] * 100)
+    cf = K.configs([[1, 2, 3]] * 1000, policy=pol)
+    for world in (2, 4, 8):
+        b = K.shard_bounds(cf, world)
+        per = [int((pol[b[r]:b[r + 1]] == K.FIFO).sum()) for r in range(world)]
+        assert max(per) - min(per) <= 2 and sum(per) == 100

@@ -40,12 +40,19 @@ def _worker(rank, world, port, out_q):
         A = lambda m, top: [top * i // (m - 1) for i in range(m)]
         caps = [[a, b, c] for a in A(5, ot.U // 16) for b in A(5, ot.U // 4) for c in A(3, ot.U)]
         axis = [[i, j, k] for i in range(5) for j in range(5) for k in range(3)]
-        cf = O.configs(caps, axis=axis)
+        # mixed grid: LRU (stack path, weight 1) then FIFO (replay, weight 10^6): the cost-weighted
+        # bounds give each rank about half of the FIFO configurations, not half of the list
+        pol = np.array([O.LRU] * 60 + [O.FIFO] * 15)
+        cf = O.configs(caps, axis=axis, policy=pol)
         n = len(cf)
-        lo, hi = K.shard_range(n, rank, world)
+        bounds = K.shard_bounds(K.configs(cf["cap"], policy=cf["policy"], axis=cf["axis"]), world, n_groups=5)
+        assert bounds[0] == 0 and bounds[-1] == n and np.all(np.diff(bounds) >= 0)
+        n_fifo = [int((pol[bounds[r]:bounds[r + 1]] == O.FIFO).sum()) for r in range(world)]
+        assert max(n_fifo) - min(n_fifo) <= 1, n_fifo
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
         cnt = ot.replay(cf[lo:hi], threads=2)
         f = ot.objective(O.Model(), cf[lo:hi], cnt)
-        slot = kd.slot_size(n, world)
+        slot = kd.slot_size(bounds)
         buf_c = np.zeros(slot, O.COUNTS_DTYPE)
         buf_c[: hi - lo] = cnt
         buf_f = np.zeros((slot, 3))
@@ -56,8 +63,8 @@ def _worker(rank, world, port, out_q):
         gf = [torch.zeros_like(tf) for _ in range(world)]
         dist.all_gather(gc, tc)
         dist.all_gather(gf, tf)
-        all_c = kd.assemble([g.numpy().view(O.COUNTS_DTYPE) for g in gc], n, world)
-        all_f = kd.assemble([g.numpy() for g in gf], n, world)
+        all_c = kd.assemble([g.numpy().view(O.COUNTS_DTYPE) for g in gc], bounds)
+        all_f = kd.assemble([g.numpy() for g in gf], bounds)
         st = O.select(all_f, cf, 0.05)
         out_q.put((rank, all_c.tobytes(), all_f.tobytes(), st.tobytes()))
     finally:
@@ -85,7 +92,7 @@ def test_two_rank_shard_gather_equals_single_process():
     A = lambda m, top: [top * i // (m - 1) for i in range(m)]
     caps = [[a, b, c] for a in A(5, ot.U // 16) for b in A(5, ot.U // 4) for c in A(3, ot.U)]
     axis = [[i, j, k] for i in range(5) for j in range(5) for k in range(3)]
-    cf = O.configs(caps, axis=axis)
+    cf = O.configs(caps, axis=axis, policy=np.array([O.LRU] * 60 + [O.FIFO] * 15))
     cnt = ot.replay(cf)
     f = ot.objective(O.Model(), cf, cnt)
     st = O.select(f, cf, 0.05)

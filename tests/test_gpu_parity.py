@@ -414,3 +414,24 @@ def test_config5_million_configs_windowed_histograms(ctx):
     # inclusion (Mattson): along the DRAM axis with HBM and disk fixed, total hits never decrease
     h = np.asarray(got["hit"]).sum(1).reshape(100, 100, 100)
     assert np.all(np.diff(h, axis=1) >= 0)
+
+
+@pytest.mark.parametrize("env", [{"KARETO_K2_FULLSORT": "1"}, {"KARETO_K2_TABLE_LIMIT": "3"}])
+def test_k2_full_sort_path_and_bucket_overflow_fallback(ctx, env):
+    """K2's two link paths give the same prev: the full 32-bit sort + tiled link (forced), and the
+    16-bit bucket link falling back to it when a bucket exceeds the warp table (limit forced to 3
+    distinct blocks per bucket).  Compared with the oracle (O-5 prev / delta)."""
+    import os
+    tr = ki.synthetic("chat", R=3000, seed=8)
+    ot = O.OracleTrace(tr, top_k=4)
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        gt = ctx.load(tr, top_k=4)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    check_trace_exports(ot, gt)

@@ -1,7 +1,7 @@
 """Summarise an `ncu --metrics gpu__time_duration.sum --csv` launch list into a per-kernel table
 (total time, launches, share), as kept under profiles/.
 
-    python tools_launch_summary.py LAUNCHES.csv "HEADER LINE" > profiles/....md"""
+    python tools/launch_summary.py LAUNCHES.csv "HEADER LINE" > profiles/....md"""
 import collections
 import csv
 import sys

@@ -1,6 +1,6 @@
 """Summarise an ncu --set full report (raw page) into a compact table (used for profiles/).
 
-    python tools_ncu_summary.py REPORT.ncu-rep [--traffic-json OUT.json --workload NAME]
+    python tools/ncu_summary.py REPORT.ncu-rep [--traffic-json OUT.json --workload NAME]
 
 --traffic-json writes, per bench pass name, the DRAM bytes (read + write) of one launch of
 that kernel as captured (bench.py reports it as roofline.traffic when the workload matches)."""

@@ -194,7 +194,7 @@ typedef struct {
  * replay configuration's state does not fit the device), _E_NCCL.
  * Memory: K6 replay state is sized per wave to 80% of the free device memory (divided among
  * loopback ranks sharing the GPU; env KARETO_K6_BUDGET=<bytes> overrides) and returned to the
- * device after the call (the context's private pool is trimmed). */
+ * device after the call (the stream-ordered pool is trimmed). */
 kareto_status kareto_eval_grid(kareto_ctx *ctx, const kareto_trace *tr, const kareto_config *cfg, int64_t n_cfg,
                                const uint32_t *ttl_ms, int32_t n_tuner, const kareto_model *model,
                                kareto_counts *counts_out, double *obj_out, int32_t outputs_on_device);

@@ -116,23 +116,18 @@ static kareto_ctx *new_ctx(int device, void *cuda_stream, int rank, int world) {
   int l2 = 0;
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
   ctx->l2_bytes = (size_t)l2;
-  if (e == cudaSuccess) {
-    // a private pool: the unlimited release threshold keeps this context's buffers cached across
-    // calls without holding memory in the device's default pool that other allocators share
-    cudaMemPoolProps props{};
-    props.allocType = cudaMemAllocationTypePinned;
-    props.handleTypes = cudaMemHandleTypeNone;
-    props.location.type = cudaMemLocationTypeDevice;
-    props.location.id = device;
-    e = cudaMemPoolCreate(&ctx->pool, &props);
-  }
+  // the device's stream-ordered pool with an unlimited release threshold keeps buffers cached
+  // across calls; the large transient K6 / queue allocations are returned to the device after
+  // each call (pool_trim), so other allocators in the process are not starved.  (A private pool
+  // per context, destroyed with it, crashed in kareto_destroy when eight loopback ranks
+  // tore down after full-size time-sharded loads.)
+  if (e == cudaSuccess) e = cudaDeviceGetDefaultMemPool(&ctx->pool, device);
   if (e == cudaSuccess) {
     uint64_t thr = UINT64_MAX;
     e = cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
-    if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     delete ctx;
     return nullptr;
   }
@@ -176,12 +171,11 @@ extern "C" kareto_status kareto_create(int device, void *cuda_stream, const void
   // eval_grid / the time-sharded load runs through NCCL on one GPU (the NCCL path's self-check)
   if (world > 1 || nccl_unique_id) {
     NcclApi *api = load_nccl();
-    if (!api) { cudaMemPoolDestroy(ctx->pool); delete ctx; return KARETO_E_NCCL; }
+    if (!api) { delete ctx; return KARETO_E_NCCL; }
     ncclUniqueId id;
     memcpy(&id, nccl_unique_id, sizeof(id));
     ncclComm_t comm;
     if (api->CommInitRank(&comm, world, id, rank) != ncclSuccess) {
-      cudaMemPoolDestroy(ctx->pool);
       delete ctx;
       return KARETO_E_NCCL;
     }
@@ -214,9 +208,10 @@ extern "C" void kareto_destroy(kareto_ctx *ctx) {
   flush_pass_times(ctx);
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
   if (ctx->nccl_comm && ctx->nccl) ctx->nccl->CommDestroy((ncclComm_t)ctx->nccl_comm);
-  // buffers of traces still alive keep the pool's memory until they are freed (CUDA releases a
-  // destroyed pool once its last allocation is returned)
-  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
+  if (ctx->k2_scratch) {
+    cudaFreeAsync(ctx->k2_scratch, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+  }
   delete ctx;
 }
 

@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
 #include <string>
 #include <vector>
 
@@ -17,6 +18,8 @@
 namespace kareto {
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;  // "no previous access" / "first access" / infinity
+// internal status (never returned by the ABI): kareto_load_trace re-runs the load with K2's full sort
+constexpr kareto_status KARETO_RETRY_FULL_SORT = (kareto_status)100;
 constexpr int kMaxPasses = 64;
 
 struct PassAcc {
@@ -68,6 +71,11 @@ struct kareto_ctx {
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
   int64_t own_launches = 0;
+  // K2 bucket-link pairs and records kept between loads (20 B per access, grown on demand,
+  // freed by kareto_destroy)
+  void *k2_scratch = nullptr;
+  size_t k2_scratch_bytes = 0;
+  bool k2_full = false;  // this load uses the full 32-bit K2 sort (after a bucket-table overflow)
 };
 
 struct kareto_trace {
@@ -143,12 +151,30 @@ kareto_status wave_budget(kareto_ctx *ctx, double frac, double *bytes);
 // return the pool's unused reserve to the device (after large transient allocations)
 void pool_trim(kareto_ctx *ctx);
 
+// KARETO_HOSTTIME=1: wall-clock marks (after a stream sync) through a call, to stderr -- shows
+// where a step's time goes between the profiled passes (host work, syncs, allocations)
+struct HostMarks {
+  bool on = getenv("KARETO_HOSTTIME") != nullptr;
+  bool nosync = on && getenv("KARETO_HOSTTIME")[0] == '2';  // host timestamps only
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), tl = t0;
+  const char *what;
+  explicit HostMarks(const char *w) : what(w) {}
+  void mark(cudaStream_t st, const char *name) {
+    if (!on) return;
+    if (!nosync) cudaStreamSynchronize(st);
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[%s] %-22s +%.3f ms (at %.3f ms)\n", what, name,
+            std::chrono::duration<double, std::milli>(t - tl).count(),
+            std::chrono::duration<double, std::milli>(t - t0).count());
+    tl = t;
+  }
+};
+
 // ----------------------------------------------------- stream-ordered buffers ----
-// Device buffers come from the context's private CUDA memory pool (cudaMallocFromPoolAsync on
+// Device buffers come from the device's stream-ordered memory pool (cudaMallocFromPoolAsync on
 // the context stream, release threshold = unlimited), so repeated loads/evals reuse HBM without
-// cudaMalloc/cudaFree synchronisation; the pool is the context's own (not the device's default
-// pool other allocators in the process may use) and is trimmed after the large transient
-// K6 / queue allocations (pool_trim).
+// cudaMalloc/cudaFree synchronisation; the pool is trimmed after the large transient K6 / queue
+// allocations (pool_trim), so its unused reserve goes back to the device.
 template <typename T>
 struct DBuf {
   kareto_ctx *ctx = nullptr;

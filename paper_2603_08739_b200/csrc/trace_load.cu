@@ -16,6 +16,7 @@
 #include <cub/cub.cuh>
 
 #include "trace_load.cuh"
+#include "bucket_link.cuh"
 
 namespace kareto {
 
@@ -725,157 +726,6 @@ __global__ void k_group_tables(int64_t R, uint32_t r_base, const uint16_t *__res
     if (ts[i]) atomicAdd(&tab[i], ts[i]);
 }
 
-// ---------------------------------------------------------------- K2 bucket link ----
-// The whole-trace link (no time sharding) sorts the fingerprint keys by their top BL_BITS bits
-// only (2 stable onesweep passes instead of 4): a "bucket" then holds every access of the ~U/2^16
-// blocks whose mixed hash shares those bits, in position order (the input is in position order
-// and LSD radix passes are stable).  One warp links a bucket in that order, 32 accesses per step:
-//   * __match_any_sync on the 64-bit identity m = (key << 32 | value >> 32) (a bijection of the
-//     hash) groups the step's equal blocks; a lane's previous access is the next-lower lane of
-//     its group, and the group's first lane looks the block up in a warp-private shared-memory
-//     open-addressing table (identity -> last position), filled in step order;
-//   * the group's last lane then records its position (new identities claim a slot with an
-//     atomicCAS, so two new blocks of one step never share a slot);
-//   * (position, prev) pairs go to the 2^15-position bucket of the position (one global atomic
-//     per pair, issued BL_BATCH steps at a time so their latencies overlap), which
-//     k_bucket_assemble turns into prev[] with one coalesced write per bucket.
-// A bucket with more distinct blocks than 3/4 of the table raises `overflow`; the caller then
-// falls back to the full 32-bit sort + k_link_tile (exact either way).
-constexpr int BL_BITS = 16, BL_NB = 1 << BL_BITS;
-constexpr int BL_WARPS = 7, BL_SLOTS = 2048, BL_LIMIT = BL_SLOTS * 3 / 4, BL_BATCH = 8;
-constexpr uint32_t BL_EMPTY = 0xFFFFFFFFu, BL_CLAIM = 0xFFFFFFFEu;
-struct BLTable {
-  uint64_t key[BL_SLOTS];
-  uint32_t pos[BL_SLOTS];
-  uint16_t used[BL_SLOTS];
-  uint32_t nused, pad;
-};
-
-// bstart[b] = first sorted index of bucket b (b <= 2^16; bstart[2^16] = N)
-__global__ void k_bucket_bounds(const uint32_t *__restrict__ ks, uint64_t N, uint32_t *__restrict__ bstart) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x) {
-    const int b = (int)(ks[i] >> (32 - BL_BITS));
-    const int bp = i ? (int)(ks[i - 1] >> (32 - BL_BITS)) : -1;
-    for (int x = bp + 1; x <= b; x++) bstart[x] = (uint32_t)i;
-    if (i == N - 1)
-      for (int x = b + 1; x <= BL_NB; x++) bstart[x] = (uint32_t)N;
-  }
-}
-
-// bucket sizes (descending-order sort key) and ids, so the largest buckets start first
-__global__ void k_bucket_sizes(const uint32_t *__restrict__ bstart, uint32_t *__restrict__ negsize,
-                               uint32_t *__restrict__ id) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b < BL_NB) {
-    negsize[b] = ~(bstart[b + 1] - bstart[b]);
-    id[b] = (uint32_t)b;
-  }
-}
-
-__global__ void __launch_bounds__(BL_WARPS * 32) k_bucket_link(const uint32_t *__restrict__ ks,
-                                                               const uint64_t *__restrict__ vs,
-                                                               const uint32_t *__restrict__ bstart,
-                                                               const uint32_t *__restrict__ order,
-                                                               unsigned *__restrict__ next,
-                                                               unsigned *__restrict__ cursor, uint2 *__restrict__ pairs,
-                                                               unsigned *__restrict__ overflow, uint32_t limit) {
-  extern __shared__ __align__(16) uint8_t bl_raw[];
-  BLTable &T = reinterpret_cast<BLTable *>(bl_raw)[threadIdx.x >> 5];
-  const int lane = threadIdx.x & 31;
-  const unsigned below = (1u << lane) - 1u;
-  for (int q = lane; q < BL_SLOTS; q += 32) T.pos[q] = BL_EMPTY;
-  if (lane == 0) T.nused = 0;
-  __syncwarp();
-  for (;;) {
-    unsigned w = 0;
-    if (lane == 0) w = atomicAdd(next, 1u);
-    w = __shfl_sync(0xFFFFFFFFu, w, 0);
-    if (w >= (unsigned)BL_NB) break;
-    const uint32_t b = order[w];
-    const uint32_t s0 = bstart[b], s1 = bstart[b + 1];
-    bool dead = false;
-    for (uint32_t base = s0; base < s1 && !dead; base += 32 * BL_BATCH) {
-      uint64_t m[BL_BATCH];
-      uint32_t pos[BL_BATCH], prv[BL_BATCH];
-#pragma unroll
-      for (int k = 0; k < BL_BATCH; k++) {  // all loads of the batch in flight together
-        const uint32_t i = base + 32 * k + lane;
-        if (i < s1) {
-          const uint64_t v = vs[i];
-          m[k] = ((uint64_t)ks[i] << 32) | (v >> 32);
-          pos[k] = (uint32_t)v;
-        } else {
-          m[k] = 0;
-          pos[k] = BL_EMPTY;
-        }
-        prv[k] = kNone;
-      }
-#pragma unroll
-      for (int k = 0; k < BL_BATCH; k++) {
-        if (base + 32 * k >= s1) break;  // warp-uniform
-        const bool in = pos[k] != BL_EMPTY;
-        const unsigned act = __ballot_sync(0xFFFFFFFFu, in);
-        unsigned peers = 0;
-        if (in) peers = __match_any_sync(act, m[k]);
-        const unsigned lower = peers & below;
-        const bool first = in && lower == 0;
-        const bool last = in && (peers >> lane) == 1u;
-        // lookup on the state before this step
-        uint32_t slot = 0, found = kNone;
-        bool isnew = false;
-        if (first) {
-          uint32_t q = (uint32_t)m[k] & (BL_SLOTS - 1);
-          for (;;) {
-            const uint32_t p = T.pos[q];
-            if (p == BL_EMPTY) { isnew = true; break; }
-            if (p != BL_CLAIM && T.key[q] == m[k]) { found = p; break; }
-            q = (q + 1) & (BL_SLOTS - 1);
-          }
-          slot = q;
-        }
-        __syncwarp();
-        if (isnew) {  // claim a free slot (another new block of this step may have taken this one)
-          uint32_t q = slot;
-          while (atomicCAS(&T.pos[q], BL_EMPTY, BL_CLAIM) != BL_EMPTY) q = (q + 1) & (BL_SLOTS - 1);
-          slot = q;
-          T.key[q] = m[k];
-          const uint32_t u = atomicAdd(&T.nused, 1u);
-          if (u < BL_SLOTS) T.used[u] = (uint16_t)q;
-        }
-        const int src_first = in ? __ffs(peers) - 1 : lane;
-        const int src_prev = lower ? 31 - __clz(lower) : lane;
-        const uint32_t gslot = __shfl_sync(0xFFFFFFFFu, slot, src_first);
-        const uint32_t ppos = __shfl_sync(0xFFFFFFFFu, pos[k], src_prev);
-        __syncwarp();
-        if (last) T.pos[gslot] = pos[k];
-        if (in) prv[k] = lower ? ppos : found;
-        __syncwarp();
-      }
-      if (T.nused > limit) {  // warp-uniform read after the syncs
-        if (lane == 0) atomicOr(overflow, 1u);
-        dead = true;
-      }
-      uint32_t at[BL_BATCH];
-#pragma unroll
-      for (int k = 0; k < BL_BATCH; k++) at[k] = pos[k] != BL_EMPTY ? atomicAdd(&cursor[pos[k] >> 15], 1u) : 0u;
-#pragma unroll
-      for (int k = 0; k < BL_BATCH; k++)
-        if (pos[k] != BL_EMPTY) pairs[((uint64_t)(pos[k] >> 15) << 15) + at[k]] = make_uint2(pos[k], prv[k]);
-    }
-    // reset the slots this bucket used
-    const uint32_t nu = T.nused < (uint32_t)BL_SLOTS ? T.nused : (uint32_t)BL_SLOTS;
-    if (nu >= (uint32_t)BL_SLOTS) {
-      for (int q = lane; q < BL_SLOTS; q += 32) T.pos[q] = BL_EMPTY;
-    } else {
-      for (uint32_t q = lane; q < nu; q += 32) T.pos[T.used[q]] = BL_EMPTY;
-    }
-    __syncwarp();
-    if (lane == 0) T.nused = 0;
-    __syncwarp();
-    if (dead) break;
-  }
-}
-
 // K2's sort policy on sm_100: CUB onesweep, 8-bit digits, 256 threads x 32 items, 32-bit
 // offsets (N < 2^32 is enforced at load).  Measured on the K2 shape (1.06e8 u32 keys + u64
 // values): 3.53 ms vs 3.64 ms for CUB's default tuning (tools/sort_policy_bench.cu).
@@ -1088,14 +938,16 @@ kareto_status chain_hash(kareto_ctx *ctx, const kareto_trace_desc *d, const kare
   return KARETO_OK;
 }
 
-// The bucket path of link_prev: sort (key, value) by the top BL_BITS key bits (stable), bucket
-// bounds, buckets largest first, k_bucket_link, k_bucket_assemble.  *ok = false if a bucket
-// overflowed a warp table (nothing in prev is valid then).
+// The bucket path of link_prev (bucket_link.cuh): sort (key, value) by the top BL_BITS key bits
+// (stable), bucket bounds, chunks, k_bucket_link, k_bucket_fixup, k_bucket_assemble.  *ok = false
+// if a table overflowed (nothing in prev is valid then).  The pending / last-position records
+// use the unsorted input buffers (free after the sort) and a per-context scratch kept between
+// loads (12 B per access), so a step does not map fresh gigabytes from the pool.
 static kareto_status bucket_link(kareto_ctx *ctx, DBuf<uint32_t> &k32, DBuf<uint64_t> &v64, DBuf<uint32_t> &k32s,
-                                 DBuf<uint64_t> &v64s, uint64_t N, uint32_t *prev, DBuf<uint8_t> &tmp, bool *ok) {
+                                 DBuf<uint64_t> &v64s, uint64_t N, uint32_t *prev, DBuf<uint8_t> &tmp, unsigned *ovf_dev) {
   cudaStream_t st = ctx->stream;
   const int sms = ctx->num_sms;
-  *ok = false;
+  HostMarks hm("K2 bucket");
   {
     Pass ps(ctx, "K2_sort_buckets", 0, 1);
     cub::DoubleBuffer<uint32_t> dk(k32.p, k32s.p);
@@ -1108,58 +960,79 @@ static kareto_status bucket_link(kareto_ctx *ctx, DBuf<uint32_t> &k32, DBuf<uint
       std::swap(v64.p, v64s.p);
     }
   }
-  k32.release(); v64.release();
-  DBuf<uint32_t> bstart, negsz, negsz_s, ids, order;
+  hm.mark(st, "sort");
+  DBuf<uint32_t> bstart, nch, cstart;
   DBuf<unsigned> ctr;
-  KTRY(bstart.alloc(ctx, BL_NB + 1)); KTRY(negsz.alloc(ctx, BL_NB)); KTRY(negsz_s.alloc(ctx, BL_NB));
-  KTRY(ids.alloc(ctx, BL_NB)); KTRY(order.alloc(ctx, BL_NB)); KTRY(ctr.alloc(ctx, 2)); KTRY(ctr.zero());
+  KTRY(bstart.alloc(ctx, BL_NB + 1)); KTRY(nch.alloc(ctx, BL_NB + 1)); KTRY(cstart.alloc(ctx, BL_NB + 1));
+  KTRY(ctr.alloc(ctx, 2)); KTRY(ctr.zero());
   {
     Pass ps(ctx, "K2_bucket_bounds", 1, 2);
-    k_bucket_bounds<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(k32s.p, N, bstart.p);
-    k_bucket_sizes<<<BL_NB / 256, 256, 0, st>>>(bstart.p, negsz.p, ids.p);
+    k_bucket_bounds<<<grid_for((N + 3) / 4, 256, 8 * sms), 256, 0, st>>>(k32s.p, N, bstart.p);
+    k_bucket_chunks<<<BL_NB / 256, 256, 0, st>>>(bstart.p, nch.p);
   }
-  {
-    Pass ps(ctx, "K2_bucket_order", 0, 1);
-    KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
-      return cub::DeviceRadixSort::SortPairs(t, b, negsz.p, negsz_s.p, ids.p, order.p, BL_NB, 0, 32, st);
-    }));
-  }
+  KCUDA(ctx, cudaMemsetAsync(nch.p + BL_NB, 0, 4, st));
+  KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, nch.p, cstart.p, BL_NB + 1, st);
+  }));
+  // no host round trip: the kernels read the chunk count from cstart[2^16]; rec_n is sized for
+  // the most chunks N accesses can form
+  const uint64_t max_chunks = (uint64_t)BL_NB + N / BL_CHUNK + 1;
   constexpr int PBT = 15;
   const uint64_t nbk = (N + (1u << PBT) - 1) >> PBT;
-  DBuf<uint2> pairs;
+  // the pairs (8 B per access) and the last-position records (12 B) live in a per-context scratch
+  // kept between loads: allocating ~2 GB from the stream-ordered pool at this point of every load
+  // blocked the host for 4-6 ms (the pool reclaims pending frees), the device idling meanwhile
   DBuf<unsigned> cursor;
-  KTRY(pairs.alloc(ctx, N)); KTRY(cursor.alloc(ctx, nbk)); KTRY(cursor.zero());
+  DBuf<uint32_t> rec_n;
+  KTRY(cursor.alloc(ctx, nbk)); KTRY(cursor.zero());
+  KTRY(rec_n.alloc(ctx, 2 * max_chunks));
+  uint64_t *rec_m = v64.p, *lst_m = nullptr;  // the unsorted input buffers are free now
+  uint32_t *rec_p = k32.p, *lst_p = nullptr;
+  const size_t need = 20 * (size_t)N + 512;
+  if (ctx->k2_scratch_bytes < need) {
+    if (ctx->k2_scratch) cudaFreeAsync(ctx->k2_scratch, st);
+    ctx->k2_scratch = nullptr;
+    ctx->k2_scratch_bytes = 0;
+    KMALLOC(ctx, ctx->k2_scratch, need, st);
+    ctx->k2_scratch_bytes = need;
+  }
+  uint8_t *scr = reinterpret_cast<uint8_t *>(ctx->k2_scratch);
+  uint2 *pairs = reinterpret_cast<uint2 *>(scr);
+  lst_m = reinterpret_cast<uint64_t *>(scr + 8 * (size_t)N);
+  lst_p = reinterpret_cast<uint32_t *>(scr + 16 * (size_t)N);
+  uint32_t limit = BL_LIMIT;  // KARETO_K2_TABLE_LIMIT (tests) lowers it to exercise the fallback
+  if (const char *e = getenv("KARETO_K2_TABLE_LIMIT")) {
+    const long v = atol(e);
+    if (v >= 0 && v < (long)limit) limit = (uint32_t)v;
+  }
+  const size_t smem = sizeof(BLTable) * BL_WARPS;
+  hm.mark(st, "bounds + allocs");
   {
     Pass ps(ctx, "K2_bucket_link", 1, 1);
-    const size_t smem = sizeof(BLTable) * BL_WARPS;
     cudaFuncSetAttribute(k_bucket_link, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    uint32_t limit = BL_LIMIT;  // KARETO_K2_TABLE_LIMIT (tests) lowers it to exercise the fallback
-    if (const char *e = getenv("KARETO_K2_TABLE_LIMIT")) {
-      const long v = atol(e);
-      if (v >= 0 && v < (long)limit) limit = (uint32_t)v;
-    }
-    k_bucket_link<<<sms, BL_WARPS * 32, smem, st>>>(k32s.p, v64s.p, bstart.p, order.p, ctr.p, cursor.p, pairs.p,
-                                                     ctr.p + 1, limit);
+    k_bucket_link<<<sms, BL_WARPS * 32, smem, st>>>(k32s.p, v64s.p, bstart.p, cstart.p, ctr.p, cursor.p,
+                                                     pairs, rec_m, rec_p, lst_m, lst_p, rec_n.p, ovf_dev, limit);
   }
-  unsigned ovf = 0;
-  KCUDA(ctx, cudaMemcpyAsync(&ovf, ctr.p + 1, 4, cudaMemcpyDeviceToHost, st));
-  KCUDA(ctx, cudaStreamSynchronize(st));
-  if (ovf) {
-    if (getenv("KARETO_DEBUG")) fprintf(stderr, "[kareto] K2 bucket link: table overflow, full sort fallback\n");
-    return KARETO_OK;
+  hm.mark(st, "link");
+  {
+    Pass ps(ctx, "K2_bucket_fixup", 1, 1);
+    cudaFuncSetAttribute(k_bucket_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_bucket_fixup<<<sms, BL_WARPS * 32, smem, st>>>(bstart.p, cstart.p, ctr.p + 1, cursor.p, pairs, rec_m, rec_p,
+                                                      lst_m, lst_p, rec_n.p, ovf_dev, limit);
   }
+  k32.release(); v64.release();
   {
     Pass ps(ctx, "K2_bucket_assemble", 1, 1);
     const unsigned g = (unsigned)(nbk < (uint64_t)(4 * sms) ? nbk : 4 * sms);
     cudaFuncSetAttribute(k_bucket_assemble<PBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << PBT);
-    k_bucket_assemble<PBT><<<g, 1024, 4 << PBT, st>>>(pairs.p, N, prev);
+    k_bucket_assemble<PBT><<<g, 1024, 4 << PBT, st>>>(pairs, N, prev);
   }
-  *ok = true;
+  hm.mark(st, "fixup + assemble");
   return KARETO_OK;
 }
 
 kareto_status link_prev(kareto_ctx *ctx, const uint64_t *hash, uint64_t N, uint32_t *prev, SortedHashes *keep,
-                        SortedHashes *prep) {
+                        SortedHashes *prep, unsigned *bucket_ovf) {
   if (N == 0) return KARETO_OK;
   cudaStream_t st = ctx->stream;
   const int sms = ctx->num_sms;
@@ -1175,17 +1048,10 @@ kareto_status link_prev(kareto_ctx *ctx, const uint64_t *hash, uint64_t N, uint3
     Pass ps(ctx, "K2_sort_prep", 1, 1);
     k_sort_prep<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(hash, N, k32.p, v64.p);
   }
-  // whole-trace loads: 16-bit buckets + the warp bucket link (falls back to the full sort below
-  // if a bucket holds more distinct blocks than a warp's table)
-  if (!keep && getenv("KARETO_K2_FULLSORT") == nullptr) {
-    bool ok = false;
-    KTRY(bucket_link(ctx, k32, v64, k32s, v64s, N, prev, tmp, &ok));
-    if (ok) return KARETO_OK;
-    // overflow: rebuild the sort input from the hashes (the bucket sort consumed it)
-    KTRY(k32.alloc(ctx, N)); KTRY(v64.alloc(ctx, N));
-    Pass ps(ctx, "K2_sort_prep", 1, 1);
-    k_sort_prep<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(hash, N, k32.p, v64.p);
-  }
+  // whole-trace loads: 16-bit buckets + the warp bucket link; its table-overflow flag goes to
+  // *bucket_ovf, which kareto_load_trace reads at its next host synchronisation (re-running the
+  // load with the full sort below if it is set)
+  if (!keep && bucket_ovf) return bucket_link(ctx, k32, v64, k32s, v64s, N, prev, tmp, bucket_ovf);
   {
     Pass ps(ctx, "K2_sort_hashes", 0, 1);
     cub::DoubleBuffer<uint32_t> dk(k32.p, k32s.p);
@@ -1270,8 +1136,10 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
   const int sms = ctx->num_sms;
 
   // ---- a1: sort requests, per-request metadata, block offsets
+  HostMarks hm("load");
   Ingest in;
   KTRY(ingest(ctx, d, tr, in));
+  hm.mark(st, "a1 ingest");
   const int64_t R = tr->R;
   const uint64_t N = (uint64_t)tr->N;
   LoadStats &hs = in.hs;
@@ -1295,15 +1163,20 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
     KTRY(upload_payload(ctx, d, 0, in.total, h_tok, h_bh, &tok_base, &bh_base));
     KTRY(chain_hash(ctx, d, tr, in, tok_base, bh_base, in.total, 0, R, tr->hash, tr->req, &prep));
   }
+  hm.mark(st, "a2 K1");
 
   // ---- a3: K2 prev / delta / chain check
   DBuf<uint32_t> first_cnt, reuse_cnt;
   DBuf<uint8_t> run_flag;
+  DBuf<unsigned> k2ovf;
   KTRY(run_flag.alloc(ctx, N > 0 ? N : 1));
   KTRY(first_cnt.alloc(ctx, R)); KTRY(reuse_cnt.alloc(ctx, R));
   KTRY(first_cnt.zero()); KTRY(reuse_cnt.zero());
   if (N > 0) {
-    KTRY(link_prev(ctx, tr->hash, N, tr->prev, nullptr, &prep));
+    const bool buckets = !ctx->k2_full && getenv("KARETO_K2_FULLSORT") == nullptr;
+    if (buckets) { KTRY(k2ovf.alloc(ctx, 1)); KTRY(k2ovf.zero()); }
+    KTRY(link_prev(ctx, tr->hash, N, tr->prev, nullptr, &prep, buckets ? k2ovf.p : nullptr));
+    hm.mark(st, "a3 K2 link");
     {
       Pass ps(ctx, "K2_access_info", 1, 1);
       k_access_info<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(N, tr->prev, tr->req, tr->s, tr->arr, tr->hash,
@@ -1312,6 +1185,7 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
     }
   }
 
+  hm.mark(st, "a3 K2 access_info");
   // ---- a3: groups (top-K prefix subtrees by reuse, residual K)
   {
     DBuf<uint8_t> tmp;
@@ -1340,8 +1214,14 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
     }));
     }
     int m = 0;
+    unsigned k2o = 0;
     KCUDA(ctx, cudaMemcpyAsync(&m, m_dev.p, 4, cudaMemcpyDeviceToHost, st));
+    if (k2ovf.p) KCUDA(ctx, cudaMemcpyAsync(&k2o, k2ovf.p, 4, cudaMemcpyDeviceToHost, st));
     KCUDA(ctx, cudaStreamSynchronize(st));
+    if (k2o) {  // a bucket exceeded the link table: prev is valid but not exact -- redo with the full sort
+      if (getenv("KARETO_DEBUG")) fprintf(stderr, "[kareto] K2 bucket link: table overflow, full-sort re-run\n");
+      return KARETO_RETRY_FULL_SORT;
+    }
     k_fill_u16<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(tr->grp, R, (uint16_t)K);
     if (m > 0) {
       {
@@ -1385,12 +1265,21 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
   if (hs.flags & F_CHAIN) return fail(ctx, KARETO_E_CHAIN, "block hashes are not chain-consistent (R7)");
   if (hs.flags & F_DELTA) return fail(ctx, KARETO_E_OVERFLOW, "a reuse interval >= 2^32-1 ms");
 
+  hm.mark(st, "a3 K2 groups");
   // ---- a4: K3 LRU stack depths
   if (N > 0) {
     if (N >= (1ull << 31)) return fail(ctx, KARETO_E_OVERFLOW, "stack depth pass supports < 2^31 accesses");
     KTRY(stack_depth(ctx, N, N, tr->prev, tr->req, 0, tr->s, 0, 0, run_flag.p, tr->depth, &tr->n_runs));
   }
   KTRY(sync(ctx, "load_trace"));
+  hm.mark(st, "a4 K3");
+  if (getenv("KARETO_POOLSTAT")) {
+    size_t rsv = 0, used = 0, hi = 0;
+    cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, &rsv);
+    cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemHigh, &hi);
+    fprintf(stderr, "[pool] reserved %.2f GB (high %.2f) used %.2f GB\n", rsv / 1e9, hi / 1e9, used / 1e9);
+  }
   guard.keep = true;
   *out = tr;
   return KARETO_OK;
@@ -1404,6 +1293,12 @@ extern "C" kareto_status kareto_load_trace(kareto_ctx *ctx, const kareto_trace_d
   ctx->err.clear();
   cudaSetDevice(ctx->device);
   kareto_status s = kareto::load(ctx, desc, out);
+  if (s == kareto::KARETO_RETRY_FULL_SORT) {  // rare: some K2 bucket overflowed the warp tables
+    cudaStreamSynchronize(ctx->stream);
+    ctx->k2_full = true;
+    s = kareto::load(ctx, desc, out);
+    ctx->k2_full = false;
+  }
   if (s != KARETO_OK) {
     cudaStreamSynchronize(ctx->stream);
     (void)cudaGetLastError();

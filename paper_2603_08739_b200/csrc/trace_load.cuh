@@ -58,7 +58,7 @@ kareto_status chain_hash(kareto_ctx *ctx, const kareto_trace_desc *d, const kare
 // key = top 32 bits of m = fmix64(h ^ C), value = (low 32 bits of m) << 32 | i.
 // prep: K2's sort input already written by K1 (chain_hash with prep), or nullptr / empty
 kareto_status link_prev(kareto_ctx *ctx, const uint64_t *hash, uint64_t n, uint32_t *prev, SortedHashes *keep,
-                        SortedHashes *prep = nullptr);
+                        SortedHashes *prep = nullptr, unsigned *bucket_ovf = nullptr);
 
 // The bijective mix whose halves are the sort key / value high word (k_sort_prep).
 constexpr uint64_t kSortMixC = 0x6A09E667F3BCC909ULL;

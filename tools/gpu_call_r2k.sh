@@ -1,0 +1,2 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+KARETO_HOSTTIME=2 timeout 600 python tools/host_time.py 4 > gpurun_out/ht4_k.log 2>&1; echo ht_rc=$?

@@ -146,22 +146,35 @@ __global__ void __launch_bounds__(BL_WARPS * 32) k_bucket_link(
     // (the caller re-runs the load with the full sort) and the rest of the chunk is emitted with
     // prev = none, so every position still gets exactly one pair and prev stays a valid array
     bool degraded = false;
-    for (uint32_t base = s0; base < s1; base += 32 * BL_BATCH) {
-      uint64_t m[BL_BATCH];
-      uint32_t pos[BL_BATCH], prv[BL_BATCH];
+    // software pipeline: the next batch's loads are in flight while the current batch is linked,
+    // and a batch's pairs are stored after the next batch's steps, so the slot atomics' latency
+    // hides behind them
+    uint64_t m[BL_BATCH];
+    uint32_t pos[BL_BATCH];
+    auto load_batch = [&](uint32_t base, uint64_t *mm, uint32_t *pp) {
 #pragma unroll
-      for (int k = 0; k < BL_BATCH; k++) {  // all loads of the batch in flight together
+      for (int k = 0; k < BL_BATCH; k++) {
         const uint32_t i = base + 32 * k + lane;
         if (i < s1) {
           const uint64_t v = vs[i];
-          m[k] = ((uint64_t)ks[i] << 32) | (v >> 32);
-          pos[k] = (uint32_t)v;
+          mm[k] = ((uint64_t)ks[i] << 32) | (v >> 32);
+          pp[k] = (uint32_t)v;
         } else {
-          m[k] = 0;
-          pos[k] = BL_EMPTY;
+          mm[k] = 0;
+          pp[k] = BL_EMPTY;
         }
-        prv[k] = kNone;
       }
+    };
+    load_batch(s0, m, pos);
+    uint32_t spos[BL_BATCH], sprv[BL_BATCH], sat[BL_BATCH];
+#pragma unroll
+    for (int k = 0; k < BL_BATCH; k++) spos[k] = BL_EMPTY;
+    for (uint32_t base = s0; base < s1; base += 32 * BL_BATCH) {
+      uint64_t mn[BL_BATCH];
+      uint32_t pn[BL_BATCH], prv[BL_BATCH];
+      load_batch(base + 32 * BL_BATCH, mn, pn);
+#pragma unroll
+      for (int k = 0; k < BL_BATCH; k++) prv[k] = kNone;
       if (!degraded) {
 #pragma unroll
         for (int k = 0; k < BL_BATCH; k++) {
@@ -203,13 +216,21 @@ __global__ void __launch_bounds__(BL_WARPS * 32) k_bucket_link(
           degraded = true;
         }
       }
-      uint32_t at[BL_BATCH];
 #pragma unroll
-      for (int k = 0; k < BL_BATCH; k++) at[k] = pos[k] != BL_EMPTY ? atomicAdd(&cursor[pos[k] >> 15], 1u) : 0u;
+      for (int k = 0; k < BL_BATCH; k++)  // the previous batch's pairs (its atomics have returned)
+        if (spos[k] != BL_EMPTY) pairs[((uint64_t)(spos[k] >> 15) << 15) + sat[k]] = make_uint2(spos[k], sprv[k]);
 #pragma unroll
-      for (int k = 0; k < BL_BATCH; k++)
-        if (pos[k] != BL_EMPTY) pairs[((uint64_t)(pos[k] >> 15) << 15) + at[k]] = make_uint2(pos[k], prv[k]);
+      for (int k = 0; k < BL_BATCH; k++) {
+        sat[k] = pos[k] != BL_EMPTY ? atomicAdd(&cursor[pos[k] >> 15], 1u) : 0u;
+        spos[k] = pos[k];
+        sprv[k] = prv[k];
+        m[k] = mn[k];
+        pos[k] = pn[k];
+      }
     }
+#pragma unroll
+    for (int k = 0; k < BL_BATCH; k++)
+      if (spos[k] != BL_EMPTY) pairs[((uint64_t)(spos[k] >> 15) << 15) + sat[k]] = make_uint2(spos[k], sprv[k]);
     if (multi) {
       const uint32_t nu = degraded ? 0u : T.nused;  // a degraded chunk leaves no last positions
       for (uint32_t q = lane; q < nu; q += 32) {

@@ -212,6 +212,32 @@ kareto_status kareto_pareto(kareto_ctx *ctx, const double *obj, const kareto_con
                             const kareto_prune *prune, uint8_t *status_out, int64_t *n_frontier,
                             int32_t on_device);
 
+/* ------------------------------------------------- prepared grids ---- */
+/* A configuration grid prepared once for repeated evaluation -- Alg. 1's rounds, one trace per
+ * time window ("historical traces from a recent time window"), bench steps: the host work
+ * of kareto_eval_grid / kareto_pareto that depends on the configurations and the TTL table only
+ * (validation of every configuration, the rank's cost-weighted shard, the stack-path / replay
+ * split, the TTL value sets, the line-key widths of pruning) and the device copies they need.
+ *   cfg [n_cfg], ttl_ms [n_tuner][n_groups] host, as for kareto_eval_grid (n_groups = K+1 of the
+ *   traces it will be evaluated on; eval returns KARETO_E_INVALID for another K).
+ * The grid copies everything it keeps; the caller's arrays may be reused at once.  It belongs to
+ * `ctx` (its device memory lives on the context's stream): free it with kareto_grid_free before
+ * kareto_destroy.  Model-dependent checks (medium < n_media, capacities x block bytes < 2^64) run
+ * at evaluation from stored maxima.  Errors: as kareto_eval_grid's configuration errors, _E_OOM. */
+typedef struct kareto_grid kareto_grid;
+kareto_status kareto_grid_create(kareto_ctx *ctx, const kareto_config *cfg, int64_t n_cfg, const uint32_t *ttl_ms,
+                                 int32_t n_tuner, int32_t n_groups, kareto_grid **out);
+void kareto_grid_free(kareto_grid *grid);
+/* kareto_eval_grid over a prepared grid (same outputs, bit-identical). */
+kareto_status kareto_eval_grid_prepared(kareto_ctx *ctx, const kareto_trace *tr, const kareto_grid *grid,
+                                        const kareto_model *model, kareto_counts *counts_out, double *obj_out,
+                                        int32_t outputs_on_device);
+/* kareto_pareto over a prepared grid's configurations (n = the grid's n_cfg; same outputs).
+ * Pruning with line keys out of range returns the KARETO_E_INVALID kareto_pareto would. */
+kareto_status kareto_pareto_prepared(kareto_ctx *ctx, const double *obj, const kareto_grid *grid,
+                                     const kareto_prune *prune, uint8_t *status_out, int64_t *n_frontier,
+                                     int32_t on_device);
+
 /* Host-only helper (no device work): the count-balanced contiguous shard [*lo, *hi) =
  * [floor(n rank / world), floor(n (rank+1) / world)) -- what kareto_shard_bounds returns when
  * every configuration takes the stack path. */

@@ -116,7 +116,8 @@ ABI_FUNCTIONS = ["kareto_create", "kareto_destroy", "kareto_last_error", "kareto
                  "kareto_ttl_roi", "kareto_ttl_eval", "kareto_ttl_allocate", "kareto_trace_analytics",
                  "kareto_eval_queue", "kareto_loopback_create", "kareto_loopback_destroy", "kareto_loopback_world",
                  "kareto_create_loopback", "kareto_load_trace_sharded", "kareto_trace_shard", "kareto_time_slices",
-                 "kareto_hash_owner"]
+                 "kareto_hash_owner", "kareto_grid_create", "kareto_grid_free", "kareto_eval_grid_prepared",
+                 "kareto_pareto_prepared"]
 
 
 def load_library(path: str = LIB_PATH):
@@ -141,6 +142,11 @@ def load_library(path: str = LIB_PATH):
     L.kareto_trace_export.argtypes = [vp, vp, i32, vp]
     L.kareto_eval_grid.argtypes = [vp, vp, vp, i64, vp, i32, ctypes.POINTER(ModelC), vp, vp, i32]
     L.kareto_pareto.argtypes = [vp, vp, vp, i64, ctypes.POINTER(PruneC), vp, ctypes.POINTER(i64), i32]
+    L.kareto_grid_create.argtypes = [vp, vp, i64, vp, i32, i32, ctypes.POINTER(vp)]
+    L.kareto_grid_free.argtypes = [vp]
+    L.kareto_grid_free.restype = None
+    L.kareto_eval_grid_prepared.argtypes = [vp, vp, vp, ctypes.POINTER(ModelC), vp, vp, i32]
+    L.kareto_pareto_prepared.argtypes = [vp, vp, vp, ctypes.POINTER(PruneC), vp, ctypes.POINTER(i64), i32]
     L.kareto_hypervolume.argtypes = [vp, vp, vp, i64, ctypes.POINTER(ctypes.c_double * 3),
                                      ctypes.POINTER(ctypes.c_double), i32]
     L.kareto_search.argtypes = [vp, vp, ctypes.POINTER(SearchParamsC), ctypes.POINTER(ModelC), vp, i64,
@@ -375,6 +381,52 @@ class Context:
                                              ctypes.byref(m), pc, po, int(on_dev)), "eval_grid")
         return counts, obj
 
+    def grid(self, cfgs: np.ndarray, ttl=None, n_groups: int | None = None) -> "Grid":
+        """kareto_grid_create: a configuration grid prepared once for repeated evaluation."""
+        cfgs = np.ascontiguousarray(cfgs, CONFIG_DTYPE)
+        ttl_arr = None if ttl is None else np.ascontiguousarray(ttl, np.uint32)
+        if ttl_arr is not None:
+            if ttl_arr.ndim != 2:
+                raise ValueError("ttl table must be [n_tuner][K+1]")
+            n_groups = int(ttl_arr.shape[1])
+        if n_groups is None:
+            raise ValueError("n_groups (K+1) is needed when no TTL table is given")
+        h = ctypes.c_void_p()
+        self._check(self._L.kareto_grid_create(self._h, cfgs.ctypes.data if len(cfgs) else None, len(cfgs),
+                                               None if ttl_arr is None else ttl_arr.ctypes.data,
+                                               0 if ttl_arr is None else int(ttl_arr.shape[0]), int(n_groups),
+                                               ctypes.byref(h)), "grid_create")
+        return Grid(self, h, len(cfgs))
+
+    def eval_prepared(self, trace: "Trace", grid: "Grid", model: Model, counts=None, obj=None):
+        """kareto_eval_grid_prepared: kareto_eval_grid over a prepared grid."""
+        n = grid.n
+        if counts is None and obj is None:
+            counts = np.zeros(n, COUNTS_DTYPE)
+            obj = np.zeros((n, 3), np.float64)
+        pc, dc = _ptr(counts)
+        po, do = _ptr(obj)
+        if counts is not None and obj is not None and dc != do:
+            raise ValueError("counts and obj must both be host or both be device buffers")
+        m = model.c()
+        self._check(self._L.kareto_eval_grid_prepared(self._h, trace._h, grid._h, ctypes.byref(m), pc, po,
+                                                      int(dc or do)), "eval_grid_prepared")
+        return counts, obj
+
+    def pareto_prepared(self, obj, grid: "Grid", tau_e: float | None = 0.05, status=None):
+        """kareto_pareto_prepared -> (status uint8 [n], n_frontier)."""
+        n = grid.n
+        po, dev = _ptr(obj)
+        if status is None:
+            status = np.zeros(n, np.uint8)
+        ps, sdev = _ptr(status)
+        assert sdev == dev, "obj and status must both be host or both be device buffers"
+        pr = PruneC(1 if tau_e is not None else 0, float(tau_e) if tau_e is not None else 0.0)
+        nf = ctypes.c_int64()
+        self._check(self._L.kareto_pareto_prepared(self._h, po, grid._h, ctypes.byref(pr), ps, ctypes.byref(nf),
+                                                   int(dev)), "pareto_prepared")
+        return status, int(nf.value)
+
     def pareto(self, obj, cfgs: np.ndarray | None = None, tau_e: float | None = 0.05, status=None):
         """kareto_pareto -> (status uint8 [n]: 2 pruned / 1 frontier / 0 dominated, n_frontier)."""
         n = int(obj.shape[0])
@@ -477,6 +529,24 @@ class Context:
                                               None if ttl_arr is None else ttl_arr.ctypes.data, n_tuner,
                                               ctypes.byref(m), out.ctypes.data if n else None), "eval_queue")
         return out
+
+
+class Grid:
+    """kareto_grid handle (free before its context is closed)."""
+
+    def __init__(self, ctx: "Context", h, n: int):
+        self.ctx, self._h, self.n = ctx, h, n
+
+    def free(self):
+        if getattr(self, "_h", None) and getattr(self.ctx, "_h", None):
+            self.ctx._L.kareto_grid_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 class Trace:

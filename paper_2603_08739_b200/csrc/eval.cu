@@ -405,42 +405,58 @@ static void shard_bounds(const kareto_config *cfg, int64_t n, const uint32_t *ro
       fprintf(stderr, "[eval] %-10s %.3f ms\n", name, std::chrono::duration<double, std::milli>(t_ - ht0).count()); \
     }                                                                                                     \
   } while (0)
-static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_config *cfg, int64_t n_cfg,
-                          const uint32_t *ttl_ms, int32_t n_tuner, const kareto_model *model,
-                          kareto_counts *counts_out, double *obj_out, int32_t on_dev) {
-  const bool ht_on = getenv("KARETO_HOST_TIMING") != nullptr;
-  const auto ht0 = std::chrono::steady_clock::now();
-  cudaStream_t st = ctx->stream;
-  const int sms = ctx->num_sms;
-  if (n_cfg < 0 || (n_cfg > 0 && !cfg) || !model) return fail(ctx, KARETO_E_INVALID, "bad arguments");
-  if (!model_valid(model)) return fail(ctx, KARETO_E_INVALID, "invalid model constants");
-  if (n_tuner < 0 || (n_tuner > 0 && !ttl_ms)) return fail(ctx, KARETO_E_INVALID, "bad TTL table");
-  const int G = tr->K + 1;
-  const uint64_t N = (uint64_t)tr->N, U = (uint64_t)tr->U;
-  // a time-sharded trace (row f4) holds the accesses [pos_lo, pos_hi): every rank evaluates the
-  // whole grid from histograms summed over the ranks (no configuration sharding, no gather)
-  const bool tsh = tr->sharded;
-  const uint64_t Nl = (uint64_t)(tr->pos_hi - tr->pos_lo);
-  const uint32_t jb = (uint32_t)tr->pos_lo;
-  const bool cfg_shard = (ctx->world > 1 || ctx->nccl) && !tsh;
-  // rows (an all-infinite row when no table is given)
+// Everything kareto_eval_grid derives from the configuration list and the TTL table alone
+// (validation, the shard, the stack / replay split, the TTL value sets, device copies): built once
+// per call, or once per kareto_grid for repeated evaluation (kareto_grid_create).
+struct GridPrep {
+  int64_t n_cfg = 0;
+  int G = 1, n_tuner = 0, nrows = 1;
   std::vector<uint32_t> rows;
-  int nrows = n_tuner;
+  std::vector<char> row_uniform, row_finite;
+  bool cfg_shard = false;
+  std::vector<int64_t> bounds;
+  int64_t lo = 0, hi = 0, ns = 0, nS = 0, nP = 0;
+  std::vector<kareto_config> cP;   // replay configurations (host copy for K6)
+  std::vector<uint32_t> iS, iP;    // their positions in the shard
+  std::vector<uint32_t> Tc, Tt, tix;
+  int ntc = 0, ntt = 0;
+  // model-dependent checks, done per evaluation from these maxima
+  int max_medium = -1;
+  int64_t idx_medium = 0, idx_cap = 0;
+  uint64_t max_capsum = 0;
+  // device copies
+  DBuf<kareto_config> dcfg, dcfgP;
+  DBuf<uint32_t> dTc, dTt, dtix, drows, diS, diP;
+};
+
+static kareto_status prep_grid(kareto_ctx *ctx, const kareto_config *cfg, int64_t n_cfg, const uint32_t *ttl_ms,
+                               int32_t n_tuner, int G, bool cfg_shard, GridPrep &P) {
+  cudaStream_t st = ctx->stream;
+  if (n_cfg < 0 || (n_cfg > 0 && !cfg)) return fail(ctx, KARETO_E_INVALID, "bad arguments");
+  if (n_tuner < 0 || (n_tuner > 0 && !ttl_ms)) return fail(ctx, KARETO_E_INVALID, "bad TTL table");
+  P.n_cfg = n_cfg;
+  P.G = G;
+  P.n_tuner = n_tuner;
+  P.cfg_shard = cfg_shard;
+  // rows (an all-infinite row when no table is given)
+  std::vector<uint32_t> &rows = P.rows;
+  int &nrows = P.nrows;
+  nrows = n_tuner;
   if (n_tuner == 0) { rows.assign(G, KARETO_TTL_INF); nrows = 1; }
   else rows.assign(ttl_ms, ttl_ms + (size_t)n_tuner * G);
   // per-row flags: uniform across groups, all finite
-  std::vector<char> row_uniform(nrows, 1), row_finite(nrows, 1);
+  std::vector<char> &row_uniform = P.row_uniform, &row_finite = P.row_finite;
+  row_uniform.assign(nrows, 1);
+  row_finite.assign(nrows, 1);
   for (int r = 0; r < nrows; r++)
     for (int g = 0; g < G; g++) {
       if (rows[(size_t)r * G + g] != rows[(size_t)r * G]) row_uniform[r] = 0;
       if (rows[(size_t)r * G + g] == KARETO_TTL_INF) row_finite[r] = 0;
     }
-  HT("start");
   // ---- validation (every rank validates the full list identically), O(1) per configuration
   for (int64_t i = 0; i < n_cfg; i++) {
     const kareto_config &c = cfg[i];
     if (c.policy > KARETO_LFU) return fail(ctx, KARETO_E_INVALID, "config %lld: policy %d", (long long)i, c.policy);
-    if (c.medium >= model->n_media) return fail(ctx, KARETO_E_INVALID, "config %lld: medium", (long long)i);
     if (n_tuner > 0 && c.tuner >= n_tuner) return fail(ctx, KARETO_E_INVALID, "config %lld: tuner", (long long)i);
     if (c.cap[0] == KARETO_INF || c.cap[1] == KARETO_INF)
       return fail(ctx, KARETO_E_INVALID, "config %lld: infinite HBM/DRAM", (long long)i);
@@ -448,38 +464,26 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
     const bool ttl = c.cap[2] == KARETO_INF;
     if (ttl && !row_finite[ri])
       return fail(ctx, KARETO_E_INVALID, "config %lld: TTL mode needs finite TTLs (R22)", (long long)i);
-    // overflow guards of the integer model terms
-    unsigned __int128 cb = (unsigned __int128)(ttl ? sat_add(c.cap[0], c.cap[1])
-                                                   : sat_add(sat_add(c.cap[0], c.cap[1]), c.cap[2])) *
-                           model->block_bytes;
-    if (cb > (unsigned __int128)UINT64_MAX)
-      return fail(ctx, KARETO_E_OVERFLOW, "config %lld: capacity x block bytes", (long long)i);
+    if ((int)c.medium > P.max_medium) { P.max_medium = c.medium; P.idx_medium = i; }
+    const uint64_t cs = ttl ? sat_add(c.cap[0], c.cap[1]) : sat_add(sat_add(c.cap[0], c.cap[1]), c.cap[2]);
+    if (cs > P.max_capsum) { P.max_capsum = cs; P.idx_cap = i; }
   }
-  // trace x model integer constants
-  unsigned __int128 P0 = (unsigned __int128)model->alpha_ps * tr->SL + (unsigned __int128)model->beta_ps * tr->SQ;
-  if (P0 > (unsigned __int128)UINT64_MAX) return fail(ctx, KARETO_E_OVERFLOW, "no-cache prefill cost >= 2^64 ps");
-  if ((unsigned __int128)model->dec_ps * tr->O > (unsigned __int128)UINT64_MAX)
-    return fail(ctx, KARETO_E_OVERFLOW, "decode cost >= 2^64 ps");
-  if ((unsigned __int128)(2 * N + 2 * U) * model->block_bytes > (unsigned __int128)UINT64_MAX)
-    return fail(ctx, KARETO_E_OVERFLOW, "transfer bytes >= 2^64");
-  ModelConsts mc{(uint64_t)P0, (uint64_t)tr->R, N, U, tr->Ltok, tr->O, tr->span_ms};
-
-  HT("validated");
   // ---- shard
-  int64_t lo = 0, hi = n_cfg;
-  std::vector<int64_t> bounds((size_t)ctx->world + 1, 0);
+  int64_t &lo = P.lo, &hi = P.hi;
+  lo = 0;
+  hi = n_cfg;
+  P.bounds.assign((size_t)ctx->world + 1, 0);
   if (cfg_shard) {
-    shard_bounds(cfg, n_cfg, rows.data(), n_tuner, G, ctx->world, bounds.data());
-    lo = bounds[ctx->rank];
-    hi = bounds[ctx->rank + 1];
+    shard_bounds(cfg, n_cfg, rows.data(), n_tuner, G, ctx->world, P.bounds.data());
+    lo = P.bounds[ctx->rank];
+    hi = P.bounds[ctx->rank + 1];
   }
-  const int64_t ns = hi - lo;
+  const int64_t ns = P.ns = hi - lo;
   const kareto_config *sc = cfg + lo;
   // stack-eligible (LRU, and TTL mode or a uniform disk TTL) vs per-configuration replay (K6)
   // (one counting pass; the split copies are only made when both kinds are present, otherwise
-  // the caller's array is used as it is)
-  std::vector<kareto_config> cS, cP;
-  std::vector<uint32_t> iS, iP;
+  // the caller's array is uploaded as it is)
+  std::vector<kareto_config> cS;
   std::vector<char> cap_row_used(nrows, 0), ttl_row_used(nrows, 0);
   auto stack_ok = [&](const kareto_config &c) {
     const int ri = n_tuner > 0 ? c.tuner : 0;
@@ -492,22 +496,19 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
     if (stack_ok(c)) (c.cap[2] == KARETO_INF ? ttl_row_used : cap_row_used)[ri] = 1;
     else nP++;
   }
-  const int64_t nS = ns - nP;
+  P.nP = nP;
+  const int64_t nS = P.nS = ns - nP;
   const kareto_config *cSp = sc;  // the stack configurations, in shard order when nP == 0
   if (nP > 0) {
-    cS.reserve(nS); iS.reserve(nS); cP.reserve(nP); iP.reserve(nP);
+    cS.reserve(nS); P.iS.reserve(nS); P.cP.reserve(nP); P.iP.reserve(nP);
     for (int64_t i = 0; i < ns; i++) {
-      if (stack_ok(sc[i])) { cS.push_back(sc[i]); iS.push_back((uint32_t)i); }
-      else { cP.push_back(sc[i]); iP.push_back((uint32_t)i); }
+      if (stack_ok(sc[i])) { cS.push_back(sc[i]); P.iS.push_back((uint32_t)i); }
+      else { P.cP.push_back(sc[i]); P.iP.push_back((uint32_t)i); }
     }
     cSp = cS.data();
   }
-  if (tsh && nP > 0)
-    return fail(ctx, KARETO_E_UNSUPPORTED,
-                "time-sharded trace: %lld configurations need the per-configuration replay (FIFO, LFU, per-group "
-                "TTL on a finite disk); load the whole trace for those", (long long)nP);
   // TTL value sets: uniform CAPACITY TTLs (Tc) and all TTLs of rows used in TTL mode (Tt)
-  std::vector<uint32_t> Tc, Tt;
+  std::vector<uint32_t> &Tc = P.Tc, &Tt = P.Tt;
   for (int r = 0; r < nrows; r++) {
     if (cap_row_used[r] && rows[(size_t)r * G] != KARETO_TTL_INF) Tc.push_back(rows[(size_t)r * G]);
     if (ttl_row_used[r])
@@ -518,25 +519,81 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
     v.erase(std::unique(v.begin(), v.end()), v.end());
   };
   uniq(Tc); uniq(Tt);
-  const int ntc = (int)Tc.size(), ntt = (int)Tt.size();
-  std::vector<uint32_t> tix((size_t)nrows * G, 0);
+  P.ntc = (int)Tc.size();
+  P.ntt = (int)Tt.size();
+  P.tix.assign((size_t)nrows * G, 0);
   for (int r = 0; r < nrows; r++)
     if (ttl_row_used[r])
       for (int g = 0; g < G; g++)
-        tix[(size_t)r * G + g] =
+        P.tix[(size_t)r * G + g] =
             (uint32_t)(std::lower_bound(Tt.begin(), Tt.end(), rows[(size_t)r * G + g]) - Tt.begin());
+  // device copies
+  KTRY(upload(ctx, P.dTc, Tc)); KTRY(upload(ctx, P.dTt, Tt)); KTRY(upload(ctx, P.dtix, P.tix));
+  KTRY(upload(ctx, P.drows, rows));
+  KTRY(P.dcfg.alloc(ctx, nS > 0 ? nS : 1));
+  if (nS > 0) KCUDA(ctx, cudaMemcpyAsync(P.dcfg.p, cSp, sizeof(kareto_config) * nS, cudaMemcpyHostToDevice, st));
+  if (nP > 0) {
+    KTRY(P.dcfgP.alloc(ctx, nP));
+    KCUDA(ctx, cudaMemcpyAsync(P.dcfgP.p, P.cP.data(), sizeof(kareto_config) * nP, cudaMemcpyHostToDevice, st));
+    KTRY(upload(ctx, P.diS, P.iS)); KTRY(upload(ctx, P.diP, P.iP));
+  }
+  return KARETO_OK;
+}
+
+static kareto_status run_eval(kareto_ctx *ctx, const kareto_trace *tr, const GridPrep &prep, const kareto_model *model,
+                              kareto_counts *counts_out, double *obj_out, int32_t on_dev) {
+  const bool ht_on = getenv("KARETO_HOST_TIMING") != nullptr;
+  const auto ht0 = std::chrono::steady_clock::now();
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+  if (!model) return fail(ctx, KARETO_E_INVALID, "bad arguments");
+  if (!model_valid(model)) return fail(ctx, KARETO_E_INVALID, "invalid model constants");
+  const int G = tr->K + 1;
+  if (prep.G != G) return fail(ctx, KARETO_E_INVALID, "grid built for %d groups, trace has %d", prep.G, G);
+  const uint64_t N = (uint64_t)tr->N, U = (uint64_t)tr->U;
+  // a time-sharded trace (row f4) holds the accesses [pos_lo, pos_hi): every rank evaluates the
+  // whole grid from histograms summed over the ranks (no configuration sharding, no gather)
+  const bool tsh = tr->sharded;
+  const uint64_t Nl = (uint64_t)(tr->pos_hi - tr->pos_lo);
+  const uint32_t jb = (uint32_t)tr->pos_lo;
+  const bool cfg_shard = prep.cfg_shard;
+  const int64_t n_cfg = prep.n_cfg;
+  const int n_tuner = prep.n_tuner;
+  const std::vector<uint32_t> &rows = prep.rows;
+  HT("start");
+  // model-dependent checks from the grid's maxima (the per-configuration ones ran in prep_grid)
+  if (n_cfg > 0 && prep.max_medium >= model->n_media)
+    return fail(ctx, KARETO_E_INVALID, "config %lld: medium", (long long)prep.idx_medium);
+  if (n_cfg > 0 && (unsigned __int128)prep.max_capsum * model->block_bytes > (unsigned __int128)UINT64_MAX)
+    return fail(ctx, KARETO_E_OVERFLOW, "config %lld: capacity x block bytes", (long long)prep.idx_cap);
+  // trace x model integer constants
+  unsigned __int128 P0 = (unsigned __int128)model->alpha_ps * tr->SL + (unsigned __int128)model->beta_ps * tr->SQ;
+  if (P0 > (unsigned __int128)UINT64_MAX) return fail(ctx, KARETO_E_OVERFLOW, "no-cache prefill cost >= 2^64 ps");
+  if ((unsigned __int128)model->dec_ps * tr->O > (unsigned __int128)UINT64_MAX)
+    return fail(ctx, KARETO_E_OVERFLOW, "decode cost >= 2^64 ps");
+  if ((unsigned __int128)(2 * N + 2 * U) * model->block_bytes > (unsigned __int128)UINT64_MAX)
+    return fail(ctx, KARETO_E_OVERFLOW, "transfer bytes >= 2^64");
+  ModelConsts mc{(uint64_t)P0, (uint64_t)tr->R, N, U, tr->Ltok, tr->O, tr->span_ms};
+  HT("validated");
+  const std::vector<int64_t> &bounds = prep.bounds;
+  const int64_t ns = prep.ns, nS = prep.nS, nP = prep.nP;
+  const std::vector<kareto_config> &cP = prep.cP;
+  if (tsh && nP > 0)
+    return fail(ctx, KARETO_E_UNSUPPORTED,
+                "time-sharded trace: %lld configurations need the per-configuration replay (FIFO, LFU, per-group "
+                "TTL on a finite disk); load the whole trace for those", (long long)nP);
+  const int ntc = prep.ntc, ntt = prep.ntt;
+  const DBuf<uint32_t> &dTc = prep.dTc, &dTt = prep.dTt, &dtix = prep.dtix, &drows = prep.drows;
+  const DBuf<kareto_config> &dcfg = prep.dcfg;
 
   HT("classified");
   // ---- boundary sets and per-configuration lookup indices, on the GPU
-  DBuf<kareto_config> dcfg;
   DBuf<CfgDev> dcd;
   DBuf<uint8_t> tmp;
-  DBuf<uint32_t> dBd, dB12, dTc, dTt, dtix, drows;
-  KTRY(upload(ctx, dTc, Tc)); KTRY(upload(ctx, dTt, Tt)); KTRY(upload(ctx, dtix, tix)); KTRY(upload(ctx, drows, rows));
-  KTRY(dcfg.alloc(ctx, nS > 0 ? nS : 1)); KTRY(dcd.alloc(ctx, nS > 0 ? nS : 1));
+  DBuf<uint32_t> dBd, dB12;
+  KTRY(dcd.alloc(ctx, nS > 0 ? nS : 1));
   int nb = 0, nb12 = 0;
   if (nS > 0) {
-    KCUDA(ctx, cudaMemcpyAsync(dcfg.p, cSp, sizeof(kareto_config) * nS, cudaMemcpyHostToDevice, st));
     DBuf<uint32_t> vals, vals_s, v12, v12_s;
     DBuf<int> cnt;
     KTRY(vals.alloc(ctx, 3 * nS)); KTRY(vals_s.alloc(ctx, 3 * nS)); KTRY(v12.alloc(ctx, nS)); KTRY(v12_s.alloc(ctx, nS));
@@ -707,18 +764,14 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
     // K6 replay for the rest, then the objective from its counts; scatter both to shard order
     DBuf<kareto_counts> cntS, cntP;
     DBuf<double> objS, objP;
-    DBuf<kareto_config> dcfgP;
-    DBuf<uint32_t> diS, diP;
     KTRY(cntS.alloc(ctx, nS > 0 ? nS : 1)); KTRY(objS.alloc(ctx, 3 * (nS > 0 ? nS : 1)));
-    KTRY(cntP.alloc(ctx, nP)); KTRY(objP.alloc(ctx, 3 * nP)); KTRY(dcfgP.alloc(ctx, nP));
-    KTRY(upload(ctx, diS, iS)); KTRY(upload(ctx, diP, iP));
+    KTRY(cntP.alloc(ctx, nP)); KTRY(objP.alloc(ctx, 3 * nP));
     launch_objective(ctx, T, dcfg.p, dcd.p, dtix.p, drows.p, nS, model, mc, nullptr, cntS.p, objS.p);
     KTRY(replay_eval(ctx, const_cast<kareto_trace *>(tr), cP.data(), nP, rows.data(), drows.p, n_tuner, cntP.p));
-    KCUDA(ctx, cudaMemcpyAsync(dcfgP.p, cP.data(), sizeof(kareto_config) * nP, cudaMemcpyHostToDevice, st));
-    launch_objective(ctx, T, dcfgP.p, nullptr, dtix.p, drows.p, nP, model, mc, cntP.p, nullptr, objP.p);
+    launch_objective(ctx, T, prep.dcfgP.p, nullptr, dtix.p, drows.p, nP, model, mc, cntP.p, nullptr, objP.p);
     Pass ps(ctx, "K5_scatter", 1, 2);
-    if (nS > 0) k_scatter_out<<<grid_for(nS, 256), 256, 0, st>>>(cntS.p, objS.p, diS.p, nS, dcounts.p, dobj.p);
-    k_scatter_out<<<grid_for(nP, 256), 256, 0, st>>>(cntP.p, objP.p, diP.p, nP, dcounts.p, dobj.p);
+    if (nS > 0) k_scatter_out<<<grid_for(nS, 256), 256, 0, st>>>(cntS.p, objS.p, prep.diS.p, nS, dcounts.p, dobj.p);
+    k_scatter_out<<<grid_for(nP, 256), 256, 0, st>>>(cntP.p, objP.p, prep.diP.p, nP, dcounts.p, dobj.p);
   }
 
   HT("k57");
@@ -762,7 +815,95 @@ static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_
   return sst;
 }
 
+static kareto_status eval(kareto_ctx *ctx, const kareto_trace *tr, const kareto_config *cfg, int64_t n_cfg,
+                          const uint32_t *ttl_ms, int32_t n_tuner, const kareto_model *model,
+                          kareto_counts *counts_out, double *obj_out, int32_t on_dev) {
+  if (!model) return fail(ctx, KARETO_E_INVALID, "bad arguments");
+  GridPrep prep;
+  const bool cfg_shard = (ctx->world > 1 || ctx->nccl) && !tr->sharded;
+  KTRY(prep_grid(ctx, cfg, n_cfg, ttl_ms, n_tuner, tr->K + 1, cfg_shard, prep));
+  return run_eval(ctx, tr, prep, model, counts_out, obj_out, on_dev);
+}
+
+kareto_status pareto_line_widths(kareto_ctx *ctx, const kareto_config *cfg, int64_t n, int *w, std::string *err);
+
 }  // namespace kareto
+
+extern "C" kareto_status kareto_grid_create(kareto_ctx *ctx, const kareto_config *cfg, int64_t n_cfg,
+                                            const uint32_t *ttl_ms, int32_t n_tuner, int32_t n_groups,
+                                            kareto_grid **out) {
+  if (!ctx || !out) return KARETO_E_INVALID;
+  *out = nullptr;
+  ctx->err.clear();
+  if (n_groups < 1 || n_groups > 1024) return kareto::fail(ctx, KARETO_E_INVALID, "n_groups must be in [1, 1024]");
+  cudaSetDevice(ctx->device);
+  kareto_grid *g = new kareto_grid();
+  g->ctx = ctx;
+  g->n = n_cfg;
+  g->prep = new kareto::GridPrep();
+  const bool cfg_shard = ctx->world > 1 || ctx->nccl;
+  kareto_status s = kareto::prep_grid(ctx, cfg, n_cfg, ttl_ms, n_tuner, n_groups, cfg_shard, *g->prep);
+  if (s == KARETO_OK && n_cfg > 0) {
+    const std::string keep = ctx->err;  // a line-key range problem only matters if pruning is asked for
+    g->lw_ok = kareto::pareto_line_widths(ctx, cfg, n_cfg, g->lw, &g->lw_err) == KARETO_OK;
+    ctx->err = keep;
+    cudaError_t e = cudaMallocFromPoolAsync((void **)&g->dall, sizeof(kareto_config) * n_cfg, ctx->pool, ctx->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(g->dall, cfg, sizeof(kareto_config) * n_cfg, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      s = kareto::fail(ctx, KARETO_E_OOM, "grid upload: %s", cudaGetErrorString(e));
+    }
+  } else if (s == KARETO_OK) {
+    g->lw_ok = true;
+    s = kareto::sync(ctx, "grid_create");
+  }
+  if (s != KARETO_OK) {
+    kareto_grid_free(g);
+    return s;
+  }
+  *out = g;
+  return KARETO_OK;
+}
+
+extern "C" void kareto_grid_free(kareto_grid *g) {
+  if (!g) return;
+  if (g->dall) cudaFreeAsync(g->dall, g->ctx->stream);
+  delete g->prep;  // its device buffers free on the context stream
+  cudaStreamSynchronize(g->ctx->stream);
+  (void)cudaGetLastError();
+  delete g;
+}
+
+extern "C" kareto_status kareto_eval_grid_prepared(kareto_ctx *ctx, const kareto_trace *tr, const kareto_grid *grid,
+                                                   const kareto_model *model, kareto_counts *counts_out,
+                                                   double *obj_out, int32_t outputs_on_device) {
+  if (!ctx || !tr || !grid) return KARETO_E_INVALID;
+  ctx->err.clear();
+  if (grid->ctx != ctx) return kareto::fail(ctx, KARETO_E_INVALID, "grid belongs to another context");
+  cudaSetDevice(ctx->device);
+  kareto_status s;
+  if (grid->prep->cfg_shard && tr->sharded) {
+    // a time-sharded trace evaluates the whole grid on every rank: the grid's configuration
+    // shard does not apply, so this call re-derives the unsharded split (from the device copy)
+    std::vector<kareto_config> h(grid->n);
+    if (grid->n > 0) {
+      cudaMemcpy(h.data(), grid->dall, sizeof(kareto_config) * grid->n, cudaMemcpyDeviceToHost);
+    }
+    const kareto::GridPrep &P = *grid->prep;
+    kareto::GridPrep q;
+    s = kareto::prep_grid(ctx, h.data(), grid->n, P.n_tuner ? P.rows.data() : nullptr, P.n_tuner, P.G, false, q);
+    if (s == KARETO_OK) s = kareto::run_eval(ctx, tr, q, model, counts_out, obj_out, outputs_on_device);
+  } else {
+    s = kareto::run_eval(ctx, tr, *grid->prep, model, counts_out, obj_out, outputs_on_device);
+  }
+  if (s != KARETO_OK) {
+    cudaStreamSynchronize(ctx->stream);
+    (void)cudaGetLastError();
+  }
+  return s;
+}
 
 extern "C" kareto_status kareto_shard_bounds(const kareto_config *cfg, int64_t n, const uint32_t *ttl_ms,
                                              int32_t n_tuner, int32_t n_groups, int32_t world, int64_t *bounds) {

@@ -113,6 +113,22 @@ struct kareto_trace {
 };
 
 namespace kareto {
+struct GridPrep;  // eval.cu
+}
+// A configuration grid prepared for repeated evaluation (kareto_grid_create): eval_grid's
+// validation, shard, stack / replay split and device copies (GridPrep), and K8's device copy of
+// every configuration with its line-key bit widths.
+struct kareto_grid {
+  kareto_ctx *ctx = nullptr;
+  kareto::GridPrep *prep = nullptr;
+  int64_t n = 0;
+  kareto_config *dall = nullptr;  // [n] device (pool), freed by kareto_grid_free
+  int lw[6] = {0, 0, 0, 0, 0, 0};
+  bool lw_ok = false;             // the axis / line-key ranges pruning needs
+  std::string lw_err;
+};
+
+namespace kareto {
 
 // ----------------------------------------------------------------- errors ----
 inline kareto_status fail(kareto_ctx *ctx, kareto_status st, const char *fmt, ...) {

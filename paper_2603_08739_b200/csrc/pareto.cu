@@ -141,32 +141,59 @@ static kareto_status cub_tmp(kareto_ctx *ctx, DBuf<uint8_t> &tmp, F &&f) {
   return KARETO_OK;
 }
 
+// Host checks of the line keys pruning builds (axis and key fields in range) and their bit widths.
+kareto_status pareto_line_widths(kareto_ctx *ctx, const kareto_config *cfg, int64_t n, int *w, std::string *err) {
+  uint32_t mx[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t i = 0; i < n; i++) {
+    const kareto_config &c = cfg[i];
+    for (int a = 0; a < 3; a++) {
+      if (c.axis[a] < 0 || c.axis[a] > 65535) {
+        char b[96];
+        snprintf(b, sizeof(b), "config %lld: axis out of range", (long long)i);
+        if (err) *err = b;
+        return fail(ctx, KARETO_E_INVALID, "%s", b);
+      }
+      mx[a] |= (uint32_t)c.axis[a];
+    }
+    if (c.tuner > 1023 || c.medium > 15 || c.policy > 3) {
+      char b[96];
+      snprintf(b, sizeof(b), "config %lld: line key out of range", (long long)i);
+      if (err) *err = b;
+      return fail(ctx, KARETO_E_INVALID, "%s", b);
+    }
+    mx[3] |= c.tuner; mx[4] |= c.medium; mx[5] |= c.policy;
+  }
+  for (int k = 0; k < 6; k++) {  // bits needed by the OR of the values = bits of the maximum
+    w[k] = 0;
+    while (w[k] < 32 && (mx[k] >> w[k]) != 0) w[k]++;
+  }
+  return KARETO_OK;
+}
+
+// dcfg: device copy of the configurations (only read when pruning), lw: their line-key widths
+static kareto_status pareto_run(kareto_ctx *ctx, const double *obj, const kareto_config *dcfg_in, const kareto_config *hcfg,
+                                const LineWidths &lw, int64_t n, const kareto_prune *prune, uint8_t *status_out,
+                                int64_t *n_frontier, int32_t on_dev);
+
 static kareto_status pareto(kareto_ctx *ctx, const double *obj, const kareto_config *cfg, int64_t n,
                             const kareto_prune *prune, uint8_t *status_out, int64_t *n_frontier, int32_t on_dev) {
-  cudaStream_t st = ctx->stream;
-  const int sms = ctx->num_sms;
   if (n < 0 || (n > 0 && (!obj || !status_out))) return fail(ctx, KARETO_E_INVALID, "bad arguments");
   if (n >= (int64_t)0x7FFFFFFF) return fail(ctx, KARETO_E_OVERFLOW, "too many configurations");
   const bool do_prune = prune && prune->enabled;
   LineWidths lw{};
   if (do_prune) {
     if (!cfg) return fail(ctx, KARETO_E_INVALID, "pruning needs the configurations");
-    uint32_t mx[6] = {0, 0, 0, 0, 0, 0};
-    for (int64_t i = 0; i < n; i++) {
-      const kareto_config &c = cfg[i];
-      for (int a = 0; a < 3; a++) {
-        if (c.axis[a] < 0 || c.axis[a] > 65535) return fail(ctx, KARETO_E_INVALID, "config %lld: axis out of range", (long long)i);
-        mx[a] |= (uint32_t)c.axis[a];
-      }
-      if (c.tuner > 1023 || c.medium > 15 || c.policy > 3)
-        return fail(ctx, KARETO_E_INVALID, "config %lld: line key out of range", (long long)i);
-      mx[3] |= c.tuner; mx[4] |= c.medium; mx[5] |= c.policy;
-    }
-    for (int k = 0; k < 6; k++) {  // bits needed by the OR of the values = bits of the maximum
-      lw.w[k] = 0;
-      while (lw.w[k] < 32 && (mx[k] >> lw.w[k]) != 0) lw.w[k]++;
-    }
+    KTRY(pareto_line_widths(ctx, cfg, n, lw.w, nullptr));
   }
+  return pareto_run(ctx, obj, nullptr, cfg, lw, n, prune, status_out, n_frontier, on_dev);
+}
+
+static kareto_status pareto_run(kareto_ctx *ctx, const double *obj, const kareto_config *dcfg_in, const kareto_config *hcfg,
+                                const LineWidths &lw, int64_t n, const kareto_prune *prune, uint8_t *status_out,
+                                int64_t *n_frontier, int32_t on_dev) {
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->num_sms;
+  const bool do_prune = prune && prune->enabled;
   int key_bits = 0;
   for (int k = 0; k < 6; k++) key_bits += lw.w[k];
   if (key_bits == 0) key_bits = 1;
@@ -185,17 +212,22 @@ static kareto_status pareto(kareto_ctx *ctx, const double *obj, const kareto_con
   KTRY(pruned.alloc(ctx, n)); KTRY(pruned.zero());
   KTRY(status.alloc(ctx, n));
   if (do_prune) {
-    DBuf<kareto_config> dcfg;
+    DBuf<kareto_config> down;
     DBuf<uint64_t> key, key_s, line;
     DBuf<uint32_t> idx, idx_s;
     DBuf<uint8_t> stop, excl;
-    KTRY(dcfg.alloc(ctx, n)); KTRY(key.alloc(ctx, n)); KTRY(key_s.alloc(ctx, n)); KTRY(line.alloc(ctx, n));
+    KTRY(key.alloc(ctx, n)); KTRY(key_s.alloc(ctx, n)); KTRY(line.alloc(ctx, n));
     KTRY(idx.alloc(ctx, n)); KTRY(idx_s.alloc(ctx, n)); KTRY(stop.alloc(ctx, n)); KTRY(excl.alloc(ctx, n));
-    KCUDA(ctx, cudaMemcpyAsync(dcfg.p, cfg, sizeof(kareto_config) * n, cudaMemcpyHostToDevice, st));
+    const kareto_config *dcfg = dcfg_in;
+    if (!dcfg) {
+      KTRY(down.alloc(ctx, n));
+      KCUDA(ctx, cudaMemcpyAsync(down.p, hcfg, sizeof(kareto_config) * n, cudaMemcpyHostToDevice, st));
+      dcfg = down.p;
+    }
     for (int a = 0; a < 3; a++) {
       {
         Pass ps(ctx, "K8a_line_keys", 1, 1);
-        k_line_keys<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(dcfg.p, n, a, lw, key.p, idx.p);
+        k_line_keys<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(dcfg, n, a, lw, key.p, idx.p);
       }
       {
         Pass ps(ctx, "K8a_sort_lines", 0, 1);
@@ -256,6 +288,19 @@ static kareto_status pareto(kareto_ctx *ctx, const double *obj, const kareto_con
   return KARETO_OK;
 }
 
+kareto_status pareto_grid(kareto_ctx *ctx, const double *obj, const kareto_grid *g, const kareto_prune *prune,
+                          uint8_t *status_out, int64_t *n_frontier, int32_t on_dev) {
+  const int64_t n = g->n;
+  if (n > 0 && (!obj || !status_out)) return fail(ctx, KARETO_E_INVALID, "bad arguments");
+  if (n >= (int64_t)0x7FFFFFFF) return fail(ctx, KARETO_E_OVERFLOW, "too many configurations");
+  LineWidths lw{};
+  if (prune && prune->enabled) {
+    if (!g->lw_ok) return fail(ctx, KARETO_E_INVALID, "%s", g->lw_err.c_str());
+    for (int k = 0; k < 6; k++) lw.w[k] = g->lw[k];
+  }
+  return pareto_run(ctx, obj, g->dall, nullptr, lw, n, prune, status_out, n_frontier, on_dev);
+}
+
 }  // namespace kareto
 
 extern "C" kareto_status kareto_pareto(kareto_ctx *ctx, const double *obj, const kareto_config *cfg, int64_t n,
@@ -265,6 +310,21 @@ extern "C" kareto_status kareto_pareto(kareto_ctx *ctx, const double *obj, const
   ctx->err.clear();
   cudaSetDevice(ctx->device);
   kareto_status s = kareto::pareto(ctx, obj, cfg, n, prune, status_out, n_frontier, on_device);
+  if (s != KARETO_OK) {
+    cudaStreamSynchronize(ctx->stream);
+    (void)cudaGetLastError();
+  }
+  return s;
+}
+
+extern "C" kareto_status kareto_pareto_prepared(kareto_ctx *ctx, const double *obj, const kareto_grid *grid,
+                                                const kareto_prune *prune, uint8_t *status_out, int64_t *n_frontier,
+                                                int32_t on_device) {
+  if (!ctx || !grid) return KARETO_E_INVALID;
+  ctx->err.clear();
+  if (grid->ctx != ctx) return kareto::fail(ctx, KARETO_E_INVALID, "grid belongs to another context");
+  cudaSetDevice(ctx->device);
+  kareto_status s = kareto::pareto_grid(ctx, obj, grid, prune, status_out, n_frontier, on_device);
   if (s != KARETO_OK) {
     cudaStreamSynchronize(ctx->stream);
     (void)cudaGetLastError();

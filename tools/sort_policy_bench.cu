@@ -5,6 +5,9 @@
 #include <cub/cub.cuh>
 #include <cstdio>
 #include <vector>
+#ifndef BEGIN_BIT
+#define BEGIN_BIT 16  // K2 sorts the top 16 key bits only (2 passes); 0 = the full 32-bit sort
+#endif
 
 template <int BITS, int THREADS, int ITEMS>
 struct Hub {
@@ -65,7 +68,7 @@ static float run(const char *name, uint32_t *k0, uint64_t *v0, uint32_t *k1, uin
     size_t tb = tmp_bytes;
     cudaEventRecord(a);
     cudaError_t e = cub::DispatchRadixSort<false, uint32_t, uint64_t, uint32_t, Hub_>::Dispatch(
-        tmp, tb, dk, dv, (uint32_t)n, 0, 32, true, 0);
+        tmp, tb, dk, dv, (uint32_t)n, BEGIN_BIT, 32, true, 0);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     if (e != cudaSuccess) { printf("%s: error %s\n", name, cudaGetErrorString(e)); return -1; }
@@ -80,7 +83,10 @@ static float run(const char *name, uint32_t *k0, uint64_t *v0, uint32_t *k1, uin
       std::vector<uint32_t> rk(n);
       cudaMemcpy(rk.data(), ref, 4 * n, cudaMemcpyDeviceToHost);
       bool ok = true;
-      for (int64_t i = 0; i < n && ok; i++) ok = hk[i] == rk[i] && (i == 0 || hk[i] != hk[i - 1] || (uint32_t)hv[i] > (uint32_t)hv[i - 1]);
+      for (int64_t i = 1; i < n && ok; i++) {
+        const uint32_t a = hk[i - 1] >> BEGIN_BIT, b = hk[i] >> BEGIN_BIT;
+        ok = a < b || (a == b && (uint32_t)hv[i] > (uint32_t)hv[i - 1]);  // ordered, stable
+      }
       printf("%s: %s\n", name, ok ? "sorted, stable" : "MISMATCH");
     }
   }
@@ -115,14 +121,10 @@ int main() {
     float ms; cudaEventElapsedTime(&ms, a, b); best = ms < best ? ms : best;
   }
   printf("%-28s %8.3f ms (cub::DeviceRadixSort::SortPairs, not in place)\n", "default", best);
-  run<Hub<8, 384, 29>>("bits8 t384 i29 (default-like)", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
-  run<Hub<8, 256, 32>>("bits8 t256 i32", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, true, kref);
-  run<Hub<8, 256, 36>>("bits8 t256 i36", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
-  run<Hub<8, 256, 40>>("bits8 t256 i40", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
-  run<Hub<8, 256, 44>>("bits8 t256 i44", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
-  run<Hub<8, 192, 40>>("bits8 t192 i40", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
-  run<Hub<8, 128, 48>>("bits8 t128 i48", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
-  run<Hub<8, 320, 32>>("bits8 t320 i32", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
+  run<Hub<8, 256, 32>>("bits8 t256 i32 (K2 now)", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, true, kref);
+  run<Hub<8, 384, 29>>("bits8 t384 i29", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
+  run<Hub<8, 128, 64>>("bits8 t128 i64", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
+  run<Hub<7, 256, 32>>("bits7 t256 i32", k0, v0, k1, v1, kr, vr, n, tmp, tmp_bytes, 5, false, kref);
   printf("done\n");
   return 0;
 }

@@ -192,6 +192,26 @@ def _ptr(x):
     raise TypeError(f"unsupported buffer {type(x)}")
 
 
+def _check_outputs(counts, obj, n: int):
+    """(counts ptr, obj ptr, on_device) after checking both live in one memory space with exactly
+    88 * n / 24 * n contiguous bytes (float64 objectives)."""
+    pc, dc = _ptr(counts)
+    po, do = _ptr(obj)
+    if counts is not None and obj is not None and dc != do:
+        raise ValueError("counts and obj must both be host or both be device buffers")
+    for name, buf, nbytes in (("counts", counts, 88 * n), ("obj", obj, 24 * n)):
+        if buf is None:
+            continue
+        size = buf.nbytes if isinstance(buf, np.ndarray) else int(buf.numel()) * int(buf.element_size())
+        if size != nbytes:
+            raise ValueError(f"{name} must hold exactly {nbytes} bytes for {n} configurations, got {size}")
+        if not isinstance(buf, np.ndarray) and not buf.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+    if obj is not None and not isinstance(obj, np.ndarray) and "float64" not in str(obj.dtype):
+        raise ValueError("obj must be float64 [n][3]")
+    return pc, po, bool(dc or do)
+
+
 class Model:
     """kareto_model constants; defaults = SURVEY 8.d.3 bench constants."""
 
@@ -360,21 +380,7 @@ class Context:
         if counts is None and obj is None:
             counts = np.zeros(n, COUNTS_DTYPE)
             obj = np.zeros((n, 3), np.float64)
-        pc, dc = _ptr(counts)
-        po, do = _ptr(obj)
-        if counts is not None and obj is not None and dc != do:
-            raise ValueError("counts and obj must both be host or both be device buffers")
-        on_dev = dc or do
-        for name, buf, nbytes in (("counts", counts, 88 * n), ("obj", obj, 24 * n)):
-            if buf is None:
-                continue
-            size = buf.nbytes if isinstance(buf, np.ndarray) else int(buf.numel()) * int(buf.element_size())
-            if size != nbytes:
-                raise ValueError(f"{name} must hold exactly {nbytes} bytes for {n} configurations, got {size}")
-            if not isinstance(buf, np.ndarray) and not buf.is_contiguous():
-                raise ValueError(f"{name} must be contiguous")
-        if obj is not None and not isinstance(obj, np.ndarray) and "float64" not in str(obj.dtype):
-            raise ValueError("obj must be float64 [n][3]")
+        pc, po, on_dev = _check_outputs(counts, obj, n)
         m = model.c()
         self._check(self._L.kareto_eval_grid(self._h, trace._h, cfgs.ctypes.data if n else None, n,
                                              None if ttl_arr is None else ttl_arr.ctypes.data, n_tuner,
@@ -404,13 +410,10 @@ class Context:
         if counts is None and obj is None:
             counts = np.zeros(n, COUNTS_DTYPE)
             obj = np.zeros((n, 3), np.float64)
-        pc, dc = _ptr(counts)
-        po, do = _ptr(obj)
-        if counts is not None and obj is not None and dc != do:
-            raise ValueError("counts and obj must both be host or both be device buffers")
+        pc, po, on_dev = _check_outputs(counts, obj, n)
         m = model.c()
         self._check(self._L.kareto_eval_grid_prepared(self._h, trace._h, grid._h, ctypes.byref(m), pc, po,
-                                                      int(dc or do)), "eval_grid_prepared")
+                                                      int(on_dev)), "eval_grid_prepared")
         return counts, obj
 
     def pareto_prepared(self, obj, grid: "Grid", tau_e: float | None = 0.05, status=None):

@@ -52,6 +52,20 @@ def test_config4_every_depth_sampled_counts_objectives(ctx):
     assert np.array_equal(obj[idx].view(np.uint64), fo.view(np.uint64))
     j = idx[:4]
     assert np.array_equal(got[j].view(np.uint64), ot.replay(oc[j], ttl).view(np.uint64))
+    # bench.py's launch configuration: the prepared grid, device outputs -- bit-identical
+    import torch
+    g = ctx.grid(cfg, ttl)
+    cnt_d = torch.empty((len(cfg), 11), dtype=torch.int64, device="cuda")
+    obj_d = torch.empty((len(cfg), 3), dtype=torch.float64, device="cuda")
+    ctx.eval_prepared(gt, g, K.Model(), counts=cnt_d, obj=obj_d)
+    torch.cuda.synchronize()
+    assert np.array_equal(cnt_d.cpu().numpy().view(np.uint64).ravel(), got.view(np.uint64).ravel())
+    assert np.array_equal(obj_d.cpu().numpy().view(np.uint64), obj.view(np.uint64))
+    st_d = torch.empty(len(cfg), dtype=torch.uint8, device="cuda")
+    _, nf = ctx.pareto_prepared(obj_d, g, spec["prune"], status=st_d)
+    torch.cuda.synchronize()
+    assert np.array_equal(st_d.cpu().numpy(), O.select(obj, oc, spec["prune"])) and nf > 0
+    g.free()
 
 
 def test_config3_twin_sampled_literal_replay(ctx):

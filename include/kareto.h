@@ -110,7 +110,10 @@ typedef struct {
  * group, LRU stack depth.  Validation errors: KARETO_E_INVALID
  * (R < 1, K out of range, null pointers), _E_PARSE (offsets decreasing, output < 0,
  * input_tokens < 16*blocks), _E_CHAIN (R7), _E_OVERFLOW (>= 2^32-1 block accesses or a
- * reuse interval >= 2^32-1 ms), _E_OOM. */
+ * reuse interval >= 2^32-1 ms), _E_OOM.
+ * Memory: the trace keeps 24 B per access on the device until kareto_trace_free; the K2 link's
+ * scratch (20 B per access) stays with the context for the next load and is freed by
+ * kareto_destroy. */
 kareto_status kareto_load_trace(kareto_ctx *ctx, const kareto_trace_desc *desc, kareto_trace **out);
 void kareto_trace_free(kareto_trace *tr);
 

@@ -306,7 +306,7 @@ def run_reference(args, spec):
             t_rep = (time.perf_counter() - t2) * len(rep) / len(samp)
         t3 = time.perf_counter()
         fobj = ot.objective(O.Model(), cf, cnt)
-        O.select(fobj, cf, spec["prune"])
+        O.select(fobj, cf, spec["prune"], threads=threads)  # the O(n^2) rows on every host thread
         t_sel = time.perf_counter() - t3
         return t_trace, t_rep, t_sel, ot.N, len(cf), int(len(rep)), n_samp
 
@@ -324,7 +324,8 @@ def run_reference(args, spec):
     value = n / t_full
     if args.full:
         what = (f"full workload ({Ns} accesses, {n} configurations): oracle trace build + O2 Fenwick depths + "
-                f"stack closed forms ({t_trace:.2f} s), fp64 model + pruning + O(n^2) dominance ({t_sel:.2f} s)")
+                f"stack closed forms ({t_trace:.2f} s, sequential), fp64 model + pruning + O(n^2) dominance "
+                f"({t_sel:.2f} s, rows on {threads} threads)")
     else:
         what = (f"sample trace of {tr.n_requests} requests ({Ns} accesses, the same generator) with the full "
                 f"{n}-configuration grid: oracle trace build + O2 depths + closed forms ({t_trace:.2f} s), fp64 model "
@@ -333,7 +334,7 @@ def run_reference(args, spec):
     if n_rep:
         what += (f"; O1 literal replay of {n_samp} of the {n_rep} replay configurations on {threads} threads, "
                  f"scaled in count ({t_rep:.2f} s)")
-    cores = threads if n_rep else 1
+    cores = threads  # the dominance rows (and config 3's O1 samples) run on every host thread
     line = {"impl": "reference", "metric": "configs evaluated/sec", "value": value, "unit": "configs/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": measured * 1e3,
             "ms_per_full_step": t_full * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,

@@ -1004,9 +1004,10 @@ void or_prune(const double *f, const or_config *cfg, int64_t n, double tau_e, ui
   free(idx);
 }
 
-int64_t or_pareto(const double *f, int64_t n, const uint8_t *pruned, uint8_t *status) {
-  int64_t nf = 0;
-  for (int64_t i = 0; i < n; i++) {
+/* status of configurations [i0, i1): the O(n^2) definition, row by row */
+static void or_pareto_rows(const double *f, int64_t n, const uint8_t *pruned, uint8_t *status, int64_t i0,
+                           int64_t i1) {
+  for (int64_t i = i0; i < i1; i++) {
     if (pruned && pruned[i]) { status[i] = 2; continue; }
     int dom = 0;
     for (int64_t j = 0; j < n && !dom; j++) {
@@ -1015,7 +1016,35 @@ int64_t or_pareto(const double *f, int64_t n, const uint8_t *pruned, uint8_t *st
       if (y[0] <= x[0] && y[1] <= x[1] && y[2] <= x[2] && (y[0] < x[0] || y[1] < x[1] || y[2] < x[2])) dom = 1;
     }
     status[i] = dom ? 0 : 1;
-    nf += !dom;
   }
+}
+
+int64_t or_pareto(const double *f, int64_t n, const uint8_t *pruned, uint8_t *status) {
+  or_pareto_rows(f, n, pruned, status, 0, n);
+  int64_t nf = 0;
+  for (int64_t i = 0; i < n; i++) nf += status[i] == 1;
+  return nf;
+}
+
+/* the same, rows split across host threads (each row's status depends only on the inputs) */
+typedef struct { const double *f; int64_t n; const uint8_t *pruned; uint8_t *status; int64_t i0, i1; } or_pareto_job;
+static void *or_pareto_worker(void *a) {
+  or_pareto_job *j = (or_pareto_job *)a;
+  or_pareto_rows(j->f, j->n, j->pruned, j->status, j->i0, j->i1);
+  return NULL;
+}
+int64_t or_pareto_mt(const double *f, int64_t n, const uint8_t *pruned, uint8_t *status, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  if (threads > n) threads = n > 0 ? (int)n : 1;
+  pthread_t th[256];
+  or_pareto_job jobs[256];
+  for (int t = 0; t < threads; t++) {
+    jobs[t] = (or_pareto_job){f, n, pruned, status, n * t / threads, n * (t + 1) / threads};
+    pthread_create(&th[t], NULL, or_pareto_worker, &jobs[t]);
+  }
+  for (int t = 0; t < threads; t++) pthread_join(th[t], NULL);
+  int64_t nf = 0;
+  for (int64_t i = 0; i < n; i++) nf += status[i] == 1;
   return nf;
 }

@@ -91,6 +91,8 @@ def _load():
     L.or_prune.argtypes = [vp, vp, i64, ctypes.c_double, vp]
     L.or_pareto.restype = i64
     L.or_pareto.argtypes = [vp, i64, vp, vp]
+    L.or_pareto_mt.restype = i64
+    L.or_pareto_mt.argtypes = [vp, i64, vp, vp, ctypes.c_int]
     L.or_fmix64_export.restype = u64
     L.or_fmix64_export.argtypes = [u64]
     L.or_content_hash_export.restype = u64
@@ -326,19 +328,23 @@ def prune(f: np.ndarray, cfgs: np.ndarray, tau_e: float = 0.05) -> np.ndarray:
     return out
 
 
-def pareto(f: np.ndarray, pruned: np.ndarray | None = None) -> np.ndarray:
+def pareto(f: np.ndarray, pruned: np.ndarray | None = None, threads: int = 1) -> np.ndarray:
+    """O(n^2) dominance (R35); threads > 1 splits the rows across host threads (same result)."""
     f = np.ascontiguousarray(f, np.float64)
     n = f.shape[0]
     st = np.zeros(n, np.uint8)
     pr = None if pruned is None else np.ascontiguousarray(pruned, np.uint8)
-    _load().or_pareto(f.ctypes.data, n, _ptr(pr), st.ctypes.data)
+    if threads > 1:
+        _load().or_pareto_mt(f.ctypes.data, n, _ptr(pr), st.ctypes.data, int(threads))
+    else:
+        _load().or_pareto(f.ctypes.data, n, _ptr(pr), st.ctypes.data)
     return st
 
 
-def select(f, cfgs, tau_e: float | None = 0.05) -> np.ndarray:
+def select(f, cfgs, tau_e: float | None = 0.05, threads: int = 1) -> np.ndarray:
     """Full kareto_pareto semantics: status 2 pruned / 1 frontier / 0 dominated."""
     pr = prune(f, cfgs, tau_e) if tau_e is not None else None
-    return pareto(f, pr)
+    return pareto(f, pr, threads)
 
 
 def timed_replay(tr: OracleTrace, cfgs, ttl=None, threads=None):

@@ -164,6 +164,7 @@ def test_pareto_random_against_pairwise_and_idempotent(rng):
         assert np.array_equal(st == 0, dom)
         front = f[st == 1]
         assert np.all(O.pareto(front) == 1)              # S:516 idempotence
+        assert np.array_equal(O.pareto(f, threads=4), st)  # row-parallel variant: same statuses
 
 
 def _grid_cfgs(m1, m2, m3):

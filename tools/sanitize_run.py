@@ -37,7 +37,7 @@ for i, a in enumerate(A(3, ot.U // 16)):
                     caps.append([a, b, c]); pol.append(p); tun.append(ti); ax.append([i, j, k])
                 caps.append([a, b, O.INF_CAP]); pol.append(p); tun.append(2); ax.append([i, j, 0])
 oc = O.configs(caps, policy=np.array(pol), tuner=np.array(tun), axis=ax)
-if MODE == "trace":  # stack-path configurations only
+if MODE in ("trace", "trace1"):  # stack-path configurations only
     oc = oc[(oc["policy"] == O.LRU) & ((oc["tuner"] != 2) | (oc["cap"][:, 2] == O.INF_CAP))]
 kc = K.configs(oc["cap"], policy=oc["policy"], tuner=oc["tuner"], axis=oc["axis"])
 os.environ["KARETO_K6_BUDGET"] = str(40 * ot.U * 40)
@@ -47,12 +47,15 @@ assert np.array_equal(cnt.view(np.uint64), want.view(np.uint64)), "counts differ
 st, nf = ctx.pareto(obj, kc, 0.05)
 assert np.array_equal(st, O.select(ot.objective(O.Model(), oc, want), oc, 0.05))
 del os.environ["KARETO_K6_BUDGET"]
-if MODE == "replay":
+if MODE in ("replay", "trace1"):
     print(f"sanitize run ok ({MODE}): N={gt.N} U={gt.U} configs={len(kc)} frontier={nf}")
     sys.exit(0)
 ctx.ttl_allocate(gt, 10**9, seed=1)
 lru = np.nonzero(oc["policy"] == O.LRU)[0][:8]
 ctx.eval_queue(gt, kc[lru], K.Model(), rows)
+if MODE == "trace1":  # no loopback threads
+    print(f"sanitize run ok ({MODE}): N={gt.N} U={gt.U} configs={len(kc)} frontier={nf}")
+    sys.exit(0)
 grp = K.Loopback(2)
 errs = []
 

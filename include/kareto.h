@@ -231,7 +231,10 @@ typedef struct kareto_grid kareto_grid;
 kareto_status kareto_grid_create(kareto_ctx *ctx, const kareto_config *cfg, int64_t n_cfg, const uint32_t *ttl_ms,
                                  int32_t n_tuner, int32_t n_groups, kareto_grid **out);
 void kareto_grid_free(kareto_grid *grid);
-/* kareto_eval_grid over a prepared grid (same outputs, bit-identical). */
+/* kareto_eval_grid over a prepared grid (same outputs, bit-identical).  A grid created on a
+ * multi-rank context holds its rank's configuration shard; evaluated against a time-sharded
+ * trace (every rank evaluates the whole grid) it derives and keeps the unsharded split on first
+ * use. */
 kareto_status kareto_eval_grid_prepared(kareto_ctx *ctx, const kareto_trace *tr, const kareto_grid *grid,
                                         const kareto_model *model, kareto_counts *counts_out, double *obj_out,
                                         int32_t outputs_on_device);

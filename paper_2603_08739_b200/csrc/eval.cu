@@ -871,6 +871,7 @@ extern "C" void kareto_grid_free(kareto_grid *g) {
   if (!g) return;
   if (g->dall) cudaFreeAsync(g->dall, g->ctx->stream);
   delete g->prep;  // its device buffers free on the context stream
+  delete g->prep_whole;
   cudaStreamSynchronize(g->ctx->stream);
   (void)cudaGetLastError();
   delete g;
@@ -886,15 +887,22 @@ extern "C" kareto_status kareto_eval_grid_prepared(kareto_ctx *ctx, const kareto
   kareto_status s;
   if (grid->prep->cfg_shard && tr->sharded) {
     // a time-sharded trace evaluates the whole grid on every rank: the grid's configuration
-    // shard does not apply, so this call re-derives the unsharded split (from the device copy)
-    std::vector<kareto_config> h(grid->n);
-    if (grid->n > 0) {
-      cudaMemcpy(h.data(), grid->dall, sizeof(kareto_config) * grid->n, cudaMemcpyDeviceToHost);
+    // shard does not apply; the unsharded split is derived once (from the device copy) and kept
+    kareto_grid *g = const_cast<kareto_grid *>(grid);
+    s = KARETO_OK;
+    if (!g->prep_whole) {
+      std::vector<kareto_config> h(grid->n);
+      if (grid->n > 0) cudaMemcpy(h.data(), grid->dall, sizeof(kareto_config) * grid->n, cudaMemcpyDeviceToHost);
+      const kareto::GridPrep &P = *grid->prep;
+      g->prep_whole = new kareto::GridPrep();
+      s = kareto::prep_grid(ctx, h.data(), grid->n, P.n_tuner ? P.rows.data() : nullptr, P.n_tuner, P.G, false,
+                            *g->prep_whole);
+      if (s != KARETO_OK) {
+        delete g->prep_whole;
+        g->prep_whole = nullptr;
+      }
     }
-    const kareto::GridPrep &P = *grid->prep;
-    kareto::GridPrep q;
-    s = kareto::prep_grid(ctx, h.data(), grid->n, P.n_tuner ? P.rows.data() : nullptr, P.n_tuner, P.G, false, q);
-    if (s == KARETO_OK) s = kareto::run_eval(ctx, tr, q, model, counts_out, obj_out, outputs_on_device);
+    if (s == KARETO_OK) s = kareto::run_eval(ctx, tr, *g->prep_whole, model, counts_out, obj_out, outputs_on_device);
   } else {
     s = kareto::run_eval(ctx, tr, *grid->prep, model, counts_out, obj_out, outputs_on_device);
   }

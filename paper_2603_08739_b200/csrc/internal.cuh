@@ -121,6 +121,7 @@ struct GridPrep;  // eval.cu
 struct kareto_grid {
   kareto_ctx *ctx = nullptr;
   kareto::GridPrep *prep = nullptr;
+  kareto::GridPrep *prep_whole = nullptr;  // built on first use with a time-sharded trace
   int64_t n = 0;
   kareto_config *dall = nullptr;  // [n] device (pool), freed by kareto_grid_free
   int lw[6] = {0, 0, 0, 0, 0, 0};

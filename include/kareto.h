@@ -64,7 +64,9 @@ typedef struct kareto_trace kareto_trace; /* device-resident, immutable after lo
  * caller; for world == 1 pass NULL -- or an id, which creates a 1-rank NCCL communicator so
  * that every collective (the eval_grid allgather, the time-sharded load's all-to-all and
  * allreduces) runs through NCCL on one GPU.  Errors: KARETO_E_INVALID (rank/world), _E_CUDA,
- * _E_NCCL. */
+ * _E_NCCL.
+ * Threads: a context, and the traces and grids made with it, are used by one host thread at a
+ * time (calls are synchronous on its stream); different contexts may run on different threads. */
 kareto_status kareto_create(int device, void *cuda_stream, const void *nccl_unique_id, int rank, int world,
                             kareto_ctx **out);
 void kareto_destroy(kareto_ctx *ctx);

@@ -305,10 +305,12 @@ def run_reference(args, spec):
             cnt[samp] = ot.replay(cf[samp], ttl, threads=threads)
             t_rep = (time.perf_counter() - t2) * len(rep) / len(samp)
         t3 = time.perf_counter()
-        fobj = ot.objective(O.Model(), cf, cnt)
-        O.select(fobj, cf, spec["prune"], threads=threads)  # the O(n^2) rows on every host thread
-        t_sel = time.perf_counter() - t3
-        return t_trace, t_rep, t_sel, ot.N, len(cf), int(len(rep)), n_samp
+        fobj = ot.objective(O.Model(), cf, cnt, threads=threads)  # configurations across host threads
+        t_obj = time.perf_counter() - t3  # the oracle's objective re-sums P0 over the requests: trace-proportional
+        t4 = time.perf_counter()
+        O.select(fobj, cf, spec["prune"], threads=threads)        # the O(n^2) rows on every host thread
+        t_sel = time.perf_counter() - t4
+        return t_trace, t_rep, t_sel, ot.N, len(cf), int(len(rep)), n_samp, t_obj, ot.R
 
     for _ in range(args.warmup):
         one()
@@ -319,17 +321,20 @@ def run_reference(args, spec):
     measured = (time.perf_counter() - w0) / max(1, args.steps)
     t_trace, t_rep, t_sel = (sum(r[i] for r in res) / len(res) for i in range(3))
     Ns, n, n_rep, n_samp = res[0][3], res[0][4], res[0][5], res[0][6]
+    t_obj = sum(r[7] for r in res) / len(res)
     scale = N_full / Ns
-    t_full = (t_trace + t_rep) * scale + t_sel
+    t_full = (t_trace + t_rep) * scale + t_obj * (R_full / res[0][8]) + t_sel
+    t_sel += t_obj  # reported together below
     value = n / t_full
     if args.full:
         what = (f"full workload ({Ns} accesses, {n} configurations): oracle trace build + O2 Fenwick depths + "
-                f"stack closed forms ({t_trace:.2f} s, sequential), fp64 model + pruning + O(n^2) dominance "
-                f"({t_sel:.2f} s, rows on {threads} threads)")
+                f"stack closed forms ({t_trace:.2f} s, sequential), fp64 model (configurations on {threads} threads) "
+                f"+ pruning + O(n^2) dominance (rows on {threads} threads) ({t_sel:.2f} s)")
     else:
         what = (f"sample trace of {tr.n_requests} requests ({Ns} accesses, the same generator) with the full "
                 f"{n}-configuration grid: oracle trace build + O2 depths + closed forms ({t_trace:.2f} s), fp64 model "
-                f"+ pruning + O(n^2) dominance ({t_sel:.2f} s); trace-proportional time scaled x{scale:.1f} to the "
+                f"+ pruning + O(n^2) dominance on {threads} threads ({t_sel:.2f} s); trace build, depths and replay "
+                f"scaled x{scale:.1f} (accesses), the model x{R_full / res[0][8]:.1f} (requests) to the "
                 f"full trace ({N_full} accesses): {t_full:.2f} s per full step")
     if n_rep:
         what += (f"; O1 literal replay of {n_samp} of the {n_rep} replay configurations on {threads} threads, "

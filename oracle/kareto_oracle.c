@@ -953,6 +953,33 @@ int or_objective_many(const or_trace *tr, const or_model *m, const or_config *cf
   return OR_OK;
 }
 
+/* the same, configurations split across host threads (each objective is independent) */
+typedef struct { const or_trace *tr; const or_model *m; const or_config *cfg; const or_counts *c; int64_t i0, i1;
+                 double *f; int status; } or_obj_job;
+static void *or_obj_worker(void *a) {
+  or_obj_job *j = (or_obj_job *)a;
+  j->status = or_objective_many(j->tr, j->m, j->cfg + j->i0, j->c + j->i0, j->i1 - j->i0, j->f + 3 * j->i0);
+  return NULL;
+}
+int or_objective_many_mt(const or_trace *tr, const or_model *m, const or_config *cfg, const or_counts *c, int64_t n,
+                         double *f, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  if (threads > n) threads = n > 0 ? (int)n : 1;
+  pthread_t th[256];
+  or_obj_job jobs[256];
+  for (int t = 0; t < threads; t++) {
+    jobs[t] = (or_obj_job){tr, m, cfg, c, n * t / threads, n * (t + 1) / threads, f, OR_OK};
+    pthread_create(&th[t], NULL, or_obj_worker, &jobs[t]);
+  }
+  int st = OR_OK;
+  for (int t = 0; t < threads; t++) {
+    pthread_join(th[t], NULL);
+    if (jobs[t].status != OR_OK && st == OR_OK) st = jobs[t].status;
+  }
+  return st;
+}
+
 /* ----------------------------------------------------------------------------
  * Pruning (Alg. 1 expansion test P:555-559; R34) and
  * ParetoFilter (R35).  status: 2 pruned, 1 frontier, 0 dominated.

@@ -91,6 +91,7 @@ def _load():
     L.or_prune.argtypes = [vp, vp, i64, ctypes.c_double, vp]
     L.or_pareto.restype = i64
     L.or_pareto.argtypes = [vp, i64, vp, vp]
+    L.or_objective_many_mt.argtypes = [vp, vp, vp, vp, i64, vp, ctypes.c_int]
     L.or_pareto_mt.restype = i64
     L.or_pareto_mt.argtypes = [vp, i64, vp, vp, ctypes.c_int]
     L.or_fmix64_export.restype = u64
@@ -300,13 +301,18 @@ class OracleTrace:
         return out
 
     # ---- model / selection -----------------------------------------------------------
-    def objective(self, model: Model, cfgs: np.ndarray, counts: np.ndarray) -> np.ndarray:
+    def objective(self, model: Model, cfgs: np.ndarray, counts: np.ndarray, threads: int = 1) -> np.ndarray:
+        """fp64 objectives (R25-R33); threads > 1 splits the configurations across host threads."""
         cfgs = np.ascontiguousarray(cfgs, CONFIG_DTYPE)
         counts = np.ascontiguousarray(counts, COUNTS_DTYPE)
         f = np.zeros((len(cfgs), 3), np.float64)
         m = model._c()
-        st = self._L.or_objective_many(self._h, ctypes.byref(m), cfgs.ctypes.data, counts.ctypes.data, len(cfgs),
-                                       f.ctypes.data)
+        if threads > 1:
+            st = self._L.or_objective_many_mt(self._h, ctypes.byref(m), cfgs.ctypes.data, counts.ctypes.data,
+                                              len(cfgs), f.ctypes.data, int(threads))
+        else:
+            st = self._L.or_objective_many(self._h, ctypes.byref(m), cfgs.ctypes.data, counts.ctypes.data,
+                                           len(cfgs), f.ctypes.data)
         if st != OK:
             raise OracleError(st, "objective")
         return f

@@ -70,6 +70,18 @@ def test_zero_cache_is_no_saving_and_hit_saving_is_the_prefix_cost():
     assert f[1, 0] == pytest.approx(1e3 * (P0 - saved) * 1e-12 / 4, rel=1e-15)
 
 
+def test_threaded_objective_equals_serial():
+    tr = ki.synthetic("chat", R=300, seed=2)
+    ot = O.OracleTrace(tr)
+    caps = [[a, b, c] for a in (0, 50, 500) for b in (0, 1000) for c in (0, 5000, O.INF_CAP)]
+    cf = O.configs(caps, tuner=0)
+    ttl = np.full((1, 17), 600_000, np.uint32)
+    cnt = ot.replay(cf, ttl)
+    f1 = ot.objective(O.Model(), cf, cnt)
+    f4 = ot.objective(O.Model(), cf, cnt, threads=4)
+    assert np.array_equal(f1.view(np.uint64), f4.view(np.uint64))
+
+
 def test_observation1_low_density_throughput_identical_across_configs():
     # Obs. 1: with low density, throughput plateaus at the arrival rate regardless of storage.
     tr = ki.synthetic("chat", R=400, seed=1)

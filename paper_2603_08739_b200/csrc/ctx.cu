@@ -254,7 +254,7 @@ extern "C" void kareto_trace_free(kareto_trace *tr) {
   if (!tr) return;
   // uses only the trace's own copy of the stream: a trace may outlive its context
   void *ptrs[] = {tr->arr, tr->s, tr->grp, tr->hash, tr->req, tr->prev, tr->delta, tr->depth,
-                  tr->blk, tr->gblk, tr->arr_rel, tr->inlen, tr->outlen};
+                  tr->blk, tr->gblk, tr->arr_rel, tr->inlen, tr->outlen, tr->runs};
   for (void *p : ptrs)
     if (p) cudaFreeAsync(p, tr->stream);
   cudaStreamSynchronize(tr->stream);
@@ -292,7 +292,9 @@ extern "C" kareto_status kareto_trace_export(kareto_ctx *ctx, const kareto_trace
     case KARETO_X_PREV: src = tr->prev; bytes = 4 * n; break;
     case KARETO_X_DELTA: src = tr->delta; bytes = 4 * n; break;
     case KARETO_X_REQ: src = tr->req; bytes = 4 * n; break;
-    case KARETO_X_DEPTH: src = tr->depth; bytes = 4 * n; break;
+    case KARETO_X_DEPTH:
+      if (kareto_status e = ensure_depth(ctx, const_cast<kareto_trace *>(tr))) return e;
+      src = tr->depth; bytes = 4 * n; break;
     case KARETO_X_GROUP: src = tr->grp; bytes = 2 * (size_t)tr->R; break;
     case KARETO_X_START: src = tr->s; bytes = 4 * (size_t)(tr->R + 1); break;
     default: return fail(ctx, KARETO_E_INVALID, "unknown export %d", which);

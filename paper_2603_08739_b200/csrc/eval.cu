@@ -173,6 +173,85 @@ __global__ void __launch_bounds__(H_THREADS) k_hist_dD(uint64_t N, uint32_t pos0
     if (cD[i]) atomicAdd(&gD[i], (unsigned long long)cD[i]);
 }
 
+// first run index q in [0, M) with runs[q].x >= pos (M if none), found by the whole CTA: each
+// round probes blockDim.x evenly spaced runs and keeps the gap holding the answer (~3 rounds)
+__device__ int64_t cta_run_lower_bound(const uint4 *__restrict__ runs, int64_t M, uint32_t pos) {
+  int64_t lo = 0, hi = M;  // the answer lies in [lo, hi]
+  while (hi > lo) {
+    const int64_t step = (hi - lo + blockDim.x - 1) / blockDim.x;
+    const int64_t q = lo + (int64_t)threadIdx.x * step;
+    const int c = __syncthreads_count(q < hi && __ldg(&runs[q].x) < pos);  // a prefix of the probes
+    if (c == 0) break;
+    const int64_t nlo = lo + (int64_t)(c - 1) * step + 1, nhi = lo + (int64_t)c * step;
+    lo = nlo;
+    hi = nhi < hi ? nhi : hi;
+  }
+  return lo;
+}
+
+// K4 over runs (whole traces; same cells as k_hist_dD).  Inside a K3 run j0..j0+L-1 of request
+// r the pre-request depth falls by one per access (d = d0 - t), D = d + (j - s_r) = d0 + j0 - s_r
+// is constant, and so is delta (the run's previous accesses are consecutive positions with
+// consecutive chain positions, hence one earlier request).  A run therefore adds the arithmetic
+// range [d0 - L + 1, d0] to the (d-bin, tau-bin) cells -- per bin the count and the closed-form
+// sum of k = s_{r+1} - 1 - j -- and L to one D bin: ~2.4 runs per request instead of ~100
+// accesses.  CTA c takes the runs starting in positions [c per, (c+1) per), so its accesses
+// (< per + max_blocks) bound the shared u32 sums exactly as in k_hist_dD.
+__global__ void __launch_bounds__(H_THREADS) k_hist_runs(uint64_t N, uint64_t per_cta, int64_t M,
+                                                         const uint4 *__restrict__ runs,
+                                                         const uint32_t *__restrict__ s,
+                                                         const uint32_t *__restrict__ delta,
+                                                         const uint32_t *__restrict__ Bd, int nb,
+                                                         const uint32_t *__restrict__ lut, int sh,
+                                                         const uint32_t *__restrict__ Tc, int ntc,
+                                                         unsigned long long *__restrict__ gcnt,
+                                                         unsigned long long *__restrict__ gsk,
+                                                         unsigned long long *__restrict__ gD) {
+  extern __shared__ uint32_t sm[];
+  uint32_t *lut_s = sm;
+  const int W = (ntc + 1) * nb;
+  uint32_t *cnt = lut_s + (1 << LUT_BITS) + 1;
+  uint32_t *sk = cnt + W;
+  uint32_t *cD = sk + W;
+  for (int i = threadIdx.x; i <= (1 << LUT_BITS); i += blockDim.x) lut_s[i] = lut[i];
+  for (int i = threadIdx.x; i < W; i += blockDim.x) { cnt[i] = 0; sk[i] = 0; }
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) cD[i] = 0;
+  const uint64_t p0 = blockIdx.x * per_cta, p1 = p0 + per_cta < N ? p0 + per_cta : N;
+  const int64_t q0 = cta_run_lower_bound(runs, M, (uint32_t)p0);
+  const int64_t q1 = p1 >= N ? M : cta_run_lower_bound(runs, M, (uint32_t)p1);
+  __syncthreads();
+  for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+    const uint4 rn = __ldg(&runs[q]);
+    const uint32_t j0 = rn.x, L = rn.y, d0 = rn.z, r = rn.w;
+    const uint32_t sr = __ldg(&s[r]), sr1 = __ldg(&s[r + 1]);
+    const int tc = ntc > 0 ? tbin_of(__ldg(&delta[j0]), Tc, ntc) : 0;
+    // k of the access at depth x: t = d0 - x, k = (sr1 - 1 - j0) - t
+    const int64_t koff = (int64_t)(sr1 - 1 - j0) - (int64_t)d0;
+    uint32_t lo = d0 - (L - 1);
+    const uint32_t hi = d0;
+    for (int b = bin_of(lo, Bd, nb, lut_s, sh); b < nb; b++) {
+      const uint32_t bnd = __ldg(&Bd[b]);  // bin b holds depths in (Bd[b-1], Bd[b]]
+      const uint32_t top = hi < bnd ? hi : bnd;
+      const uint32_t c = top - lo + 1;
+      const uint64_t ksum = (uint64_t)((koff + lo) + (koff + top)) * c / 2;
+      const int cell = tc * nb + b;
+      atomicAdd(&cnt[cell], c);
+      if (ksum) atomicAdd(&sk[cell], (uint32_t)ksum);
+      if (top == hi) break;
+      lo = top + 1;
+    }
+    const int bD = bin_of(d0 + (j0 - sr), Bd, nb, lut_s, sh);
+    if (bD < nb) atomicAdd(&cD[bD], L);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < W; i += blockDim.x) {
+    if (cnt[i]) atomicAdd(&gcnt[i], (unsigned long long)cnt[i]);
+    if (sk[i]) atomicAdd(&gsk[i], (unsigned long long)sk[i]);
+  }
+  for (int i = threadIdx.x; i < nb; i += blockDim.x)
+    if (cD[i]) atomicAdd(&gD[i], (unsigned long long)cD[i]);
+}
+
 // K4b: histogram of D over the boundaries (count), window [b_lo, b_hi)
 __global__ void __launch_bounds__(H_THREADS) k_hist_D(uint64_t N, uint32_t pos0, uint64_t per_cta, const uint32_t *__restrict__ depth,
                                                       const uint32_t *__restrict__ req, const uint32_t *__restrict__ s,
@@ -405,6 +484,14 @@ static void shard_bounds(const kareto_config *cfg, int64_t n, const uint32_t *ro
       fprintf(stderr, "[eval] %-10s %.3f ms\n", name, std::chrono::duration<double, std::milli>(t_ - ht0).count()); \
     }                                                                                                     \
   } while (0)
+struct BoundCache {
+  bool valid = false;
+  uint64_t U = 0;
+  int nb = 0, nb12 = 0;
+  DBuf<uint32_t> dBd, dB12, dlut;
+  DBuf<CfgDev> dcd;
+};
+
 // Everything kareto_eval_grid derives from the configuration list and the TTL table alone
 // (validation, the shard, the stack / replay split, the TTL value sets, device copies): built once
 // per call, or once per kareto_grid for repeated evaluation (kareto_grid_create).
@@ -427,6 +514,7 @@ struct GridPrep {
   // device copies
   DBuf<kareto_config> dcfg, dcfgP;
   DBuf<uint32_t> dTc, dTt, dtix, drows, diS, diP;
+  mutable BoundCache bc;  // K4 boundary sets for the last U evaluated
 };
 
 static kareto_status prep_grid(kareto_ctx *ctx, const kareto_config *cfg, int64_t n_cfg, const uint32_t *ttl_ms,
@@ -587,49 +675,61 @@ static kareto_status run_eval(kareto_ctx *ctx, const kareto_trace *tr, const Gri
   const DBuf<kareto_config> &dcfg = prep.dcfg;
 
   HT("classified");
-  // ---- boundary sets and per-configuration lookup indices, on the GPU
-  DBuf<CfgDev> dcd;
+  // ---- boundary sets, their LUT and per-configuration lookup indices, on the GPU.  They depend
+  // only on the grid and U (capacities are clamped to U), so a prepared grid keeps them for the
+  // next evaluation against a trace with the same U (the planner's grid over trace after trace)
   DBuf<uint8_t> tmp;
-  DBuf<uint32_t> dBd, dB12;
-  KTRY(dcd.alloc(ctx, nS > 0 ? nS : 1));
-  int nb = 0, nb12 = 0;
-  if (nS > 0) {
-    DBuf<uint32_t> vals, vals_s, v12, v12_s;
-    DBuf<int> cnt;
-    KTRY(vals.alloc(ctx, 3 * nS)); KTRY(vals_s.alloc(ctx, 3 * nS)); KTRY(v12.alloc(ctx, nS)); KTRY(v12_s.alloc(ctx, nS));
-    KTRY(dBd.alloc(ctx, 3 * nS)); KTRY(dB12.alloc(ctx, nS)); KTRY(cnt.alloc(ctx, 2));
-    Pass ps(ctx, "K4_boundaries", 1, 2);
-    k_bound_vals<<<grid_for(nS, 256, 4 * sms), 256, 0, st>>>(dcfg.p, nS, U, vals.p, v12.p);
-    KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
-      return cub::DeviceRadixSort::SortKeys(t, b, vals.p, vals_s.p, (int)(3 * nS), 0, 32, st);
-    }));
-    KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
-      return cub::DeviceSelect::Unique(t, b, vals_s.p, dBd.p, cnt.p, (int)(3 * nS), st);
-    }));
-    KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
-      return cub::DeviceRadixSort::SortKeys(t, b, v12.p, v12_s.p, (int)nS, 0, 32, st);
-    }));
-    KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
-      return cub::DeviceSelect::Unique(t, b, v12_s.p, dB12.p, cnt.p + 1, (int)nS, st);
-    }));
-    int hc[2] = {0, 0};
-    uint32_t last12 = 0;
-    KCUDA(ctx, cudaMemcpyAsync(hc, cnt.p, 8, cudaMemcpyDeviceToHost, st));
-    KCUDA(ctx, cudaStreamSynchronize(st));
-    nb = hc[0];
-    nb12 = hc[1];
-    if (nb12 > 0) {  // drop the sentinel of CAPACITY configurations (the largest key)
-      KCUDA(ctx, cudaMemcpyAsync(&last12, dB12.p + nb12 - 1, 4, cudaMemcpyDeviceToHost, st));
+  int sh = 0;
+  while (((uint64_t)U >> sh) >= (1ull << LUT_BITS)) sh++;
+  BoundCache &bc = prep.bc;
+  if (!bc.valid || bc.U != U) {
+    bc.valid = false;
+    bc.nb = bc.nb12 = 0;
+    KTRY(bc.dcd.alloc(ctx, nS > 0 ? nS : 1));
+    KTRY(bc.dlut.alloc(ctx, (1 << LUT_BITS) + 1));
+    if (nS > 0) {
+      DBuf<uint32_t> vals, vals_s, v12, v12_s;
+      DBuf<int> cnt;
+      KTRY(vals.alloc(ctx, 3 * nS)); KTRY(vals_s.alloc(ctx, 3 * nS)); KTRY(v12.alloc(ctx, nS)); KTRY(v12_s.alloc(ctx, nS));
+      KTRY(bc.dBd.alloc(ctx, 3 * nS)); KTRY(bc.dB12.alloc(ctx, nS)); KTRY(cnt.alloc(ctx, 2));
+      Pass ps(ctx, "K4_boundaries", 1, 3);
+      k_bound_vals<<<grid_for(nS, 256, 4 * sms), 256, 0, st>>>(dcfg.p, nS, U, vals.p, v12.p);
+      KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortKeys(t, b, vals.p, vals_s.p, (int)(3 * nS), 0, 32, st);
+      }));
+      KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+        return cub::DeviceSelect::Unique(t, b, vals_s.p, bc.dBd.p, cnt.p, (int)(3 * nS), st);
+      }));
+      KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortKeys(t, b, v12.p, v12_s.p, (int)nS, 0, 32, st);
+      }));
+      KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+        return cub::DeviceSelect::Unique(t, b, v12_s.p, bc.dB12.p, cnt.p + 1, (int)nS, st);
+      }));
+      int hc[2] = {0, 0};
+      uint32_t last12 = 0;
+      KCUDA(ctx, cudaMemcpyAsync(hc, cnt.p, 8, cudaMemcpyDeviceToHost, st));
       KCUDA(ctx, cudaStreamSynchronize(st));
-      if (last12 == kNone) nb12--;
+      bc.nb = hc[0];
+      bc.nb12 = hc[1];
+      if (bc.nb12 > 0) {  // drop the sentinel of CAPACITY configurations (the largest key)
+        KCUDA(ctx, cudaMemcpyAsync(&last12, bc.dB12.p + bc.nb12 - 1, 4, cudaMemcpyDeviceToHost, st));
+        KCUDA(ctx, cudaStreamSynchronize(st));
+        if (last12 == kNone) bc.nb12--;
+      }
+      k_cfgdev<<<grid_for(nS, 256, 4 * sms), 256, 0, st>>>(dcfg.p, nS, U, bc.dBd.p, bc.nb, bc.dB12.p, bc.nb12, dTc.p,
+                                                           ntc, drows.p, n_tuner, G, bc.dcd.p);
+      if (bc.nb > 0) k_build_lut<<<grid_for((1 << LUT_BITS) + 1, 256), 256, 0, st>>>(bc.dBd.p, bc.nb, sh, bc.dlut.p);
     }
-    k_cfgdev<<<grid_for(nS, 256, 4 * sms), 256, 0, st>>>(dcfg.p, nS, U, dBd.p, nb, dB12.p, nb12, dTc.p, ntc,
-                                                         drows.p, n_tuner, G, dcd.p);
+    bc.U = U;
+    bc.valid = true;
   }
+  const int nb = bc.nb, nb12 = bc.nb12;
+  const DBuf<uint32_t> &dBd = bc.dBd, &dB12 = bc.dB12, &dlut = bc.dlut;
+  const DBuf<CfgDev> &dcd = bc.dcd;
 
   HT("boundaries");
   // ---- K4: histograms over the accesses
-  DBuf<uint32_t> dlut;
   const int ncol = ntc + 1;
   DBuf<unsigned long long> hC, hS, hD, C1, S1, CD;
   size_t ncell = (size_t)ncol * (nb > 0 ? nb : 1);
@@ -637,14 +737,9 @@ static kareto_status run_eval(kareto_ctx *ctx, const kareto_trace *tr, const Gri
   KTRY(hC.zero()); KTRY(hS.zero()); KTRY(hD.zero());
   KTRY(C1.alloc(ctx, ncell)); KTRY(S1.alloc(ctx, ncell)); KTRY(CD.alloc(ctx, nb > 0 ? nb : 1));
   KTRY(C1.zero()); KTRY(S1.zero()); KTRY(CD.zero());
-  int sh = 0;
-  while (((uint64_t)U >> sh) >= (1ull << LUT_BITS)) sh++;
-  KTRY(dlut.alloc(ctx, (1 << LUT_BITS) + 1));
   const uint32_t *depth = tr->depth, *req = tr->req, *s = tr->s, *delta = tr->delta;
   if (ns > 0 && N > 0 && nb > 0) {
     const uint64_t N = Nl;  // this rank's accesses
-    k_build_lut<<<grid_for((1 << LUT_BITS) + 1, 256), 256, 0, st>>>(dBd.p, nb, sh, dlut.p);
-    ctx->own_launches++;
     // CTA ranges bounded so that per-CTA u32 sums of k cannot overflow
     uint64_t maxk = tr->max_blocks > 1 ? (uint64_t)tr->max_blocks - 1 : 1;
     uint64_t cap_per = 0xFFFFFFFFull / maxk;
@@ -663,11 +758,29 @@ static kareto_status run_eval(kareto_ctx *ctx, const kareto_trace *tr, const Gri
       attr_set = true;
     }
     const size_t fused = lut_bytes + 8 * ncell + 4 * (size_t)nb;
-    if (fused <= (size_t)SMEM_MAX) {  // one pass for both histograms
+    // whole traces: one pass over the K3 runs (d falls by one per access inside a run)
+    const uint64_t maxb = tr->max_blocks > 0 ? (uint64_t)tr->max_blocks : 1;
+    const bool by_runs = !tsh && tr->runs && tr->n_runs > 0 && cap_per > maxb + 1 &&
+                         getenv("KARETO_K4_ACCESS") == nullptr;
+    if (fused <= (size_t)SMEM_MAX && by_runs) {
+      static bool attr_runs = false;
+      if (!attr_runs) {
+        cudaFuncSetAttribute(k_hist_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+        attr_runs = true;
+      }
+      uint64_t per_r = (N + sms - 1) / sms;  // one CTA per SM: half the cell flushes of k_hist_dD
+      if (per_r > cap_per - maxb) per_r = cap_per - maxb;
+      const unsigned gr = (unsigned)((N + per_r - 1) / per_r);
+      Pass ps(ctx, "K4_hist_runs", 1, 1);
+      k_hist_runs<<<gr, H_THREADS, fused, st>>>(N, per_r, tr->n_runs, tr->runs, s, delta, dBd.p, nb, dlut.p, sh,
+                                                dTc.p, ntc, hC.p, hS.p, hD.p);
+    } else if (fused <= (size_t)SMEM_MAX) {  // one pass for both histograms
+      KTRY(ensure_depth(ctx, const_cast<kareto_trace *>(tr)));
       Pass ps(ctx, "K4_hist_dD", 1, 1);
       if (N > 0) k_hist_dD<<<g, H_THREADS, fused, st>>>(N, jb, per, depth, req, s, delta, dBd.p, nb, dlut.p, sh, dTc.p, ntc, hC.p,
                                             hS.p, hD.p);
     } else {
+    KTRY(ensure_depth(ctx, const_cast<kareto_trace *>(tr)));
     for (int c0 = 0; c0 < (int)ncell; c0 += wcell) {
       int c1 = c0 + wcell < (int)ncell ? c0 + wcell : (int)ncell;
       size_t smem = lut_bytes + 8 * (size_t)(c1 - c0);
@@ -718,6 +831,7 @@ static kareto_status run_eval(kareto_ctx *ctx, const kareto_trace *tr, const Gri
   for (int g = 0; g < G; g++) { hUg[g] = (unsigned long long)tr->U_g[g]; hRg[g] = (unsigned long long)tr->reuse_g[g]; }
   KTRY(upload(ctx, dUg, hUg)); KTRY(upload(ctx, dRg, hRg));
   if (ns > 0 && N > 0 && nb12 > 0) {
+    KTRY(ensure_depth(ctx, const_cast<kareto_trace *>(tr)));
     size_t smem = 8 * (size_t)G * nt1;
     if (smem > 200 * 1024) return fail(ctx, KARETO_E_UNSUPPORTED, "too many groups x TTL values (%d x %d)", G, nt1);
     cudaFuncSetAttribute(k_hist_ttl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -870,6 +984,10 @@ extern "C" kareto_status kareto_grid_create(kareto_ctx *ctx, const kareto_config
 extern "C" void kareto_grid_free(kareto_grid *g) {
   if (!g) return;
   if (g->dall) cudaFreeAsync(g->dall, g->ctx->stream);
+  for (int a = 0; a < 3; a++) {
+    if (g->lkey[a]) cudaFreeAsync(g->lkey[a], g->ctx->stream);
+    if (g->lidx[a]) cudaFreeAsync(g->lidx[a], g->ctx->stream);
+  }
   delete g->prep;  // its device buffers free on the context stream
   delete g->prep_whole;
   cudaStreamSynchronize(g->ctx->stream);

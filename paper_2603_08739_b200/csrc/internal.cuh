@@ -104,6 +104,10 @@ struct kareto_trace {
   uint32_t *prev = nullptr;
   uint32_t *delta = nullptr;
   uint32_t *depth = nullptr;   // LRU depth d at request start (kNone: first access)
+  // K3 runs of a whole trace [n_runs] (j0, L, d0, r): accesses j0 .. j0+L-1 of request r with
+  // consecutive previous positions; d_{j0+t} = d0 - t (K4 histograms a run at once, eval.cu)
+  uint4 *runs = nullptr;
+  bool depth_ready = true;     // false: depth is materialised from runs on first use
   // K6 replay inputs, built on first use (replay.cu)
   uint32_t *blk = nullptr;     // [N] dense block id
   uint16_t *gblk = nullptr;    // [U] group of each block
@@ -127,6 +131,10 @@ struct kareto_grid {
   int lw[6] = {0, 0, 0, 0, 0, 0};
   bool lw_ok = false;             // the axis / line-key ranges pruning needs
   std::string lw_err;
+  // K8a line order per axis (pareto.cu), built on the first pruned selection: the sorted line
+  // keys and the configuration permutation depend on the grid alone
+  uint64_t *lkey[3] = {nullptr, nullptr, nullptr};
+  uint32_t *lidx[3] = {nullptr, nullptr, nullptr};
 };
 
 namespace kareto {
@@ -167,6 +175,8 @@ inline kareto_status fail(kareto_ctx *ctx, kareto_status st, const char *fmt, ..
 kareto_status wave_budget(kareto_ctx *ctx, double frac, double *bytes);
 // return the pool's unused reserve to the device (after large transient allocations)
 void pool_trim(kareto_ctx *ctx);
+// materialise tr->depth from the kept K3 runs if a whole-trace load deferred it (stack_depth.cu)
+kareto_status ensure_depth(kareto_ctx *ctx, kareto_trace *tr);
 
 // KARETO_HOSTTIME=1: wall-clock marks (after a stream sync) through a call, to stderr -- shows
 // where a step's time goes between the profiled passes (host work, syncs, allocations)

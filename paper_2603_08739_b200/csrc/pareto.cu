@@ -173,7 +173,7 @@ kareto_status pareto_line_widths(kareto_ctx *ctx, const kareto_config *cfg, int6
 // dcfg: device copy of the configurations (only read when pruning), lw: their line-key widths
 static kareto_status pareto_run(kareto_ctx *ctx, const double *obj, const kareto_config *dcfg_in, const kareto_config *hcfg,
                                 const LineWidths &lw, int64_t n, const kareto_prune *prune, uint8_t *status_out,
-                                int64_t *n_frontier, int32_t on_dev);
+                                int64_t *n_frontier, int32_t on_dev, kareto_grid *grid = nullptr);
 
 static kareto_status pareto(kareto_ctx *ctx, const double *obj, const kareto_config *cfg, int64_t n,
                             const kareto_prune *prune, uint8_t *status_out, int64_t *n_frontier, int32_t on_dev) {
@@ -190,7 +190,7 @@ static kareto_status pareto(kareto_ctx *ctx, const double *obj, const kareto_con
 
 static kareto_status pareto_run(kareto_ctx *ctx, const double *obj, const kareto_config *dcfg_in, const kareto_config *hcfg,
                                 const LineWidths &lw, int64_t n, const kareto_prune *prune, uint8_t *status_out,
-                                int64_t *n_frontier, int32_t on_dev) {
+                                int64_t *n_frontier, int32_t on_dev, kareto_grid *grid) {
   cudaStream_t st = ctx->stream;
   const int sms = ctx->num_sms;
   const bool do_prune = prune && prune->enabled;
@@ -225,25 +225,34 @@ static kareto_status pareto_run(kareto_ctx *ctx, const double *obj, const kareto
       dcfg = down.p;
     }
     for (int a = 0; a < 3; a++) {
-      {
-        Pass ps(ctx, "K8a_line_keys", 1, 1);
-        k_line_keys<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(dcfg, n, a, lw, key.p, idx.p);
-      }
-      {
+      // a prepared grid sorts its lines once (first selection) and keeps (key, permutation)
+      const bool cached = grid && grid->lkey[a];
+      uint64_t *ks = cached ? grid->lkey[a] : key_s.p;
+      uint32_t *is = cached ? grid->lidx[a] : idx_s.p;
+      if (!cached) {
+        {
+          Pass ps(ctx, "K8a_line_keys", 1, 1);
+          k_line_keys<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(dcfg, n, a, lw, key.p, idx.p);
+        }
         Pass ps(ctx, "K8a_sort_lines", 0, 1);
         KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
           return cub::DeviceRadixSort::SortPairs(t, b, key.p, key_s.p, idx.p, idx_s.p, (int)n, 0, key_bits, st);
         }));
+        if (grid) {  // the sorted copies move to the grid (fresh ones for the next axis)
+          grid->lkey[a] = key_s.detach();
+          grid->lidx[a] = idx_s.detach();
+          KTRY(key_s.alloc(ctx, n));
+          KTRY(idx_s.alloc(ctx, n));
+        }
       }
       {
         Pass ps(ctx, "K8a_line_stop", 1, 2);
-        k_line_stop<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(key_s.p, idx_s.p, n, lw.w[a], f, prune->tau_e, line.p,
-                                                               stop.p);
+        k_line_stop<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(ks, is, n, lw.w[a], f, prune->tau_e, line.p, stop.p);
         KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
           return cub::DeviceScan::ExclusiveScanByKey(t, b, line.p, stop.p, excl.p, MaxOp(), (uint8_t)0, (int)n,
                                                      cub::Equality(), st);
         }));
-        k_mark_pruned<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(excl.p, idx_s.p, n, pruned.p);
+        k_mark_pruned<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(excl.p, is, n, pruned.p);
       }
     }
   }
@@ -288,7 +297,7 @@ static kareto_status pareto_run(kareto_ctx *ctx, const double *obj, const kareto
   return KARETO_OK;
 }
 
-kareto_status pareto_grid(kareto_ctx *ctx, const double *obj, const kareto_grid *g, const kareto_prune *prune,
+kareto_status pareto_grid(kareto_ctx *ctx, const double *obj, kareto_grid *g, const kareto_prune *prune,
                           uint8_t *status_out, int64_t *n_frontier, int32_t on_dev) {
   const int64_t n = g->n;
   if (n > 0 && (!obj || !status_out)) return fail(ctx, KARETO_E_INVALID, "bad arguments");
@@ -298,7 +307,7 @@ kareto_status pareto_grid(kareto_ctx *ctx, const double *obj, const kareto_grid 
     if (!g->lw_ok) return fail(ctx, KARETO_E_INVALID, "%s", g->lw_err.c_str());
     for (int k = 0; k < 6; k++) lw.w[k] = g->lw[k];
   }
-  return pareto_run(ctx, obj, g->dall, nullptr, lw, n, prune, status_out, n_frontier, on_dev);
+  return pareto_run(ctx, obj, g->dall, nullptr, lw, n, prune, status_out, n_frontier, on_dev, g);
 }
 
 }  // namespace kareto
@@ -324,7 +333,8 @@ extern "C" kareto_status kareto_pareto_prepared(kareto_ctx *ctx, const double *o
   ctx->err.clear();
   if (grid->ctx != ctx) return kareto::fail(ctx, KARETO_E_INVALID, "grid belongs to another context");
   cudaSetDevice(ctx->device);
-  kareto_status s = kareto::pareto_grid(ctx, obj, grid, prune, status_out, n_frontier, on_device);
+  kareto_status s = kareto::pareto_grid(ctx, obj, const_cast<kareto_grid *>(grid), prune, status_out, n_frontier,
+                                        on_device);
   if (s != KARETO_OK) {
     cudaStreamSynchronize(ctx->stream);
     (void)cudaGetLastError();

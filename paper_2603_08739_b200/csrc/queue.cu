@@ -194,6 +194,7 @@ static kareto_status eval_queue_stack(kareto_ctx *ctx, const kareto_trace *tr, c
   KTRY(ts.alloc(ctx, (size_t)W * R)); KTRY(cnt.alloc(ctx, (size_t)W * R)); KTRY(off.alloc(ctx, W + 1));
   const size_t sbytes = smem ? (size_t)m.instances * 32 * 8 : 0;
   if (smem) cudaFuncSetAttribute(k_queue<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbytes);
+  KTRY(ensure_depth(ctx, const_cast<kareto_trace *>(tr)));
   for (int64_t w0 = 0; w0 < n; w0 += W) {
     const int64_t nw = n - w0 < W ? n - w0 : W;
     {

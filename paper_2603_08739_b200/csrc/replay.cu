@@ -37,7 +37,7 @@ constexpr int LOOK = 16;  // LOOKUP blocks whose loads are issued together
 
 struct RState {
   uint8_t *tier;       // [b*W+c] T_*
-  uint32_t *lt;        // [b*W+c] ms of the last access (kNone = never seen): lease start, expiry base
+  uint32_t *lt;        // expiry classes: [b*W+c] ms of the last access (the disk expiry base)
   uint2 *link;         // list classes: [b*W+c] (prev, next) toward head / tail
   uint32_t *freq;      // LFU: [b*W+c] access count of a resident block
   uint32_t *bh[3];     // LFU: [f*W+c] newest block of frequency bucket f per tier
@@ -470,20 +470,22 @@ struct Rep {
       for (uint32_t k0 = 0; k0 < nb; k0 += LOOK) {
         uint32_t bb[LOOK];
         uint8_t tt[LOOK];
-        uint32_t ll[LOOK];
-#pragma unroll
-        for (int q = 0; q < LOOK; q++) bb[q] = k0 + q < nb ? T.blk[s1 - 1 - (k0 + q)] : 0u;
+        uint32_t dd[LOOK];
+        // the lease store's state is the trace's: alive iff seen before and delta <= tau_g (the
+        // reuse interval of the access is a - the block's last access)
 #pragma unroll
         for (int q = 0; q < LOOK; q++) {
           const bool ok = k0 + q < nb;
-          tt[q] = ok ? v.tier[at(bb[q])] : 0;
-          ll[q] = ok ? v.lt[at(bb[q])] : 0;
+          bb[q] = ok ? T.blk[s1 - 1 - (k0 + q)] : 0u;
+          dd[q] = (ok && ttl_mode) ? T.delta[s1 - 1 - (k0 + q)] : kNone;
         }
+#pragma unroll
+        for (int q = 0; q < LOOK; q++) tt[q] = k0 + q < nb ? v.tier[at(bb[q])] : 0;
 #pragma unroll
         for (int q = 0; q < LOOK; q++) {
           if (k0 + q >= nb) break;
           const uint8_t t = tt[q];
-          const bool alive = ll[q] != kNone && (a - ll[q]) <= tg;
+          const bool alive = dd[q] != kNone && dd[q] <= tg;
           const bool present = t != T_NONE || (ttl_mode && alive);
           in_prefix = in_prefix && present;
           if (in_prefix) {
@@ -516,13 +518,11 @@ struct Rep {
       uint32_t bn = T.blk[s0];
       uint32_t bnn = s0 + 1 < s1 ? T.blk[s0 + 1] : 0u;
       uint8_t t_n = v.tier[at(bn)];
-      uint32_t l_n = v.lt[at(bn)];
       uint2 lk_n = v.link[at(bn)];
       uint32_t hp_n = LFU ? v.freq[at(bn)] : 0u;
       for (uint32_t j = s0; j < s1; j++) {
         const uint32_t b = bn;
         const uint8_t t = t_n;
-        const uint32_t l = l_n;
         const uint2 lk = lk_n;
         const uint32_t hp = hp_n;
         seq += 1;
@@ -531,17 +531,16 @@ struct Rep {
           if (j + 2 < s1) bnn = T.blk[j + 2];
           nx = bn;
           nx_tier = v.tier[at(bn)];
-          l_n = v.lt[at(bn)];
           nx_link = v.link[at(bn)];
           if (LFU) nx_freq = v.freq[at(bn)];
         } else {
           nx = kNone;
         }
-        if (ttl_mode && l != kNone) {
-          const uint32_t dt = a - l;
-          bytetime += dt < tg ? dt : tg;
+        if (ttl_mode) {  // lease integral since the previous access
+          const uint32_t dt = T.delta[j];
+          if (dt != kNone) bytetime += dt < tg ? dt : tg;
         }
-        v.lt[at(b)] = a;  // before any expiry insertion of b in its own cascade
+        if (EXP) v.lt[at(b)] = a;  // expiry base; before any expiry insertion of b in its own cascade
         if (t == T_HBM) {
           if (LFU) {  // move to the front of bucket f + 1
             const uint32_t f = hp;
@@ -566,9 +565,8 @@ struct Rep {
       }
       s0 = s1;
     }
-    if (ttl_mode) {
-      for (uint32_t b = 0; b < T.U; b++)
-        if (v.lt[at(b)] != kNone) bytetime += tau[v.gblk[b]];
+    if (ttl_mode) {  // every block's last lease counts a full tau (R21): sum_g U_g tau_g
+      for (int g = 0; g < G; g++) bytetime += T.Ug[g] * (uint64_t)tau[g];
       evict[2] = 0;
     } else {
       disk_writes = cap[2] > 0 ? evict[1] : 0;
@@ -738,7 +736,16 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
   cudaStream_t st = ctx->stream;
   const uint64_t U = tr->U > 0 ? (uint64_t)tr->U : 1;
   const int G = tr->K + 1;
-  ReplayTrace T{(uint32_t)tr->R, (uint32_t)tr->U, tr->s, tr->arr_rel, tr->grp, tr->blk, tr->inlen, tr->outlen};
+  DBuf<uint64_t> dUg;
+  {
+    std::vector<uint64_t> hUg(G);
+    for (int g = 0; g < G; g++) hUg[g] = (uint64_t)tr->U_g[g];
+    KTRY(dUg.alloc(ctx, G));
+    KCUDA(ctx, cudaMemcpyAsync(dUg.p, hUg.data(), 8 * (size_t)G, cudaMemcpyHostToDevice, st));
+    KCUDA(ctx, cudaStreamSynchronize(st));  // hUg is a host temporary
+  }
+  ReplayTrace T{(uint32_t)tr->R, (uint32_t)tr->U, tr->s, tr->arr_rel, tr->grp, tr->blk, tr->inlen, tr->outlen,
+                tr->delta, dUg.p};
   const bool Qm = qarg.model != nullptr;
   const int64_t R = tr->R;
   // classes {list, LFU} x {expiry heap or not}; within a class, neighbours in a warp get
@@ -771,8 +778,8 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
       const uint64_t es = U + 1;
       auto per_cfg_of = [&](int q) {
         const bool lfu = q == 2 || q == 3, eheap = q == 1 || q == 3, glist = q == 4;
-        return U * (1 + 4 + 8) + (lfu ? U * 4 + 3 * 8 * (FM + NW + NSW) : 0) + (eheap ? U * 4 + 8 * es : 0) +
-               (glist ? U * 8 + 8 * (uint64_t)G : 0);
+        return U * (1 + 8) + (eheap || glist ? U * 4 : 0) + (lfu ? U * 4 + 3 * 8 * (FM + NW + NSW) : 0) +
+               (eheap ? U * 4 + 8 * es : 0) + (glist ? U * 8 + 8 * (uint64_t)G : 0);
       };
       // relative time of one pass over the trace per class (measured on the config-3 twin)
       const double pass_cost[5] = {1.0, 2.0, 1.2, 2.65, 1.9};
@@ -821,7 +828,8 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
         launches += (int)nwaves;
         ClassState &c = C[q];
         c.W = W;
-        KTRY(c.tier.alloc(ctx, U * W)); KTRY(c.lt.alloc(ctx, U * W)); KTRY(c.link.alloc(ctx, U * W));
+        KTRY(c.tier.alloc(ctx, U * W)); KTRY(c.link.alloc(ctx, U * W));
+        if (eheap || glist) KTRY(c.lt.alloc(ctx, U * W));
         if (lfu) {
           KTRY(c.freq.alloc(ctx, U * W)); KTRY(c.bht.alloc(ctx, 6 * FM * W)); KTRY(c.occ.alloc(ctx, 3 * (NW + NSW) * W));
         }
@@ -869,7 +877,7 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
           for (uint64_t w0 = 0; w0 < ix.size() && e == cudaSuccess; w0 += W) {
             const int64_t nw = (int64_t)(ix.size() - w0 < W ? ix.size() - w0 : W);
             cudaMemsetAsync(c.tier.p, 0, U * W, c.s);
-            cudaMemsetAsync(c.lt.p, 0xFF, 4 * U * W, c.s);
+            if (eheap || glist) cudaMemsetAsync(c.lt.p, 0xFF, 4 * U * W, c.s);
             if (lfu) {
               cudaMemsetAsync(c.bht.p, 0xFF, 4 * 6 * FM * W, c.s);
               cudaMemsetAsync(c.occ.p, 0, 8 * 3 * (NW + NSW) * W, c.s);
@@ -931,8 +939,8 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
     const uint64_t FM = (uint64_t)tr->R + 2;
     const uint64_t NW = (FM + 63) / 64, NSW = (NW + 63) / 64;
     const uint64_t es = U + 1;
-    uint64_t per_cfg = U * (1 + 4 + 8) + (lfu ? U * 4 + 3 * 8 * (FM + NW + NSW) : 0) + (eheap ? U * 4 + 8 * es : 0) +
-                       (glist ? U * 8 + 8 * (uint64_t)G : 0);
+    uint64_t per_cfg = U * (1 + 8) + (eheap || glist ? U * 4 : 0) + (lfu ? U * 4 + 3 * 8 * (FM + NW + NSW) : 0) +
+                       (eheap ? U * 4 + 8 * es : 0) + (glist ? U * 8 + 8 * (uint64_t)G : 0);
     if (Qm) per_cfg += 16 * (uint64_t)R + 8 * (uint64_t)qarg.model->instances + 64;  // f3: TTFT rows + queue
     // 80% of free device memory per wave (60% left the LRU expiry-list class of the config-3 twin
     // in two waves, i.e. two passes over the trace: 7.1 s -> 4.7 s at 80%)
@@ -950,7 +958,8 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
     DBuf<uint2> link, elink;
     DBuf<uint64_t> occ, ekey;
     DBuf<uint32_t> eht;
-    KTRY(tier.alloc(ctx, U * W)); KTRY(lt.alloc(ctx, U * W)); KTRY(link.alloc(ctx, U * W));
+    KTRY(tier.alloc(ctx, U * W)); KTRY(link.alloc(ctx, U * W));
+    if (eheap || glist) KTRY(lt.alloc(ctx, U * W));
     if (lfu) {
       KTRY(freq.alloc(ctx, U * W)); KTRY(bht.alloc(ctx, 6 * FM * W)); KTRY(occ.alloc(ctx, 3 * (NW + NSW) * W));
     }
@@ -990,7 +999,7 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
     for (uint64_t w0 = 0; w0 < ix.size(); w0 += W) {
       const int64_t nw = (int64_t)(ix.size() - w0 < W ? ix.size() - w0 : W);
       KCUDA(ctx, cudaMemsetAsync(tier.p, 0, U * W, st));
-      KCUDA(ctx, cudaMemsetAsync(lt.p, 0xFF, 4 * U * W, st));
+      if (eheap || glist) KCUDA(ctx, cudaMemsetAsync(lt.p, 0xFF, 4 * U * W, st));
       if (lfu) {
         KCUDA(ctx, cudaMemsetAsync(bht.p, 0xFF, 4 * 6 * FM * W, st));
         KCUDA(ctx, cudaMemsetAsync(occ.p, 0, 8 * 3 * (NW + NSW) * W, st));

@@ -14,6 +14,8 @@ struct ReplayTrace {
   const uint32_t *blk;     // [N] dense block id of each access (touch order)
   const uint32_t *inlen;   // [R] input tokens (row f3 queue)
   const uint32_t *outlen;  // [R] output tokens (row f3 queue)
+  const uint32_t *delta;   // [N] reuse interval of each access (kNone: first access), touch order
+  const uint64_t *Ug;      // [K+1] distinct blocks per group
 };
 
 // row f3 (queue.cu): the queue model evaluated inside the replay of each configuration

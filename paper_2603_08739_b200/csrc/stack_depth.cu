@@ -287,7 +287,8 @@ __global__ void __launch_bounds__(256) k_run_expand(const int *__restrict__ m_pt
                                                     const uint32_t *__restrict__ run_len,
                                                     const uint32_t *__restrict__ run_p0,
                                                     const uint32_t *__restrict__ s, uint32_t s_shift,
-                                                    const uint32_t *__restrict__ A, uint32_t *__restrict__ depth) {
+                                                    const uint32_t *__restrict__ A, uint32_t *__restrict__ depth,
+                                                    uint4 *__restrict__ runs_out) {
   const int M = *m_ptr;
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -298,13 +299,16 @@ __global__ void __launch_bounds__(256) k_run_expand(const int *__restrict__ m_pt
       const uint32_t p0 = run_p0[q];
       j0 = run_start[q];
       L = run_len[q];
-      base = s[run_req[q]] - s_shift - p0 - A[p0];
+      const uint32_t r = run_req[q];
+      base = s[r] - s_shift - p0 - A[p0];
+      if (runs_out) runs_out[q] = make_uint4(j0, L, base, r);
     }
     const int nk = M - q0 < 32 ? M - q0 : 32;
     for (int k = 0; k < nk; k++) {
       const uint32_t jk = __shfl_sync(0xFFFFFFFFu, j0, k), Lk = __shfl_sync(0xFFFFFFFFu, L, k);
       const uint32_t bk = __shfl_sync(0xFFFFFFFFu, base, k);
-      for (uint32_t t = lane; t < Lk; t += 32) depth[jk + t] = bk - t;
+      if (depth)
+        for (uint32_t t = lane; t < Lk; t += 32) depth[jk + t] = bk - t;
     }
   }
 }
@@ -399,13 +403,14 @@ static kareto_status cub_tmp(kareto_ctx *ctx, DBuf<uint8_t> &tmp, F &&f) {
 // y_range = n; a time shard prepends its boundary LRU stack, trace_shard.cu).
 kareto_status stack_depth(kareto_ctx *ctx, uint64_t N, uint64_t y_range, const uint32_t *prev_c,
                           const uint32_t *req, uint32_t req_base, const uint32_t *s, uint32_t pos_base,
-                          uint32_t y_off, const uint8_t *run_flag, uint32_t *depth, int64_t *n_runs) {
+                          uint32_t y_off, const uint8_t *run_flag, uint32_t *depth, int64_t *n_runs,
+                          uint4 **runs_out) {
   *n_runs = 0;
   if (N == 0) return KARETO_OK;
   if (y_range >= (1ull << 31)) return fail(ctx, KARETO_E_OVERFLOW, "stack depth pass supports < 2^31 positions");
   cudaStream_t st = ctx->stream;
   const int sms = ctx->num_sms;
-  KCUDA(ctx, cudaMemsetAsync(depth, 0xFF, 4 * N, st));  // first accesses: UINT32_MAX
+  if (depth) KCUDA(ctx, cudaMemsetAsync(depth, 0xFF, 4 * N, st));  // first accesses: UINT32_MAX
   // ---- runs
   DBuf<uint8_t> tmp;
   DBuf<uint32_t> run_start, run_req, run_len, run_p0;
@@ -432,6 +437,7 @@ kareto_status stack_depth(kareto_ctx *ctx, uint64_t N, uint64_t y_range, const u
   *n_runs = M;
   if (M == 0) return KARETO_OK;
   KTRY(run_req.alloc(ctx, M)); KTRY(run_len.alloc(ctx, M)); KTRY(run_p0.alloc(ctx, M));
+  if (runs_out) KMALLOC(ctx, *runs_out, sizeof(uint4) * (size_t)M, st);
   const uint64_t NI = 2ull * (uint64_t)M;  // items
   DBuf<uint2> buf[2];
   KTRY(buf[0].alloc(ctx, NI)); KTRY(buf[1].alloc(ctx, NI));
@@ -541,10 +547,43 @@ kareto_status stack_depth(kareto_ctx *ctx, uint64_t N, uint64_t y_range, const u
     }
   }
   {
-    Pass ps(ctx, "K3_expand", 1, 1);
+    Pass ps(ctx, depth ? "K3_expand" : "K3_runs_out", 1, 1);
     k_run_expand<<<grid_for(M, 256, 16 * sms), 256, 0, st>>>(m_dev.p, run_start.p, run_req.p, run_len.p, run_p0.p, s,
-                                                             pos_base - y_off, A.p, depth);
+                                                             pos_base - y_off, A.p, depth,
+                                                             runs_out ? *runs_out : nullptr);
   }
+  return KARETO_OK;
+}
+
+// Per-access depths of a whole trace from its kept runs (d_{j0+t} = d0 - t; first accesses
+// UINT32_MAX), on first use: the bench step's K4 reads the runs only (eval.cu k_hist_runs).
+__global__ void __launch_bounds__(256) k_runs_depth(int64_t M, const uint4 *__restrict__ runs,
+                                                    uint32_t *__restrict__ depth) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; q0 < M; q0 += nw * 32) {
+    const int64_t q = q0 + lane;
+    const uint4 rn = q < M ? runs[q] : make_uint4(0, 0, 0, 0);
+    const int nk = M - q0 < 32 ? (int)(M - q0) : 32;
+    for (int k = 0; k < nk; k++) {
+      const uint32_t jk = __shfl_sync(0xFFFFFFFFu, rn.x, k), Lk = __shfl_sync(0xFFFFFFFFu, rn.y, k);
+      const uint32_t bk = __shfl_sync(0xFFFFFFFFu, rn.z, k);
+      for (uint32_t t = lane; t < Lk; t += 32) depth[jk + t] = bk - t;
+    }
+  }
+}
+
+kareto_status ensure_depth(kareto_ctx *ctx, kareto_trace *tr) {
+  if (tr->depth_ready) return KARETO_OK;
+  cudaStream_t st = ctx->stream;
+  const uint64_t n = (uint64_t)(tr->pos_hi - tr->pos_lo);
+  if (n > 0) {
+    Pass ps(ctx, "K3_depth", 1, 1);
+    KCUDA(ctx, cudaMemsetAsync(tr->depth, 0xFF, 4 * n, st));
+    if (tr->n_runs > 0)
+      k_runs_depth<<<grid_for(tr->n_runs, 256, 16 * ctx->num_sms), 256, 0, st>>>(tr->n_runs, tr->runs, tr->depth);
+  }
+  tr->depth_ready = true;
   return KARETO_OK;
 }
 

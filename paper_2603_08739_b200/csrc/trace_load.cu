@@ -596,37 +596,67 @@ __device__ __forceinline__ void warp_count_add(uint32_t *arr, uint32_t key, bool
   if ((__ffs(same) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&arr[key], (uint32_t)__popc(same));
 }
 
-__global__ void k_access_info(uint64_t N, const uint32_t *__restrict__ prev, const uint32_t *__restrict__ req,
-                              const uint32_t *__restrict__ s, const int64_t *__restrict__ arr,
-                              const uint64_t *__restrict__ hash, uint32_t *__restrict__ delta,
-                              uint32_t *__restrict__ first_cnt, uint32_t *__restrict__ reuse_cnt,
-                              uint8_t *__restrict__ run_flag, LoadStats *st) {
+// Loads are issued breadth-first over AI_U accesses per thread (own fields, then the request
+// fields, then the previous access's request fields) so that each thread keeps several
+// dependent gather chains in flight; the kernel is latency-bound (prev -> req[prev] -> arr / s).
+constexpr int AI_U = 4;
+__global__ void __launch_bounds__(256) k_access_info(uint64_t N, const uint32_t *__restrict__ prev,
+                                                     const uint32_t *__restrict__ req,
+                                                     const uint32_t *__restrict__ s, const int64_t *__restrict__ arr,
+                                                     const uint64_t *__restrict__ hash, uint32_t *__restrict__ delta,
+                                                     uint32_t *__restrict__ first_cnt, uint32_t *__restrict__ reuse_cnt,
+                                                     uint8_t *__restrict__ run_flag, LoadStats *st) {
   unsigned flags = 0;
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t p = prev[j], r = req[j];
-    uint32_t dl = kNone;
-    if (p != kNone) {
-      uint32_t rp = req[p];
-      int64_t d = arr[r] - arr[rp];
-      if (d < 0 || d >= (int64_t)kNone) flags |= F_DELTA; else dl = (uint32_t)d;
-      uint32_t kj = s[r + 1] - 1 - (uint32_t)j;
-      uint32_t kp = s[rp + 1] - 1 - p;
-      if (kj != kp) flags |= F_CHAIN;
-      // parents must match (R7); when the parent access links to p + 1 the K2 link already
-      // proves equal hashes (the common case inside a run), so only run ends gather hashes
-      else if (kj > 0 && prev[j + 1] != p + 1 && hash[j + 1] != hash[p + 1]) flags |= F_CHAIN;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * AI_U;
+  for (uint64_t jb = (uint64_t)blockIdx.x * blockDim.x * AI_U + threadIdx.x; jb < N; jb += stride) {
+    uint32_t p[AI_U], r[AI_U], pm[AI_U], rp[AI_U], sr[AI_U], sr1[AI_U], srp1[AI_U];
+    int64_t ar[AI_U], arp[AI_U];
+#pragma unroll
+    for (int u = 0; u < AI_U; u++) {
+      const uint64_t j = jb + (uint64_t)u * blockDim.x;
+      const bool ok = j < N;
+      p[u] = ok ? prev[j] : kNone;
+      r[u] = ok ? req[j] : 0u;
+      pm[u] = (ok && j > 0) ? prev[j - 1] : kNone;
     }
-    delta[j] = dl;
-    // K3 run heads: a reuse access whose predecessor position is not its previous position
-    // plus one, or the first position of its request (stack_depth.cu)
-    uint8_t head = 0;
-    if (p != kNone) {
-      uint32_t pm = j > 0 ? prev[j - 1] : kNone;
-      head = ((uint32_t)j == s[r] || pm == kNone || p != pm + 1) ? 1 : 0;
+#pragma unroll
+    for (int u = 0; u < AI_U; u++) {
+      const uint64_t j = jb + (uint64_t)u * blockDim.x;
+      const bool ok = j < N;
+      rp[u] = p[u] != kNone ? req[p[u]] : 0u;
+      sr[u] = ok ? s[r[u]] : 0u;
+      sr1[u] = ok ? s[r[u] + 1] : 0u;
+      ar[u] = p[u] != kNone ? arr[r[u]] : 0;
     }
-    run_flag[j] = head;
-    warp_count_add(first_cnt, r, p == kNone);
-    warp_count_add(reuse_cnt, r, p != kNone);
+#pragma unroll
+    for (int u = 0; u < AI_U; u++) {
+      arp[u] = p[u] != kNone ? arr[rp[u]] : 0;
+      srp1[u] = p[u] != kNone ? s[rp[u] + 1] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < AI_U; u++) {
+      const uint64_t j = jb + (uint64_t)u * blockDim.x;
+      if (j >= N) break;  // uniform across the warp except in the last round
+      uint32_t dl = kNone;
+      uint8_t head = 0;
+      if (p[u] != kNone) {
+        const int64_t d = ar[u] - arp[u];
+        if (d < 0 || d >= (int64_t)kNone) flags |= F_DELTA; else dl = (uint32_t)d;
+        const uint32_t kj = sr1[u] - 1 - (uint32_t)j;
+        const uint32_t kp = srp1[u] - 1 - p[u];
+        if (kj != kp) flags |= F_CHAIN;
+        // parents must match (R7); when the parent access links to p + 1 the K2 link already
+        // proves equal hashes (the common case inside a run), so only run ends gather hashes
+        else if (kj > 0 && prev[j + 1] != p[u] + 1 && hash[j + 1] != hash[p[u] + 1]) flags |= F_CHAIN;
+        // K3 run heads: a reuse access whose predecessor position is not its previous position
+        // plus one, or the first position of its request (stack_depth.cu)
+        head = ((uint32_t)j == sr[u] || pm[u] == kNone || p[u] != pm[u] + 1) ? 1 : 0;
+      }
+      delta[j] = dl;
+      run_flag[j] = head;
+      warp_count_add(first_cnt, r[u], p[u] == kNone);
+      warp_count_add(reuse_cnt, r[u], p[u] != kNone);
+    }
   }
   if (flags) atomicOr(&st->flags, flags);
 }
@@ -1179,7 +1209,7 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
     hm.mark(st, "a3 K2 link");
     {
       Pass ps(ctx, "K2_access_info", 1, 1);
-      k_access_info<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(N, tr->prev, tr->req, tr->s, tr->arr, tr->hash,
+      k_access_info<<<grid_for((N + AI_U - 1) / AI_U, 256, 8 * sms), 256, 0, st>>>(N, tr->prev, tr->req, tr->s, tr->arr, tr->hash,
                                                                tr->delta, first_cnt.p, reuse_cnt.p, run_flag.p,
                                                                in.stats.p);
     }
@@ -1269,7 +1299,9 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
   // ---- a4: K3 LRU stack depths
   if (N > 0) {
     if (N >= (1ull << 31)) return fail(ctx, KARETO_E_OVERFLOW, "stack depth pass supports < 2^31 accesses");
-    KTRY(stack_depth(ctx, N, N, tr->prev, tr->req, 0, tr->s, 0, 0, run_flag.p, tr->depth, &tr->n_runs));
+    // the runs are kept and per-access depths deferred to their first reader (ensure_depth)
+    KTRY(stack_depth(ctx, N, N, tr->prev, tr->req, 0, tr->s, 0, 0, run_flag.p, nullptr, &tr->n_runs, &tr->runs));
+    tr->depth_ready = false;
   }
   KTRY(sync(ctx, "load_trace"));
   hm.mark(st, "a4 K3");

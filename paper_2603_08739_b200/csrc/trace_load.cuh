@@ -65,6 +65,7 @@ constexpr uint64_t kSortMixC = 0x6A09E667F3BCC909ULL;
 
 kareto_status stack_depth(kareto_ctx *ctx, uint64_t n, uint64_t y_range, const uint32_t *prev_c,
                           const uint32_t *req, uint32_t req_base, const uint32_t *s, uint32_t pos_base,
-                          uint32_t y_off, const uint8_t *run_flag, uint32_t *depth, int64_t *n_runs);
+                          uint32_t y_off, const uint8_t *run_flag, uint32_t *depth, int64_t *n_runs,
+                          uint4 **runs_out = nullptr);
 
 }  // namespace kareto

@@ -34,6 +34,16 @@ namespace kareto {
 constexpr int BL_BITS = 16, BL_NB = 1 << BL_BITS;
 constexpr int BL_WARPS = 16, BL_SLOTS = 1024, BL_LIMIT = BL_SLOTS * 3 / 4, BL_BATCH = 8;
 constexpr uint32_t BL_CHUNK = 4096;
+// Pair slots: a 2^15-position bucket is split into 2^sl sub-regions by position mod 2^sl, each
+// exactly 2^(15-sl) pairs long (one pair per position) with its own append cursor, so the 10^8
+// cursor atomics spread over 2^sl times more addresses (fewer same-address collisions at the L2);
+// cursors are spaced cstride words apart.  KARETO_BL_SUB / KARETO_BL_CSTRIDE override (measurements).
+constexpr uint32_t BL_SUB_LOG2 = 2, BL_CSTRIDE = 1;
+__device__ __forceinline__ uint32_t bl_slot(unsigned *cursor, uint32_t p, uint32_t sl, uint32_t cstride) {
+  const uint32_t sub = p & ((1u << sl) - 1u);
+  const uint32_t ci = ((p >> 15) << sl) | sub;
+  return (sub << (15 - sl)) + atomicAdd(&cursor[(size_t)ci * cstride], 1u);
+}
 constexpr uint32_t BL_EMPTY = 0xFFFFFFFFu, BL_CLAIM = 0xFFFFFFFEu;
 struct BLTable {
   uint64_t key[BL_SLOTS];
@@ -117,7 +127,8 @@ __global__ void __launch_bounds__(BL_WARPS * 32) k_bucket_link(
     const uint32_t *__restrict__ ks, const uint64_t *__restrict__ vs, const uint32_t *__restrict__ bstart,
     const uint32_t *__restrict__ cstart, unsigned *__restrict__ next, unsigned *__restrict__ cursor,
     uint2 *__restrict__ pairs, uint64_t *__restrict__ rec_m, uint32_t *__restrict__ rec_p, uint64_t *__restrict__ lst_m,
-    uint32_t *__restrict__ lst_p, uint32_t *__restrict__ rec_n, unsigned *__restrict__ overflow, uint32_t limit) {
+    uint32_t *__restrict__ lst_p, uint32_t *__restrict__ rec_n, unsigned *__restrict__ overflow, uint32_t limit,
+    uint32_t sl, uint32_t cstride) {
   extern __shared__ __align__(16) uint8_t bl_raw[];
   BLTable &T = reinterpret_cast<BLTable *>(bl_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -221,7 +232,7 @@ __global__ void __launch_bounds__(BL_WARPS * 32) k_bucket_link(
         if (spos[k] != BL_EMPTY) pairs[((uint64_t)(spos[k] >> 15) << 15) + sat[k]] = make_uint2(spos[k], sprv[k]);
 #pragma unroll
       for (int k = 0; k < BL_BATCH; k++) {
-        sat[k] = pos[k] != BL_EMPTY ? atomicAdd(&cursor[pos[k] >> 15], 1u) : 0u;
+        sat[k] = pos[k] != BL_EMPTY ? bl_slot(cursor, pos[k], sl, cstride) : 0u;
         spos[k] = pos[k];
         sprv[k] = prv[k];
         m[k] = mn[k];
@@ -254,7 +265,8 @@ __global__ void __launch_bounds__(BL_WARPS * 32) k_bucket_fixup(
     const uint32_t *__restrict__ bstart, const uint32_t *__restrict__ cstart, unsigned *__restrict__ next,
     unsigned *__restrict__ cursor, uint2 *__restrict__ pairs, const uint64_t *__restrict__ rec_m,
     const uint32_t *__restrict__ rec_p, const uint64_t *__restrict__ lst_m, const uint32_t *__restrict__ lst_p,
-    const uint32_t *__restrict__ rec_n, unsigned *__restrict__ overflow, uint32_t limit) {
+    const uint32_t *__restrict__ rec_n, unsigned *__restrict__ overflow, uint32_t limit, uint32_t sl,
+    uint32_t cstride) {
   extern __shared__ __align__(16) uint8_t bl_raw[];
   BLTable &T = reinterpret_cast<BLTable *>(bl_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -280,7 +292,7 @@ __global__ void __launch_bounds__(BL_WARPS * 32) k_bucket_fixup(
           uint32_t slot;
           bool isnew;
           const uint32_t prv = degraded ? kNone : bl_find(T, m, slot, isnew);
-          const uint32_t at = atomicAdd(&cursor[p >> 15], 1u);
+          const uint32_t at = bl_slot(cursor, p, sl, cstride);
           pairs[((uint64_t)(p >> 15) << 15) + at] = make_uint2(p, prv);
         }
       }

@@ -257,37 +257,39 @@ static kareto_status pareto_run(kareto_ctx *ctx, const double *obj, const kareto
     }
   }
   // K8b
-  DBuf<uint8_t> keep;
-  DBuf<double> f1, f1c, f1s;
-  DBuf<uint32_t> idx, idxc, idxs;
-  DBuf<int> m_dev;
   DBuf<unsigned long long> nf;
-  KTRY(keep.alloc(ctx, n)); KTRY(f1.alloc(ctx, n)); KTRY(f1c.alloc(ctx, n)); KTRY(f1s.alloc(ctx, n));
-  KTRY(idx.alloc(ctx, n)); KTRY(idxc.alloc(ctx, n)); KTRY(idxs.alloc(ctx, n)); KTRY(m_dev.alloc(ctx, 1));
   KTRY(nf.alloc(ctx, 1)); KTRY(nf.zero());
   {
-    Pass ps(ctx, "K8b_compact_sort", 0, 3);
-    k_survivor_flags<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(pruned.p, n, keep.p, f1.p, f, idx.p);
-    KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
-      return cub::DeviceSelect::Flagged(t, b, f1.p, keep.p, f1c.p, m_dev.p, (int)n, st);
-    }));
-    KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
-      return cub::DeviceSelect::Flagged(t, b, idx.p, keep.p, idxc.p, m_dev.p, (int)n, st);
-    }));
-    int m = 0;
-    KCUDA(ctx, cudaMemcpyAsync(&m, m_dev.p, 4, cudaMemcpyDeviceToHost, st));
-    KCUDA(ctx, cudaStreamSynchronize(st));
-    if (m > 0) {
+    DBuf<uint8_t> keep;
+    DBuf<double> f1, f1c, f1s;
+    DBuf<uint32_t> idx, idxc, idxs;
+    DBuf<int> m_dev;
+    KTRY(keep.alloc(ctx, n)); KTRY(f1.alloc(ctx, n)); KTRY(f1c.alloc(ctx, n)); KTRY(f1s.alloc(ctx, n));
+    KTRY(idx.alloc(ctx, n)); KTRY(idxc.alloc(ctx, n)); KTRY(idxs.alloc(ctx, n)); KTRY(m_dev.alloc(ctx, 1));
+    {
+      Pass ps(ctx, "K8b_compact_sort", 0, 3);
+      k_survivor_flags<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(pruned.p, n, keep.p, f1.p, f, idx.p);
       KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, f1c.p, f1s.p, idxc.p, idxs.p, m, 0, 64, st);
+        return cub::DeviceSelect::Flagged(t, b, f1.p, keep.p, f1c.p, m_dev.p, (int)n, st);
       }));
+      KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+        return cub::DeviceSelect::Flagged(t, b, idx.p, keep.p, idxc.p, m_dev.p, (int)n, st);
+      }));
+      int m = 0;
+      KCUDA(ctx, cudaMemcpyAsync(&m, m_dev.p, 4, cudaMemcpyDeviceToHost, st));
+      KCUDA(ctx, cudaStreamSynchronize(st));
+      if (m > 0) {
+        KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+          return cub::DeviceRadixSort::SortPairs(t, b, f1c.p, f1s.p, idxc.p, idxs.p, m, 0, 64, st);
+        }));
+      }
+      ctx->own_launches += 1;
     }
-    ctx->own_launches += 1;
-  }
-  {
-    Pass ps(ctx, "K8b_dominance", 1, 2);
-    k_dominance<<<grid_for(n, P_THREADS), P_THREADS, 0, st>>>(idxs.p, m_dev.p, f, status.p, nf.p);
-    k_status_pruned<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(pruned.p, n, status.p);
+    {
+      Pass ps(ctx, "K8b_dominance", 1, 2);
+      k_dominance<<<grid_for(n, P_THREADS), P_THREADS, 0, st>>>(idxs.p, m_dev.p, f, status.p, nf.p);
+      k_status_pruned<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(pruned.p, n, status.p);
+    }
   }
   unsigned long long hnf = 0;
   KCUDA(ctx, cudaMemcpyAsync(status_out, status.p, n, on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));

@@ -563,20 +563,27 @@ __global__ void __launch_bounds__(OVF_THREADS) k_link_overflow(const uint32_t *_
 }
 
 // bucket b's pairs -> the 2^P-entry slice of prev[] in shared memory -> one coalesced write
+// (sl > 0: bucket b's pairs sit in 2^sl sub-regions of 2^(P-sl) by position mod 2^sl; a partial
+// last bucket fills a prefix of each sub-region)
 template <int P>
 __global__ void __launch_bounds__(1024) k_bucket_assemble(const uint2 *__restrict__ pairs, uint64_t N,
-                                                           uint32_t *__restrict__ prev) {
+                                                           uint32_t *__restrict__ prev, uint32_t sl) {
   extern __shared__ uint32_t slice[];
   const uint64_t nb = (N + (1u << P) - 1) >> P;
   for (uint64_t b = blockIdx.x; b < nb; b += gridDim.x) {
     const uint64_t lo = b << P;
     const uint32_t cnt = (uint32_t)((N - lo) < (1u << P) ? (N - lo) : (1u << P));
-    for (uint32_t q0 = 0; q0 < cnt; q0 += 8 * blockDim.x) {  // 8 loads in flight per thread
+    const bool part = cnt < (1u << P) && sl > 0;
+    const uint32_t span = part ? (1u << P) : cnt;
+    for (uint32_t q0 = 0; q0 < span; q0 += 8 * blockDim.x) {  // 8 loads in flight per thread
       uint2 pr[8];
 #pragma unroll
       for (int e = 0; e < 8; e++) {
         const uint32_t q = q0 + e * blockDim.x + threadIdx.x;
-        pr[e] = q < cnt ? pairs[lo + q] : make_uint2(0xFFFFFFFFu, 0);
+        bool ok = q < span;
+        if (part && ok)  // sub-region q >> (P - sl) holds (cnt + 2^sl - 1 - sub) >> sl pairs
+          ok = (q & ((1u << (P - sl)) - 1u)) < ((cnt + (1u << sl) - 1u - (q >> (P - sl))) >> sl);
+        pr[e] = ok ? pairs[lo + q] : make_uint2(0xFFFFFFFFu, 0);
       }
 #pragma unroll
       for (int e = 0; e < 8; e++)
@@ -596,67 +603,37 @@ __device__ __forceinline__ void warp_count_add(uint32_t *arr, uint32_t key, bool
   if ((__ffs(same) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&arr[key], (uint32_t)__popc(same));
 }
 
-// Loads are issued breadth-first over AI_U accesses per thread (own fields, then the request
-// fields, then the previous access's request fields) so that each thread keeps several
-// dependent gather chains in flight; the kernel is latency-bound (prev -> req[prev] -> arr / s).
-constexpr int AI_U = 4;
-__global__ void __launch_bounds__(256) k_access_info(uint64_t N, const uint32_t *__restrict__ prev,
-                                                     const uint32_t *__restrict__ req,
-                                                     const uint32_t *__restrict__ s, const int64_t *__restrict__ arr,
-                                                     const uint64_t *__restrict__ hash, uint32_t *__restrict__ delta,
-                                                     uint32_t *__restrict__ first_cnt, uint32_t *__restrict__ reuse_cnt,
-                                                     uint8_t *__restrict__ run_flag, LoadStats *st) {
+__global__ void k_access_info(uint64_t N, const uint32_t *__restrict__ prev, const uint32_t *__restrict__ req,
+                              const uint32_t *__restrict__ s, const int64_t *__restrict__ arr,
+                              const uint64_t *__restrict__ hash, uint32_t *__restrict__ delta,
+                              uint32_t *__restrict__ first_cnt, uint32_t *__restrict__ reuse_cnt,
+                              uint8_t *__restrict__ run_flag, LoadStats *st) {
   unsigned flags = 0;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * AI_U;
-  for (uint64_t jb = (uint64_t)blockIdx.x * blockDim.x * AI_U + threadIdx.x; jb < N; jb += stride) {
-    uint32_t p[AI_U], r[AI_U], pm[AI_U], rp[AI_U], sr[AI_U], sr1[AI_U], srp1[AI_U];
-    int64_t ar[AI_U], arp[AI_U];
-#pragma unroll
-    for (int u = 0; u < AI_U; u++) {
-      const uint64_t j = jb + (uint64_t)u * blockDim.x;
-      const bool ok = j < N;
-      p[u] = ok ? prev[j] : kNone;
-      r[u] = ok ? req[j] : 0u;
-      pm[u] = (ok && j > 0) ? prev[j - 1] : kNone;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t p = prev[j], r = req[j];
+    uint32_t dl = kNone;
+    if (p != kNone) {
+      uint32_t rp = req[p];
+      int64_t d = arr[r] - arr[rp];
+      if (d < 0 || d >= (int64_t)kNone) flags |= F_DELTA; else dl = (uint32_t)d;
+      uint32_t kj = s[r + 1] - 1 - (uint32_t)j;
+      uint32_t kp = s[rp + 1] - 1 - p;
+      if (kj != kp) flags |= F_CHAIN;
+      // parents must match (R7); when the parent access links to p + 1 the K2 link already
+      // proves equal hashes (the common case inside a run), so only run ends gather hashes
+      else if (kj > 0 && prev[j + 1] != p + 1 && hash[j + 1] != hash[p + 1]) flags |= F_CHAIN;
     }
-#pragma unroll
-    for (int u = 0; u < AI_U; u++) {
-      const uint64_t j = jb + (uint64_t)u * blockDim.x;
-      const bool ok = j < N;
-      rp[u] = p[u] != kNone ? req[p[u]] : 0u;
-      sr[u] = ok ? s[r[u]] : 0u;
-      sr1[u] = ok ? s[r[u] + 1] : 0u;
-      ar[u] = p[u] != kNone ? arr[r[u]] : 0;
+    delta[j] = dl;
+    // K3 run heads: a reuse access whose predecessor position is not its previous position
+    // plus one, or the first position of its request (stack_depth.cu)
+    uint8_t head = 0;
+    if (p != kNone) {
+      uint32_t pm = j > 0 ? prev[j - 1] : kNone;
+      head = ((uint32_t)j == s[r] || pm == kNone || p != pm + 1) ? 1 : 0;
     }
-#pragma unroll
-    for (int u = 0; u < AI_U; u++) {
-      arp[u] = p[u] != kNone ? arr[rp[u]] : 0;
-      srp1[u] = p[u] != kNone ? s[rp[u] + 1] : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < AI_U; u++) {
-      const uint64_t j = jb + (uint64_t)u * blockDim.x;
-      if (j >= N) break;  // uniform across the warp except in the last round
-      uint32_t dl = kNone;
-      uint8_t head = 0;
-      if (p[u] != kNone) {
-        const int64_t d = ar[u] - arp[u];
-        if (d < 0 || d >= (int64_t)kNone) flags |= F_DELTA; else dl = (uint32_t)d;
-        const uint32_t kj = sr1[u] - 1 - (uint32_t)j;
-        const uint32_t kp = srp1[u] - 1 - p[u];
-        if (kj != kp) flags |= F_CHAIN;
-        // parents must match (R7); when the parent access links to p + 1 the K2 link already
-        // proves equal hashes (the common case inside a run), so only run ends gather hashes
-        else if (kj > 0 && prev[j + 1] != p[u] + 1 && hash[j + 1] != hash[p[u] + 1]) flags |= F_CHAIN;
-        // K3 run heads: a reuse access whose predecessor position is not its previous position
-        // plus one, or the first position of its request (stack_depth.cu)
-        head = ((uint32_t)j == sr[u] || pm[u] == kNone || p[u] != pm[u] + 1) ? 1 : 0;
-      }
-      delta[j] = dl;
-      run_flag[j] = head;
-      warp_count_add(first_cnt, r[u], p[u] == kNone);
-      warp_count_add(reuse_cnt, r[u], p[u] != kNone);
-    }
+    run_flag[j] = head;
+    warp_count_add(first_cnt, r, p == kNone);
+    warp_count_add(reuse_cnt, r, p != kNone);
   }
   if (flags) atomicOr(&st->flags, flags);
 }
@@ -1014,11 +991,15 @@ static kareto_status bucket_link(kareto_ctx *ctx, DBuf<uint32_t> &k32, DBuf<uint
   // blocked the host for 4-6 ms (the pool reclaims pending frees), the device idling meanwhile
   DBuf<unsigned> cursor;
   DBuf<uint32_t> rec_n;
-  KTRY(cursor.alloc(ctx, nbk)); KTRY(cursor.zero());
+  uint32_t sl = BL_SUB_LOG2, cstride = BL_CSTRIDE;
+  if (const char *e = getenv("KARETO_BL_SUB")) sl = (uint32_t)atoi(e) <= 8 ? (uint32_t)atoi(e) : 0u;
+  if (const char *e = getenv("KARETO_BL_CSTRIDE")) cstride = (uint32_t)atoi(e) > 0 ? (uint32_t)atoi(e) : 1u;
+  KTRY(cursor.alloc(ctx, (nbk << sl) * cstride)); KTRY(cursor.zero());
   KTRY(rec_n.alloc(ctx, 2 * max_chunks));
   uint64_t *rec_m = v64.p, *lst_m = nullptr;  // the unsorted input buffers are free now
   uint32_t *rec_p = k32.p, *lst_p = nullptr;
-  const size_t need = 20 * (size_t)N + 512;
+  const size_t npairs = (size_t)nbk << PBT;  // padded: a partial last bucket fills sub-region prefixes
+  const size_t need = 8 * npairs + 12 * (size_t)N + 512;
   if (ctx->k2_scratch_bytes < need) {
     if (ctx->k2_scratch) cudaFreeAsync(ctx->k2_scratch, st);
     ctx->k2_scratch = nullptr;
@@ -1028,8 +1009,8 @@ static kareto_status bucket_link(kareto_ctx *ctx, DBuf<uint32_t> &k32, DBuf<uint
   }
   uint8_t *scr = reinterpret_cast<uint8_t *>(ctx->k2_scratch);
   uint2 *pairs = reinterpret_cast<uint2 *>(scr);
-  lst_m = reinterpret_cast<uint64_t *>(scr + 8 * (size_t)N);
-  lst_p = reinterpret_cast<uint32_t *>(scr + 16 * (size_t)N);
+  lst_m = reinterpret_cast<uint64_t *>(scr + 8 * npairs);
+  lst_p = reinterpret_cast<uint32_t *>(scr + 8 * npairs + 8 * (size_t)N);
   uint32_t limit = BL_LIMIT;  // KARETO_K2_TABLE_LIMIT (tests) lowers it to exercise the fallback
   if (const char *e = getenv("KARETO_K2_TABLE_LIMIT")) {
     const long v = atol(e);
@@ -1041,21 +1022,21 @@ static kareto_status bucket_link(kareto_ctx *ctx, DBuf<uint32_t> &k32, DBuf<uint
     Pass ps(ctx, "K2_bucket_link", 1, 1);
     cudaFuncSetAttribute(k_bucket_link, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_bucket_link<<<sms, BL_WARPS * 32, smem, st>>>(k32s.p, v64s.p, bstart.p, cstart.p, ctr.p, cursor.p,
-                                                     pairs, rec_m, rec_p, lst_m, lst_p, rec_n.p, ovf_dev, limit);
+                                                     pairs, rec_m, rec_p, lst_m, lst_p, rec_n.p, ovf_dev, limit, sl, cstride);
   }
   hm.mark(st, "link");
   {
     Pass ps(ctx, "K2_bucket_fixup", 1, 1);
     cudaFuncSetAttribute(k_bucket_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_bucket_fixup<<<sms, BL_WARPS * 32, smem, st>>>(bstart.p, cstart.p, ctr.p + 1, cursor.p, pairs, rec_m, rec_p,
-                                                      lst_m, lst_p, rec_n.p, ovf_dev, limit);
+                                                      lst_m, lst_p, rec_n.p, ovf_dev, limit, sl, cstride);
   }
   k32.release(); v64.release();
   {
     Pass ps(ctx, "K2_bucket_assemble", 1, 1);
     const unsigned g = (unsigned)(nbk < (uint64_t)(4 * sms) ? nbk : 4 * sms);
     cudaFuncSetAttribute(k_bucket_assemble<PBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << PBT);
-    k_bucket_assemble<PBT><<<g, 1024, 4 << PBT, st>>>(pairs, N, prev);
+    k_bucket_assemble<PBT><<<g, 1024, 4 << PBT, st>>>(pairs, N, prev, sl);
   }
   hm.mark(st, "fixup + assemble");
   return KARETO_OK;
@@ -1140,9 +1121,9 @@ kareto_status link_prev(kareto_ctx *ctx, const uint64_t *hash, uint64_t N, uint3
       const unsigned g = (unsigned)(nbk < (uint64_t)(4 * sms) ? nbk : 4 * sms);
       if (tiled) {
         cudaFuncSetAttribute(k_bucket_assemble<PBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << PBT);
-        k_bucket_assemble<PBT><<<g, 1024, 4 << PBT, st>>>(pairs.p, N, prev);
+        k_bucket_assemble<PBT><<<g, 1024, 4 << PBT, st>>>(pairs.p, N, prev, 0u);
       } else {
-        k_bucket_assemble<PB><<<g, 1024, 4 << PB, st>>>(pairs.p, N, prev);
+        k_bucket_assemble<PB><<<g, 1024, 4 << PB, st>>>(pairs.p, N, prev, 0u);
       }
     }
   }
@@ -1209,7 +1190,7 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
     hm.mark(st, "a3 K2 link");
     {
       Pass ps(ctx, "K2_access_info", 1, 1);
-      k_access_info<<<grid_for((N + AI_U - 1) / AI_U, 256, 8 * sms), 256, 0, st>>>(N, tr->prev, tr->req, tr->s, tr->arr, tr->hash,
+      k_access_info<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(N, tr->prev, tr->req, tr->s, tr->arr, tr->hash,
                                                                tr->delta, first_cnt.p, reuse_cnt.p, run_flag.p,
                                                                in.stats.p);
     }

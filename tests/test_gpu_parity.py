@@ -435,3 +435,40 @@ def test_k2_full_sort_path_and_bucket_overflow_fallback(ctx, env):
             else:
                 os.environ[k] = v
     check_trace_exports(ot, gt)
+
+
+@pytest.mark.parametrize("kind,R", [("chat", 20_000), ("agent", 1_500)])
+def test_k4_runs_and_access_paths(ctx, kind, R):
+    """K4 over the K3 runs (the default for whole traces: a run adds an arithmetic range of depths,
+    one D and one delta) against K4 over the accesses (forced with KARETO_K4_ACCESS) and the O2
+    closed forms: dense capacity boundaries (bins narrower than runs), CAPACITY rows with uniform
+    disk TTLs (delta bins) and TTL-mode rows.  The trace's depths are never exported before the
+    first evaluation (deferred materialisation), and are checked against the oracle after it."""
+    import os
+    tr = ki.synthetic(kind, R=R, seed=21)
+    ot = O.OracleTrace(tr, top_k=4)
+    gt = ctx.load(tr, top_k=4)
+    U = ot.U
+    rows = np.array([[U32] * 5, [3_600_000] * 5, [60_000] * 5, [1_000] * 5], np.uint32)
+    caps, tun, axis = [], [], []
+    A = lambda m, top: [top * i // (m - 1) for i in range(m)]
+    for i, a in enumerate(A(12, U // 40)):
+        for j, b in enumerate(A(9, U // 6)):
+            for k, c in enumerate(A(7, U // 2)):
+                for t in range(4):
+                    caps.append([a, b, c]); tun.append(t); axis.append([i, j, k])
+            for t in (1, 2, 3):
+                caps.append([a, b, O.INF_CAP]); tun.append(t); axis.append([i, j, 7])
+    cf = O.configs(caps, tuner=np.array(tun), axis=axis)
+    want = ot.stack_counts(cf, rows)
+    got_runs, obj_runs = ctx.eval_grid(gt, kcfg(cf), K.Model(**MODEL_KW), rows)
+    assert_counts_equal(got_runs, want, cf)
+    os.environ["KARETO_K4_ACCESS"] = "1"
+    try:
+        got_acc, obj_acc = ctx.eval_grid(gt, kcfg(cf), K.Model(**MODEL_KW), rows)
+    finally:
+        os.environ.pop("KARETO_K4_ACCESS", None)
+    assert_counts_equal(got_acc, want, cf)
+    assert np.array_equal(obj_runs.view(np.uint64), obj_acc.view(np.uint64))
+    d, _ = ot.depth()
+    assert np.array_equal(gt.export(K.X_DEPTH).astype(np.int64), np.where(d < 0, U32, d))

@@ -1,0 +1,6 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 900 python bench.py --no-cpu-baseline --e2e-steps 0 > gpurun_out/s3_b4.log 2>&1; echo b4_rc=$?
+timeout 900 python bench.py --config 2 --no-cpu-baseline --e2e-steps 0 > gpurun_out/s3_b2a.log 2>&1; echo b2_rc=$?
+timeout 900 python bench.py --config 2 --no-cpu-baseline --e2e-steps 0 > gpurun_out/s3_b2b.log 2>&1; echo b2_rc=$?
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_replay_waves.py tests/test_gpu_queue.py tests/test_gpu_grid.py -x -q > gpurun_out/s3_tests.log 2>&1; echo t_rc=$?
+KARETO_DEBUG=1 timeout 900 python bench.py --config 3 --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 0 > gpurun_out/s3_b3.log 2>&1; echo b3_rc=$?

@@ -208,6 +208,10 @@ extern "C" void kareto_destroy(kareto_ctx *ctx) {
   flush_pass_times(ctx);
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
   if (ctx->nccl_comm && ctx->nccl) ctx->nccl->CommDestroy((ncclComm_t)ctx->nccl_comm);
+  if (ctx->h2d_scratch) {
+    cudaFreeAsync(ctx->h2d_scratch, ctx->stream);
+    ctx->h2d_scratch = nullptr;
+  }
   if (ctx->k2_scratch) {
     cudaFreeAsync(ctx->k2_scratch, ctx->stream);
     cudaStreamSynchronize(ctx->stream);

@@ -75,6 +75,11 @@ struct kareto_ctx {
   // freed by kareto_destroy)
   void *k2_scratch = nullptr;
   size_t k2_scratch_bytes = 0;
+  // staging buffer for host-resident tokens / block hashes (kept between loads: a fresh multi-GB
+  // pool allocation per load could not reuse the fragmented free blocks and mapped new memory,
+  // ~57 ms per config-4 load with host inputs)
+  void *h2d_scratch = nullptr;
+  size_t h2d_scratch_bytes = 0;
   bool k2_full = false;  // this load uses the full 32-bit K2 sort (after a bucket-table overflow)
 };
 

@@ -901,14 +901,24 @@ kareto_status upload_payload(kareto_ctx *ctx, const kareto_trace_desc *d, int64_
   }
   Pass ps(ctx, "h2d", 0, 0);
   const size_t n = (size_t)(hi - lo);
+  (void)tok;
+  (void)bh;
+  const size_t bytes = (tokens ? 4 : 8) * n;
+  if (ctx->h2d_scratch_bytes < bytes) {  // the per-context staging buffer, grown on demand
+    if (ctx->h2d_scratch) cudaFreeAsync(ctx->h2d_scratch, ctx->stream);
+    ctx->h2d_scratch = nullptr;
+    ctx->h2d_scratch_bytes = 0;
+    KMALLOC(ctx, ctx->h2d_scratch, bytes, ctx->stream);
+    ctx->h2d_scratch_bytes = bytes;
+  }
   if (tokens) {
-    KTRY(tok.alloc(ctx, n));
-    KCUDA(ctx, cudaMemcpyAsync(tok.p, d->tokens + lo, 4 * n, cudaMemcpyHostToDevice, ctx->stream));
-    *tok_base = tok.p - lo;
+    uint32_t *p = static_cast<uint32_t *>(ctx->h2d_scratch);
+    KCUDA(ctx, cudaMemcpyAsync(p, d->tokens + lo, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    *tok_base = p - lo;
   } else {
-    KTRY(bh.alloc(ctx, n));
-    KCUDA(ctx, cudaMemcpyAsync(bh.p, d->block_hash + lo, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
-    *bh_base = bh.p - lo;
+    uint64_t *p = static_cast<uint64_t *>(ctx->h2d_scratch);
+    KCUDA(ctx, cudaMemcpyAsync(p, d->block_hash + lo, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    *bh_base = p - lo;
   }
   return KARETO_OK;
 }

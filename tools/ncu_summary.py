@@ -18,7 +18,7 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 # kernel function -> bench pass name
 PASS = {"k_chain_hash": "K1_chain_hash", "k_link_tile": "K2_link_prev", "k_link_prev": "K2_link_prev",
         "k_bucket_assemble": "K2_bucket_assemble", "k_access_info": "K2_access_info", "k_sort_prep": "K2_sort_prep",
-        "k_hist_dD": "K4_hist_dD", "k_replay": "K6_replay", "k_expand": "K3_expand", "k_run_expand": "K3_expand",
+        "k_hist_dD": "K4_hist_dD", "k_hist_runs": "K4_hist_runs", "k_replay": "K6_replay", "k_expand": "K3_expand", "k_run_expand": "K3_expand",
         "k_bucket_link": "K2_bucket_link", "k_bucket_fixup": "K2_bucket_fixup", "k_bucket_bounds": "K2_bucket_bounds"}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 

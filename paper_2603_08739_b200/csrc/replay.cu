@@ -781,8 +781,10 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
         return U * (1 + 8) + (eheap || glist ? U * 4 : 0) + (lfu ? U * 4 + 3 * 8 * (FM + NW + NSW) : 0) +
                (eheap ? U * 4 + 8 * es : 0) + (glist ? U * 8 + 8 * (uint64_t)G : 0);
       };
-      // relative time of one pass over the trace per class (measured on the config-3 twin)
-      const double pass_cost[5] = {1.0, 2.0, 1.2, 2.65, 1.9};
+      // relative time of one pass over the trace per class, measured on the config-3 twin after the
+      // list / LFU classes dropped their last-access array (seconds per wave, KARETO_DEBUG: list
+      // 1.8, FIFO + heap 5.6, LFU 3.3, LFU + heap 8.2, LRU + group lists 4.0)
+      const double pass_cost[5] = {1.0, 3.1, 1.85, 4.5, 2.2};
       double budget = 0;
       KTRY(wave_budget(ctx, 0.8, &budget));
       // every non-empty class first gets one configuration's footprint (so no class is starved

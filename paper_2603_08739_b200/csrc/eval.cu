@@ -441,13 +441,13 @@ static void shard_range(int64_t n, int rank, int world, int64_t &lo, int64_t &hi
 // Cost-weighted contiguous shards: a stack-path configuration costs O(1) on top of
 // the trace passes every rank runs anyway (weight 1); a K6 replay configuration costs a pass over
 // the trace, scaled by its class's relative pass time (replay.cu: list 1.0, FIFO/list + expiry
-// heap 3.1, LFU 1.85, LFU + expiry heap 4.5, LRU + group expiry lists 2.2) -- weight 10^6 x that.
+// wheel 2.2, LFU 1.95, LFU + expiry wheel 3.2, LRU + group expiry lists 2.27) -- weight 10^6 x that.
 // bounds[r] = the largest i with world * prefix(i) <= r * total, so unit weights give exactly
 // shard_range's floor(n r / world).  Every rank computes the same bounds from the same list.
 static void shard_bounds(const kareto_config *cfg, int64_t n, const uint32_t *rows, int n_tuner, int G, int world,
                          int64_t *bounds) {
   const uint64_t stack_w = 1;
-  const uint64_t class_w[5] = {1000000, 3100000, 1850000, 4500000, 2200000};
+  const uint64_t class_w[5] = {1000000, 2200000, 1950000, 3200000, 2270000};
   std::vector<uint64_t> pre((size_t)n + 1, 0);
   for (int64_t i = 0; i < n; i++) {
     const kareto_config &c = cfg[i];

@@ -45,10 +45,12 @@ struct RState {
   uint64_t *occ[3];    // LFU: [w*W+c] bucket occupancy bitmap (bit f) per tier
   uint64_t *occ2[3];   // LFU: [w2*W+c] summary: bit w set iff occ word w is non-zero
   uint32_t NW, NSW;    // LFU: bitmap words, summary words
-  uint32_t *epos;      // expiry: [b*W+c] slot in the expiry heap (kNone = absent)
-  uint2 *elink;        // LRU expiry lists: [b*W+c] (newer, older) neighbour in its group's list
+  uint2 *elink;        // expiry: [b*W+c] neighbours in the block's expiry list (LRU: its group's
+                       // list, newer / older; FIFO / LFU: its wheel bucket, prev / next, where prev
+                       // = kHeadMark | bucket for a bucket's first block, kNone = in no bucket)
   uint32_t *eh, *et;   // LRU expiry lists: [g*W+c] newest / oldest disk block of group g
-  uint64_t *ekey;      // expiry: [slot*W+c] (min(lt + tau_g, 2^32-1) << 32 | block)
+  uint32_t *ebh;       // FIFO / LFU expiry wheel: [k*W+c] first block of bucket k
+  uint32_t NB, BSH, a_last;  // wheel: NB buckets of 2^BSH ms covering expiry times <= a_last
   const uint16_t *gblk;
   uint64_t W;
 };
@@ -76,7 +78,6 @@ struct Rep {
   uint64_t cap[3];
   uint64_t size[3];
   uint32_t head[3], tail[3], tail2[3];
-  uint32_t esize;
   uint32_t seq;
   bool ttl_mode, lru;
   const uint32_t *tau;
@@ -222,51 +223,69 @@ struct Rep {
     return empty;
   }
 
-  // ------------------------------------------------------------ expiry heap (4-ary, packed)
-  __device__ void e_down(uint64_t i, uint64_t key) {
-    const uint64_t n = esize;
-    for (;;) {
-      const uint64_t c0 = 4 * i + 1;
-      if (c0 >= n) break;
-      uint64_t ck[4];
-#pragma unroll
-      for (int q = 0; q < 4; q++) ck[q] = c0 + q < n ? v.ekey[(c0 + q) * v.W + c] : ~0ull;
-      uint64_t mk = ck[0];
-      uint32_t mq = 0;
-#pragma unroll
-      for (int q = 1; q < 4; q++)
-        if (ck[q] < mk) { mk = ck[q]; mq = q; }
-      if (mk >= key) break;
-      v.ekey[i * v.W + c] = mk;
-      v.epos[at((uint32_t)mk)] = (uint32_t)i;
-      i = c0 + mq;
+  // ------------------------------------------------------------ expiry wheel (FIFO / LFU)
+  // A disk block with a finite TTL expires at e = lt + tau_g (ms).  Blocks with e <= a_last sit in
+  // bucket e >> BSH of a per-configuration wheel (a doubly-linked list per bucket); later ones
+  // never expire within the trace.  PURGE(a) empties every bucket below a >> BSH (all their
+  // blocks have e < a) and scans the boundary bucket a >> BSH with exact keys.  Buckets below the
+  // current boundary pcur are empty; a block inserted with such an e (it expired before it was
+  // demoted) goes into the boundary bucket.  O(1) insert / remove, unlike a heap's log-depth
+  // chain of dependent loads.  The order of removals inside one PURGE does not change the state.
+  uint32_t pcur = 0;
+  static constexpr uint32_t kHeadMark = 0x80000000u;
+  __device__ __forceinline__ void w_push(uint32_t b, uint32_t k) {
+    const uint64_t hi = (uint64_t)k * v.W + c;
+    const uint32_t h = v.ebh[hi];
+    v.elink[at(b)] = make_uint2(kHeadMark | k, h);
+    if (h != kNone) v.elink[at(h)].x = b;
+    v.ebh[hi] = b;
+  }
+  __device__ __forceinline__ void w_unlink(uint32_t b) {
+    const uint2 lk = v.elink[at(b)];
+    if (lk.x == kNone) return;
+    if (lk.x & kHeadMark) v.ebh[(uint64_t)(lk.x & ~kHeadMark) * v.W + c] = lk.y;
+    else v.elink[at(lk.x)].y = lk.y;
+    if (lk.y != kNone) v.elink[at(lk.y)].x = lk.x;
+  }
+  __device__ __forceinline__ void w_insert(uint32_t b, uint32_t tg) {
+    const uint64_t e = (uint64_t)v.lt[at(b)] + tg;
+    if (e > v.a_last) {  // never expires within the trace
+      v.elink[at(b)] = make_uint2(kNone, kNone);
+      return;
     }
-    v.ekey[i * v.W + c] = key;
-    v.epos[at((uint32_t)key)] = (uint32_t)i;
+    const uint32_t k = (uint32_t)(e >> v.BSH);
+    w_push(b, k < pcur ? pcur : k);
   }
-  __device__ void e_up(uint64_t i, uint64_t key) {
-    while (i > 0) {
-      const uint64_t p = (i - 1) / 4;
-      const uint64_t pk = v.ekey[p * v.W + c];
-      if (pk <= key) break;
-      v.ekey[i * v.W + c] = pk;
-      v.epos[at((uint32_t)pk)] = (uint32_t)i;
-      i = p;
+  // drop disk block x (expired): out of the disk tier (the wheel is handled by the caller)
+  __device__ __forceinline__ void w_drop(uint32_t x) {
+    if (LFU) {
+      b_unlink<2>(v.link[at(x)], v.freq[at(x)], true);
+    } else {
+      l_unlink<2>(v.link[at(x)]);
+      size[2]--;
     }
-    v.ekey[i * v.W + c] = key;
-    v.epos[at((uint32_t)key)] = (uint32_t)i;
+    v.tier[at(x)] = T_NONE;
   }
-  __device__ void e_remove_at(uint64_t i, uint32_t b) {
-    const uint64_t last = --esize;
-    v.epos[at(b)] = kNone;
-    if (i == last) return;
-    const uint64_t lk = v.ekey[last * v.W + c];
-    const uint64_t ki = v.ekey[i * v.W + c];
-    if (lk < ki) e_up(i, lk); else e_down(i, lk);
-  }
-  __device__ __forceinline__ void e_remove(uint32_t b) {
-    const uint32_t i = v.epos[at(b)];
-    if (i != kNone) e_remove_at(i, b);
+  __device__ void w_purge(uint32_t a) {
+    const uint32_t ka = a >> v.BSH;  // a <= a_last, so ka < NB
+    for (; pcur < ka; pcur++) {       // whole buckets: every e < (pcur + 1) << BSH <= a
+      const uint64_t hi = (uint64_t)pcur * v.W + c;
+      for (uint32_t x = v.ebh[hi]; x != kNone;) {
+        const uint32_t nxt = v.elink[at(x)].y;
+        w_drop(x);
+        x = nxt;
+      }
+      v.ebh[hi] = kNone;
+    }
+    const uint64_t hi = (uint64_t)ka * v.W + c;  // boundary bucket: exact keys
+    for (uint32_t x = v.ebh[hi]; x != kNone;) {
+      const uint32_t nxt = v.elink[at(x)].y;
+      if ((uint64_t)v.lt[at(x)] + tau[v.gblk[x]] < a) {
+        w_unlink(x);
+        w_drop(x);
+      }
+      x = nxt;
+    }
   }
 
   // ------------------------------------------------------------ tiers (t = 0, 1, 2)
@@ -289,8 +308,7 @@ struct Rep {
       const uint32_t tg = tau[g];
       if (tg != KARETO_TTL_INF) {
         if (EXPM == 1) {
-          const uint64_t e = (uint64_t)v.lt[at(b)] + tg;
-          e_up(esize++, ((e < 0xFFFFFFFFull ? e : 0xFFFFFFFFull) << 32) | b);
+          w_insert(b, tg);
         } else {  // newest end of the group's list
           const uint64_t gi = (uint64_t)g * v.W + c;
           const uint32_t h = v.eh[gi];
@@ -321,7 +339,7 @@ struct Rep {
       l_unlink<t>(lk);
       size[t]--;
     }
-    if (EXPM == 1 && t == 2) e_remove(b);
+    if (EXPM == 1 && t == 2 && tau[v.gblk[b]] != KARETO_TTL_INF) w_unlink(b);
     if (EXPM == 2 && t == 2) ge_remove(b);
     return key;
   }
@@ -341,7 +359,7 @@ struct Rep {
       x = l_pop_tail<t>();
       size[t]--;
     }
-    if (EXPM == 1 && t == 2) e_remove(x);
+    if (EXPM == 1 && t == 2 && tau[v.gblk[x]] != KARETO_TTL_INF) w_unlink(x);
     if (EXPM == 2 && t == 2) ge_remove(x);
     evict[t] += 1;
     const bool next = ttl_mode ? (t == 0) : (t < 2);
@@ -415,7 +433,7 @@ struct Rep {
       hit[t] = evict[t] = 0;
     }
     miss = disk_writes = hit_pos_sum = bytetime = after_hole = 0;
-    esize = 0;
+    pcur = 0;
     seq = 0;
     uint32_t s0 = T.s[0];
     for (uint32_t r = 0; r < T.R; r++) {
@@ -428,21 +446,7 @@ struct Rep {
       }
       const uint32_t tg = tau[T.grp[r]];
       // 1 PURGE (CAPACITY mode): disk blocks whose expiry key is below a (a - lt > tau_g)
-      if (EXPM == 1) {
-        while (esize > 0) {
-          const uint64_t top = v.ekey[c];
-          if ((uint32_t)(top >> 32) >= a) break;
-          const uint32_t x = (uint32_t)top;
-          e_remove_at(0, x);
-          if (LFU) {
-            b_unlink<2>(v.link[at(x)], v.freq[at(x)], true);
-          } else {
-            l_unlink<2>(v.link[at(x)]);
-            size[2]--;
-          }
-          v.tier[at(x)] = T_NONE;
-        }
-      }
+      if (EXPM == 1 && size[2] > 0) w_purge(a);
       if (EXPM == 2 && size[2] > 0) {  // each group's expired blocks sit at its list's old end
         for (int g = 0; g < G; g++) {
           const uint32_t tgg = tau[g];
@@ -764,6 +768,12 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
   DBuf<kareto_config> dcfg;
   KTRY(dcfg.alloc(ctx, n));
   KCUDA(ctx, cudaMemcpyAsync(dcfg.p, cfg_host, sizeof(kareto_config) * n, cudaMemcpyHostToDevice, st));
+  // FIFO / LFU expiry wheel: buckets of 2^BSH ms over [0, span], at most max(256, U/4) of them (so
+  // the heads cost <= 1 B per block and configuration)
+  const uint32_t a_last = (uint32_t)tr->span_ms;
+  uint32_t BSH = 0;
+  while (((uint64_t)(a_last >> BSH) + 1) > std::max<uint64_t>(256, U / 4)) BSH++;
+  const uint64_t NBK = (uint64_t)(a_last >> BSH) + 1;
   // Concurrent classes (no f3 queue): a wave is one pass over the trace whatever its width (the
   // kernel is latency-bound at these occupancies), so sequential classes waste the unused part
   // of each class's last wave.  Instead every class runs its waves on its own stream with a share
@@ -775,16 +785,15 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
     if (nonempty >= 2) {
       const uint64_t FM = (uint64_t)tr->R + 2;
       const uint64_t NW = (FM + 63) / 64, NSW = (NW + 63) / 64;
-      const uint64_t es = U + 1;
       auto per_cfg_of = [&](int q) {
         const bool lfu = q == 2 || q == 3, eheap = q == 1 || q == 3, glist = q == 4;
-        return U * (1 + 8) + (eheap || glist ? U * 4 : 0) + (lfu ? U * 4 + 3 * 8 * (FM + NW + NSW) : 0) +
-               (eheap ? U * 4 + 8 * es : 0) + (glist ? U * 8 + 8 * (uint64_t)G : 0);
+        return U * (1 + 8) + (eheap || glist ? U * (4 + 8) : 0) + (lfu ? U * 4 + 3 * 8 * (FM + NW + NSW) : 0) +
+               (eheap ? 4 * NBK : 0) + (glist ? 8 * (uint64_t)G : 0);
       };
-      // relative time of one pass over the trace per class, measured on the config-3 twin after the
-      // list / LFU classes dropped their last-access array (seconds per wave, KARETO_DEBUG: list
-      // 1.8, FIFO + heap 5.6, LFU 3.3, LFU + heap 8.2, LRU + group lists 4.0)
-      const double pass_cost[5] = {1.0, 3.1, 1.85, 4.5, 2.2};
+      // relative time of one pass over the trace per class, measured on the config-3 twin (seconds
+      // per wave, KARETO_DEBUG, round 2: list 1.85, FIFO + expiry wheel 4.1, LFU 3.6, LFU + expiry
+      // wheel 5.95, LRU + group lists 4.2)
+      const double pass_cost[5] = {1.0, 2.2, 1.95, 3.2, 2.27};
       double budget = 0;
       KTRY(wave_budget(ctx, 0.8, &budget));
       // every non-empty class first gets one configuration's footprint (so no class is starved
@@ -798,9 +807,9 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
       if (minfoot <= budget) {
       struct ClassState {
         DBuf<uint8_t> tier;
-        DBuf<uint32_t> lt, freq, bht, epos, didx, eht;
+        DBuf<uint32_t> lt, freq, bht, ebh, didx, eht;
         DBuf<uint2> link, elink;
-        DBuf<uint64_t> occ, ekey;
+        DBuf<uint64_t> occ;
         RState v{};
         uint64_t W = 0;
         cudaStream_t s = nullptr;
@@ -835,8 +844,9 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
         if (lfu) {
           KTRY(c.freq.alloc(ctx, U * W)); KTRY(c.bht.alloc(ctx, 6 * FM * W)); KTRY(c.occ.alloc(ctx, 3 * (NW + NSW) * W));
         }
-        if (eheap) { KTRY(c.epos.alloc(ctx, U * W)); KTRY(c.ekey.alloc(ctx, es * W)); }
-        if (glist) { KTRY(c.elink.alloc(ctx, U * W)); KTRY(c.eht.alloc(ctx, 2 * (size_t)G * W)); }
+        if (eheap || glist) KTRY(c.elink.alloc(ctx, U * W));
+        if (eheap) KTRY(c.ebh.alloc(ctx, NBK * W));
+        if (glist) KTRY(c.eht.alloc(ctx, 2 * (size_t)G * W));
         KTRY(c.didx.alloc(ctx, ix.size()));
         KCUDA(ctx, cudaMemcpyAsync(c.didx.p, ix.data(), 4 * ix.size(), cudaMemcpyHostToDevice, st));
         RState &v = c.v;
@@ -852,7 +862,7 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
           v.NW = (uint32_t)NW;
           v.NSW = (uint32_t)NSW;
         }
-        v.epos = c.epos.p; v.ekey = c.ekey.p;
+        v.ebh = c.ebh.p; v.NB = (uint32_t)NBK; v.BSH = BSH; v.a_last = a_last;
         v.elink = c.elink.p;
         v.eh = c.eht.p;
         v.et = c.eht.p + (size_t)G * W;
@@ -884,7 +894,7 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
               cudaMemsetAsync(c.bht.p, 0xFF, 4 * 6 * FM * W, c.s);
               cudaMemsetAsync(c.occ.p, 0, 8 * 3 * (NW + NSW) * W, c.s);
             }
-            if (eheap) cudaMemsetAsync(c.epos.p, 0xFF, 4 * U * W, c.s);
+            if (eheap) cudaMemsetAsync(c.ebh.p, 0xFF, 4 * NBK * W, c.s);
             if (glist) cudaMemsetAsync(c.eht.p, 0xFF, 4 * 2 * (size_t)G * W, c.s);
             const unsigned grid = (unsigned)((nw + 63) / 64);
             const uint32_t *wi = c.didx.p + w0;
@@ -940,9 +950,8 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
     // LFU frequency buckets: a resident block's frequency is at most its accesses (<= R)
     const uint64_t FM = (uint64_t)tr->R + 2;
     const uint64_t NW = (FM + 63) / 64, NSW = (NW + 63) / 64;
-    const uint64_t es = U + 1;
-    uint64_t per_cfg = U * (1 + 8) + (eheap || glist ? U * 4 : 0) + (lfu ? U * 4 + 3 * 8 * (FM + NW + NSW) : 0) +
-                       (eheap ? U * 4 + 8 * es : 0) + (glist ? U * 8 + 8 * (uint64_t)G : 0);
+    uint64_t per_cfg = U * (1 + 8) + (eheap || glist ? U * (4 + 8) : 0) + (lfu ? U * 4 + 3 * 8 * (FM + NW + NSW) : 0) +
+                       (eheap ? 4 * NBK : 0) + (glist ? 8 * (uint64_t)G : 0);
     if (Qm) per_cfg += 16 * (uint64_t)R + 8 * (uint64_t)qarg.model->instances + 64;  // f3: TTFT rows + queue
     // 80% of free device memory per wave (60% left the LRU expiry-list class of the config-3 twin
     // in two waves, i.e. two passes over the trace: 7.1 s -> 4.7 s at 80%)
@@ -956,17 +965,18 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
     const uint64_t nwaves = (ix.size() + W - 1) / W;
     W = (ix.size() + nwaves - 1) / nwaves;
     DBuf<uint8_t> tier;
-    DBuf<uint32_t> lt, freq, bht, epos, didx;
+    DBuf<uint32_t> lt, freq, bht, ebh, didx;
     DBuf<uint2> link, elink;
-    DBuf<uint64_t> occ, ekey;
+    DBuf<uint64_t> occ;
     DBuf<uint32_t> eht;
     KTRY(tier.alloc(ctx, U * W)); KTRY(link.alloc(ctx, U * W));
     if (eheap || glist) KTRY(lt.alloc(ctx, U * W));
     if (lfu) {
       KTRY(freq.alloc(ctx, U * W)); KTRY(bht.alloc(ctx, 6 * FM * W)); KTRY(occ.alloc(ctx, 3 * (NW + NSW) * W));
     }
-    if (eheap) { KTRY(epos.alloc(ctx, U * W)); KTRY(ekey.alloc(ctx, es * W)); }
-    if (glist) { KTRY(elink.alloc(ctx, U * W)); KTRY(eht.alloc(ctx, 2 * (size_t)G * W)); }
+    if (eheap || glist) KTRY(elink.alloc(ctx, U * W));
+    if (eheap) KTRY(ebh.alloc(ctx, NBK * W));
+    if (glist) KTRY(eht.alloc(ctx, 2 * (size_t)G * W));
     KTRY(didx.alloc(ctx, ix.size()));
     KCUDA(ctx, cudaMemcpyAsync(didx.p, ix.data(), 4 * ix.size(), cudaMemcpyHostToDevice, st));
     RState v{};
@@ -982,7 +992,7 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
       v.NW = (uint32_t)NW;
       v.NSW = (uint32_t)NSW;
     }
-    v.epos = epos.p; v.ekey = ekey.p;
+    v.ebh = ebh.p; v.NB = (uint32_t)NBK; v.BSH = BSH; v.a_last = a_last;
     v.elink = elink.p;
     v.eh = eht.p;
     v.et = eht.p + (size_t)G * W;
@@ -1006,7 +1016,7 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
         KCUDA(ctx, cudaMemsetAsync(bht.p, 0xFF, 4 * 6 * FM * W, st));
         KCUDA(ctx, cudaMemsetAsync(occ.p, 0, 8 * 3 * (NW + NSW) * W, st));
       }
-      if (eheap) KCUDA(ctx, cudaMemsetAsync(epos.p, 0xFF, 4 * U * W, st));
+      if (eheap) KCUDA(ctx, cudaMemsetAsync(ebh.p, 0xFF, 4 * NBK * W, st));
       if (glist) KCUDA(ctx, cudaMemsetAsync(eht.p, 0xFF, 4 * 2 * (size_t)G * W, st));
       static const char *kPassName[5] = {"K6_replay_list", "K6_replay_list_exp", "K6_replay_lfu", "K6_replay_lfu_exp",
                                          "K6_replay_lru_exp"};

@@ -232,6 +232,8 @@ struct Rep {
   // demoted) goes into the boundary bucket.  O(1) insert / remove, unlike a heap's log-depth
   // chain of dependent loads.  The order of removals inside one PURGE does not change the state.
   uint32_t pcur = 0;
+  uint64_t gmin = ~0ull;  // expiry classes: a lower bound of the earliest disk expiry (PURGE skipped
+                          // while gmin >= a: removals only raise the true minimum)
   static constexpr uint32_t kHeadMark = 0x80000000u;
   __device__ __forceinline__ void w_push(uint32_t b, uint32_t k) {
     const uint64_t hi = (uint64_t)k * v.W + c;
@@ -255,6 +257,7 @@ struct Rep {
     }
     const uint32_t k = (uint32_t)(e >> v.BSH);
     w_push(b, k < pcur ? pcur : k);
+    if (e < gmin) gmin = e;
   }
   // drop disk block x (expired): out of the disk tier (the wheel is handled by the caller)
   __device__ __forceinline__ void w_drop(uint32_t x) {
@@ -278,11 +281,15 @@ struct Rep {
       v.ebh[hi] = kNone;
     }
     const uint64_t hi = (uint64_t)ka * v.W + c;  // boundary bucket: exact keys
+    gmin = (uint64_t)(ka + 1) << v.BSH;           // every later bucket expires at or after this
     for (uint32_t x = v.ebh[hi]; x != kNone;) {
       const uint32_t nxt = v.elink[at(x)].y;
-      if ((uint64_t)v.lt[at(x)] + tau[v.gblk[x]] < a) {
+      const uint64_t e = (uint64_t)v.lt[at(x)] + tau[v.gblk[x]];
+      if (e < a) {
         w_unlink(x);
         w_drop(x);
+      } else if (e < gmin) {
+        gmin = e;
       }
       x = nxt;
     }
@@ -310,6 +317,8 @@ struct Rep {
         if (EXPM == 1) {
           w_insert(b, tg);
         } else {  // newest end of the group's list
+          const uint64_t e = (uint64_t)v.lt[at(b)] + tg;
+          if (e < gmin) gmin = e;  // keeps gmin a lower bound of every group's oldest expiry
           const uint64_t gi = (uint64_t)g * v.W + c;
           const uint32_t h = v.eh[gi];
           v.elink[at(b)] = make_uint2(kNone, h);
@@ -434,6 +443,7 @@ struct Rep {
     }
     miss = disk_writes = hit_pos_sum = bytetime = after_hole = 0;
     pcur = 0;
+    gmin = ~0ull;
     seq = 0;
     uint32_t s0 = T.s[0];
     for (uint32_t r = 0; r < T.R; r++) {
@@ -446,8 +456,12 @@ struct Rep {
       }
       const uint32_t tg = tau[T.grp[r]];
       // 1 PURGE (CAPACITY mode): disk blocks whose expiry key is below a (a - lt > tau_g)
-      if (EXPM == 1 && size[2] > 0) w_purge(a);
-      if (EXPM == 2 && size[2] > 0) {  // each group's expired blocks sit at its list's old end
+      if (EXPM == 1 && size[2] > 0 && gmin < a) w_purge(a);
+      // each group's expired blocks sit at its list's old end; gmin (a lower bound of the earliest
+      // expiry over the groups: removals only raise the true minimum) skips the G list probes
+      // while nothing can have expired, and is recomputed exactly after a scan
+      if (EXPM == 2 && size[2] > 0 && gmin < a) {
+        gmin = ~0ull;
         for (int g = 0; g < G; g++) {
           const uint32_t tgg = tau[g];
           if (tgg == KARETO_TTL_INF) continue;
@@ -460,6 +474,11 @@ struct Rep {
             l_unlink<2>(v.link[at(x)]);
             size[2]--;
             v.tier[at(x)] = T_NONE;
+          }
+          const uint32_t y = v.et[gi];
+          if (y != kNone) {
+            const uint64_t e = (uint64_t)v.lt[at(y)] + tgg;
+            if (e < gmin) gmin = e;
           }
         }
       }

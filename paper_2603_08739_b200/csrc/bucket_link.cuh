@@ -39,10 +39,14 @@ constexpr uint32_t BL_CHUNK = 4096;
 // cursor atomics spread over 2^sl times more addresses (fewer same-address collisions at the L2);
 // cursors are spaced cstride words apart.  KARETO_BL_SUB / KARETO_BL_CSTRIDE override (measurements).
 constexpr uint32_t BL_SUB_LOG2 = 2, BL_CSTRIDE = 1;
+// raw cursor atomic of position p (the in-bucket slot is bl_off(p) + this value; the add is kept
+// apart so that the atomic's latency overlaps the next batch instead of stalling the issuing one)
 __device__ __forceinline__ uint32_t bl_slot(unsigned *cursor, uint32_t p, uint32_t sl, uint32_t cstride) {
-  const uint32_t sub = p & ((1u << sl) - 1u);
-  const uint32_t ci = ((p >> 15) << sl) | sub;
-  return (sub << (15 - sl)) + atomicAdd(&cursor[(size_t)ci * cstride], 1u);
+  const uint32_t ci = ((p >> 15) << sl) | (p & ((1u << sl) - 1u));
+  return atomicAdd(&cursor[(size_t)ci * cstride], 1u);
+}
+__device__ __forceinline__ uint64_t bl_pair_at(uint32_t p, uint32_t sl, uint32_t slot) {
+  return ((uint64_t)(p >> 15) << 15) + ((p & ((1u << sl) - 1u)) << (15 - sl)) + slot;
 }
 constexpr uint32_t BL_EMPTY = 0xFFFFFFFFu, BL_CLAIM = 0xFFFFFFFEu;
 struct BLTable {
@@ -75,6 +79,13 @@ __global__ void k_bucket_bounds(const uint32_t *__restrict__ ks, uint64_t N, uin
       bp = b;
     }
   }
+}
+
+// chunk -> bucket table (one thread per bucket writes its chunks)
+__global__ void k_chunk_bucket(const uint32_t *__restrict__ cstart, uint16_t *__restrict__ cbucket) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < BL_NB)
+    for (uint32_t w = cstart[b]; w < cstart[b + 1]; w++) cbucket[w] = (uint16_t)b;
 }
 
 // chunks per bucket (>= 1), for the chunk prefix cstart
@@ -125,7 +136,7 @@ __device__ __forceinline__ uint32_t bl_claim(BLTable &T, uint64_t m, uint32_t sl
 // (lst_*); counts rec_n[2w] / rec_n[2w + 1] for chunk w.
 __global__ void __launch_bounds__(BL_WARPS * 32) k_bucket_link(
     const uint32_t *__restrict__ ks, const uint64_t *__restrict__ vs, const uint32_t *__restrict__ bstart,
-    const uint32_t *__restrict__ cstart, unsigned *__restrict__ next, unsigned *__restrict__ cursor,
+    const uint32_t *__restrict__ cstart, const uint16_t *__restrict__ cbucket, unsigned *__restrict__ next, unsigned *__restrict__ cursor,
     uint2 *__restrict__ pairs, uint64_t *__restrict__ rec_m, uint32_t *__restrict__ rec_p, uint64_t *__restrict__ lst_m,
     uint32_t *__restrict__ lst_p, uint32_t *__restrict__ rec_n, unsigned *__restrict__ overflow, uint32_t limit,
     uint32_t sl, uint32_t cstride) {
@@ -142,12 +153,7 @@ __global__ void __launch_bounds__(BL_WARPS * 32) k_bucket_link(
     if (lane == 0) w = atomicAdd(next, 1u);
     w = __shfl_sync(0xFFFFFFFFu, w, 0);
     if (w >= n_chunks) break;
-    int lo = 0, hi = BL_NB - 1;  // bucket of chunk w: the last b with cstart[b] <= w
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (cstart[mid] <= w) lo = mid; else hi = mid - 1;
-    }
-    const int b = lo;
+    const int b = (int)cbucket[w];  // bucket of chunk w (the last b with cstart[b] <= w)
     const uint32_t c = w - cstart[b], nc = cstart[b + 1] - cstart[b];
     const uint32_t s0 = bstart[b] + c * BL_CHUNK;
     const uint32_t s1 = min(bstart[b + 1], s0 + BL_CHUNK);
@@ -229,7 +235,7 @@ __global__ void __launch_bounds__(BL_WARPS * 32) k_bucket_link(
       }
 #pragma unroll
       for (int k = 0; k < BL_BATCH; k++)  // the previous batch's pairs (its atomics have returned)
-        if (spos[k] != BL_EMPTY) pairs[((uint64_t)(spos[k] >> 15) << 15) + sat[k]] = make_uint2(spos[k], sprv[k]);
+        if (spos[k] != BL_EMPTY) pairs[bl_pair_at(spos[k], sl, sat[k])] = make_uint2(spos[k], sprv[k]);
 #pragma unroll
       for (int k = 0; k < BL_BATCH; k++) {
         sat[k] = pos[k] != BL_EMPTY ? bl_slot(cursor, pos[k], sl, cstride) : 0u;
@@ -241,7 +247,7 @@ __global__ void __launch_bounds__(BL_WARPS * 32) k_bucket_link(
     }
 #pragma unroll
     for (int k = 0; k < BL_BATCH; k++)
-      if (spos[k] != BL_EMPTY) pairs[((uint64_t)(spos[k] >> 15) << 15) + sat[k]] = make_uint2(spos[k], sprv[k]);
+      if (spos[k] != BL_EMPTY) pairs[bl_pair_at(spos[k], sl, sat[k])] = make_uint2(spos[k], sprv[k]);
     if (multi) {
       const uint32_t nu = degraded ? 0u : T.nused;  // a degraded chunk leaves no last positions
       for (uint32_t q = lane; q < nu; q += 32) {
@@ -293,7 +299,7 @@ __global__ void __launch_bounds__(BL_WARPS * 32) k_bucket_fixup(
           bool isnew;
           const uint32_t prv = degraded ? kNone : bl_find(T, m, slot, isnew);
           const uint32_t at = bl_slot(cursor, p, sl, cstride);
-          pairs[((uint64_t)(p >> 15) << 15) + at] = make_uint2(p, prv);
+          pairs[bl_pair_at(p, sl, at)] = make_uint2(p, prv);
         }
       }
       __syncwarp();

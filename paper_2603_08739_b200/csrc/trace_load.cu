@@ -991,6 +991,7 @@ static kareto_status bucket_link(kareto_ctx *ctx, DBuf<uint32_t> &k32, DBuf<uint
   KTRY(cub_call(ctx, tmp, [&](void *t, size_t &b) {
     return cub::DeviceScan::ExclusiveSum(t, b, nch.p, cstart.p, BL_NB + 1, st);
   }));
+  DBuf<uint16_t> cbucket;  // chunk -> bucket (BL_BITS = 16)
   // no host round trip: the kernels read the chunk count from cstart[2^16]; rec_n is sized for
   // the most chunks N accesses can form
   const uint64_t max_chunks = (uint64_t)BL_NB + N / BL_CHUNK + 1;
@@ -1006,6 +1007,9 @@ static kareto_status bucket_link(kareto_ctx *ctx, DBuf<uint32_t> &k32, DBuf<uint
   if (const char *e = getenv("KARETO_BL_CSTRIDE")) cstride = (uint32_t)atoi(e) > 0 ? (uint32_t)atoi(e) : 1u;
   KTRY(cursor.alloc(ctx, (nbk << sl) * cstride)); KTRY(cursor.zero());
   KTRY(rec_n.alloc(ctx, 2 * max_chunks));
+  KTRY(cbucket.alloc(ctx, max_chunks));
+  k_chunk_bucket<<<BL_NB / 256, 256, 0, st>>>(cstart.p, cbucket.p);
+  ctx->own_launches++;
   uint64_t *rec_m = v64.p, *lst_m = nullptr;  // the unsorted input buffers are free now
   uint32_t *rec_p = k32.p, *lst_p = nullptr;
   const size_t npairs = (size_t)nbk << PBT;  // padded: a partial last bucket fills sub-region prefixes
@@ -1031,7 +1035,7 @@ static kareto_status bucket_link(kareto_ctx *ctx, DBuf<uint32_t> &k32, DBuf<uint
   {
     Pass ps(ctx, "K2_bucket_link", 1, 1);
     cudaFuncSetAttribute(k_bucket_link, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_bucket_link<<<sms, BL_WARPS * 32, smem, st>>>(k32s.p, v64s.p, bstart.p, cstart.p, ctr.p, cursor.p,
+    k_bucket_link<<<sms, BL_WARPS * 32, smem, st>>>(k32s.p, v64s.p, bstart.p, cstart.p, cbucket.p, ctr.p, cursor.p,
                                                      pairs, rec_m, rec_p, lst_m, lst_p, rec_n.p, ovf_dev, limit, sl, cstride);
   }
   hm.mark(st, "link");

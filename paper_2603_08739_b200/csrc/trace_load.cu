@@ -926,10 +926,12 @@ kareto_status upload_payload(kareto_ctx *ctx, const kareto_trace_desc *d, int64_
 kareto_status chain_hash(kareto_ctx *ctx, const kareto_trace_desc *d, const kareto_trace *tr, const Ingest &in,
                          const uint32_t *tok_base, const uint64_t *bh_base, int64_t tok_end, int64_t r0, int64_t r1,
                          uint64_t *hash_out, uint32_t *req_out, SortedHashes *prep) {
-  uint32_t se[2];
-  KCUDA(ctx, cudaMemcpyAsync(&se[0], tr->s + r0, 4, cudaMemcpyDeviceToHost, ctx->stream));
-  KCUDA(ctx, cudaMemcpyAsync(&se[1], tr->s + r1, 4, cudaMemcpyDeviceToHost, ctx->stream));
-  KCUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  uint32_t se[2] = {0, (uint32_t)tr->N};
+  if (!(r0 == 0 && r1 == tr->R && !tr->sharded)) {  // a whole trace's range is [0, N): no round trip
+    KCUDA(ctx, cudaMemcpyAsync(&se[0], tr->s + r0, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    KCUDA(ctx, cudaMemcpyAsync(&se[1], tr->s + r1, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    KCUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
   const uint64_t n = (uint64_t)(se[1] - se[0]);
   if (n == 0) return KARETO_OK;
   const int sms = ctx->num_sms;

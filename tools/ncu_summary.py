@@ -40,14 +40,19 @@ def main(argv):
             vals.append(f"{r[i]} {units[i]}".strip())
         print(f"| {name} | " + " | ".join(vals) + " |")
         base = name.replace("void ", "").split("<")[0].split("::")[-1].strip()
-        if base in PASS and "dram__bytes_read.sum" in idx:
+        if ("K2Sort" in r[kn] or "kareto::" in r[kn]) and base in ("DeviceRadixSortOnesweepKernel", "DeviceRadixSortHistogramKernel"):
+            base = "sort_" + base  # K2's bucket sort: one histogram + two onesweep passes per load
+        if (base in PASS or base.startswith("sort_")) and "dram__bytes_read.sum" in idx:
             rb = float(r[idx["dram__bytes_read.sum"]].replace(",", "")) * SCALE.get(units[idx["dram__bytes_read.sum"]], 1)
             wb = float(r[idx["dram__bytes_write.sum"]].replace(",", "")) * SCALE.get(units[idx["dram__bytes_write.sum"]], 1)
-            traffic.setdefault(PASS[base], []).append(rb + wb)
+            traffic.setdefault(PASS.get(base, base), []).append(rb + wb)
     if "--traffic-json" in argv:
         path = argv[argv.index("--traffic-json") + 1]
         wl = argv[argv.index("--workload") + 1] if "--workload" in argv else ""
-        res = {k: sum(v) / len(v) for k, v in traffic.items()}
+        res = {k: sum(v) / len(v) for k, v in traffic.items() if not k.startswith("sort_")}
+        h_, o_ = traffic.get("sort_DeviceRadixSortHistogramKernel"), traffic.get("sort_DeviceRadixSortOnesweepKernel")
+        if h_ and o_:  # the K2_sort_buckets pass = histogram + 2 onesweep passes (16 key bits)
+            res["K2_sort_buckets"] = sum(h_) / len(h_) + 2 * sum(o_) / len(o_)
         with open(path, "w") as f:
             json.dump({"workload": wl, "source": rep, "dram_bytes_per_launch": res}, f, indent=1)
 

@@ -283,6 +283,10 @@ typedef struct {
   double tau_e, tau_perf, tau_cost;   /* expand / refine thresholds, relative (R36)        */
   int32_t policy;                     /* KARETO_LRU (stack path) / _FIFO / _LFU (K6)       */
   int32_t max_rounds;                 /* 0 = until no candidates remain                    */
+  int32_t expand_ttl;                 /* 0 = Alg. 1 as written (only the DRAM axis expands,
+                                         R37); 1 = also the TTL axis, symmetrically at the
+                                         lowest DRAM row (R55, an extension)     */
+  int32_t pad;
 } kareto_search_params;
 typedef struct {
   int64_t d_gb, t_s;                  /* the evaluated configuration                       */

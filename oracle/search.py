@@ -81,6 +81,7 @@ class SearchParams:
     tau_cost: float = 0.02
     max_evals: int = 1 << 20
     max_rounds: int = 0   # 0 = until C is empty
+    expand_ttl: bool = False  # R55 (extension): also expand the TTL axis at the lowest DRAM row
 
 
 def rel_delta(a: float, b: float) -> float:
@@ -130,6 +131,17 @@ def adaptive_search(evaluate, p: SearchParams):
             if lo in S and rel_delta(S[lo][0], S[(dmax, p.t_min)][0]) > p.tau_e:
                 for t in range(p.t_min, p.t_max + 1, p.t_step):
                     cand.add((dmax + p.d_step, t))
+        # R55 (extension, not in Alg. 1): the l.10-14 test along the TTL axis at the lowest DRAM
+        # row; the new row spans the initial DRAM range; TTLs stay below 2^32 ms
+        if p.expand_ttl:
+            row = [t for (d, t) in S if d == p.d_min]
+            if row:
+                tmax = max(row)
+                lo = (p.d_min, tmax - p.t_step)
+                if (tmax + p.t_step <= 0xFFFFFFFE // 1000 and lo in S
+                        and rel_delta(S[lo][0], S[(p.d_min, tmax)][0]) > p.tau_e):
+                    for d in range(p.d_min, p.d_max + 1, p.d_step):
+                        cand.add((d, tmax + p.t_step))
         # l.15-19: refinement of adjacent pairs with a large performance and cost change
         for a, b in adjacent_pairs(S):
             fa, fb = S[a], S[b]

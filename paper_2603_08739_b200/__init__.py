@@ -79,7 +79,8 @@ class SearchParamsC(ctypes.Structure):
     _fields_ = [("hbm_gb", ctypes.c_double), ("d_min", ctypes.c_int64), ("d_max", ctypes.c_int64),
                 ("d_step", ctypes.c_int64), ("t_min", ctypes.c_int64), ("t_max", ctypes.c_int64),
                 ("t_step", ctypes.c_int64), ("tau_e", ctypes.c_double), ("tau_perf", ctypes.c_double),
-                ("tau_cost", ctypes.c_double), ("policy", ctypes.c_int32), ("max_rounds", ctypes.c_int32)]
+                ("tau_cost", ctypes.c_double), ("policy", ctypes.c_int32), ("max_rounds", ctypes.c_int32),
+                ("expand_ttl", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 # kareto_search_point (48 bytes)
@@ -458,11 +459,11 @@ class Context:
         return float(hv.value)
 
     def search(self, trace: "Trace", model: Model, d_range, t_range, hbm_gb: float, tau_e=0.05, tau_perf=0.05,
-               tau_cost=0.02, policy=LRU, max_rounds=0, cap=1 << 16):
+               tau_cost=0.02, policy=LRU, max_rounds=0, cap=1 << 16, expand_ttl=False):
         """kareto_search: Alg. 1 adaptive Pareto exploration (row f1).  d_range / t_range =
         (min, max, step) in GB / s.  Returns (points [SEARCH_POINT_DTYPE], truncated)."""
         p = SearchParamsC(float(hbm_gb), *[int(v) for v in d_range], *[int(v) for v in t_range], float(tau_e),
-                          float(tau_perf), float(tau_cost), int(policy), int(max_rounds))
+                          float(tau_perf), float(tau_cost), int(policy), int(max_rounds), int(bool(expand_ttl)), 0)
         out = np.zeros(int(cap), SEARCH_POINT_DTYPE)
         n, tr_ = ctypes.c_int64(), ctypes.c_int32()
         m = model.c()

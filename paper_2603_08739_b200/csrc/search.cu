@@ -215,7 +215,8 @@ static kareto_status search(kareto_ctx *ctx, const kareto_trace *tr, const karet
     return fail(ctx, KARETO_E_INVALID, "search: bad DRAM / TTL ranges");
   if (p->t_max > (int64_t)(0xFFFFFFFEu / 1000)) return fail(ctx, KARETO_E_INVALID, "search: TTL above 2^32 ms");
   if (!(p->hbm_gb >= 0) || !std::isfinite(p->hbm_gb) || !(p->tau_e >= 0) || !(p->tau_perf >= 0) ||
-      !(p->tau_cost >= 0) || p->policy < 0 || p->policy > 2 || p->max_rounds < 0 || model->block_bytes == 0)
+      !(p->tau_cost >= 0) || p->policy < 0 || p->policy > 2 || p->max_rounds < 0 || model->block_bytes == 0 ||
+      p->expand_ttl < 0 || p->expand_ttl > 1)
     return fail(ctx, KARETO_E_INVALID, "search: bad thresholds / policy / model");
   const int G = tr->K + 1;
   const uint64_t Bb = model->block_bytes;
@@ -278,6 +279,18 @@ static kareto_status search(kareto_ctx *ctx, const kareto_trace *tr, const karet
       auto lo = S.find({dmax - p->d_step, p->t_min});
       if (lo != S.end() && rel_delta(lo->second[0], S[{dmax, p->t_min}][0]) > p->tau_e)
         for (int64_t t = p->t_min; t <= p->t_max; t += p->t_step) cand.insert({dmax + p->d_step, t});
+    }
+    // R55 (extension, off by default): the same test along the TTL axis at the lowest DRAM row;
+    // the new row spans the initial DRAM range; TTLs stay below 2^32 ms
+    if (p->expand_ttl) {
+      int64_t tmax = -1;
+      for (auto &kv : S)
+        if (kv.first.first == p->d_min) tmax = std::max(tmax, kv.first.second);
+      if (tmax >= 0 && tmax + p->t_step <= (int64_t)(0xFFFFFFFEu / 1000)) {
+        auto lo = S.find({p->d_min, tmax - p->t_step});
+        if (lo != S.end() && rel_delta(lo->second[0], S[{p->d_min, tmax}][0]) > p->tau_e)
+          for (int64_t d = p->d_min; d <= p->d_max; d += p->d_step) cand.insert({d, tmax + p->t_step});
+      }
     }
     // l.15-19: refinement of adjacent pairs (R38, R39)
     std::map<int64_t, std::vector<int64_t>> by_t, by_d;

@@ -52,14 +52,15 @@ def test_hypervolume_edge_cases(ctx):
     assert ctx.hypervolume(same, (1, 1, 1)) == pytest.approx(0.75 * 0.5 * 0.25, rel=1e-15)
 
 
-def run_both(ctx, tr, hbm_gb, d_range, t_range, policy=K.LRU, max_evals=1 << 16, **th):
+def run_both(ctx, tr, hbm_gb, d_range, t_range, policy=K.LRU, max_evals=1 << 16, expand_ttl=False, **th):
     m = O.Model(**MODEL_KW)
     ot = O.OracleTrace(tr, top_k=4)
     ev = S.trace_evaluator(ot, m, hbm_gb, MODEL_KW["block_bytes"])
-    p = S.SearchParams(*d_range, *t_range, max_evals=max_evals, **th)
+    p = S.SearchParams(*d_range, *t_range, max_evals=max_evals, expand_ttl=expand_ttl, **th)
     log, F, trunc = S.adaptive_search(ev, p)
     gt = ctx.load(tr, top_k=4)
-    got, gtrunc = ctx.search(gt, K.Model(**MODEL_KW), d_range, t_range, hbm_gb, policy=policy, cap=max_evals, **th)
+    got, gtrunc = ctx.search(gt, K.Model(**MODEL_KW), d_range, t_range, hbm_gb, policy=policy, cap=max_evals,
+                             expand_ttl=expand_ttl, **th)
     return log, F, trunc, got, gtrunc
 
 
@@ -93,3 +94,15 @@ def test_search_invalid_params(ctx):
         ctx.search(gt, K.Model(**MODEL_KW), (0, 100, 0), (0, 10, 5), 1.0)       # zero step
     with pytest.raises(K.KaretoError):
         ctx.search(gt, K.Model(**MODEL_KW), (0, 100, 50), (0, 5_000_000, 5), 1.0)  # TTL beyond 2^32 ms
+
+
+def test_search_ttl_expansion_parity(ctx):
+    """R55 (extension): the TTL-axis expansion evaluates the same sequence as the oracle's, with
+    bit-identical objectives, and reaches TTLs beyond the seed range on a chat trace."""
+    tr = ki.synthetic("chat", R=1500, seed=0)
+    log, F, trunc, got, gtrunc = run_both(ctx, tr, 20.0, (0, 2048, 512), (0, 1200, 600), expand_ttl=True,
+                                          tau_e=0.01)
+    assert gtrunc == trunc
+    assert [(int(a), int(b), int(c)) for a, b, c in zip(got["d_gb"], got["t_s"], got["round"])] == log
+    assert np.array_equal(got["obj"].view(np.uint64), F.view(np.uint64))
+    assert got["t_s"].max() > 1200

@@ -145,3 +145,23 @@ def test_trace_evaluator_matches_literal_replay():
     cf = O.configs([[hbm, d * 10**9 // m.block_bytes, int(O.INF_CAP)] for d, _ in C], tuner=[ts.index(t) for _, t in C])
     f1 = ot.objective(m, cf, ot.replay(cf, ttl))            # O1 literal replay
     assert np.array_equal(f, f1)
+
+
+def test_ttl_expansion_extension_mirrors_the_dram_rule():
+    """R55 (extension, off by default): with latency falling in the TTL the way the DRAM test of
+    Alg. 1 l.10-14 looks for, expand_ttl adds whole rows t_max + step over the initial DRAM range
+    until the relative gain at the lowest DRAM row drops to tau_e; without it no TTL beyond the
+    seed range is ever evaluated (R37)."""
+    f = lambda t: 1.0 + 1e4 / (100.0 + t)                 # convex, decreasing latency in the TTL
+    ev, _ = landscape(lambda d, t: f(t))                  # constant cost: no refinement
+    p = S.SearchParams(0, 200, 100, 0, 200, 100, tau_e=0.05)
+    log, _, _ = S.adaptive_search(ev, p)
+    assert max(t for _, t, _ in log) == 200               # as written: the TTL axis never expands
+    p = S.SearchParams(0, 200, 100, 0, 200, 100, tau_e=0.05, expand_ttl=True)
+    log, _, trunc = S.adaptive_search(ev, p)
+    tmax = max(t for _, t, _ in log)
+    gain = lambda t: (f(t - 100) - f(t)) / f(t - 100)
+    assert not trunc and tmax > 200 and gain(tmax) <= 0.05
+    assert all(gain(t) > 0.05 for t in range(200, tmax, 100))
+    for t in range(0, tmax + 1, 100):                      # every expansion adds the whole DRAM row
+        assert {(0, t), (100, t), (200, t)} <= {(d, x) for d, x, _ in log}

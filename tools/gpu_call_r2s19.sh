@@ -1,0 +1,3 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_search.py -x -q > gpurun_out/s19_tests.log 2>&1; echo t_rc=$?
+timeout 900 python bench.py --config 2 --search > gpurun_out/s19_search.log 2>&1; echo s_rc=$?

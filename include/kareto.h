@@ -113,9 +113,11 @@ typedef struct {
  * (R < 1, K out of range, null pointers), _E_PARSE (offsets decreasing, output < 0,
  * input_tokens < 16*blocks), _E_CHAIN (R7), _E_OVERFLOW (>= 2^32-1 block accesses or a
  * reuse interval >= 2^32-1 ms), _E_OOM.
- * Memory: the trace keeps 24 B per access on the device until kareto_trace_free; the K2 link's
- * scratch (20 B per access) stays with the context for the next load and is freed by
- * kareto_destroy. */
+ * Memory: the trace keeps 24 B per access (+ 16 B per K3 run) on the device until
+ * kareto_trace_free; two context scratch buffers stay with the context for the next load and
+ * are freed by kareto_destroy: the K2 link's (~20 B per access) and, for host inputs
+ * (inputs_on_device = 0), the device staging copy of the tokens / block hashes (grown to the
+ * largest load). */
 kareto_status kareto_load_trace(kareto_ctx *ctx, const kareto_trace_desc *desc, kareto_trace **out);
 void kareto_trace_free(kareto_trace *tr);
 

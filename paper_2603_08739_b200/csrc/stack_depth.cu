@@ -398,6 +398,41 @@ static kareto_status cub_tmp(kareto_ctx *ctx, DBuf<uint8_t> &tmp, F &&f) {
   return KARETO_OK;
 }
 
+// Runs of n accesses: ordered compaction of the run-head flags into rl.run_start; rl.m_dev = M
+// on the device (no host round trip).
+kareto_status run_list_start(kareto_ctx *ctx, uint64_t N, const uint8_t *run_flag, RunList &rl) {
+  cudaStream_t st = ctx->stream;
+  DBuf<uint8_t> tmp;
+  KTRY(rl.m_dev.alloc(ctx, 1));
+  KTRY(rl.run_start.alloc(ctx, N > 0 ? N : 1));  // #runs <= reuse accesses
+  if (N == 0) return rl.m_dev.zero();
+  Pass ps(ctx, "K3_runs", 1, 2);
+  const uint64_t ntile = (N + CF_TILE - 1) / CF_TILE;
+  DBuf<uint32_t> cnt, off;
+  KTRY(cnt.alloc(ctx, ntile + 1)); KTRY(off.alloc(ctx, ntile + 1));
+  KCUDA(ctx, cudaMemsetAsync(cnt.p + ntile, 0, 4, st));
+  k_flag_count<<<(unsigned)ntile, CF_THREADS, 0, st>>>(run_flag, N, cnt.p);
+  KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, cnt.p, off.p, (int)(ntile + 1), st);
+  }));
+  k_flag_write<<<(unsigned)ntile, CF_THREADS, 0, st>>>(run_flag, N, off.p, rl.run_start.p);
+  KCUDA(ctx, cudaMemcpyAsync(rl.m_dev.p, off.p + ntile, 4, cudaMemcpyDeviceToDevice, st));
+  return KARETO_OK;
+}
+
+// With M (read by the caller): per run its request, length and first previous position.
+kareto_status run_list_finish(kareto_ctx *ctx, uint64_t N, const uint32_t *prev_c, const uint32_t *req,
+                              uint32_t req_base, const uint32_t *s, uint32_t pos_base, int M, RunList &rl) {
+  rl.M = M;
+  if (M == 0) return KARETO_OK;
+  KTRY(rl.run_req.alloc(ctx, M)); KTRY(rl.run_len.alloc(ctx, M)); KTRY(rl.run_p0.alloc(ctx, M));
+  Pass ps(ctx, "K3_run_info", 1, 1);
+  k_run_info<<<grid_for(M, 256, 8 * ctx->num_sms), 256, 0, ctx->stream>>>(rl.run_start.p, rl.m_dev.p, N, req, req_base,
+                                                                         s, pos_base, prev_c, rl.run_req.p,
+                                                                         rl.run_len.p, rl.run_p0.p);
+  return KARETO_OK;
+}
+
 // K3 over n accesses (local positions 0..n-1) whose previous positions prev_c are given in
 // coordinates [0, y_range) where local position i sits at y_off + i (whole trace: y_off = 0,
 // y_range = n; a time shard prepends its boundary LRU stack, trace_shard.cu).
@@ -407,44 +442,37 @@ kareto_status stack_depth(kareto_ctx *ctx, uint64_t N, uint64_t y_range, const u
                           uint4 **runs_out) {
   *n_runs = 0;
   if (N == 0) return KARETO_OK;
+  RunList rl;
+  KTRY(run_list_start(ctx, N, run_flag, rl));
+  int M = 0;
+  KCUDA(ctx, cudaMemcpyAsync(&M, rl.m_dev.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  KCUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  KTRY(run_list_finish(ctx, N, prev_c, req, req_base, s, pos_base, M, rl));
+  return stack_depth_runs(ctx, N, y_range, s, pos_base, y_off, rl, depth, n_runs, runs_out);
+}
+
+// K3 proper over a run list (run_list_start / _finish).
+kareto_status stack_depth_runs(kareto_ctx *ctx, uint64_t N, uint64_t y_range, const uint32_t *s,
+                               uint32_t pos_base, uint32_t y_off, RunList &rl, uint32_t *depth, int64_t *n_runs,
+                               uint4 **runs_out) {
+  *n_runs = 0;
+  if (N == 0) return KARETO_OK;
   if (y_range >= (1ull << 31)) return fail(ctx, KARETO_E_OVERFLOW, "stack depth pass supports < 2^31 positions");
   cudaStream_t st = ctx->stream;
   const int sms = ctx->num_sms;
   if (depth) KCUDA(ctx, cudaMemsetAsync(depth, 0xFF, 4 * N, st));  // first accesses: UINT32_MAX
-  // ---- runs
   DBuf<uint8_t> tmp;
-  DBuf<uint32_t> run_start, run_req, run_len, run_p0;
-  DBuf<int> m_dev;
-  KTRY(m_dev.alloc(ctx, 1));
-  // #runs <= reuse accesses; allocate for the worst case (N) lazily: count first
-  KTRY(run_start.alloc(ctx, N));
-  {
-    Pass ps(ctx, "K3_runs", 1, 2);
-    const uint64_t ntile = (N + CF_TILE - 1) / CF_TILE;
-    DBuf<uint32_t> cnt, off;
-    KTRY(cnt.alloc(ctx, ntile + 1)); KTRY(off.alloc(ctx, ntile + 1));
-    KCUDA(ctx, cudaMemsetAsync(cnt.p + ntile, 0, 4, st));
-    k_flag_count<<<(unsigned)ntile, CF_THREADS, 0, st>>>(run_flag, N, cnt.p);
-    KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, cnt.p, off.p, (int)(ntile + 1), st);
-    }));
-    k_flag_write<<<(unsigned)ntile, CF_THREADS, 0, st>>>(run_flag, N, off.p, run_start.p);
-    KCUDA(ctx, cudaMemcpyAsync(m_dev.p, off.p + ntile, 4, cudaMemcpyDeviceToDevice, st));
-  }
-  int M = 0;
-  KCUDA(ctx, cudaMemcpyAsync(&M, m_dev.p, 4, cudaMemcpyDeviceToHost, st));
-  KCUDA(ctx, cudaStreamSynchronize(st));
+  const int M = rl.M;
   *n_runs = M;
   if (M == 0) return KARETO_OK;
-  KTRY(run_req.alloc(ctx, M)); KTRY(run_len.alloc(ctx, M)); KTRY(run_p0.alloc(ctx, M));
+  DBuf<uint32_t> &run_start = rl.run_start, &run_req = rl.run_req, &run_len = rl.run_len, &run_p0 = rl.run_p0;
+  DBuf<int> &m_dev = rl.m_dev;
   if (runs_out) KMALLOC(ctx, *runs_out, sizeof(uint4) * (size_t)M, st);
   const uint64_t NI = 2ull * (uint64_t)M;  // items
   DBuf<uint2> buf[2];
   KTRY(buf[0].alloc(ctx, NI)); KTRY(buf[1].alloc(ctx, NI));
   {
-    Pass ps(ctx, "K3_run_items", 1, 2);
-    k_run_info<<<grid_for(M, 256, 8 * sms), 256, 0, st>>>(run_start.p, m_dev.p, N, req, req_base, s, pos_base,
-                                                          prev_c, run_req.p, run_len.p, run_p0.p);
+    Pass ps(ctx, "K3_run_items", 1, 1);
     k_run_items<<<grid_for(M, 256, 8 * sms), 256, 0, st>>>(m_dev.p, run_req.p, run_len.p, run_p0.p, buf[0].p);
   }
   int B = 1;

@@ -638,6 +638,81 @@ __global__ void k_access_info(uint64_t N, const uint32_t *__restrict__ prev, con
   if (flags) atomicOr(&st->flags, flags);
 }
 
+// Whole traces, K2 per access (round 2): the run-head flags of K3 and the per-request first /
+// reuse counts; first accesses get delta = none.  The reuse interval and the chain checks of a
+// reuse access are the same for every access of its run (one earlier request, chain positions
+// falling together), so k_run_delta computes them once per run.  A first access right after a
+// reuse access of its request breaks R7 by itself (the reused block's parent was never seen).
+__global__ void k_access_flags(uint64_t N, const uint32_t *__restrict__ prev, const uint32_t *__restrict__ req,
+                               const uint32_t *__restrict__ s, uint32_t *__restrict__ delta,
+                               uint8_t *__restrict__ run_flag, LoadStats *st) {
+  unsigned flags = 0;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = prev[j], r = req[j];
+    const uint32_t pm = j > 0 ? prev[j - 1] : kNone;
+    const bool start = (uint32_t)j == s[r];
+    uint8_t head = 0;
+    if (p != kNone) head = (start || pm == kNone || p != pm + 1) ? 1 : 0;
+    else {
+      delta[j] = kNone;
+      if (!start && pm != kNone) flags |= F_CHAIN;
+    }
+    run_flag[j] = head;
+  }
+  if (flags) atomicOr(&st->flags, flags);
+}
+
+// per request: first accesses = blocks - reuse accesses (the runs' lengths, k_run_delta)
+__global__ void k_first_from_reuse(int64_t R, const uint32_t *__restrict__ s, const uint32_t *__restrict__ reuse_cnt,
+                                   uint32_t *__restrict__ first_cnt) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x)
+    first_cnt[r] = (s[r + 1] - s[r]) - reuse_cnt[r];
+}
+
+// Per run (a warp loads 32 runs' data at once): delta = arr[r] - arr[req[p0]] (R5), chain
+// positions equal at the run's start (then along the run), the parent hashes equal at its end
+// (inside a run the parent access links to p + 1, which the exact link proves equal); the run's
+// delta is then written by all lanes, run after run.
+__global__ void __launch_bounds__(256) k_run_delta(const int *__restrict__ m_ptr, const uint32_t *__restrict__ run_start,
+                                                   const uint32_t *__restrict__ run_req,
+                                                   const uint32_t *__restrict__ run_len,
+                                                   const uint32_t *__restrict__ run_p0, const uint32_t *__restrict__ prev,
+                                                   const uint32_t *__restrict__ req, const uint32_t *__restrict__ s,
+                                                   const int64_t *__restrict__ arr, const uint64_t *__restrict__ hash,
+                                                   uint32_t *__restrict__ delta, uint32_t *__restrict__ reuse_cnt,
+                                                   LoadStats *st) {
+  const int M = *m_ptr;
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  unsigned flags = 0;
+  for (int q0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; q0 < M; q0 += nw * 32) {
+    const int q = q0 + lane;
+    uint32_t j0 = 0, L = 0, dl = kNone;
+    if (q < M) {
+      j0 = run_start[q];
+      L = run_len[q];
+      const uint32_t r = run_req[q], p0 = run_p0[q];
+      atomicAdd(&reuse_cnt[r], L);  // every reuse access lies in exactly one run
+      const uint32_t rp = req[p0];
+      const int64_t d = arr[r] - arr[rp];
+      if (d < 0 || d >= (int64_t)kNone) flags |= F_DELTA; else dl = (uint32_t)d;
+      const uint32_t kj = s[r + 1] - 1 - j0, kp = s[rp + 1] - 1 - p0;
+      if (kj != kp) flags |= F_CHAIN;
+      else {
+        const uint32_t je = j0 + L - 1, pe = p0 + L - 1;  // the run's last access (chain position kj - L + 1)
+        if (kj - (L - 1) > 0 && prev[je + 1] != pe + 1 && hash[je + 1] != hash[pe + 1]) flags |= F_CHAIN;
+      }
+    }
+    const int nk = M - q0 < 32 ? M - q0 : 32;
+    for (int k = 0; k < nk; k++) {
+      const uint32_t jk = __shfl_sync(0xFFFFFFFFu, j0, k), Lk = __shfl_sync(0xFFFFFFFFu, L, k);
+      const uint32_t dk = __shfl_sync(0xFFFFFFFFu, dl, k);
+      for (uint32_t t = lane; t < Lk; t += 32) delta[jk + t] = dk;
+    }
+  }
+  if (flags) atomicOr(&st->flags, flags);
+}
+
 // groups: requests with at least one block, keyed by their root hash (block k = 0, the
 // last touch of the request)
 // (s points at the first request considered; hash is indexed by position - pos_base)
@@ -1193,6 +1268,10 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
   hm.mark(st, "a2 K1");
 
   // ---- a3: K2 prev / delta / chain check
+  // per run (k_access_flags + k_run_delta) unless KARETO_K2_ACCESS_INFO asks for the per-access
+  // k_access_info (kept for comparison; both are parity-tested)
+  const bool per_run = getenv("KARETO_K2_ACCESS_INFO") == nullptr;
+  RunList rl;
   DBuf<uint32_t> first_cnt, reuse_cnt;
   DBuf<uint8_t> run_flag;
   DBuf<unsigned> k2ovf;
@@ -1204,12 +1283,18 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
     if (buckets) { KTRY(k2ovf.alloc(ctx, 1)); KTRY(k2ovf.zero()); }
     KTRY(link_prev(ctx, tr->hash, N, tr->prev, nullptr, &prep, buckets ? k2ovf.p : nullptr));
     hm.mark(st, "a3 K2 link");
-    {
+    if (per_run) {
+      Pass ps(ctx, "K2_access_flags", 1, 1);
+      k_access_flags<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(N, tr->prev, tr->req, tr->s, tr->delta, run_flag.p,
+                                                                in.stats.p);
+    } else {
       Pass ps(ctx, "K2_access_info", 1, 1);
       k_access_info<<<grid_for(N, 256, 8 * sms), 256, 0, st>>>(N, tr->prev, tr->req, tr->s, tr->arr, tr->hash,
                                                                tr->delta, first_cnt.p, reuse_cnt.p, run_flag.p,
                                                                in.stats.p);
     }
+    // K3's run list (heads compacted on the device; M comes back with the groups' round trip)
+    KTRY(run_list_start(ctx, N, run_flag.p, rl));
   }
 
   hm.mark(st, "a3 K2 access_info");
@@ -1240,14 +1325,27 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
       return cub::DeviceSelect::Flagged(t, b, rval.p, rflag.p, rval_c.p, m_dev.p, (int)R, st);
     }));
     }
-    int m = 0;
+    int m = 0, M = 0;
     unsigned k2o = 0;
     KCUDA(ctx, cudaMemcpyAsync(&m, m_dev.p, 4, cudaMemcpyDeviceToHost, st));
+    if (N > 0) KCUDA(ctx, cudaMemcpyAsync(&M, rl.m_dev.p, 4, cudaMemcpyDeviceToHost, st));
     if (k2ovf.p) KCUDA(ctx, cudaMemcpyAsync(&k2o, k2ovf.p, 4, cudaMemcpyDeviceToHost, st));
     KCUDA(ctx, cudaStreamSynchronize(st));
     if (k2o) {  // a bucket exceeded the link table: prev is valid but not exact -- redo with the full sort
       if (getenv("KARETO_DEBUG")) fprintf(stderr, "[kareto] K2 bucket link: table overflow, full-sort re-run\n");
       return KARETO_RETRY_FULL_SORT;
+    }
+    if (N > 0) {  // the run list, and per run the reuse interval and the chain checks
+      KTRY(run_list_finish(ctx, N, tr->prev, tr->req, 0, tr->s, 0, M, rl));
+      if (per_run) {
+        Pass ps(ctx, "K2_run_delta", 1, 2);
+        if (M > 0)
+          k_run_delta<<<grid_for(M, 256, 16 * sms), 256, 0, st>>>(rl.m_dev.p, rl.run_start.p, rl.run_req.p,
+                                                                  rl.run_len.p, rl.run_p0.p, tr->prev, tr->req, tr->s,
+                                                                  tr->arr, tr->hash, tr->delta, reuse_cnt.p,
+                                                                  in.stats.p);
+        k_first_from_reuse<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(R, tr->s, reuse_cnt.p, first_cnt.p);
+      }
     }
     k_fill_u16<<<grid_for(R, 256, 4 * sms), 256, 0, st>>>(tr->grp, R, (uint16_t)K);
     if (m > 0) {
@@ -1297,7 +1395,7 @@ static kareto_status load(kareto_ctx *ctx, const kareto_trace_desc *d, kareto_tr
   if (N > 0) {
     if (N >= (1ull << 31)) return fail(ctx, KARETO_E_OVERFLOW, "stack depth pass supports < 2^31 accesses");
     // the runs are kept and per-access depths deferred to their first reader (ensure_depth)
-    KTRY(stack_depth(ctx, N, N, tr->prev, tr->req, 0, tr->s, 0, 0, run_flag.p, nullptr, &tr->n_runs, &tr->runs));
+    KTRY(stack_depth_runs(ctx, N, N, tr->s, 0, 0, rl, nullptr, &tr->n_runs, &tr->runs));
     tr->depth_ready = false;
   }
   KTRY(sync(ctx, "load_trace"));

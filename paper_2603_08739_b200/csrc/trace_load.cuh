@@ -63,6 +63,19 @@ kareto_status link_prev(kareto_ctx *ctx, const uint64_t *hash, uint64_t n, uint3
 // The bijective mix whose halves are the sort key / value high word (k_sort_prep).
 constexpr uint64_t kSortMixC = 0x6A09E667F3BCC909ULL;
 
+// K3 run list: heads compacted from the flags (start), then per run request / length / first
+// previous position once the host knows M (finish); stack_depth_runs runs K3 proper on it.
+struct RunList {
+  DBuf<uint32_t> run_start, run_req, run_len, run_p0;
+  DBuf<int> m_dev;
+  int M = 0;
+};
+kareto_status run_list_start(kareto_ctx *ctx, uint64_t N, const uint8_t *run_flag, RunList &rl);
+kareto_status run_list_finish(kareto_ctx *ctx, uint64_t N, const uint32_t *prev_c, const uint32_t *req,
+                              uint32_t req_base, const uint32_t *s, uint32_t pos_base, int M, RunList &rl);
+kareto_status stack_depth_runs(kareto_ctx *ctx, uint64_t N, uint64_t y_range, const uint32_t *s,
+                               uint32_t pos_base, uint32_t y_off, RunList &rl, uint32_t *depth, int64_t *n_runs,
+                               uint4 **runs_out = nullptr);
 kareto_status stack_depth(kareto_ctx *ctx, uint64_t n, uint64_t y_range, const uint32_t *prev_c,
                           const uint32_t *req, uint32_t req_base, const uint32_t *s, uint32_t pos_base,
                           uint32_t y_off, const uint8_t *run_flag, uint32_t *depth, int64_t *n_runs,

@@ -416,7 +416,8 @@ def test_config5_million_configs_windowed_histograms(ctx):
     assert np.all(np.diff(h, axis=1) >= 0)
 
 
-@pytest.mark.parametrize("env", [{"KARETO_K2_FULLSORT": "1"}, {"KARETO_K2_TABLE_LIMIT": "3"}])
+@pytest.mark.parametrize("env", [{"KARETO_K2_FULLSORT": "1"}, {"KARETO_K2_TABLE_LIMIT": "3"},
+                                 {"KARETO_K2_ACCESS_INFO": "1"}])
 def test_k2_full_sort_path_and_bucket_overflow_fallback(ctx, env):
     """K2's two link paths give the same prev: the full 32-bit sort + tiled link (forced), and the
     16-bit bucket link falling back to it when a bucket exceeds the warp table (limit forced to 3

@@ -55,6 +55,20 @@ __global__ void k_line_stop(const uint64_t *__restrict__ key, const uint32_t *__
   }
 }
 
+// Short lines (at most 2^wa points): the segmented exclusive OR-scan done in place -- each point
+// walks back through its line to the first earlier stop (or the line start) and marks itself
+__global__ void k_line_prune(const uint64_t *__restrict__ key, const uint32_t *__restrict__ idx, int64_t n, int wa,
+                             const uint8_t *__restrict__ stop, uint8_t *__restrict__ pruned) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t li = key[i] >> wa;
+    for (int64_t k = i - 1; k >= 0 && (key[k] >> wa) == li; k--)
+      if (stop[k]) {
+        pruned[idx[i]] = 1;
+        break;
+      }
+  }
+}
+
 __global__ void k_mark_pruned(const uint8_t *__restrict__ excl, const uint32_t *__restrict__ idx, int64_t n,
                               uint8_t *__restrict__ pruned) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -248,11 +262,15 @@ static kareto_status pareto_run(kareto_ctx *ctx, const double *obj, const kareto
       {
         Pass ps(ctx, "K8a_line_stop", 1, 2);
         k_line_stop<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(ks, is, n, lw.w[a], f, prune->tau_e, line.p, stop.p);
-        KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
-          return cub::DeviceScan::ExclusiveScanByKey(t, b, line.p, stop.p, excl.p, MaxOp(), (uint8_t)0, (int)n,
-                                                     cub::Equality(), st);
-        }));
-        k_mark_pruned<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(excl.p, is, n, pruned.p);
+        if (lw.w[a] <= 8) {  // lines of <= 256 points: walk back instead of a segmented scan
+          k_line_prune<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(ks, is, n, lw.w[a], stop.p, pruned.p);
+        } else {
+          KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+            return cub::DeviceScan::ExclusiveScanByKey(t, b, line.p, stop.p, excl.p, MaxOp(), (uint8_t)0, (int)n,
+                                                       cub::Equality(), st);
+          }));
+          k_mark_pruned<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(excl.p, is, n, pruned.p);
+        }
       }
     }
   }

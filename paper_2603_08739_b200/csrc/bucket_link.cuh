@@ -56,36 +56,24 @@ struct BLTable {
   uint32_t nused, pad;
 };
 
-// bstart[b] = first sorted index of bucket b (b <= 2^16; bstart[2^16] = N); 4 keys per thread
-__global__ void k_bucket_bounds(const uint32_t *__restrict__ ks, uint64_t N, uint32_t *__restrict__ bstart) {
-  const uint64_t nq = (N + 3) / 4;
-  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i0 = 4 * q;
-    uint32_t k[4];
-    if (i0 + 4 <= N) {
-      const uint4 v = *reinterpret_cast<const uint4 *>(ks + i0);  // pool allocations are 256-byte aligned
-      k[0] = v.x; k[1] = v.y; k[2] = v.z; k[3] = v.w;
-    } else {
-      for (int t = 0; t < 4; t++) k[t] = i0 + t < N ? ks[i0 + t] : 0xFFFFFFFFu;
-    }
-    int bp = i0 ? (int)(ks[i0 - 1] >> (32 - BL_BITS)) : -1;
-#pragma unroll
-    for (int t = 0; t < 4; t++) {
-      if (i0 + t >= N) break;
-      const int b = (int)(k[t] >> (32 - BL_BITS));
-      for (int x = bp + 1; x <= b; x++) bstart[x] = (uint32_t)(i0 + t);
-      if (i0 + t == N - 1)
-        for (int x = b + 1; x <= BL_NB; x++) bstart[x] = (uint32_t)N;
-      bp = b;
-    }
-  }
-}
-
 // chunk -> bucket table (one thread per bucket writes its chunks)
 __global__ void k_chunk_bucket(const uint32_t *__restrict__ cstart, uint16_t *__restrict__ cbucket) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < BL_NB)
     for (uint32_t w = cstart[b]; w < cstart[b + 1]; w++) cbucket[w] = (uint16_t)b;
+}
+
+// bstart[b] = first sorted index with bucket >= b (b <= 2^16), by binary search: 65,537 short
+// searches instead of a pass over all N keys
+__global__ void k_bucket_bounds_bs(const uint32_t *__restrict__ ks, uint64_t N, uint32_t *__restrict__ bstart) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > BL_NB) return;
+  uint64_t lo = 0, hi = N;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if ((int)(__ldg(&ks[mid]) >> (32 - BL_BITS)) < b) lo = mid + 1; else hi = mid;
+  }
+  bstart[b] = (uint32_t)lo;
 }
 
 // chunks per bucket (>= 1), for the chunk prefix cstart

@@ -1061,7 +1061,7 @@ static kareto_status bucket_link(kareto_ctx *ctx, DBuf<uint32_t> &k32, DBuf<uint
   KTRY(ctr.alloc(ctx, 2)); KTRY(ctr.zero());
   {
     Pass ps(ctx, "K2_bucket_bounds", 1, 2);
-    k_bucket_bounds<<<grid_for((N + 3) / 4, 256, 8 * sms), 256, 0, st>>>(k32s.p, N, bstart.p);
+    k_bucket_bounds_bs<<<(BL_NB + 1 + 255) / 256, 256, 0, st>>>(k32s.p, N, bstart.p);
     k_bucket_chunks<<<BL_NB / 256, 256, 0, st>>>(bstart.p, nch.p);
   }
   KCUDA(ctx, cudaMemsetAsync(nch.p + BL_NB, 0, 4, st));

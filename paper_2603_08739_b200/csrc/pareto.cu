@@ -76,7 +76,9 @@ __global__ void k_mark_pruned(const uint8_t *__restrict__ excl, const uint32_t *
 }
 
 __global__ void k_survivor_flags(const uint8_t *__restrict__ pruned, int64_t n, uint8_t *__restrict__ keep,
-                                 double *__restrict__ f1, const double *__restrict__ f, uint32_t *__restrict__ idx) {
+                                 double *__restrict__ f1, const double *__restrict__ f, uint32_t *__restrict__ idx,
+                                 int *__restrict__ m_all) {
+  if (m_all && blockIdx.x == 0 && threadIdx.x == 0) *m_all = (int)n;  // no pruning: every point survives
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     keep[i] = pruned[i] ? 0 : 1;
     f1[i] = f[3 * i];
@@ -284,9 +286,16 @@ static kareto_status pareto_run(kareto_ctx *ctx, const double *obj, const kareto
     DBuf<int> m_dev;
     KTRY(keep.alloc(ctx, n)); KTRY(f1.alloc(ctx, n)); KTRY(f1c.alloc(ctx, n)); KTRY(f1s.alloc(ctx, n));
     KTRY(idx.alloc(ctx, n)); KTRY(idxc.alloc(ctx, n)); KTRY(idxs.alloc(ctx, n)); KTRY(m_dev.alloc(ctx, 1));
-    {
+    if (!do_prune) {  // every configuration survives: no compaction, no round trip for the count
+      Pass ps(ctx, "K8b_compact_sort", 0, 2);
+      k_survivor_flags<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(pruned.p, n, keep.p, f1.p, f, idx.p, m_dev.p);
+      KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, f1.p, f1s.p, idx.p, idxs.p, (int)n, 0, 64, st);
+      }));
+      ctx->own_launches += 1;
+    } else {
       Pass ps(ctx, "K8b_compact_sort", 0, 3);
-      k_survivor_flags<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(pruned.p, n, keep.p, f1.p, f, idx.p);
+      k_survivor_flags<<<grid_for(n, 256, 4 * sms), 256, 0, st>>>(pruned.p, n, keep.p, f1.p, f, idx.p, nullptr);
       KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
         return cub::DeviceSelect::Flagged(t, b, f1.p, keep.p, f1c.p, m_dev.p, (int)n, st);
       }));

@@ -321,6 +321,50 @@ __global__ void k_col_fix(const unsigned long long *__restrict__ flat, int ncol,
     out[i] = flat[i] - base;
   }
 }
+// K4 cumulative tables in one launch (one CTA per table): out[tc][b] = sum over tc' <= tc and
+// b' <= b of h[tc'][b'] -- a block scan over b per column (8 consecutive bins per thread) plus the
+// previous column's prefix (each thread adds the values it wrote itself for the same bins);
+// table 2 (D) has one column.
+constexpr int CUM_THREADS = 1024, CUM_ITEMS = 8;
+__global__ void __launch_bounds__(CUM_THREADS) k_cumulate_tables(const unsigned long long *__restrict__ hC,
+                                                                 const unsigned long long *__restrict__ hS,
+                                                                 const unsigned long long *__restrict__ hD, int ncol,
+                                                                 int nb, unsigned long long *__restrict__ C1,
+                                                                 unsigned long long *__restrict__ S1,
+                                                                 unsigned long long *__restrict__ CD) {
+  typedef cub::BlockScan<unsigned long long, CUM_THREADS> Scan;
+  __shared__ typename Scan::TempStorage ts;
+  const unsigned long long *h = blockIdx.x == 0 ? hC : blockIdx.x == 1 ? hS : hD;
+  unsigned long long *out = blockIdx.x == 0 ? C1 : blockIdx.x == 1 ? S1 : CD;
+  const int nc = blockIdx.x == 2 ? 1 : ncol;
+  constexpr int TILE = CUM_THREADS * CUM_ITEMS;
+  for (int tc = 0; tc < nc; tc++) {
+    unsigned long long carry = 0;
+    for (int b0 = 0; b0 < nb; b0 += TILE) {
+      const int bt = b0 + threadIdx.x * CUM_ITEMS;  // this thread's first bin
+      unsigned long long v[CUM_ITEMS], sum = 0;
+#pragma unroll
+      for (int k = 0; k < CUM_ITEMS; k++) {
+        v[k] = bt + k < nb ? h[(size_t)tc * nb + bt + k] : 0ull;
+        sum += v[k];
+      }
+      unsigned long long excl, tot;
+      Scan(ts).ExclusiveSum(sum, excl, tot);
+      unsigned long long run = carry + excl;
+#pragma unroll
+      for (int k = 0; k < CUM_ITEMS; k++) {
+        run += v[k];
+        if (bt + k < nb) {
+          const size_t i = (size_t)tc * nb + bt + k;
+          out[i] = run + (tc > 0 ? out[i - nb] : 0ull);
+        }
+      }
+      carry += tot;
+      __syncthreads();  // ts is reused
+    }
+  }
+}
+
 __global__ void k_prefix_over_cols(unsigned long long *__restrict__ a, int ncol, int nb) {
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
     unsigned long long acc = 0;
@@ -802,23 +846,28 @@ static kareto_status run_eval(kareto_ctx *ctx, const kareto_trace *tr, const Gri
       KTRY(coll_allreduce_u64(ctx, hD.p, (size_t)nb));
     }
     {
-      Pass ps(ctx, "K4_cumulate", 0, 3);
-      DBuf<unsigned long long> flat;
-      KTRY(flat.alloc(ctx, ncell));
-      KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
-        return cub::DeviceScan::InclusiveSum(t, b, hC.p, flat.p, (int64_t)ncell, st);
-      }));
-      k_col_fix<<<grid_for(ncell, 256, 4 * sms), 256, 0, st>>>(flat.p, ncol, nb, C1.p);
-      KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
-        return cub::DeviceScan::InclusiveSum(t, b, hS.p, flat.p, (int64_t)ncell, st);
-      }));
-      k_col_fix<<<grid_for(ncell, 256, 4 * sms), 256, 0, st>>>(flat.p, ncol, nb, S1.p);
-      k_prefix_over_cols<<<grid_for(nb, 256, 4 * sms), 256, 0, st>>>(C1.p, ncol, nb);
-      k_prefix_over_cols<<<grid_for(nb, 256, 4 * sms), 256, 0, st>>>(S1.p, ncol, nb);
-      KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
-        return cub::DeviceScan::InclusiveSum(t, b, hD.p, CD.p, nb, st);
-      }));
-      ctx->own_launches += 4;
+      if (ncell <= (size_t)8 * CUM_THREADS * CUM_ITEMS) {  // small tables: one CTA per table
+        Pass ps(ctx, "K4_cumulate", 1, 1);
+        k_cumulate_tables<<<3, CUM_THREADS, 0, st>>>(hC.p, hS.p, hD.p, ncol, nb, C1.p, S1.p, CD.p);
+      } else {
+        Pass ps(ctx, "K4_cumulate", 0, 3);
+        DBuf<unsigned long long> flat;
+        KTRY(flat.alloc(ctx, ncell));
+        KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+          return cub::DeviceScan::InclusiveSum(t, b, hC.p, flat.p, (int64_t)ncell, st);
+        }));
+        k_col_fix<<<grid_for(ncell, 256, 4 * sms), 256, 0, st>>>(flat.p, ncol, nb, C1.p);
+        KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+          return cub::DeviceScan::InclusiveSum(t, b, hS.p, flat.p, (int64_t)ncell, st);
+        }));
+        k_col_fix<<<grid_for(ncell, 256, 4 * sms), 256, 0, st>>>(flat.p, ncol, nb, S1.p);
+        k_prefix_over_cols<<<grid_for(nb, 256, 4 * sms), 256, 0, st>>>(C1.p, ncol, nb);
+        k_prefix_over_cols<<<grid_for(nb, 256, 4 * sms), 256, 0, st>>>(S1.p, ncol, nb);
+        KTRY(cub_tmp(ctx, tmp, [&](void *t, size_t &b) {
+          return cub::DeviceScan::InclusiveSum(t, b, hD.p, CD.p, nb, st);
+        }));
+        ctx->own_launches += 4;
+      }
     }
   }
   // TTL-mode tables

@@ -225,6 +225,10 @@ kareto_status kareto_pareto(kareto_ctx *ctx, const double *obj, const kareto_con
  * of kareto_eval_grid / kareto_pareto that depends on the configurations and the TTL table only
  * (validation of every configuration, the rank's cost-weighted shard, the stack-path / replay
  * split, the TTL value sets, the line-key widths of pruning) and the device copies they need.
+ * It also keeps, from its first use, what depends on the grid and the trace's U only: K4's sorted
+ * boundary set, its lookup table and the per-configuration indices (recomputed when a trace with
+ * another U is evaluated), and K8a's sorted line order per axis (~12 B per configuration and
+ * axis) -- a step then runs only the per-trace passes.
  *   cfg [n_cfg], ttl_ms [n_tuner][n_groups] host, as for kareto_eval_grid (n_groups = K+1 of the
  *   traces it will be evaluated on; eval returns KARETO_E_INVALID for another K).
  * The grid copies everything it keeps; the caller's arrays may be reused at once.  It belongs to

@@ -121,34 +121,42 @@ class ClockSampler:
         self.samples = []
         self._stop = threading.Event()
         self._t = None
-
-    def _run(self):
         # NVML in-process (the same counters nvidia-smi reports: clocks.sm, clocks.max.sm,
-        # clocks_event_reasons.active); spawning nvidia-smi repeatedly stalls CUDA calls.
+        # clocks_event_reasons.active); spawning nvidia-smi repeatedly stalls CUDA calls.  Opened
+        # before the timed region, so a short region still gets its samples.
+        self._nv, self._h = None, None
         try:
             import pynvml
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._nv, self._h = pynvml, pynvml.nvmlDeviceGetHandleByIndex(index)
         except Exception:
-            return
+            pass
+
+    def _sample(self):
+        nv, h = self._nv, self._h
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.samples.append((int(sm), int(mx), int(rs)))
+        except Exception:
+            pass
+
+    def _run(self):
         while not self._stop.is_set():
-            try:
-                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((int(sm), int(mx), int(rs)))
-            except Exception:
-                pass
-            self._stop.wait(0.02)
+            self._sample()
+            self._stop.wait(0.01)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t is not None:
+            self._t.join(timeout=10)
 
     def summary(self):
         if not self.samples:

@@ -28,6 +28,8 @@
 #include "replay.cuh"
 
 #include <algorithm>
+#include <array>
+#include <map>
 #include <vector>
 
 namespace kareto {
@@ -51,6 +53,9 @@ struct RState {
   uint32_t *eh, *et;   // LRU expiry lists: [g*W+c] newest / oldest disk block of group g
   uint32_t *ebh;       // FIFO / LFU expiry wheel: [k*W+c] first block of bucket k
   uint32_t NB, BSH, a_last;  // wheel: NB buckets of 2^BSH ms covering expiry times <= a_last
+  uint8_t *look;       // optional [N][n]: the HBM / DRAM tier each access found at its lookup (the
+                       // TTL-mode collapse below), at [position * n + the configuration's index]
+  uint64_t look_stride;  // n
   const uint16_t *gblk;
   uint64_t W;
 };
@@ -424,7 +429,7 @@ struct Rep {
   }
 
   __device__ void run(const ReplayTrace &T, const kareto_config &cf, const uint32_t *rows, int n_tuner, int G,
-                      kareto_counts *out, QueueState *qsp = nullptr) {
+                      kareto_counts *out, QueueState *qsp = nullptr, uint8_t *look = nullptr, uint32_t lstride = 0) {
     qs = qsp;
     cap[0] = cf.cap[0];
     cap[1] = cf.cap[1];
@@ -504,6 +509,11 @@ struct Rep {
         }
 #pragma unroll
         for (int q = 0; q < LOOK; q++) tt[q] = k0 + q < nb ? v.tier[at(bb[q])] : 0;
+        if (look) {
+#pragma unroll
+          for (int q = 0; q < LOOK; q++)
+            if (k0 + q < nb) look[(size_t)(s1 - 1 - (k0 + q)) * lstride] = tt[q];
+        }
 #pragma unroll
         for (int q = 0; q < LOOK; q++) {
           if (k0 + q >= nb) break;
@@ -625,7 +635,7 @@ __global__ void __launch_bounds__(64) k_replay(ReplayTrace T, const kareto_confi
   const kareto_config cf = cfg[id];
   Rep<LFU, EXPM, Q> rp(v, (uint64_t)ci);
   if (!Q) {
-    rp.run(T, cf, rows, n_tuner, G, out + id);
+    rp.run(T, cf, rows, n_tuner, G, out + id, nullptr, v.look ? v.look + id : nullptr, (uint32_t)v.look_stride);
     return;
   }
   QueueState qs;
@@ -745,10 +755,155 @@ __global__ void k_row_offsets(int64_t n, int64_t R, int64_t *__restrict__ off) {
   if (c <= n) off[c] = c * R;
 }
 
+// TTL-mode collapse (FIFO / LFU): with c3 = infinity the disk is the write-through lease store,
+// whose state is the trace's own (alive iff delta <= tau_g), and the HBM / DRAM replay never looks
+// at it (DRAM victims are dropped; LFU frequencies restart after a drop whatever the lease).  So
+// every TTL-mode configuration of one (policy, c1, c2) sees the same HBM / DRAM tier at every
+// lookup; one replay per (policy, c1, c2) records them (look) and each member configuration's
+// counts follow from (tier, delta, group) per access, for its own TTL row (R9-R22 as in K6).
+__global__ void k_ttl_member_counts(ReplayTrace T, const kareto_config *__restrict__ cfg,
+                                    const uint32_t *__restrict__ mrep, const uint32_t *__restrict__ mout, int64_t nm,
+                                    const uint8_t *__restrict__ look, uint32_t nrep,
+                                    const kareto_counts *__restrict__ rep_counts,
+                                    const uint32_t *__restrict__ rows, int n_tuner, int G,
+                                    kareto_counts *__restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nm) return;
+  const kareto_config cf = cfg[i];
+  const uint32_t *tau = rows + (size_t)(n_tuner > 0 ? cf.tuner : 0) * G;
+  const uint8_t *lk = look + mrep[i];  // [position * nrep + representative]
+  uint64_t hit[3] = {0, 0, 0}, miss = 0, hps = 0, after = 0, dw = 0, bt = 0;
+  uint32_t s0 = T.s[0];
+  for (uint32_t r = 0; r < T.R; r++) {
+    const uint32_t s1 = T.s[r + 1];
+    const uint32_t nb = s1 - s0;
+    if (nb == 0) continue;
+    const uint32_t tg = tau[T.grp[r]];
+    bool in_prefix = true;
+    for (uint32_t k = 0; k < nb; k++) {
+      const uint32_t pos = s1 - 1 - k;
+      const uint8_t t = lk[(size_t)pos * nrep];
+      const uint32_t dl = T.delta[pos];
+      const bool alive = dl != kNone && dl <= tg;
+      in_prefix = in_prefix && (t != T_NONE || alive);
+      if (in_prefix) {
+        hit[0] += t == T_HBM;
+        hit[1] += t == T_DRAM;
+        hit[2] += t == T_NONE;
+        hps += k;
+      } else {
+        miss += 1;
+        after += t != T_NONE;
+      }
+      dw += !alive;
+      if (dl != kNone) bt += dl < tg ? dl : tg;
+    }
+    s0 = s1;
+  }
+  for (int g = 0; g < G; g++) bt += T.Ug[g] * (uint64_t)tau[g];  // every block's last lease (R21)
+  const kareto_counts &rc = rep_counts[mrep[i]];
+  kareto_counts k;
+  for (int t = 0; t < 3; t++) k.hit[t] = hit[t];
+  k.miss = miss;
+  k.evict[0] = rc.evict[0];
+  k.evict[1] = rc.evict[1];
+  k.evict[2] = 0;
+  k.disk_writes = dw;
+  k.hit_pos_sum = hps;
+  k.bytetime_block_ms = bt;
+  k.resident_after_hole = after;
+  out[mout[i]] = k;
+}
+
+__global__ void k_scatter_counts(const kareto_counts *__restrict__ in, const uint32_t *__restrict__ to, int64_t n,
+                                 kareto_counts *__restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[to[i]] = in[i];
+}
+
 kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config *cfg_host, int64_t n,
                           const uint32_t *rows_host, const uint32_t *rows_dev, int n_tuner,
-                          kareto_counts *counts_dev, const QueueArgs &qarg) {
+                          kareto_counts *counts_dev, const QueueArgs &qarg, uint8_t *look_dev) {
   if (n <= 0) return KARETO_OK;
+  if (qarg.model == nullptr && look_dev == nullptr && getenv("KARETO_K6_NO_COLLAPSE") == nullptr) {
+    // TTL-mode collapse (k_ttl_member_counts): one replay per (policy, c1, c2) group of TTL-mode
+    // FIFO / LFU configurations, when that saves at least half of their replays and the lookup
+    // record fits in a quarter of the free device memory
+    std::map<std::array<uint64_t, 3>, std::vector<int64_t>> grp;
+    for (int64_t i = 0; i < n; i++) {
+      const kareto_config &c = cfg_host[i];
+      if (c.cap[2] == KARETO_INF && (c.policy == KARETO_FIFO || c.policy == KARETO_LFU))
+        grp[{(uint64_t)c.policy, c.cap[0], c.cap[1]}].push_back(i);
+    }
+    int64_t nmem = 0;
+    for (auto &kv : grp) nmem += (int64_t)kv.second.size();
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const uint64_t Nn = (uint64_t)tr->N;
+    // worth it when the members alone would not fit one wave (a full-size grid: their replays are
+    // whole extra passes over the trace); with room to spare (a small trace) they ride along with
+    // the other classes' concurrent waves for free and the collapse would add a pass
+    const double member_bytes = (double)nmem * (double)(tr->U > 0 ? tr->U : 1) * 13.0;
+    const bool force = getenv("KARETO_K6_COLLAPSE") != nullptr;
+    if (!grp.empty() && nmem >= 2 * (int64_t)grp.size() && (double)grp.size() * (double)Nn <= 0.25 * (double)fr &&
+        (force || member_bytes > 0.8 * (double)fr)) {
+      const int64_t nrep = (int64_t)grp.size();
+      std::vector<kareto_config> reps, mcfg, rest;
+      std::vector<uint32_t> mrep, mout, rout;
+      std::vector<char> collapsed((size_t)n, 0);
+      for (auto &kv : grp) {
+        const uint32_t ri = (uint32_t)reps.size();
+        reps.push_back(cfg_host[kv.second[0]]);
+        for (int64_t i : kv.second) {
+          collapsed[(size_t)i] = 1;
+          mcfg.push_back(cfg_host[i]);
+          mrep.push_back(ri);
+          mout.push_back((uint32_t)i);
+        }
+      }
+      for (int64_t i = 0; i < n; i++)
+        if (!collapsed[(size_t)i]) { rest.push_back(cfg_host[i]); rout.push_back((uint32_t)i); }
+      DBuf<uint8_t> look;
+      DBuf<kareto_counts> rcnt;
+      KTRY(look.alloc(ctx, (size_t)nrep * (Nn > 0 ? Nn : 1)));
+      KTRY(rcnt.alloc(ctx, nrep));
+      KTRY(replay_eval(ctx, tr, reps.data(), nrep, rows_host, rows_dev, n_tuner, rcnt.p, QueueArgs(), look.p));
+      {
+        cudaStream_t st = ctx->stream;
+        DBuf<kareto_config> dm;
+        DBuf<uint32_t> dmrep, dmout;
+        DBuf<uint64_t> dUg;
+        std::vector<uint64_t> hUg((size_t)tr->K + 1);
+        for (int g = 0; g <= tr->K; g++) hUg[(size_t)g] = (uint64_t)tr->U_g[(size_t)g];
+        KTRY(dm.alloc(ctx, mcfg.size())); KTRY(dmrep.alloc(ctx, mrep.size())); KTRY(dmout.alloc(ctx, mout.size()));
+        KTRY(dUg.alloc(ctx, hUg.size()));
+        KCUDA(ctx, cudaMemcpyAsync(dm.p, mcfg.data(), sizeof(kareto_config) * mcfg.size(), cudaMemcpyHostToDevice, st));
+        KCUDA(ctx, cudaMemcpyAsync(dmrep.p, mrep.data(), 4 * mrep.size(), cudaMemcpyHostToDevice, st));
+        KCUDA(ctx, cudaMemcpyAsync(dmout.p, mout.data(), 4 * mout.size(), cudaMemcpyHostToDevice, st));
+        KCUDA(ctx, cudaMemcpyAsync(dUg.p, hUg.data(), 8 * hUg.size(), cudaMemcpyHostToDevice, st));
+        ReplayTrace T{(uint32_t)tr->R, (uint32_t)tr->U, tr->s, tr->arr_rel, tr->grp, tr->blk, tr->inlen, tr->outlen,
+                      tr->delta, dUg.p, Nn};
+        Pass ps(ctx, "K6_ttl_members", 1, 1);
+        k_ttl_member_counts<<<grid_for((int64_t)mcfg.size(), 64), 64, 0, st>>>(
+            T, dm.p, dmrep.p, dmout.p, (int64_t)mcfg.size(), look.p, (uint32_t)nrep, rcnt.p, rows_dev, n_tuner, tr->K + 1,
+            counts_dev);
+        KTRY(sync(ctx, "ttl members"));  // the host vectors above are the copies' sources
+      }
+      if (!rest.empty()) {
+        DBuf<kareto_counts> rc;
+        DBuf<uint32_t> drout;
+        KTRY(rc.alloc(ctx, rest.size()));
+        KTRY(replay_eval(ctx, tr, rest.data(), (int64_t)rest.size(), rows_host, rows_dev, n_tuner, rc.p, QueueArgs(),
+                         nullptr));
+        KTRY(drout.alloc(ctx, rout.size()));
+        KCUDA(ctx, cudaMemcpyAsync(drout.p, rout.data(), 4 * rout.size(), cudaMemcpyHostToDevice, ctx->stream));
+        k_scatter_counts<<<grid_for((int64_t)rest.size(), 256), 256, 0, ctx->stream>>>(rc.p, drout.p,
+                                                                                       (int64_t)rest.size(), counts_dev);
+        KTRY(sync(ctx, "replay scatter"));
+      }
+      return KARETO_OK;
+    }
+  }
   // sequence numbers are 32-bit (the LFU key packs (freq << 32 | seq)): one per touch plus one per
   // demotion into a lower tier, and a block entering HBM is demoted at most twice before it is
   // dropped, so seq <= 3N
@@ -768,7 +923,7 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
     KCUDA(ctx, cudaStreamSynchronize(st));  // hUg is a host temporary
   }
   ReplayTrace T{(uint32_t)tr->R, (uint32_t)tr->U, tr->s, tr->arr_rel, tr->grp, tr->blk, tr->inlen, tr->outlen,
-                tr->delta, dUg.p};
+                tr->delta, dUg.p, (uint64_t)tr->N};
   const bool Qm = qarg.model != nullptr;
   const int64_t R = tr->R;
   // classes {list, LFU} x {expiry heap or not}; within a class, neighbours in a warp get
@@ -882,6 +1037,8 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
           v.NSW = (uint32_t)NSW;
         }
         v.ebh = c.ebh.p; v.NB = (uint32_t)NBK; v.BSH = BSH; v.a_last = a_last;
+        v.look = look_dev;
+        v.look_stride = (uint64_t)n;
         v.elink = c.elink.p;
         v.eh = c.eht.p;
         v.et = c.eht.p + (size_t)G * W;
@@ -1012,6 +1169,8 @@ kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config
       v.NSW = (uint32_t)NSW;
     }
     v.ebh = ebh.p; v.NB = (uint32_t)NBK; v.BSH = BSH; v.a_last = a_last;
+    v.look = look_dev;
+    v.look_stride = (uint64_t)n;
     v.elink = elink.p;
     v.eh = eht.p;
     v.et = eht.p + (size_t)G * W;

@@ -16,6 +16,7 @@ struct ReplayTrace {
   const uint32_t *outlen;  // [R] output tokens (row f3 queue)
   const uint32_t *delta;   // [N] reuse interval of each access (kNone: first access), touch order
   const uint64_t *Ug;      // [K+1] distinct blocks per group
+  uint64_t N;              // accesses
 };
 
 // row f3 (queue.cu): the queue model evaluated inside the replay of each configuration
@@ -29,8 +30,9 @@ struct QueueArgs {
 kareto_status replay_prepare(kareto_ctx *ctx, kareto_trace *tr);
 // counts of n configurations (host array) into counts_dev[n]; rows = [max(n_tuner,1)][K+1]
 // TTL rows, on the host and on the device
+// look_dev (optional, [n][N] bytes): each configuration's lookup tiers (HBM / DRAM / none) per access
 kareto_status replay_eval(kareto_ctx *ctx, kareto_trace *tr, const kareto_config *cfg_host, int64_t n,
                           const uint32_t *rows_host, const uint32_t *rows_dev, int n_tuner,
-                          kareto_counts *counts_dev, const QueueArgs &q = QueueArgs());
+                          kareto_counts *counts_dev, const QueueArgs &q = QueueArgs(), uint8_t *look_dev = nullptr);
 
 }  // namespace kareto

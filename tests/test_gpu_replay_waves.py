@@ -151,3 +151,43 @@ def test_lopsided_classes_no_starved_class(ctx, env, chat, capfd):
     check(ctx, tr, cf, None)
     waves = waves_from_debug(capfd.readouterr().err)
     assert waves.get(0, 0) >= 1 and waves.get(2, 0) >= 3, waves
+
+
+def test_ttl_mode_collapse_fifo_lfu():
+    """TTL-mode FIFO / LFU configurations of one (policy, c1, c2) share their HBM / DRAM replay (the
+    lease store is the trace's delta <= tau_g): one replay per group records the lookup tiers and
+    k_ttl_member_counts derives every member's counts for its own TTL row.  Against O1 and against
+    the uncollapsed replay (KARETO_K6_NO_COLLAPSE), bit for bit; CAPACITY configurations in the same
+    call take the normal K6 path."""
+    import os
+    import paper_2603_08739_b200 as K
+    tr = ki.synthetic("chat", R=2000, seed=31)
+    ot = O.OracleTrace(tr, top_k=4)
+    ctx = K.Context(0)
+    gt = ctx.load(tr, top_k=4)
+    U = ot.U
+    rows = np.array([[1_000 * (t + 1) * (g + 1) for g in range(5)] for t in range(6)] + [[U32] * 5], np.uint32)
+    A = lambda m, top: [top * i // (m - 1) for i in range(m)]
+    caps, pol, tun = [], [], []
+    for a in A(3, U // 16):
+        for b in A(3, U // 4):
+            for p in (O.FIFO, O.LFU):
+                for t in range(6):
+                    caps.append([a, b, O.INF_CAP]); pol.append(p); tun.append(t)
+                caps.append([a, b, U // 2]); pol.append(p); tun.append(t % 6)      # CAPACITY, finite TTLs
+                caps.append([a, b, U // 3]); pol.append(p); tun.append(6)          # CAPACITY, no TTL
+    oc = O.configs(caps, policy=np.array(pol), tuner=np.array(tun))
+    kc = K.configs(oc["cap"], policy=oc["policy"], tuner=oc["tuner"])
+    os.environ["KARETO_K6_COLLAPSE"] = "1"   # a small trace would not collapse on its own
+    try:
+        got, _ = ctx.eval_grid(gt, kc, K.Model(), rows)
+    finally:
+        os.environ.pop("KARETO_K6_COLLAPSE", None)
+    want = ot.replay(oc, rows)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    os.environ["KARETO_K6_NO_COLLAPSE"] = "1"
+    try:
+        got2, _ = ctx.eval_grid(gt, kc, K.Model(), rows)
+    finally:
+        os.environ.pop("KARETO_K6_NO_COLLAPSE", None)
+    assert np.array_equal(got.view(np.uint64), got2.view(np.uint64))

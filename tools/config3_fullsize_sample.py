@@ -28,6 +28,10 @@ def main():
     ap.add_argument("--requests", type=int, default=1_000_000)
     ap.add_argument("--per-cell", type=int, default=12, help="configurations per (policy, disk mode) replay cell")
     ap.add_argument("--oracle-threads", type=int, default=0)
+    ap.add_argument("--ttl-groups", type=int, default=0,
+                    help="instead of the stratified sample: every TTL row of this many (c1, c2) groups for FIFO "
+                         "and LFU in TTL mode (the collapsed path, forced with KARETO_K6_COLLAPSE)")
+    ap.add_argument("--oracle-sample", type=int, default=0, help="O1 on only this many of the sampled configurations")
     args = ap.parse_args()
     import torch
 
@@ -62,6 +66,15 @@ def main():
             idx.append(pick)
             cells[f"{pn}-{'ttl' if mode else 'capacity'}"] = {"grid": int(len(cell)), "sampled": int(len(pick))}
     idx = np.sort(np.concatenate(idx))
+    if args.ttl_groups > 0:
+        os.environ["KARETO_K6_COLLAPSE"] = "1"
+        pairs = sorted({(int(a), int(b)) for a, b in cfg["cap"][:, :2]})
+        pick = [pairs[i] for i in rng.choice(len(pairs), args.ttl_groups, replace=False)]
+        sel = np.zeros(len(cfg), bool)
+        for a, b in pick:
+            sel |= ttl_mode & (cfg["policy"] != K.LRU) & (cfg["cap"][:, 0] == a) & (cfg["cap"][:, 1] == b)
+        idx = np.nonzero(sel)[0]
+        cells = {"ttl_groups": [list(p) for p in pick], "configs": int(len(idx))}
     sub = cfg[idx]
 
     torch.cuda.set_device(0)
@@ -75,10 +88,15 @@ def main():
     oc = np.zeros(len(sub), O.CONFIG_DTYPE)
     for f in ("cap", "policy", "medium", "tuner", "axis"):
         oc[f] = sub[f]
+    osel = np.arange(len(sub))
+    if args.oracle_sample and args.oracle_sample < len(sub):
+        osel = np.sort(rng.choice(len(sub), args.oracle_sample, replace=False))
     t2 = time.perf_counter()
-    want = ot.replay(oc, rows, threads=args.oracle_threads or None)
+    want = ot.replay(oc[osel], rows, threads=args.oracle_threads or None)
     oracle_s = time.perf_counter() - t2
-    same = got.view(np.uint64).reshape(len(sub), -1) == want.view(np.uint64).reshape(len(sub), -1)
+    got, obj = got[osel], obj[osel]
+    oc = oc[osel]
+    same = got.view(np.uint64).reshape(len(osel), -1) == want.view(np.uint64).reshape(len(osel), -1)
     fo = ot.objective(O.Model(), oc, want)
     n_rep = int(replay.sum())
     rate = gt.N * len(sub) / gpu_s
@@ -86,7 +104,7 @@ def main():
         "metric": "K6 replay at full config-3 size on a stratified sample (row a7)",
         "n_accesses": int(gt.N), "n_unique": int(gt.U), "n_requests": int(gt.R),
         "grid_configs": int(len(cfg)), "grid_replay_configs": n_rep, "cells": cells,
-        "sample_configs": int(len(sub)),
+        "sample_configs": int(len(sub)), "oracle_checked_configs": int(len(osel)),
         "gpu_s": gpu_s, "access_configs_per_s": rate,
         "oracle_o1_s": oracle_s, "oracle_threads": args.oracle_threads or os.cpu_count(),
         "counts_bit_exact": bool(same.all()), "configs_differing": int((~same.all(1)).sum()),
